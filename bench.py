@@ -1,0 +1,303 @@
+"""bench.py -- full-graph PipeGCN training epochs/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config reddit]
+
+One "step" = one full-graph iteration t of Alg. 1: forward of all L layers on
+every partition with the boundary exchange, loss, backward with stale-gradient accumulation,
+gradient all-reduce and the Adam update (Table 3) -- every row of SURVEY.md section 8(a).
+Workload at N=1: BASELINE configs[1], the synthetic Reddit-shaped graph (232,965 nodes,
+~114.6M CSR non-zeros, 602 features, 41 classes), 4-layer GraphSAGE hidden 256, 2 partitions
+hosted on the one GPU (local transport), PIPE mode, dropout 0.5, fp32.
+Timing: W untimed warm-up iterations, then K iterations bracketed by CUDA events on the
+context stream (synchronize on both sides); inputs are far larger than L2 (X alone 563 MB).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full-graph epochs/s (max over ranks)"
+UNIT = "epochs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="reddit")
+    ap.add_argument("--parts", type=int, default=0, help="partitions (default max(2, N))")
+    ap.add_argument("--mode", default="pipe", choices=["pipe", "vanilla"])
+    ap.add_argument("--smooth", default="", help="'', 'f', 'g' or 'gf'")
+    ap.add_argument("--gemm", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        self.path = os.path.join("/tmp", "pgcn_clocks_%d.csv" % os.getpid())
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(c[1]), smax=float(c[2]), hw=c[5], hwt=c[6], swt=c[7], pcap=c[8]))
+            except ValueError:
+                pass
+        if not rows:
+            return None
+        sms = sorted(r["sm"] for r in rows)
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                            ("pcap", "sw_power_cap")):
+                if r[k].lower() in ("active", "1", "yes"):
+                    reasons.add(name)
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": rows[0]["smax"], "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+                "_fallback": True}
+
+
+def build_workload(name, n_parts):
+    from synth.graphs import CONFIGS, gen_graph, glorot_params, model_for
+    t0 = time.time()
+    g = gen_graph(name, seed=1)
+    m = model_for(name)
+    params0 = glorot_params(m.widths, 3)
+    return g, m, params0, time.time() - t0
+
+
+def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2):
+    """The oracle (oracle/, numpy/scipy fp64) as it stands, on a bounded sample of the same workload:
+    the same generator recipe, degree, widths, dropout and partition count at N = sample_n, timed
+    for `iters` PipeGCN iterations; per-epoch time extrapolated linearly in N (every term of the
+    epoch -- SpMM nnz*F and GEMM N*F*F' -- is linear in N at fixed degree)."""
+    from oracle import pipegcn
+    from oracle.partition import partition as opart
+    from synth.graphs import CONFIGS, gen_graph, glorot_params, model_for
+    c = CONFIGS[name]
+    deg = c["nnz"] / c["n"]
+    g = gen_graph(name, seed=1, n=sample_n, nnz=int(sample_n * deg))
+    m = model_for(name)
+    params0 = glorot_params(m.widths, 3)
+    parts_o = opart(g.n, g.row_ptr, g.col_idx, parts)
+    t0 = time.time()
+    pipegcn.run(g, parts_o, params0, m, iters, mode=mode, smooth_f="f" in smooth, smooth_g="g" in smooth)
+    dt = (time.time() - t0) / iters
+    scale = c["n"] / sample_n
+    epoch_s = dt * scale
+    cores = len(os.sched_getaffinity(0))
+    return {"value": 1.0 / epoch_s, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "oracle PipeGCN (%s) %d iterations on a %s-recipe graph with N=%d (nnz=%d, same degree, widths, "
+                      "dropout, %d partitions); %.2f s/iteration x N_full/N_sample=%.1f" % (
+                          mode, iters, name, sample_n, g.nnz, parts, dt, scale)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    parts = args.parts or max(2, args.gpus)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1)
+    info = None
+    t0 = time.time()
+    for _ in range(args.steps):
+        info = cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1)
+        vals.append(1.0 / info["value"])
+    wall = time.time() - t0
+    ms = 1000.0 * sum(vals) / len(vals)
+    v = 1000.0 / ms
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "%s-synthetic, %d partitions, %s" % (args.config, parts, args.mode)},
+           "cpu_baseline": dict(info, value=v),
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": wall}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+
+    from paper_2203_10428_b200 import pgcn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 or args.gpus > 1:
+        raise SystemExit("multi-GPU bench needs the NCCL transport (not built in this version)")
+    dev = 0
+    torch.cuda.set_device(dev)
+    parts = args.parts or max(2, args.gpus)
+    g, m, params0, t_gen = build_workload(args.config, parts)
+    t0 = time.time()
+    part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
+    t_part = time.time() - t0
+    cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
+                           gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
+                           n_train_global=g.n_train, gemm=args.gemm)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx = pgcn.Context(part, cfg, stream=stream)
+    views = [part.view(i) for i in range(parts)]
+    host = []
+    for i, v in enumerate(views):
+        gid = v["inner_gid"]
+        X = torch.from_numpy(np.ascontiguousarray(g.X[gid])).pin_memory()
+        lab = torch.from_numpy(np.ascontiguousarray(g.labels[gid])).pin_memory()
+        tm = torch.from_numpy(np.ascontiguousarray(g.train_mask[gid])).pin_memory()
+        host.append((X, lab, tm))
+    dev_in = [tuple(a.cuda(non_blocking=True) for a in h) for h in host]
+    torch.cuda.synchronize()
+    for i in range(parts):
+        ctx.set_inputs(i, *dev_in[i])
+    theta = torch.tensor(pgcn.flatten_params(params0), device="cuda")
+    grads = torch.zeros_like(theta)
+    opt = torch.zeros(2 * theta.numel(), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    t = 0
+    W, K = max(args.warmup, 3), args.steps
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            t += 1
+            ctx.step(t, theta, grads, opt, loss)
+    torch.cuda.synchronize()
+    clocks = Clocks(dev)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    ctx.timing_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(K):
+        t += 1
+        ctx.step(t, theta, grads, opt, loss)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    kern = {name: ctx.timing_read(k) for k, name in enumerate(pgcn.KERNELS)}
+    ctx.timing_enable(False)
+    ms = ms_total / K
+    value = 1000.0 / ms
+    loss_v = float(loss.item())
+
+    # end to end through the public API: pinned host inputs copied in every step, loss read back
+    e2e = None
+    if not args.no_e2e:
+        loss_h = torch.zeros(1).pin_memory()
+        h2d = sum(sum(a.numel() * a.element_size() for a in h) for h in host)
+        torch.cuda.synchronize()
+        e0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(K):
+            t += 1
+            for i in range(parts):
+                ctx.set_inputs(i, *host[i])
+            ctx.step(t, theta, grads, opt, loss)
+            with torch.cuda.stream(stream):
+                loss_h.copy_(loss, non_blocking=True)
+            stream.synchronize()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ev0.elapsed_time(ev1) / K
+        e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
+               "ms_per_step": e_ms, "host_wall_ms_per_step": 1000.0 * (time.perf_counter() - e0) / K}
+
+    pk = peaks()
+    top = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    name, kd = top
+    if name.startswith("gemm") and args.gemm == "fp32":
+        # SIMT fp32: bound by FFMA issue, 148 SMs x 128 lanes x 2 flop x max SM clock
+        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        ach = kd["flops"] / (kd["ms"] / 1e3) / 1e12
+        roof = {"kernel": name, "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    else:
+        ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"]}
+    roof["launches_timed"] = kd["launches"]
+    roof["ms_per_launch"] = kd["ms"] / max(kd["launches"], 1)
+    roof["share_of_step"] = kd["ms"] / ms_total
+    roof["traffic"] = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        roof["traffic"] = tr.get(name)
+    except Exception:
+        pass
+    breakdown = {k: {"ms_per_step": v["ms"] / K, "share": v["ms"] / ms_total,
+                     "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
+                     "TFLOPs": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None}
+                 for k, v in kern.items() if v["launches"]}
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        try:
+            cpu = cpu_baseline(args.config, parts, args.mode, args.smooth)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"error": str(e)}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU (local transport), %s%s, "
+                                  "dropout %.1f, Adam" % (args.config, g.n, g.nnz, m.widths, parts, 1, args.mode,
+                                                          ("-" + args.smooth.upper()) if args.smooth else "",
+                                                          m.dropout),
+                      "global_batch": g.n, "parallelism": "partition x%d" % parts, "gemm": args.gemm,
+                      "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+           "breakdown": breakdown, "loss": loss_v,
+           "setup_s": {"generate": t_gen, "partition": t_part}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,251 @@
+/*
+ * pgcn.h -- C ABI of the B200-native PipeGCN training step (arXiv 2203.10428).
+ *
+ * The calls follow the paper's problem statement, Alg. 1 (PAPER.md:104 header + lines 1-7,
+ * PAPER.md:450 lines 8-35):  Input: partition id i, partition count n, G_i, P_i, X_i, Y_i,
+ * B_i, L, eta, W_0.  Output: W_T.
+ *
+ *   pgcn_partition      Alg. 1 l.1-5   inner / boundary sets, send / receive sets, P_i
+ *   pgcn_layer_fwd      Alg. 1 l.9-14  install stale boundary rows, exchange, H^(l) = s(P_i H W)
+ *   pgcn_loss           Alg. 1 l.16    J^(L) = dLoss/dH^(L)
+ *   pgcn_layer_bwd      Alg. 1 l.18-27 G_i^(l), J^(l-1), stale gradient accumulation, exchange
+ *   pgcn_update         Alg. 1 l.31-32 G = AllReduce(G_i); W_t = W_{t-1} - eta G (or Adam, Table 3)
+ *   pgcn_step           one iteration t of Alg. 1 l.8-32 (all of the above, in order)
+ *
+ * Readings of ambiguous passages (R1..R24) are listed in DESIGN.md; the ones that fix a
+ * computed value are cited where they apply below.
+ *
+ * Conventions
+ * - Every call returns 0 (PGCN_OK) or a negative PGCN_E* code; pgcn_last_error() returns a
+ *   thread-local message describing the last failure on the calling thread.
+ * - Host pointers are borrowed for the duration of the call.  Device memory is owned by the
+ *   caller: the context carves everything it needs out of one caller-allocated workspace
+ *   (size from pgcn_workspace_bytes); the library never calls cudaMalloc.  NCCL may allocate
+ *   internally.
+ * - Arguments are validated before any work is enqueued.  A CUDA or NCCL failure is sticky:
+ *   every later call on that context returns PGCN_ESTATE.
+ * - Order: within iteration t the calls must be layer_fwd(1..L), loss, layer_bwd(L..1),
+ *   update (pgcn_step does exactly that), and t must increase by exactly 1 starting at 1.
+ *   Violations return PGCN_ESTATE.  This is what keeps "one iteration stale" well defined.
+ * - Device work is asynchronous on the stream given to pgcn_ctx_create; no call synchronises
+ *   the host except pgcn_ctx_create (index upload) and pgcn_ctx_destroy.
+ * - A context hosts one or more partitions on one GPU.  Peers hosted by the same context
+ *   exchange through device gathers ("local transport"); peers in other processes through
+ *   NCCL point-to-point on a dedicated comm stream (one partition per process).
+ * - Row-major everywhere.  Feature rows are padded to ld = round_up(F, 4) floats (16 B) in
+ *   the context's internal buffers; the public X / params layouts below are unpadded.
+ */
+#ifndef PGCN_H
+#define PGCN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PGCN_OK = 0,
+  PGCN_EINVAL = -1,      /* bad argument (null pointer, size, range, layout) */
+  PGCN_ESTATE = -2,      /* call out of Alg. 1 order, or context poisoned by an earlier failure */
+  PGCN_ECUDA = -3,       /* CUDA runtime error */
+  PGCN_ENCCL = -4,       /* NCCL error */
+  PGCN_ENOMEM = -5,      /* workspace too small / host allocation failed */
+  PGCN_EUNSUPPORTED = -6 /* configuration not implemented */
+};
+
+#define PGCN_MAX_LAYERS 16
+#define PGCN_MAX_PARTS 64
+
+const char* pgcn_last_error(void);
+int pgcn_version(void); /* 100 * major + minor */
+
+/* ------------------------------------------------------------------------------------------
+ * (1) Alg. 1 l.1-5.  Host only, deterministic, multithreaded.
+ *
+ * n_nodes   : N (< 2^31).
+ * row_ptr   : [N+1] int64, CSR of the in-neighbour lists N(v) (the aggregation of Eq. 1 reads
+ *             h_u for u in N(v)); col_idx: [nnz] int32 in [0, N).  Self loops and duplicate
+ *             entries are kept as given (the generator emits neither).
+ * n_parts   : 1..PGCN_MAX_PARTS.
+ * part_of   : [N] int32 map node -> partition, or NULL for contiguous node-balanced ranges
+ *             lo_p = floor(p*N/n_parts) (reading R19; METIS, is out of scope).
+ * n_threads : host threads (<= 0: hardware concurrency).
+ * out       : receives an opaque handle owning every array returned by pgcn_partition_view.
+ * Errors    : PGCN_EINVAL (null / out-of-range ids, non-monotone row_ptr), PGCN_ENOMEM.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct pgcn_partitioning pgcn_partitioning;
+
+int pgcn_partition(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col_idx, int32_t n_parts,
+                   const int32_t* part_of, int32_t n_threads, pgcn_partitioning** out);
+
+/* Per-partition arrays (borrowed; valid until pgcn_partition_free).  Canonical orders
+ * (reading R20) make "bit-exact" well defined:
+ *   inner_gid [n_inner]      V_i, ascending gid                                  (l.1)
+ *   halo_gid  [n_halo]       B_i, sorted by (owner, gid)                         (l.1)
+ *   halo_off  [n_parts+1]    segment of B_i owned by j = S_{j,i} = B_i ∩ V_j      (l.4-5)
+ *   send_off  [n_parts+1], send_idx [n_send]
+ *                            S_{i,j} = B_j ∩ V_i as local inner ids, ascending gid;
+ *                            element-wise equal to j's halo segment for owner i  (l.2-3)
+ *   row_ptr [n_inner+1], col_idx [nnz]
+ *                            pattern of P_i: row v's neighbours in global order, local ids
+ *                            (inner: [0,n_inner), boundary: n_inner + position in B_i)
+ *   inv_deg [n_inner]        fp32(1)/fp32(d_v), d_v the FULL-graph degree (Eq. 3-4,
+ *                            PAPER.md:456-462; reading R1); 0 for isolated v
+ *   t_row_ptr [n_inner+n_halo+1], t_col_idx [nnz]
+ *                            pattern of P_i^T (Alg. 1 l.20): for local row u, the inner v
+ *                            with u in N(v), ascending v
+ *   inv_ptr [n_inner+1], inv_pos [n_send]
+ *                            inverse send map: positions k with send_idx[k] == v, ascending k
+ *                            (Alg. 1 l.23-25 accumulation)                                  */
+typedef struct {
+  int32_t part, n_parts;
+  int64_t n_inner, n_halo, nnz, n_send;
+  const int64_t* inner_gid;
+  const int64_t* halo_gid;
+  const int64_t* halo_off;
+  const int64_t* send_off;
+  const int32_t* send_idx;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const float* inv_deg;
+  const int64_t* t_row_ptr;
+  const int32_t* t_col_idx;
+  const int64_t* inv_ptr;
+  const int32_t* inv_pos;
+} pgcn_part_view;
+
+int pgcn_partition_view(const pgcn_partitioning* p, int32_t part, pgcn_part_view* out);
+int64_t pgcn_partition_n_nodes(const pgcn_partitioning* p);
+void pgcn_partition_free(pgcn_partitioning* p);
+
+/* ------------------------------------------------------------------------------------------
+ * (2) Training configuration.
+ *   width[0..n_layers]  F_0 (input features) .. F_L (classes).  GraphSAGE-mean layers
+ *                       (Table 3): Y = [Z | D] W + b,  W = [W_neigh; W_self].
+ *   mode                0 VANILLA (Fig. 1(a): exchange consumed in the same iteration),
+ *                       1 PIPE (Alg. 1: exchange consumed one iteration later).
+ *   smooth_f, smooth_g  PipeGCN-F / -G: EMA of stale boundary features (layers >= 2, R14) /
+ *                       of each received gradient message (R13); Sec. 3.4 PAPER.md:478-486.
+ *   gamma               EMA decay (default 0.95).
+ *   ema_init            0 = first receipt initialises the state (R12), 1 = zero state.
+ *   dropout, seed       p and the mask seed: keep iff (SplitMix64(key ^ seed) >> 40) >=
+ *                       floor(p*2^24 + 0.5), key = ((t(L+1)+l)N + gid)F_{l-1} + col, applied
+ *                       to every layer's input after the exchange (App. F; R5).
+ *   gemm                0 FP32 (SIMT, parity path), 1 BF16 tensor cores (tcgen05; 2e-2 tier).
+ *   loss                0 softmax cross-entropy (labels int32 [n_inner]), 1 sigmoid BCE
+ *                       (labels uint8 [n_inner x F_L]); mean over the GLOBAL train set (R6).
+ *   n_global            N (dropout keys); n_train_global: |train set| over the whole graph.
+ *   opt                 0 SGD (Alg. 1 l.32), 1 Adam (Table 3; PyTorch defaults, R7).
+ *   dump_j              1: also store the accumulated J^(l) inner rows (parity checks only).
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_layers;
+  int32_t width[PGCN_MAX_LAYERS + 1];
+  int32_t mode;
+  int32_t smooth_f, smooth_g;
+  int32_t ema_init;
+  double gamma;
+  double dropout;
+  uint64_t seed;
+  int32_t gemm;
+  int32_t loss;
+  int64_t n_global;
+  int64_t n_train_global;
+  int32_t opt;
+  int32_t dump_j;
+  double lr, beta1, beta2, eps;
+} pgcn_config;
+
+/* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this
+ * context.  Otherwise one partition per rank (rank r hosts partition r) and nccl_id_halo /
+ * nccl_id_reduce point to two 128-byte ncclUniqueId blobs shared by all ranks (the caller
+ * broadcasts them, e.g. with torch.distributed).                                           */
+typedef struct {
+  int32_t rank, nranks;
+  const void* nccl_id_halo;
+  const void* nccl_id_reduce;
+} pgcn_comm;
+
+typedef struct pgcn_ctx pgcn_ctx;
+
+/* Workspace bytes for hosting partitions local_parts[0..n_local) of p under cfg. */
+int pgcn_workspace_bytes(const pgcn_partitioning* p, const int32_t* local_parts, int32_t n_local,
+                         const pgcn_config* cfg, size_t* bytes);
+
+/* Create a context.  ws: device buffer of ws_bytes (256-byte aligned); stream: cudaStream_t
+ * (NULL = legacy default) on which all compute is enqueued.  Uploads the index arrays and
+ * zero-fills the activations (boundary rows start at 0, Alg. 1 l.6), synchronously.       */
+int pgcn_ctx_create(const pgcn_partitioning* p, const int32_t* local_parts, int32_t n_local,
+                    const pgcn_config* cfg, const pgcn_comm* comm, void* ws, size_t ws_bytes,
+                    void* stream, pgcn_ctx** out);
+int pgcn_ctx_destroy(pgcn_ctx* ctx);
+
+/* Inputs of hosted partition `local` (0..n_local-1): X_i [n_inner x F_0] fp32 row-major
+ * (unpadded), labels (see cfg.loss), train_mask uint8 [n_inner].  Host (pageable or pinned)
+ * or device pointers; copied asynchronously on the context stream into the workspace.     */
+int pgcn_set_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* labels,
+                    const uint8_t* train_mask);
+
+/* Flat parameter vector theta = vec[W^(1), b^(1), ..., W^(L), b^(L)], fp32,
+ * unpadded: W^(l) is [2F_{l-1} x F_l] row-major (rows 0..F_{l-1}-1 multiply z, the rest h;
+ * CONCAT(z_v, h_v) PAPER.md:44, reading R3), b^(l) is [F_l].                               */
+int64_t pgcn_param_count(const pgcn_config* cfg);
+
+/* (3) Alg. 1 l.9-14 for layer `layer` (1..L) of every hosted partition, iteration t.
+ * params: device pointer to theta (W_{t-1}).                                               */
+int pgcn_layer_fwd(pgcn_ctx* ctx, int64_t t, int32_t layer, const float* params);
+
+/* (4) Alg. 1 l.16.  loss_dev: device fp32 scalar receiving the sum of the hosted partitions'
+ * loss terms (each already divided by the global train count), or NULL.                    */
+int pgcn_loss(pgcn_ctx* ctx, int64_t t, float* loss_dev);
+
+/* (5) Alg. 1 l.18-27 for layer `layer` (L..1): G_i^(l) (kept in the context), J^(l-1) with
+ * stale (PIPE) or fresh (VANILLA) boundary gradients accumulated, and the exchange.        */
+int pgcn_layer_bwd(pgcn_ctx* ctx, int64_t t, int32_t layer, const float* params);
+
+/* (6) Alg. 1 l.31-32: grads = sum_i G_i (ascending i, then NCCL all-reduce SUM across ranks);
+ * params updated in place.  opt_state: [2 * param_count] fp32 device (Adam m, v; zero at t=1),
+ * may be NULL for SGD.                                                                     */
+int pgcn_update(pgcn_ctx* ctx, int64_t t, float* params, float* grads, float* opt_state);
+
+/* (7) One iteration t of Alg. 1 (l.8-32).                                                   */
+int pgcn_step(pgcn_ctx* ctx, int64_t t, float* params, float* grads, float* opt_state,
+              float* loss_dev);
+
+/* Device views of internal buffers for parity checks and diagnostics (not needed to train).
+ * kind: PGCN_T_H   layer-l output H^(l) (l = 1..L; l = L: logits), inner rows, parity of t
+ *       PGCN_T_HIN layer-l input buffer [inner; boundary] rows (l = 1..L)
+ *       PGCN_T_Z   aggregated Z of layer l (inner rows)
+ *       PGCN_T_J   accumulated J^(l) inner rows (needs cfg.dump_j; l = 1..L-1), t's parity
+ *       PGCN_T_G   this partition's G_i, flat like theta
+ * The returned pointer is valid until the next call that writes that buffer.               */
+enum { PGCN_T_H = 0, PGCN_T_HIN = 1, PGCN_T_Z = 2, PGCN_T_J = 3, PGCN_T_G = 4 };
+typedef struct {
+  void* ptr;
+  int64_t rows, cols, ld; /* elements; ld = row stride */
+} pgcn_tensor_desc;
+int pgcn_tensor(pgcn_ctx* ctx, int32_t local, int32_t kind, int32_t layer, int64_t t,
+                pgcn_tensor_desc* out);
+
+/* Number of kernels this library launched on the context so far (counted at launch). */
+int64_t pgcn_launch_count(const pgcn_ctx* ctx);
+
+/* Per-kernel device timing (diagnostics / roofline).  When enabled, every launch of the listed
+ * kernel kinds is bracketed by CUDA events on the context stream; pgcn_timing_read synchronises
+ * the stream and returns the summed elapsed milliseconds, launch count and the algorithmic bytes
+ * (or flops for GEMMs) those launches were charged with.      */
+enum {
+  PGCN_K_SPMM_FWD = 0, PGCN_K_SPMM_BWD = 1, PGCN_K_GEMM_FWD = 2, PGCN_K_GEMM_DW = 3, PGCN_K_GEMM_DA = 4,
+  PGCN_K_DROPOUT = 5, PGCN_K_GATHER = 6, PGCN_K_GRAD_REDUCE = 7, PGCN_K_LOSS = 8, PGCN_K_UPDATE = 9,
+  PGCN_K_COUNT = 10
+};
+int pgcn_timing_enable(pgcn_ctx* ctx, int32_t on); /* also resets the accumulators */
+int pgcn_timing_read(pgcn_ctx* ctx, int32_t kind, double* ms, int64_t* launches, double* alg_bytes,
+                     double* alg_flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGCN_H */

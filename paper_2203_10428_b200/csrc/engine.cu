@@ -1,0 +1,648 @@
+// Step engine: per-partition device context and the Alg. 1 state machine.
+//
+// Data layout in the caller's workspace, per hosted partition i:
+//   X        [n_all x ld0]         layer-1 input; rows [0,n_in) = X_i, [n_in,n_all) = boundary
+//   H[l][b]  [n_all x ld_l]        layer-l output / layer-(l+1) input, b = t & 1 (parity
+//                                  double buffer: the PIPE install at t reads owners' b(t-1))
+//   logits   [n_in  x ld_L]
+//   D[l]     [n_all x ld_{l-1}]    dropout(layer-l input) (absent when p = 0: D = input)
+//   Z[l]     [n_in  x ld_{l-1}]    aggregated neighbours (S3)
+//   M        [n_in  x max ld]      J o sigma' of the layer being back-propagated
+//   dA       [n_in  x 2 max ld]    [inv_deg * dZ | dD_self] (S7)
+//   J[l][b]  [n_all x ld_l]        J^(l) for inner + boundary rows (S8), parity double buffer
+//   emaG[l]  [n_send x ld_l]       EMA-G state per received gradient row (Sec. 3.4)
+//   G        [P]                   this partition's G_i, laid out like theta
+// ld_l = round_up(F_l, 4).  Boundary rows start at 0 (workspace zero-filled; Alg. 1 l.6).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "pgcn.h"
+
+namespace pgcn {
+
+struct PartCtx {
+  int32_t part = 0;
+  pgcn_part_view v{};
+  int64_t n_in = 0, n_bd = 0, n_all = 0, nnz = 0, n_send = 0;
+  int64_t *rp = nullptr, *trp = nullptr, *inv_ptr = nullptr, *gid = nullptr;
+  int32_t *col = nullptr, *tcol = nullptr, *halo_map = nullptr, *msg_map = nullptr, *send_idx = nullptr,
+          *inv_pos = nullptr;
+  float* inv_deg = nullptr;
+  float* X = nullptr;
+  float* H[PGCN_MAX_LAYERS + 1][2] = {};
+  float* logits = nullptr;
+  float* D[PGCN_MAX_LAYERS + 1] = {};
+  float* Z[PGCN_MAX_LAYERS + 1] = {};
+  float* M = nullptr;
+  float* dA = nullptr;
+  float* J[PGCN_MAX_LAYERS + 1][2] = {};
+  float* emaG[PGCN_MAX_LAYERS + 1] = {};
+  void* labels = nullptr;
+  uint8_t* train = nullptr;
+  float* row_loss = nullptr;
+  float* G = nullptr;
+};
+
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(int64_t n) {
+    off = (size_t)round_up((int64_t)off, 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * (size_t)(n > 0 ? n : 0);
+    return p;
+  }
+};
+
+enum { K_FWD = 0, K_LOSS = 1, K_BWD = 2, K_UPD = 3 };
+
+struct KTimer {
+  std::vector<cudaEvent_t> ev;  // (start, stop) pairs
+  size_t used = 0;
+  int64_t n = 0;
+  double bytes = 0.0, flops = 0.0;
+};
+
+}  // namespace pgcn
+
+struct pgcn_ctx {
+  pgcn_config cfg{};
+  int L = 0;
+  int64_t F[PGCN_MAX_LAYERS + 1] = {}, ld[PGCN_MAX_LAYERS + 1] = {}, woff[PGCN_MAX_LAYERS + 2] = {};
+  int64_t P = 0, ldmax = 0;
+  int32_t n_parts = 0;
+  std::vector<pgcn::PartCtx> parts;
+  cudaStream_t s = nullptr;
+  float* dw_ws = nullptr;
+  int64_t dw_ws_floats = 0;
+  float* part_loss = nullptr;
+  int64_t exp_t = 1;
+  int exp_kind = pgcn::K_FWD, exp_layer = 1;
+  int poisoned = 0;
+  int64_t launches = 0;
+  int timing = 0;
+  pgcn::KTimer kt[PGCN_K_COUNT];
+  ~pgcn_ctx() {
+    for (auto& k : kt)
+      for (auto e : k.ev) cudaEventDestroy(e);
+  }
+};
+
+namespace pgcn {
+namespace {
+
+int validate_cfg(const pgcn_config* c) {
+  if (!c) return fail(PGCN_EINVAL, "config is NULL");
+  if (c->n_layers < 1 || c->n_layers > PGCN_MAX_LAYERS) return fail(PGCN_EINVAL, "n_layers out of range");
+  for (int l = 0; l <= c->n_layers; ++l)
+    if (c->width[l] < 1) return fail(PGCN_EINVAL, "width[%d] < 1", l);
+  if (c->mode != 0 && c->mode != 1) return fail(PGCN_EINVAL, "mode must be 0 (VANILLA) or 1 (PIPE)");
+  if (!(c->dropout >= 0.0 && c->dropout < 1.0)) return fail(PGCN_EINVAL, "dropout must be in [0,1)");
+  if (c->gemm != 0) return fail(PGCN_EUNSUPPORTED, "gemm variant %d not built", c->gemm);
+  if (c->loss != 0 && c->loss != 1) return fail(PGCN_EINVAL, "loss must be 0 (CE) or 1 (BCE)");
+  if (c->opt != 0 && c->opt != 1) return fail(PGCN_EINVAL, "opt must be 0 (SGD) or 1 (Adam)");
+  if (c->n_train_global < 1) return fail(PGCN_EINVAL, "n_train_global < 1");
+  if (!(c->gamma >= 0.0 && c->gamma <= 1.0)) return fail(PGCN_EINVAL, "gamma out of [0,1]");
+  return PGCN_OK;
+}
+
+int64_t param_count(const pgcn_config* c) {
+  int64_t P = 0;
+  for (int l = 1; l <= c->n_layers; ++l) P += (2 * (int64_t)c->width[l - 1] + 1) * c->width[l];
+  return P;
+}
+
+// Lays out every buffer (dry run when A.base == nullptr).
+int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local, Arena& A) {
+  const int L = C->L;
+  C->parts.assign(n_local, PartCtx{});
+  int64_t dw_need = 0;
+  for (int i = 0; i < n_local; ++i) {
+    PartCtx& p = C->parts[i];
+    p.part = local[i];
+    int rc = pgcn_partition_view(part, local[i], &p.v);
+    if (rc) return rc;
+    p.n_in = p.v.n_inner;
+    p.n_bd = p.v.n_halo;
+    p.n_all = p.n_in + p.n_bd;
+    p.nnz = p.v.nnz;
+    p.n_send = p.v.n_send;
+    p.rp = A.take<int64_t>(p.n_in + 1);
+    p.col = A.take<int32_t>(p.nnz);
+    p.inv_deg = A.take<float>(p.n_in);
+    p.trp = A.take<int64_t>(p.n_all + 1);
+    p.tcol = A.take<int32_t>(p.nnz);
+    p.gid = A.take<int64_t>(p.n_all);
+    p.send_idx = A.take<int32_t>(p.n_send);
+    p.inv_ptr = A.take<int64_t>(p.n_in + 1);
+    p.inv_pos = A.take<int32_t>(p.n_send);
+    p.halo_map = A.take<int32_t>(p.n_bd);
+    p.msg_map = A.take<int32_t>(p.n_send);
+    p.X = A.take<float>(p.n_all * C->ld[0]);
+    for (int l = 1; l < L; ++l)
+      for (int b = 0; b < 2; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
+    p.logits = A.take<float>(p.n_in * C->ld[L]);
+    for (int l = 1; l <= L; ++l) {
+      if (C->cfg.dropout > 0.0) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
+      p.Z[l] = A.take<float>(p.n_in * C->ld[l - 1]);
+    }
+    p.M = A.take<float>(p.n_in * C->ldmax);
+    if (L > 1) p.dA = A.take<float>(p.n_in * 2 * C->ldmax);
+    for (int l = 1; l < L; ++l) {
+      for (int b = 0; b < 2; ++b) p.J[l][b] = A.take<float>(p.n_all * C->ld[l]);
+      if (C->cfg.smooth_g) p.emaG[l] = A.take<float>(p.n_send * C->ld[l]);
+    }
+    p.labels = C->cfg.loss == 0 ? (void*)A.take<int32_t>(p.n_in) : (void*)A.take<uint8_t>(p.n_in * C->F[L]);
+    p.train = A.take<uint8_t>(p.n_in);
+    p.row_loss = A.take<float>(p.n_in);
+    p.G = A.take<float>(C->P);
+    for (int l = 1; l <= L; ++l) {
+      int64_t w = gemm_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
+      if (w > dw_need) dw_need = w;
+    }
+  }
+  C->dw_ws_floats = dw_need;
+  C->dw_ws = A.take<float>(dw_need);
+  C->part_loss = A.take<float>(n_local);
+  return PGCN_OK;
+}
+
+int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local,
+                    const pgcn_config* cfg) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!part) return fail(PGCN_EINVAL, "partition is NULL");
+  if (!local || n_local < 1) return fail(PGCN_EINVAL, "no local partitions");
+  pgcn_part_view v0;
+  rc = pgcn_partition_view(part, local[0], &v0);
+  if (rc) return rc;
+  if (n_local != v0.n_parts)
+    return fail(PGCN_EUNSUPPORTED, "this build hosts all %d partitions in one context (got %d)", v0.n_parts, n_local);
+  for (int i = 0; i < n_local; ++i)
+    if (local[i] != i) return fail(PGCN_EINVAL, "local_parts must be 0..n_parts-1 in order");
+  if (cfg->n_global != pgcn_partition_n_nodes(part)) return fail(PGCN_EINVAL, "cfg.n_global != partition N");
+  C->cfg = *cfg;
+  C->L = cfg->n_layers;
+  C->n_parts = v0.n_parts;
+  C->ldmax = 0;
+  for (int l = 0; l <= C->L; ++l) {
+    C->F[l] = cfg->width[l];
+    C->ld[l] = ld_of(cfg->width[l]);
+    if (C->ld[l] > C->ldmax) C->ldmax = C->ld[l];
+  }
+  C->woff[1] = 0;
+  for (int l = 1; l <= C->L; ++l) C->woff[l + 1] = C->woff[l] + (2 * C->F[l - 1] + 1) * C->F[l];
+  C->P = C->woff[C->L + 1];
+  return PGCN_OK;
+}
+
+DropSpec drop_spec(const pgcn_ctx* C, int64_t t, int l) {
+  DropSpec d{};
+  const double p = C->cfg.dropout;
+  d.on = p > 0.0;
+  d.seed = C->cfg.seed;
+  d.key_base = ((uint64_t)t * (uint64_t)(C->L + 1) + (uint64_t)l) * (uint64_t)C->cfg.n_global;
+  d.thr = (uint32_t)std::floor(p * 16777216.0 + 0.5);
+  d.scale = d.on ? (float)(1.0 / (1.0 - p)) : 1.0f;
+  d.width = (int32_t)C->F[l - 1];
+  return d;
+}
+
+int check_cuda(pgcn_ctx* C, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    C->poisoned = 1;
+    return fail(PGCN_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+  }
+  return PGCN_OK;
+}
+
+int expect(pgcn_ctx* C, int64_t t, int kind, int layer, const char* name) {
+  if (C->poisoned) return fail(PGCN_ESTATE, "%s: context poisoned by an earlier failure", name);
+  if (t != C->exp_t || kind != C->exp_kind || (kind == K_FWD || kind == K_BWD ? layer != C->exp_layer : false)) {
+    static const char* kn[] = {"layer_fwd", "loss", "layer_bwd", "update"};
+    return fail(PGCN_ESTATE, "%s(t=%lld, layer=%d) out of Alg. 1 order: expected %s(t=%lld, layer=%d)", name,
+                (long long)t, layer, kn[C->exp_kind], (long long)C->exp_t, C->exp_layer);
+  }
+  return PGCN_OK;
+}
+
+void advance(pgcn_ctx* C) {
+  switch (C->exp_kind) {
+    case K_FWD:
+      if (C->exp_layer < C->L) ++C->exp_layer;
+      else C->exp_kind = K_LOSS;
+      break;
+    case K_LOSS:
+      C->exp_kind = K_BWD;
+      C->exp_layer = C->L;
+      break;
+    case K_BWD:
+      if (C->exp_layer > 1) --C->exp_layer;
+      else C->exp_kind = K_UPD;
+      break;
+    default:
+      C->exp_kind = K_FWD;
+      C->exp_layer = 1;
+      ++C->exp_t;
+  }
+}
+
+inline float* layer_in(PartCtx& p, int l, int b) { return l == 1 ? p.X : p.H[l - 1][b]; }
+
+// Brackets one launch with CUDA events (only when timing is enabled) and charges it with its
+// algorithmic bytes / flops.
+struct Scope {
+  pgcn_ctx* C;
+  int k;
+  Scope(pgcn_ctx* c, int kind, double bytes, double flops = 0.0) : C(c), k(kind) {
+    if (!C->timing) return;
+    KTimer& t = C->kt[k];
+    if (t.used + 2 > t.ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      t.ev.push_back(a);
+      t.ev.push_back(b);
+    }
+    cudaEventRecord(t.ev[t.used], C->s);
+    t.n += 1;
+    t.bytes += bytes;
+    t.flops += flops;
+  }
+  ~Scope() {
+    if (!C->timing) return;
+    KTimer& t = C->kt[k];
+    cudaEventRecord(t.ev[t.used + 1], C->s);
+    t.used += 2;
+  }
+};
+
+}  // namespace
+}  // namespace pgcn
+
+using namespace pgcn;
+
+extern "C" int64_t pgcn_param_count(const pgcn_config* cfg) { return cfg ? param_count(cfg) : -1; }
+
+extern "C" int pgcn_workspace_bytes(const pgcn_partitioning* part, const int32_t* local, int32_t n_local,
+                                    const pgcn_config* cfg, size_t* bytes) {
+  if (!bytes) return fail(PGCN_EINVAL, "bytes is NULL");
+  pgcn_ctx C;
+  int rc = init_ctx_shapes(&C, part, local, n_local, cfg);
+  if (rc) return rc;
+  Arena A;
+  rc = layout(&C, part, local, n_local, A);
+  if (rc) return rc;
+  *bytes = A.off + 256;
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* local, int32_t n_local,
+                               const pgcn_config* cfg, const pgcn_comm* comm, void* ws, size_t ws_bytes,
+                               void* stream, pgcn_ctx** out) {
+  if (!out) return fail(PGCN_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (comm && comm->nranks > 1) return fail(PGCN_EUNSUPPORTED, "NCCL transport not built in this library");
+  pgcn_ctx* C = new (std::nothrow) pgcn_ctx();
+  if (!C) return fail(PGCN_ENOMEM, "host allocation failed");
+  int rc = init_ctx_shapes(C, part, local, n_local, cfg);
+  if (rc) { delete C; return rc; }
+  Arena dry;
+  rc = layout(C, part, local, n_local, dry);
+  if (rc) { delete C; return rc; }
+  if (!ws || ((uintptr_t)ws & 255)) { delete C; return fail(PGCN_EINVAL, "workspace NULL or not 256-byte aligned"); }
+  if (ws_bytes < dry.off) {
+    delete C;
+    return fail(PGCN_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, dry.off);
+  }
+  Arena A;
+  A.base = static_cast<char*>(ws);
+  layout(C, part, local, n_local, A);
+  C->s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = C->s;
+  cudaMemsetAsync(ws, 0, A.off, s);
+  // uploads (host arrays are borrowed; synchronise before returning)
+  for (int i = 0; i < n_local; ++i) {
+    PartCtx& p = C->parts[i];
+    const pgcn_part_view& v = p.v;
+    std::vector<int64_t> gid(p.n_all);
+    std::memcpy(gid.data(), v.inner_gid, sizeof(int64_t) * p.n_in);
+    std::memcpy(gid.data() + p.n_in, v.halo_gid, sizeof(int64_t) * p.n_bd);
+    // halo_map: boundary row r (owner j) -> owner's local inner id (position in V_j, ascending gid)
+    std::vector<int32_t> hmap(p.n_bd), mmap(p.n_send);
+    for (int j = 0; j < C->n_parts; ++j) {
+      pgcn_part_view vj;
+      pgcn_partition_view(part, j, &vj);
+      for (int64_t r = v.halo_off[j]; r < v.halo_off[j + 1]; ++r) {
+        const int64_t g = v.halo_gid[r];
+        const int64_t* it = std::lower_bound(vj.inner_gid, vj.inner_gid + vj.n_inner, g);
+        hmap[r] = (int32_t)(it - vj.inner_gid);
+      }
+      // msg_map: my send position k for peer j -> row of peer j's J buffer (its boundary row)
+      for (int64_t k = v.send_off[j]; k < v.send_off[j + 1]; ++k)
+        mmap[k] = (int32_t)(vj.n_inner + vj.halo_off[p.part] + (k - v.send_off[j]));
+    }
+    cudaMemcpyAsync(p.rp, v.row_ptr, sizeof(int64_t) * (p.n_in + 1), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.col, v.col_idx, sizeof(int32_t) * p.nnz, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.inv_deg, v.inv_deg, sizeof(float) * p.n_in, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.trp, v.t_row_ptr, sizeof(int64_t) * (p.n_all + 1), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.tcol, v.t_col_idx, sizeof(int32_t) * p.nnz, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.gid, gid.data(), sizeof(int64_t) * p.n_all, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.send_idx, v.send_idx, sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.inv_ptr, v.inv_ptr, sizeof(int64_t) * (p.n_in + 1), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.inv_pos, v.inv_pos, sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.halo_map, hmap.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(p.msg_map, mmap.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      delete C;
+      return fail(PGCN_ECUDA, "pgcn_ctx_create upload: %s", cudaGetErrorString(e));
+    }
+  }
+  rc = check_cuda(C, "pgcn_ctx_create");
+  if (rc) { delete C; return rc; }
+  *out = C;
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_ctx_destroy(pgcn_ctx* C) {
+  if (!C) return PGCN_OK;
+  if (C->s) cudaStreamSynchronize(C->s);
+  delete C;
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const void* labels,
+                               const uint8_t* train_mask) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  if (C->poisoned) return fail(PGCN_ESTATE, "context poisoned");
+  if (local < 0 || local >= (int)C->parts.size()) return fail(PGCN_EINVAL, "local index out of range");
+  PartCtx& p = C->parts[local];
+  if (p.n_in > 0 && (!X || !labels || !train_mask)) return fail(PGCN_EINVAL, "null input");
+  if (p.n_in > 0) {
+    cudaMemcpy2DAsync(p.X, sizeof(float) * C->ld[0], X, sizeof(float) * C->F[0], sizeof(float) * C->F[0], p.n_in,
+                      cudaMemcpyDefault, C->s);
+    const size_t lb = C->cfg.loss == 0 ? sizeof(int32_t) * p.n_in : (size_t)p.n_in * C->F[C->L];
+    cudaMemcpyAsync(p.labels, labels, lb, cudaMemcpyDefault, C->s);
+    cudaMemcpyAsync(p.train, train_mask, (size_t)p.n_in, cudaMemcpyDefault, C->s);
+  }
+  return check_cuda(C, "pgcn_set_inputs");
+}
+
+extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* params) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_FWD, l, "pgcn_layer_fwd");
+  if (rc) return rc;
+  if (!params) return fail(PGCN_EINVAL, "params is NULL");
+  const Launch Lk{C->s, &C->launches};
+  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const bool pipe = C->cfg.mode == 1;
+  const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
+  const float* Wext = params + C->woff[l];
+  for (auto& p : C->parts) {
+    float* Hin = layer_in(p, l, b);
+    // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13; local transport = device gather)
+    if (C->n_parts > 1 && p.n_bd > 0) {
+      bool do_install = false, ema = false, first = false;
+      const float* prev = nullptr;
+      SegTable src{};
+      src.n_seg = C->n_parts;
+      for (int j = 0; j <= C->n_parts; ++j) src.off[j] = p.v.halo_off[j];
+      if (l == 1) {
+        // X is constant: one exchange at t = 1, consumed at t = 1 (VANILLA) or t = 2 (PIPE) (R10)
+        do_install = pipe ? t == 2 : t == 1;
+        for (int j = 0; j < C->n_parts; ++j) src.base[j] = C->parts[j].X;
+      } else {
+        const int sb = pipe ? bp : b;
+        do_install = pipe ? t >= 2 : true;
+        for (int j = 0; j < C->n_parts; ++j) src.base[j] = C->parts[j].H[l - 1][sb];
+        if (pipe && C->cfg.smooth_f) {
+          ema = true;
+          first = C->cfg.ema_init == 0 && t == 2;
+          prev = p.H[l - 1][bp] + p.n_in * ldi;
+        }
+      }
+      if (do_install) {
+        const double F = (double)C->F[l - 1];
+        Scope sc(C, PGCN_K_GATHER, (8.0 + (ema ? 4.0 : 0.0)) * F * p.n_bd + 4.0 * p.n_bd);
+        gather_rows(Lk, src, p.halo_map, p.n_bd, ldi, Hin + p.n_in * ldi, prev, (float)C->cfg.gamma, ema, first);
+      }
+    }
+    // S3: dropout after the exchange (App. F), aggregation
+    const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
+    const float* D = Hin;
+    if (C->cfg.dropout > 0.0) {
+      Scope sc(C, PGCN_K_DROPOUT, 8.0 * Fi * p.n_all + 8.0 * p.n_all);
+      dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, p.n_all, p.gid, drop_spec(C, t, l));
+      D = p.D[l];
+    }
+    {
+      Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, p.n_all, p.Z[l]);
+    }
+    // S4: Y = [Z | D] W + b, ReLU on hidden layers
+    float* out = l < C->L ? p.H[l][b] : p.logits;
+    {
+      Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * (2 * Fi + 1) * Fo,
+               2.0 * p.n_in * (2 * Fi + 1) * Fo);
+      gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
+    }
+  }
+  rc = check_cuda(C, "pgcn_layer_fwd");
+  if (rc) return rc;
+  advance(C);
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_LOSS, 0, "pgcn_loss");
+  if (rc) return rc;
+  const Launch Lk{C->s, &C->launches};
+  const int L = C->L;
+  for (size_t i = 0; i < C->parts.size(); ++i) {
+    PartCtx& p = C->parts[i];
+    Scope sc(C, PGCN_K_LOSS, 8.0 * p.n_in * C->F[L] + 5.0 * p.n_in);
+    loss_rows(Lk, C->cfg.loss, p.logits, p.n_in, C->F[L], C->ld[L], p.labels, p.train,
+              (double)C->cfg.n_train_global, p.M, p.row_loss);
+    reduce_sum(Lk, p.row_loss, p.n_in, C->part_loss + i);
+  }
+  if (loss_dev) reduce_sum(Lk, C->part_loss, (int64_t)C->parts.size(), loss_dev);
+  rc = check_cuda(C, "pgcn_loss");
+  if (rc) return rc;
+  advance(C);
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* params) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_BWD, l, "pgcn_layer_bwd");
+  if (rc) return rc;
+  if (!params) return fail(PGCN_EINVAL, "params is NULL");
+  const Launch Lk{C->s, &C->launches};
+  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const bool pipe = C->cfg.mode == 1;
+  const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
+  const float* Wext = params + C->woff[l];
+  // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
+  for (auto& p : C->parts) {
+    const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
+    const float* D = C->cfg.dropout > 0.0 ? p.D[l] : layer_in(p, l, b);
+    {
+      Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (2 * Fi + Fo), 2.0 * p.n_in * (2 * Fi + 1) * Fo);
+      gemm_dw_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
+                  C->dw_ws_floats);
+    }
+    if (l >= 2) {
+      {
+        Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * 2 * Fi);
+        gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
+      }
+      Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
+                                       4.0 * Fi * p.n_all + 8.0 * p.n_all);
+      spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
+               drop_spec(C, t, l));
+    }
+  }
+  // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)
+  if (l >= 2) {
+    for (auto& p : C->parts) {
+      SegTable msg{};
+      msg.n_seg = 0;
+      bool use_ema = false, first = false;
+      const bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t >= 2);
+      if (have) {
+        msg.n_seg = C->n_parts;
+        const int sb = pipe ? bp : b;
+        for (int j = 0; j <= C->n_parts; ++j) msg.off[j] = p.v.send_off[j];
+        for (int j = 0; j < C->n_parts; ++j) msg.base[j] = C->parts[j].J[l - 1][sb];
+        if (pipe && C->cfg.smooth_g) {
+          use_ema = true;
+          first = C->cfg.ema_init == 0 && t == 2;
+        }
+      }
+      const double Fi = (double)C->F[l - 1];
+      Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j) + 8.0 * p.n_in +
+                                          (msg.n_seg ? (4.0 * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
+      grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, p.msg_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
+                  p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi);
+    }
+  }
+  rc = check_cuda(C, "pgcn_layer_bwd");
+  if (rc) return rc;
+  advance(C);
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_update(pgcn_ctx* C, int64_t t, float* params, float* grads, float* opt_state) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_UPD, 0, "pgcn_update");
+  if (rc) return rc;
+  if (!params || !grads) return fail(PGCN_EINVAL, "params / grads is NULL");
+  if (C->cfg.opt == 1 && !opt_state) return fail(PGCN_EINVAL, "Adam needs opt_state");
+  const Launch Lk{C->s, &C->launches};
+  PtrList G{};
+  G.n = (int32_t)C->parts.size();
+  for (int i = 0; i < G.n; ++i) G.p[i] = C->parts[i].G;
+  Scope sc(C, PGCN_K_UPDATE, 4.0 * C->P * (G.n + 2 + (C->cfg.opt == 1 ? 4 : 1)));
+  sum_grads(Lk, G, C->P, grads);
+  OptSpec o{};
+  o.adam = C->cfg.opt == 1;
+  o.lr = (float)C->cfg.lr;
+  o.beta1 = (float)C->cfg.beta1;
+  o.beta2 = (float)C->cfg.beta2;
+  o.eps = (float)C->cfg.eps;
+  o.step_size = (float)(C->cfg.lr / (1.0 - std::pow(C->cfg.beta1, (double)t)));
+  o.inv_sqrt_bc2 = (float)(1.0 / std::sqrt(1.0 - std::pow(C->cfg.beta2, (double)t)));
+  o.apply = 1;
+  opt_update(Lk, grads, C->P, params, opt_state, opt_state ? opt_state + C->P : nullptr, o);
+  rc = check_cuda(C, "pgcn_update");
+  if (rc) return rc;
+  advance(C);
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_step(pgcn_ctx* C, int64_t t, float* params, float* grads, float* opt_state, float* loss_dev) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc;
+  for (int l = 1; l <= C->L; ++l)
+    if ((rc = pgcn_layer_fwd(C, t, l, params))) return rc;
+  if ((rc = pgcn_loss(C, t, loss_dev))) return rc;
+  for (int l = C->L; l >= 1; --l)
+    if ((rc = pgcn_layer_bwd(C, t, l, params))) return rc;
+  return pgcn_update(C, t, params, grads, opt_state);
+}
+
+extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, int64_t t, pgcn_tensor_desc* o) {
+  if (!C || !o) return fail(PGCN_EINVAL, "null argument");
+  if (local < 0 || local >= (int)C->parts.size()) return fail(PGCN_EINVAL, "local index out of range");
+  PartCtx& p = C->parts[local];
+  const int b = (int)(t & 1);
+  const bool lok = l >= 1 && l <= C->L;
+  switch (kind) {
+    case PGCN_T_H:
+      if (!lok) break;
+      *o = {l < C->L ? (void*)p.H[l][b] : (void*)p.logits, p.n_in, C->F[l], C->ld[l]};
+      return PGCN_OK;
+    case PGCN_T_HIN:
+      if (!lok) break;
+      *o = {(void*)layer_in(p, l, b), p.n_all, C->F[l - 1], C->ld[l - 1]};
+      return PGCN_OK;
+    case PGCN_T_Z:
+      if (!lok) break;
+      *o = {(void*)p.Z[l], p.n_in, C->F[l - 1], C->ld[l - 1]};
+      return PGCN_OK;
+    case PGCN_T_J:
+      if (l < 1 || l >= C->L) break;
+      *o = {(void*)p.J[l][b], p.n_in, C->F[l], C->ld[l]};
+      return PGCN_OK;
+    case PGCN_T_G:
+      *o = {(void*)p.G, 1, C->P, C->P};
+      return PGCN_OK;
+    default:
+      break;
+  }
+  return fail(PGCN_EINVAL, "pgcn_tensor: bad kind / layer");
+}
+
+extern "C" int64_t pgcn_launch_count(const pgcn_ctx* C) { return C ? C->launches : -1; }
+
+extern "C" int pgcn_timing_enable(pgcn_ctx* C, int32_t on) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  if (C->s) cudaStreamSynchronize(C->s);
+  C->timing = on ? 1 : 0;
+  for (auto& k : C->kt) {
+    k.used = 0;
+    k.n = 0;
+    k.bytes = k.flops = 0.0;
+  }
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_timing_read(pgcn_ctx* C, int32_t kind, double* ms, int64_t* launches, double* bytes,
+                                double* flops) {
+  if (!C || kind < 0 || kind >= PGCN_K_COUNT) return fail(PGCN_EINVAL, "bad argument");
+  KTimer& k = C->kt[kind];
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < k.used; i += 2) {
+    cudaError_t e = cudaEventSynchronize(k.ev[i + 1]);
+    if (e != cudaSuccess) return fail(PGCN_ECUDA, "pgcn_timing_read: %s", cudaGetErrorString(e));
+    float x = 0.f;
+    cudaEventElapsedTime(&x, k.ev[i], k.ev[i + 1]);
+    tot += x;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = k.n;
+  if (bytes) *bytes = k.bytes;
+  if (flops) *flops = k.flops;
+  return PGCN_OK;
+}

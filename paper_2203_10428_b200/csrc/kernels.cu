@@ -1,0 +1,730 @@
+// sm_100a kernels of the PipeGCN hot path: aggregation SpMM (S3), transposed SpMM (S8),
+// dropout (R5), boundary gather / EMA install (S1, S2, Sec. 3.4), stale-gradient accumulation
+// (S9), loss (S5), SIMT fp32 GEMMs (S4, S6, S7; parity path) and the optimiser (S11, S12).
+// Step numbers refer to SURVEY.md section 8(a); paper citations are in kernels.cuh / pgcn.h.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace pgcn {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSMs = 148;
+
+inline int grid_for(int64_t work, int per_block, int max_blocks = kSMs * 16) {
+  int64_t b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 output for state z
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ bool keep_el(const DropSpec& d, int64_t gid, int64_t c) {
+  uint64_t key = ((uint64_t)d.key_base + (uint64_t)gid) * (uint64_t)d.width + (uint64_t)c;
+  return (uint32_t)(smix(key ^ d.seed) >> 40) >= d.thr;
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4scale(float4 a, float s) {
+  return make_float4(a.x * s, a.y * s, a.z * s, a.w * s);
+}
+__device__ __forceinline__ float comp(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set_comp(float4& v, int j, float x) {
+  if (j == 0) v.x = x; else if (j == 1) v.y = x; else if (j == 2) v.z = x; else v.w = x;
+}
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  if (G == 32) return 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
+  return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+}
+
+__device__ __forceinline__ int find_seg(const SegTable& t, int64_t r) {
+  int lo = 0, hi = t.n_seg - 1;  // largest s with off[s] <= r
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (t.off[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------- dropout (S3 prologue, R5)
+__global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, int64_t ld4, int64_t n_rows,
+                          int64_t n_valid, const int64_t* __restrict__ gid, DropSpec d) {
+  const int64_t total = n_rows * ld4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld4, x = i - r * ld4;
+    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < n_valid) {
+      const float4 h = H[i];
+      const int64_t g = gid[r];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = 4 * x + j;
+        float v = 0.f;
+        if (c < d.width && keep_el(d, g, c)) v = comp(h, j) * d.scale;
+        set_comp(out, j, v);
+      }
+    }
+    D[i] = out;
+  }
+}
+
+// ---------------------------------------------------------------- SpMM forward (S3)
+// One group of G lanes per row; lane handles float4 columns lane + q*G (q < NC).  Neighbour
+// ids are loaded G at a time (coalesced) and broadcast with shuffles; U neighbour rows are in
+// flight per step.  Sums run in CSR order, then the row is scaled by inv_deg (reading R16).
+template <int G, int NC, int U>
+__global__ void __launch_bounds__(kThreads) k_spmm_fwd(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                       const float* __restrict__ inv_deg, const float4* __restrict__ D,
+                                                       int64_t ld4, int64_t n_rows, int64_t n_valid, float4* __restrict__ Z) {
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; row < n_rows; row += stride) {
+    float4 acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t beg = rp[row], end = rp[row + 1];
+    for (int64_t e0 = beg; e0 < end; e0 += G) {
+      const int cnt = (int)((end - e0) < G ? (end - e0) : G);
+      const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        float4 v[U][NC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = __shfl_sync(gm, my, j + u, G);
+          const bool ok = c < n_valid;
+          const float4* src = D + (int64_t)c * ld4;
+#pragma unroll
+          for (int q = 0; q < NC; ++q) {
+            const int64_t x = lane + q * G;
+            v[u][q] = (ok && x < ld4) ? __ldg(src + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+      }
+      for (; j < cnt; ++j) {
+        const int c = __shfl_sync(gm, my, j, G);
+        if (c < n_valid) {
+          const float4* src = D + (int64_t)c * ld4;
+#pragma unroll
+          for (int q = 0; q < NC; ++q) {
+            const int64_t x = lane + q * G;
+            if (x < ld4) acc[q] = f4add(acc[q], __ldg(src + x));
+          }
+        }
+      }
+    }
+    const float s = inv_deg[row];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = lane + q * G;
+      if (x < ld4) Z[row * ld4 + x] = f4scale(acc[q], s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- transposed SpMM (S8)
+template <int G, int NC, int U>
+__global__ void __launch_bounds__(kThreads) k_spmm_bwd(const int64_t* __restrict__ trp, const int32_t* __restrict__ tcol,
+                                                       const float4* __restrict__ dZs, const float4* __restrict__ dDs,
+                                                       int64_t ldA4, int64_t n_in, int64_t n_all, float4* __restrict__ J,
+                                                       int64_t ld4, const int64_t* __restrict__ gid, DropSpec d) {
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t u0 = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; u0 < n_all; u0 += stride) {
+    float4 acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = lane + q * G;
+      acc[q] = (u0 < n_in && x < ld4) ? dDs[u0 * ldA4 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int64_t beg = trp[u0], end = trp[u0 + 1];
+    for (int64_t e0 = beg; e0 < end; e0 += G) {
+      const int cnt = (int)((end - e0) < G ? (end - e0) : G);
+      const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        float4 v[U][NC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = __shfl_sync(gm, my, j + u, G);
+          const float4* src = dZs + (int64_t)c * ldA4;
+#pragma unroll
+          for (int q = 0; q < NC; ++q) {
+            const int64_t x = lane + q * G;
+            v[u][q] = x < ld4 ? __ldg(src + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+      }
+      for (; j < cnt; ++j) {
+        const int c = __shfl_sync(gm, my, j, G);
+        const float4* src = dZs + (int64_t)c * ldA4;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          const int64_t x = lane + q * G;
+          if (x < ld4) acc[q] = f4add(acc[q], __ldg(src + x));
+        }
+      }
+    }
+    const int64_t g = gid[u0];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = lane + q * G;
+      if (x >= ld4) continue;
+      float4 o = acc[q];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = 4 * x + j;
+        float val = comp(o, j);
+        if (c >= d.width) val = 0.f;
+        else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
+        set_comp(o, j, val);
+      }
+      J[u0 * ld4 + x] = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- gather rows / EMA install (S1, S2)
+__global__ void k_gather(const __grid_constant__ SegTable t, const int32_t* __restrict__ row_map, int64_t n_rows,
+                         int64_t ld4, float4* __restrict__ dst, const float4* __restrict__ prev, float gamma, int ema,
+                         int first) {
+  const int64_t total = n_rows * ld4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld4, x = i - r * ld4;
+    const int s = find_seg(t, r);
+    const int64_t srow = row_map ? (int64_t)row_map[r] : r - t.off[s];
+    float4 v = __ldg(reinterpret_cast<const float4*>(t.base[s]) + srow * ld4 + x);
+    if (ema && !first) {
+      const float4 p = prev[i];
+      const float a = gamma, b = 1.0f - gamma;
+      v = make_float4(a * p.x + b * v.x, a * p.y + b * v.y, a * p.z + b * v.z, a * p.w + b * v.w);
+    }
+    dst[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------- stale gradient accumulate + M (S9)
+__global__ void k_grad_reduce(const int64_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv_pos,
+                              const __grid_constant__ SegTable msg, const int32_t* __restrict__ row_map,
+                              float4* __restrict__ ema, float gamma, int use_ema, int first, float4* __restrict__ J,
+                              int write_j, const float4* __restrict__ Hprev, float4* __restrict__ M, int64_t n_in,
+                              int64_t ld4) {
+  const int64_t total = n_in * ld4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / ld4, x = i - v * ld4;
+    float4 acc = J[i];
+    if (msg.n_seg > 0) {
+      const int64_t kb = inv_ptr[v], ke = inv_ptr[v + 1];
+      for (int64_t q = kb; q < ke; ++q) {
+        const int64_t k = inv_pos[q];
+        const int s = find_seg(msg, k);
+        const int64_t srow = row_map ? (int64_t)row_map[k] : k - msg.off[s];
+        float4 c = __ldg(reinterpret_cast<const float4*>(msg.base[s]) + srow * ld4 + x);
+        if (use_ema) {
+          if (!first) {
+            const float4 e = ema[k * ld4 + x];
+            const float a = gamma, b = 1.0f - gamma;
+            c = make_float4(a * e.x + b * c.x, a * e.y + b * c.y, a * e.z + b * c.z, a * e.w + b * c.w);
+          }
+          ema[k * ld4 + x] = c;
+        }
+        acc = f4add(acc, c);
+      }
+    }
+    if (write_j) J[i] = acc;
+    const float4 h = Hprev[v * ld4 + x];
+    M[i] = make_float4(h.x > 0.f ? acc.x : 0.f, h.y > 0.f ? acc.y : 0.f, h.z > 0.f ? acc.z : 0.f,
+                       h.w > 0.f ? acc.w : 0.f);
+  }
+}
+
+// ---------------------------------------------------------------- loss (S5)
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void k_loss_ce(const float* __restrict__ Y, int64_t n, int64_t C, int64_t ld, const int32_t* __restrict__ lab,
+                          const uint8_t* __restrict__ train, float inv_nt, float* __restrict__ M, float* __restrict__ rl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
+    const float* y = Y + v * ld;
+    float* m = M + v * ld;
+    if (!train[v]) {
+      for (int64_t c = lane; c < ld; c += 32) m[c] = 0.f;
+      if (lane == 0) rl[v] = 0.f;
+      continue;
+    }
+    float mx = -INFINITY;
+    for (int64_t c = lane; c < C; c += 32) mx = fmaxf(mx, y[c]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int64_t c = lane; c < C; c += 32) s += expf(y[c] - mx);
+    s = warp_sum(s);
+    const int32_t t = lab[v];
+    const float ls = logf(s);
+    for (int64_t c = lane; c < ld; c += 32) {
+      float g = 0.f;
+      if (c < C) g = (expf(y[c] - mx) / s - (c == t ? 1.f : 0.f)) * inv_nt;
+      m[c] = g;
+    }
+    if (lane == 0) rl[v] = (ls + mx - y[t]) * inv_nt;
+  }
+}
+
+__global__ void k_loss_bce(const float* __restrict__ Y, int64_t n, int64_t C, int64_t ld, const uint8_t* __restrict__ lab,
+                           const uint8_t* __restrict__ train, float inv_ntc, float* __restrict__ M, float* __restrict__ rl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
+    const float* y = Y + v * ld;
+    float* m = M + v * ld;
+    const bool tr = train[v] != 0;
+    float l = 0.f;
+    for (int64_t c = lane; c < ld; c += 32) {
+      float g = 0.f;
+      if (tr && c < C) {
+        const float yc = y[c], lb = (float)lab[v * C + c];
+        g = (1.f / (1.f + expf(-yc)) - lb) * inv_ntc;
+        l += fmaxf(yc, 0.f) + log1pf(expf(-fabsf(yc))) - lb * yc;
+      }
+      m[c] = g;
+    }
+    l = warp_sum(l);
+    if (lane == 0) rl[v] = l * inv_ntc;
+  }
+}
+
+__global__ void k_reduce_sum(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+  __shared__ double sh[1024];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += (double)x[i];
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = (float)sh[0];
+}
+
+// ---------------------------------------------------------------- SIMT fp32 GEMMs (parity path)
+constexpr int BM = 64, BN = 64, BK = 16;
+
+// A_ext(m, k) = [Z | D | 1](m, k), K = 2F + 1
+__device__ __forceinline__ float a_ext(const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, int64_t m,
+                                       int64_t k) {
+  if (m >= M) return 0.f;
+  if (k < F) return __ldg(Z + m * ldA + k);
+  if (k < 2 * F) return __ldg(D + m * ldA + (k - F));
+  return k == 2 * F ? 1.f : 0.f;
+}
+
+template <int RELU>
+__global__ void __launch_bounds__(256) k_gemm_fwd(const float* __restrict__ Z, const float* __restrict__ D, int64_t ldA,
+                                                  int64_t M, int64_t F, const float* __restrict__ W, int64_t N,
+                                                  float* __restrict__ Y, int64_t ldY) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t K = 2 * F + 1;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = ty + 16 * i;
+      As[tx][r] = a_ext(Z, D, ldA, M, F, m0 + r, k0 + tx);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = ty, nn = tx + 16 * i;
+      const int64_t k = k0 + kk, n = n0 + nn;
+      Bs[kk][nn] = (k < K && n < N) ? __ldg(W + k * N + n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      if (n < N) Y[m * ldY + n] = RELU ? fmaxf(acc[i][j], 0.f) : acc[i][j];
+      else if (n < ldY) Y[m * ldY + n] = 0.f;
+    }
+  }
+}
+
+// partial[s][k][n] = sum_{m in chunk s} A_ext(m, k) Mg(m, n)
+__global__ void __launch_bounds__(256) k_gemm_dw(const float* __restrict__ Z, const float* __restrict__ D, int64_t ldA,
+                                                 int64_t M, int64_t F, const float* __restrict__ Mg, int64_t ldM, int64_t N,
+                                                 int64_t rows_per_split, float* __restrict__ part) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t k0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t K = 2 * F + 1;
+  const int64_t r_beg = (int64_t)blockIdx.z * rows_per_split;
+  const int64_t r_end = r_beg + rows_per_split < M ? r_beg + rows_per_split : M;
+  float acc[4][4] = {};
+  for (int64_t r0 = r_beg; r0 < r_end; r0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // As[r][k]: 16 rows x 64 k
+      const int kk = tx + 16 * i, rr = ty;
+      const int64_t r = r0 + rr;
+      As[rr][kk] = (r < r_end && k0 + kk < K) ? a_ext(Z, D, ldA, M, F, r, k0 + kk) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int nn = tx + 16 * i, rr = ty;
+      const int64_t r = r0 + rr, n = n0 + nn;
+      Bs[rr][nn] = (r < r_end && n < N) ? __ldg(Mg + r * ldM + n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < BK; ++rr) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[rr][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[rr][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* out = part + (int64_t)blockIdx.z * K * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t k = k0 + ty * 4 + i;
+    if (k >= K) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      if (n < N) out[k * N + n] = acc[i][j];
+    }
+  }
+}
+
+__global__ void k_split_reduce(const float* __restrict__ part, int64_t splits, int64_t len, float* __restrict__ G) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int64_t s = 0; s < splits; ++s) a += part[s * len + i];
+    G[i] = a;
+  }
+}
+
+// dA(m, oc), oc in [0, 2 ld): half h = oc / ld, c = oc % ld; value = sum_j Mg(m, j) W(hF + c, j)
+__global__ void __launch_bounds__(256) k_gemm_da(const float* __restrict__ Mg, int64_t ldM, int64_t M, int64_t N,
+                                                 const float* __restrict__ W, int64_t F, const float* __restrict__ inv_deg,
+                                                 float* __restrict__ dA, int64_t ld) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, o0 = (int64_t)blockIdx.y * BN;
+  float acc[4][4] = {};
+  for (int64_t j0 = 0; j0 < N; j0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = ty + 16 * i;
+      const int64_t m = m0 + r, j = j0 + tx;
+      As[tx][r] = (m < M && j < N) ? __ldg(Mg + m * ldM + j) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int oo = ty + 16 * i;   // output column within tile
+      const int64_t oc = o0 + oo, j = j0 + tx;
+      float w = 0.f;
+      if (oc < 2 * ld && j < N) {
+        const int64_t h = oc / ld, c = oc - h * ld;
+        if (c < F) w = __ldg(W + (h * F + c) * N + j);
+      }
+      Bs[tx][oo] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+    const float s = inv_deg[m];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t oc = o0 + tx * 4 + j;
+      if (oc >= 2 * ld) continue;
+      const int64_t h = oc / ld, c = oc - h * ld;
+      float v = c < F ? acc[i][j] : 0.f;
+      if (h == 0) v *= s;
+      dA[m * 2 * ld + oc] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- optimiser (S11, S12)
+__global__ void k_sum_grads(const __grid_constant__ PtrList G, int64_t P, float* __restrict__ grads) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    float a = G.p[0][i];
+    for (int k = 1; k < G.n; ++k) a += G.p[k][i];
+    grads[i] = a;
+  }
+}
+
+__global__ void k_opt(const float* __restrict__ grads, int64_t P, float* __restrict__ w, float* __restrict__ m,
+                      float* __restrict__ v, OptSpec o) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const float g = grads[i];
+    if (!o.adam) {
+      w[i] = w[i] - o.lr * g;
+    } else {
+      const float mi = o.beta1 * m[i] + (1.f - o.beta1) * g;
+      const float vi = o.beta2 * v[i] + (1.f - o.beta2) * g * g;
+      m[i] = mi;
+      v[i] = vi;
+      w[i] = w[i] - o.step_size * mi / (sqrtf(vi) * o.inv_sqrt_bc2 + o.eps);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- SpMM dispatch
+struct Shape {
+  int G, NC;
+};
+Shape pick_shape(int64_t ld4) {
+  static const int Gs[] = {32, 16, 8, 4, 2};
+  static const int NCs[] = {1, 2, 3, 4, 5, 6, 8, 12, 16};
+  Shape best{32, 16};
+  int64_t best_waste = INT64_MAX;
+  for (int G : Gs) {
+    int64_t need = (ld4 + G - 1) / G;
+    int NC = -1;
+    for (int c : NCs)
+      if (c >= need) { NC = c; break; }
+    if (NC < 0) continue;
+    int64_t waste = (int64_t)G * NC - ld4;
+    if (waste < best_waste) { best_waste = waste; best = {G, NC}; }
+  }
+  return best;
+}
+
+template <int G, int NC>
+constexpr int unroll_for() { return NC <= 1 ? 8 : NC <= 2 ? 4 : NC <= 4 ? 2 : 1; }
+
+#define PGCN_NC_LIST(X, G) X(G, 1) X(G, 2) X(G, 3) X(G, 4) X(G, 5) X(G, 6) X(G, 8) X(G, 12) X(G, 16)
+#define PGCN_G_LIST(X) PGCN_NC_LIST(X, 32) PGCN_NC_LIST(X, 16) PGCN_NC_LIST(X, 8) PGCN_NC_LIST(X, 4) PGCN_NC_LIST(X, 2)
+
+}  // namespace
+
+static void count(const Launch& L, int64_t n = 1) {
+  if (L.count) *L.count += n;
+}
+
+void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows, int64_t n_valid,
+                 const int64_t* gid, const DropSpec& d) {
+  const int64_t ld4 = ld / 4;
+  if (n_rows <= 0) return;
+  k_dropout<<<grid_for(n_rows * ld4, kThreads), kThreads, 0, L.s>>>(
+      reinterpret_cast<const float4*>(H), reinterpret_cast<float4*>(D), ld4, n_rows, n_valid, gid, d);
+  count(L);
+}
+
+void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
+              int64_t n_rows, int64_t n_valid, float* Z) {
+  if (n_rows <= 0) return;
+  const int64_t ld4 = ld / 4;
+  const Shape sh = pick_shape(ld4);
+  const int rows_per_block = kThreads / sh.G;
+  const int grid = grid_for(n_rows, rows_per_block, kSMs * 64);
+  auto D4 = reinterpret_cast<const float4*>(D);
+  auto Z4 = reinterpret_cast<float4*>(Z);
+#define X(G_, NC_)                                                                                              \
+  if (sh.G == G_ && sh.NC == NC_) {                                                                            \
+    k_spmm_fwd<G_, NC_, unroll_for<G_, NC_>()><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, \
+                                                                           n_valid, Z4);                         \
+  } else
+  PGCN_G_LIST(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape\n"); }
+#undef X
+  count(L);
+}
+
+void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
+              int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
+              const DropSpec& d) {
+  if (n_all <= 0) return;
+  const int64_t ld4 = ld / 4;
+  const Shape sh = pick_shape(ld4);
+  const int rows_per_block = kThreads / sh.G;
+  const int grid = grid_for(n_all, rows_per_block, kSMs * 64);
+  auto a = reinterpret_cast<const float4*>(dZs);
+  auto b = reinterpret_cast<const float4*>(dDs);
+  auto J4 = reinterpret_cast<float4*>(J);
+#define X(G_, NC_)                                                                                             \
+  if (sh.G == G_ && sh.NC == NC_) {                                                                           \
+    k_spmm_bwd<G_, NC_, unroll_for<G_, NC_>()><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, ld_dA / 4,  \
+                                                                           n_in, n_all, J4, ld4, gid, d);       \
+  } else
+  PGCN_G_LIST(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape\n"); }
+#undef X
+  count(L);
+}
+
+void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld, float* dst,
+                 const float* prev, float gamma, int ema, int first) {
+  if (n_rows <= 0) return;
+  const int64_t ld4 = ld / 4;
+  k_gather<<<grid_for(n_rows * ld4, kThreads), kThreads, 0, L.s>>>(src, row_map, n_rows, ld4,
+                                                                   reinterpret_cast<float4*>(dst),
+                                                                   reinterpret_cast<const float4*>(prev), gamma, ema,
+                                                                   first);
+  count(L);
+}
+
+void grad_reduce(Launch L, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg, const int32_t* row_map,
+                 float* ema, float gamma, int use_ema, int first, float* J, int write_j, const float* Hprev, float* M,
+                 int64_t n_in, int64_t ld) {
+  if (n_in <= 0) return;
+  const int64_t ld4 = ld / 4;
+  k_grad_reduce<<<grid_for(n_in * ld4, kThreads), kThreads, 0, L.s>>>(
+      inv_ptr, inv_pos, msg, row_map, reinterpret_cast<float4*>(ema), gamma, use_ema, first,
+      reinterpret_cast<float4*>(J), write_j, reinterpret_cast<const float4*>(Hprev), reinterpret_cast<float4*>(M), n_in,
+      ld4);
+  count(L);
+}
+
+void loss_rows(Launch L, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
+               const uint8_t* train, double n_train, float* M, float* row_loss) {
+  if (n <= 0) return;
+  const int grid = grid_for(n, kThreads / 32, kSMs * 32);
+  if (kind == 0)
+    k_loss_ce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const int32_t*>(labels), train,
+                                          (float)(1.0 / n_train), M, row_loss);
+  else
+    k_loss_bce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const uint8_t*>(labels), train,
+                                           (float)(1.0 / (n_train * (double)C)), M, row_loss);
+  count(L);
+}
+
+void reduce_sum(Launch L, const float* x, int64_t n, float* out) {
+  k_reduce_sum<<<1, 1024, 0, L.s>>>(x, n, out);
+  count(L);
+}
+
+void gemm_fwd_f32(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Wext,
+                  int64_t N, float* Y, int64_t ldY, int relu) {
+  if (M <= 0) return;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((ldY + BN - 1) / BN));
+  if (relu) k_gemm_fwd<1><<<grid, 256, 0, L.s>>>(Z, D, ldA, M, F, Wext, N, Y, ldY);
+  else k_gemm_fwd<0><<<grid, 256, 0, L.s>>>(Z, D, ldA, M, F, Wext, N, Y, ldY);
+  count(L);
+}
+
+int64_t gemm_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
+  const int64_t K = 2 * F + 1;
+  const int64_t tiles = ((K + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int64_t splits = (2 * kSMs + tiles - 1) / tiles;
+  const int64_t max_splits = (M + 255) / 256;
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  return splits * K * N;
+}
+
+void gemm_dw_f32(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
+                 int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats) {
+  const int64_t K = 2 * F + 1;
+  int64_t splits = gemm_dw_ws_floats(M, F, N) / (K * N);
+  if (splits * K * N > ws_floats) splits = ws_floats / (K * N);
+  if (splits < 1) splits = 1;
+  if (M <= 0) {
+    cudaMemsetAsync(G, 0, sizeof(float) * K * N, L.s);
+    return;
+  }
+  const int64_t rps = ((M + splits - 1) / splits + BK - 1) / BK * BK;
+  splits = (M + rps - 1) / rps;
+  dim3 grid((unsigned)((K + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)splits);
+  k_gemm_dw<<<grid, 256, 0, L.s>>>(Z, D, ldA, M, F, Mg, ldM, N, rps, ws);
+  k_split_reduce<<<grid_for(K * N, kThreads), kThreads, 0, L.s>>>(ws, splits, K * N, G);
+  count(L, 2);
+}
+
+void gemm_da_f32(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* W, int64_t F,
+                 const float* inv_deg, float* dA, int64_t ld) {
+  if (M <= 0) return;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((2 * ld + BN - 1) / BN));
+  k_gemm_da<<<grid, 256, 0, L.s>>>(Mg, ldM, M, N, W, F, inv_deg, dA, ld);
+  count(L);
+}
+
+void sum_grads(Launch L, const PtrList& G, int64_t P, float* grads) {
+  k_sum_grads<<<grid_for(P, kThreads), kThreads, 0, L.s>>>(G, P, grads);
+  count(L);
+}
+
+void opt_update(Launch L, const float* grads, int64_t P, float* params, float* m, float* v, const OptSpec& o) {
+  k_opt<<<grid_for(P, kThreads), kThreads, 0, L.s>>>(grads, P, params, m, v, o);
+  count(L);
+}
+
+}  // namespace pgcn

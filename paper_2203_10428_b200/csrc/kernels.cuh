@@ -1,0 +1,93 @@
+// Launchers of the sm_100a kernels of the PipeGCN hot path (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pgcn.h"
+
+namespace pgcn {
+
+// Rows [off[s], off[s+1]) of a gathered block come from base[s] + row_map[r] * ld.
+struct SegTable {
+  const float* base[PGCN_MAX_PARTS];
+  int64_t off[PGCN_MAX_PARTS + 1];
+  int32_t n_seg;
+};
+
+// Dropout of one layer input (reading R5): keep iff (SplitMix64(key ^ seed) >> 40) >= thr,
+// key = (key_base + gid) * width + col, key_base = (t (L+1) + l) N.
+struct DropSpec {
+  uint64_t seed;
+  uint64_t key_base;
+  uint32_t thr;
+  float scale;
+  int32_t width;
+  int32_t on;
+};
+
+// Launch counter (per context) incremented by every launcher.
+struct Launch {
+  cudaStream_t s;
+  int64_t* count;
+};
+
+// S3 prologue: D = dropout(H) over rows [0, n_rows); rows >= n_valid are written as 0.
+void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, int64_t n_valid,
+                 const int64_t* gid, const DropSpec& d);
+
+// S3: Z[v] = inv_deg[v] * sum_{e in row v} D[col[e]]   (neighbours >= n_valid contribute 0)
+void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
+              const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z);
+
+// S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
+//     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
+void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
+              const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
+              const int64_t* gid, const DropSpec& d);
+
+// S1 / S2: dst[r] = src(r) (copy) or EMA: dst[r] = first ? src : gamma*prev[r] + (1-gamma)*src.
+void gather_rows(Launch, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld,
+                 float* dst, const float* prev, float gamma, int ema, int first);
+
+// S9 + M: J[v] += sum_{k in inv(v)} C_hat[k] (ascending k; C_hat = message or its EMA, state in
+// ema[k]); M[v] = J[v] o 1[Hprev[v] > 0].  msg may have n_seg == 0 (nothing received).
+void grad_reduce(Launch, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg,
+                 const int32_t* row_map, float* ema, float gamma, int use_ema, int first, float* J,
+                 int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld);
+
+// S5: CE (labels int32) or BCE (labels uint8 [n x C]) on rows with train[v] != 0.
+// M = J^(L) (zero outside the train set), row_loss[v] = loss term of v (already / n_train).
+void loss_rows(Launch, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
+               const uint8_t* train, double n_train, float* M, float* row_loss);
+// out[0] = sum of x[0..n) (single block, fixed order -> deterministic)
+void reduce_sum(Launch, const float* x, int64_t n, float* out);
+
+// GEMMs (fp32 SIMT, parity path).  A_ext = [Z | D | 1] (K = 2F + 1), W_ext = [W; b].
+// fwd: Y = A_ext W_ext, ReLU if relu, written to Y (ldY) rows [0, M), padding cols zeroed.
+void gemm_fwd_f32(Launch, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F,
+                  const float* Wext, int64_t N, float* Y, int64_t ldY, int relu);
+// dW: G[(2F+1) x N] = A_ext^T Mg  (split over rows into ws[splits][(2F+1) N], fixed-order reduce)
+void gemm_dw_f32(Launch, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F,
+                 const float* Mg, int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats);
+int64_t gemm_dw_ws_floats(int64_t M, int64_t F, int64_t N);
+// dA = Mg W^T ([M x 2F]); first half scaled by inv_deg[row] (dZ' of S7), into dA (ld_dA = 2 ld)
+void gemm_da_f32(Launch, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* W, int64_t F,
+                 const float* inv_deg, float* dA, int64_t ld);
+
+// S11 + S12: g = sum_i G_i (ascending i); grads = g; SGD or Adam update of params.
+struct OptSpec {
+  int32_t adam;
+  float lr, beta1, beta2, eps;
+  float step_size;       // lr / (1 - beta1^t)
+  float inv_sqrt_bc2;    // 1 / sqrt(1 - beta2^t)
+  int32_t apply;         // 0: only write grads (cross-rank all-reduce follows)
+};
+struct PtrList {
+  const float* p[PGCN_MAX_PARTS];
+  int32_t n;
+};
+void sum_grads(Launch, const PtrList& G, int64_t P, float* grads);
+void opt_update(Launch, const float* grads, int64_t P, float* params, float* m, float* v, const OptSpec& o);
+
+}  // namespace pgcn

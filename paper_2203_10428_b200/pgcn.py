@@ -1,0 +1,291 @@
+"""Thin ctypes binding of libpgcn.so (include/pgcn.h).  Argument marshalling only: every step of
+the training path runs in the library's sm_100a kernels.  No CPU fallback: if the library is
+missing or a call fails, this module raises.
+
+Names follow the C ABI: `partition` (pgcn_partition, Alg. 1 l.1-5), `Context.layer_fwd`
+(l.9-14), `Context.loss` (l.16), `Context.layer_bwd` (l.18-27), `Context.update` (l.31-32),
+`Context.step` (one iteration t of Alg. 1).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpgcn.so")
+MAX_LAYERS = 16
+MAX_PARTS = 64
+
+OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+T_H, T_HIN, T_Z, T_J, T_G = 0, 1, 2, 3, 4
+KERNELS = ["spmm_fwd", "spmm_bwd", "gemm_fwd", "gemm_dw", "gemm_da", "dropout", "gather", "grad_reduce", "loss",
+           "update"]
+
+
+class PgcnError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("pgcn error %d: %s" % (code, msg))
+        self.code = code
+
+
+class PartView(C.Structure):
+    _fields_ = [("part", C.c_int32), ("n_parts", C.c_int32), ("n_inner", C.c_int64), ("n_halo", C.c_int64),
+                ("nnz", C.c_int64), ("n_send", C.c_int64),
+                ("inner_gid", C.POINTER(C.c_int64)), ("halo_gid", C.POINTER(C.c_int64)),
+                ("halo_off", C.POINTER(C.c_int64)), ("send_off", C.POINTER(C.c_int64)),
+                ("send_idx", C.POINTER(C.c_int32)), ("row_ptr", C.POINTER(C.c_int64)),
+                ("col_idx", C.POINTER(C.c_int32)), ("inv_deg", C.POINTER(C.c_float)),
+                ("t_row_ptr", C.POINTER(C.c_int64)), ("t_col_idx", C.POINTER(C.c_int32)),
+                ("inv_ptr", C.POINTER(C.c_int64)), ("inv_pos", C.POINTER(C.c_int32))]
+
+
+class Config(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("width", C.c_int32 * (MAX_LAYERS + 1)), ("mode", C.c_int32),
+                ("smooth_f", C.c_int32), ("smooth_g", C.c_int32), ("ema_init", C.c_int32),
+                ("gamma", C.c_double), ("dropout", C.c_double), ("seed", C.c_uint64), ("gemm", C.c_int32),
+                ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
+                ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double)]
+
+
+class Comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id_halo", C.c_void_p),
+                ("nccl_id_reduce", C.c_void_p)]
+
+
+class TensorDesc(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libpgcn.so not built (%s): run `python -m paper_2203_10428_b200.build`" % LIB_PATH)
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+        L.pgcn_last_error.restype = C.c_char_p
+        L.pgcn_partition.argtypes = [i64, vp, vp, i32, vp, i32, C.POINTER(vp)]
+        L.pgcn_partition_view.argtypes = [vp, i32, C.POINTER(PartView)]
+        L.pgcn_partition_n_nodes.argtypes = [vp]
+        L.pgcn_partition_n_nodes.restype = i64
+        L.pgcn_partition_free.argtypes = [vp]
+        L.pgcn_partition_free.restype = None
+        L.pgcn_workspace_bytes.argtypes = [vp, vp, i32, C.POINTER(Config), C.POINTER(C.c_size_t)]
+        L.pgcn_ctx_create.argtypes = [vp, vp, i32, C.POINTER(Config), C.POINTER(Comm), vp, C.c_size_t, vp,
+                                      C.POINTER(vp)]
+        L.pgcn_ctx_destroy.argtypes = [vp]
+        L.pgcn_set_inputs.argtypes = [vp, i32, vp, vp, vp]
+        L.pgcn_param_count.argtypes = [C.POINTER(Config)]
+        L.pgcn_param_count.restype = i64
+        L.pgcn_layer_fwd.argtypes = [vp, i64, i32, vp]
+        L.pgcn_loss.argtypes = [vp, i64, vp]
+        L.pgcn_layer_bwd.argtypes = [vp, i64, i32, vp]
+        L.pgcn_update.argtypes = [vp, i64, vp, vp, vp]
+        L.pgcn_step.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.pgcn_tensor.argtypes = [vp, i32, i32, i32, i64, C.POINTER(TensorDesc)]
+        L.pgcn_launch_count.argtypes = [vp]
+        L.pgcn_launch_count.restype = i64
+        L.pgcn_timing_enable.argtypes = [vp, i32]
+        L.pgcn_timing_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        if hasattr(L, "pgcn_nccl_get_unique_id"):
+            L.pgcn_nccl_get_unique_id.argtypes = [vp]
+            L.pgcn_nccl_id_bytes.restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise PgcnError(rc, lib().pgcn_last_error().decode(errors="replace"))
+
+
+def _ptr(a):
+    """Address of a numpy array, torch tensor, or None."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------------------------------------- partition
+class Partitioning:
+    """pgcn_partition (Alg. 1 l.1-5) over a CSR graph."""
+
+    def __init__(self, n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0):
+        self._row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self._col = np.ascontiguousarray(col_idx, dtype=np.int32)
+        self._part_of = None if part_of is None else np.ascontiguousarray(part_of, dtype=np.int32)
+        h = C.c_void_p()
+        _check(lib().pgcn_partition(int(n), _ptr(self._row_ptr), _ptr(self._col), int(n_parts),
+                                    _ptr(self._part_of), int(n_threads), C.byref(h)))
+        self.handle = h
+        self.n = int(n)
+        self.n_parts = int(n_parts)
+
+    def raw_view(self, i) -> PartView:
+        v = PartView()
+        _check(lib().pgcn_partition_view(self.handle, int(i), C.byref(v)))
+        return v
+
+    def view(self, i) -> dict:
+        """Copies of partition i's arrays (names of include/pgcn.h pgcn_part_view)."""
+        v = self.raw_view(i)
+        n_in, n_bd, nnz, ns, n_p = v.n_inner, v.n_halo, v.nnz, v.n_send, v.n_parts
+
+        def arr(p, n, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+        return dict(part=v.part, n_parts=n_p, n_inner=n_in, n_halo=n_bd, nnz=nnz, n_send=ns,
+                    inner_gid=arr(v.inner_gid, n_in, np.int64), halo_gid=arr(v.halo_gid, n_bd, np.int64),
+                    halo_off=arr(v.halo_off, n_p + 1, np.int64), send_off=arr(v.send_off, n_p + 1, np.int64),
+                    send_idx=arr(v.send_idx, ns, np.int32), row_ptr=arr(v.row_ptr, n_in + 1, np.int64),
+                    col_idx=arr(v.col_idx, nnz, np.int32), inv_deg=arr(v.inv_deg, n_in, np.float32),
+                    t_row_ptr=arr(v.t_row_ptr, n_in + n_bd + 1, np.int64), t_col_idx=arr(v.t_col_idx, nnz, np.int32),
+                    inv_ptr=arr(v.inv_ptr, n_in + 1, np.int64), inv_pos=arr(v.inv_pos, ns, np.int32))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().pgcn_partition_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partitioning:
+    return Partitioning(n, row_ptr, col_idx, n_parts, part_of, n_threads)
+
+
+# ------------------------------------------------------------------------------------------- config
+def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
+                ema_init="first", dropout=0.0, seed=4, gemm="fp32", loss="ce", n_global=0, n_train_global=1,
+                opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False) -> Config:
+    c = Config()
+    c.n_layers = len(widths) - 1
+    for i, w in enumerate(widths):
+        c.width[i] = int(w)
+    c.mode = {"vanilla": 0, "pipe": 1}[mode]
+    c.smooth_f, c.smooth_g = int(bool(smooth_f)), int(bool(smooth_g))
+    c.ema_init = {"first": 0, "zero": 1}[ema_init]
+    c.gamma, c.dropout, c.seed = float(gamma), float(dropout), int(seed)
+    c.gemm = {"fp32": 0, "bf16": 1}[gemm]
+    c.loss = {"ce": 0, "bce": 1}[loss]
+    c.n_global, c.n_train_global = int(n_global), int(n_train_global)
+    c.opt = {"sgd": 0, "adam": 1}[opt]
+    c.dump_j = int(bool(dump_j))
+    c.lr, c.beta1, c.beta2, c.eps = float(lr), float(beta1), float(beta2), float(eps)
+    return c
+
+
+def param_count(cfg: Config) -> int:
+    return int(lib().pgcn_param_count(C.byref(cfg)))
+
+
+def flatten_params(layers) -> np.ndarray:
+    """theta = vec[W^(1), b^(1), ..., W^(L), b^(L)] (include/pgcn.h layout), fp32."""
+    return np.concatenate([np.concatenate([np.asarray(W, np.float32).ravel(), np.asarray(b, np.float32).ravel()])
+                           for W, b in layers]).astype(np.float32)
+
+
+def unflatten_params(theta, widths):
+    out, o = [], 0
+    for fi, fo in zip(widths[:-1], widths[1:]):
+        W = theta[o:o + 2 * fi * fo].reshape(2 * fi, fo)
+        o += 2 * fi * fo
+        b = theta[o:o + fo]
+        o += fo
+        out.append((W, b))
+    return out
+
+
+# ------------------------------------------------------------------------------------------- context
+class Context:
+    """A pgcn_ctx hosting `local_parts` of a Partitioning on the current CUDA device."""
+
+    def __init__(self, part: Partitioning, cfg: Config, local_parts: Optional[Sequence[int]] = None,
+                 comm: Optional[Comm] = None, stream=None, device=None):
+        import torch
+        self.torch = torch
+        self.part = part
+        self.cfg = cfg
+        self.local = np.ascontiguousarray(list(range(part.n_parts)) if local_parts is None else local_parts,
+                                          dtype=np.int32)
+        nb = C.c_size_t()
+        _check(lib().pgcn_workspace_bytes(part.handle, _ptr(self.local), len(self.local), C.byref(cfg), C.byref(nb)))
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        self._comm = comm
+        _check(lib().pgcn_ctx_create(part.handle, _ptr(self.local), len(self.local), C.byref(cfg),
+                                     C.byref(comm) if comm is not None else None, self.ws.data_ptr(),
+                                     self.ws.numel(), self.stream.cuda_stream, C.byref(h)))
+        self.handle = h
+        self.P = param_count(cfg)
+        self.widths = [cfg.width[i] for i in range(cfg.n_layers + 1)]
+
+    def set_inputs(self, local, X, labels, train_mask):
+        self._keep = (X, labels, train_mask)
+        _check(lib().pgcn_set_inputs(self.handle, int(local), _ptr(X), _ptr(labels), _ptr(train_mask)))
+
+    def layer_fwd(self, t, layer, params):
+        _check(lib().pgcn_layer_fwd(self.handle, int(t), int(layer), _ptr(params)))
+
+    def loss(self, t, loss_dev=None):
+        _check(lib().pgcn_loss(self.handle, int(t), _ptr(loss_dev)))
+
+    def layer_bwd(self, t, layer, params):
+        _check(lib().pgcn_layer_bwd(self.handle, int(t), int(layer), _ptr(params)))
+
+    def update(self, t, params, grads, opt_state=None):
+        _check(lib().pgcn_update(self.handle, int(t), _ptr(params), _ptr(grads), _ptr(opt_state)))
+
+    def step(self, t, params, grads, opt_state=None, loss_dev=None):
+        _check(lib().pgcn_step(self.handle, int(t), _ptr(params), _ptr(grads), _ptr(opt_state), _ptr(loss_dev)))
+
+    def tensor(self, local, kind, layer=0, t=1):
+        """torch view (rows x cols, row stride ld) of an internal device buffer (pgcn_tensor)."""
+        d = TensorDesc()
+        _check(lib().pgcn_tensor(self.handle, int(local), int(kind), int(layer), int(t), C.byref(d)))
+        torch = self.torch
+        base = self.ws.data_ptr()
+        off = (d.ptr - base)
+        assert off % 4 == 0 and 0 <= off < self.ws.numel()
+        f = self.ws.view(torch.float32) if self.ws.numel() % 4 == 0 else self.ws[: self.ws.numel() // 4 * 4].view(
+            torch.float32)
+        return torch.as_strided(f, (d.rows, d.cols), (d.ld, 1), off // 4)
+
+    def timing_enable(self, on=True):
+        _check(lib().pgcn_timing_enable(self.handle, int(bool(on))))
+
+    def timing_read(self, kind):
+        ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        _check(lib().pgcn_timing_read(self.handle, int(kind), C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
+        return dict(ms=ms.value, launches=n.value, bytes=by.value, flops=fl.value)
+
+    def launch_count(self) -> int:
+        return int(lib().pgcn_launch_count(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().pgcn_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded
+inputs.  Tolerance (north_star): per tensor
+max|gpu - oracle| <= 1e-4 * max|oracle| for the fp32 path.
+
+Cases span several SpMM/GEMM tiles and ragged tails (widths not multiples of 4, 64, 128),
+isolated nodes, empty partitions, every mode (VANILLA, PIPE, PIPE-F/-G/-GF), dropout on/off,
+CE and BCE, SGD and Adam."""
+import numpy as np
+import pytest
+
+from oracle import pipegcn
+from oracle.partition import partition as oracle_partition
+from synth.graphs import ModelCfg, gen_graph, glorot_params
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2203_10428_b200 import build, pgcn
+    build.build()
+    return pgcn
+
+
+def rel(g, r):
+    g, r = np.asarray(g, np.float64), np.asarray(r, np.float64)
+    return np.abs(g - r).max() / max(np.abs(r).max(), 1e-30) if r.size else 0.0
+
+
+def flat(layers):
+    return np.concatenate([np.concatenate([np.ravel(W), np.ravel(b)]) for W, b in layers])
+
+
+def run_gpu(P, g, widths, n_parts, T, params0, part_of=None, **kw):
+    import torch
+    part = P.partition(g.n, g.row_ptr, g.col_idx, n_parts, part_of)
+    cfg = P.make_config(widths, n_global=g.n, n_train_global=g.n_train, dump_j=True, **kw)
+    ctx = P.Context(part, cfg)
+    keep = []
+    for i in range(n_parts):
+        gid = part.view(i)["inner_gid"]
+        X = torch.tensor(g.X[gid]).cuda()
+        lab = torch.tensor(g.labels[gid]).cuda()
+        tm = torch.tensor(g.train_mask[gid]).cuda()
+        keep.append((X, lab, tm))
+        ctx.set_inputs(i, X, lab, tm)
+    theta = torch.tensor(P.flatten_params(params0)).cuda()
+    grads = torch.zeros_like(theta)
+    opt = torch.zeros(2 * theta.numel(), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    L = len(widths) - 1
+    recs = []
+    for t in range(1, T + 1):
+        ctx.step(t, theta, grads, opt, loss)
+        torch.cuda.synchronize()
+        rec = dict(loss=float(loss.item()), G=grads.cpu().numpy().copy(), params=theta.cpu().numpy().copy(), H={},
+                   J={}, G_parts=[ctx.tensor(i, P.T_G).cpu().numpy().ravel().copy() for i in range(n_parts)])
+        for l in range(1, L + 1):
+            rec["H"][l] = [ctx.tensor(i, P.T_H, l, t)[:, :widths[l]].cpu().numpy().copy() for i in range(n_parts)]
+        for l in range(1, L):
+            rec["J"][l] = [ctx.tensor(i, P.T_J, l, t)[:, :widths[l]].cpu().numpy().copy() for i in range(n_parts)]
+        recs.append(rec)
+    return recs, ctx
+
+
+def check_against_oracle(gpu, ora, L, n_parts, tol=TOL, what=""):
+    for t, (a, b) in enumerate(zip(gpu, ora), start=1):
+        assert abs(a["loss"] - b["loss"]) <= tol * abs(b["loss"]), (what, t, a["loss"], b["loss"])
+        for l in range(1, L + 1):
+            for i in range(n_parts):
+                e = rel(a["H"][l][i], b["H"][l][i])
+                assert e <= tol, (what, "H", t, l, i, e)
+        for l in range(1, L):
+            for i in range(n_parts):
+                e = rel(a["J"][l][i], b["J"][l][i])
+                assert e <= tol, (what, "J", t, l, i, e)
+        e = rel(a["G"], flat(b["G"]))
+        assert e <= tol, (what, "G", t, e)
+        for i in range(n_parts):
+            e = rel(a["G_parts"][i], flat(b["G_parts"][i]))
+            assert e <= tol, (what, "G_i", t, i, e)
+        e = rel(a["params"], flat(b["params"]))
+        assert e <= tol, (what, "params", t, e)
+
+
+MODES = [("vanilla", False, False), ("pipe", False, False), ("pipe", True, False), ("pipe", False, True),
+         ("pipe", True, True)]
+
+
+@pytest.mark.parametrize("mode,sf,sg", MODES)
+@pytest.mark.parametrize("p", [0.0, 0.5])
+def test_cora_two_partitions(P, mode, sf, sg, p):
+    """BASELINE configs[0]: Cora-shaped graph, 2-layer GraphSAGE hidden 16, 2 partitions on 1 GPU."""
+    g = gen_graph("cora", seed=1)
+    widths = [1433, 16, 7]
+    params0 = glorot_params(widths, 3)
+    kw = dict(mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.95, dropout=p, loss="ce", opt="sgd", lr=0.5)
+    T = 4
+    gpu, _ = run_gpu(P, g, widths, 2, T, params0, **kw)
+    cfg = ModelCfg(widths=widths, dropout=p, lr=0.5, opt="sgd", loss="ce", gamma=0.95)
+    ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, 2), params0, cfg, T, mode=mode, smooth_f=sf,
+                      smooth_g=sg)
+    check_against_oracle(gpu, ora, 2, 2, what=f"cora {mode} F{sf} G{sg} p{p}")
+
+
+@pytest.mark.parametrize("mode,sf,sg,ema_init", [("pipe", True, True, "first"), ("pipe", True, True, "zero"),
+                                                 ("vanilla", False, False, "first"), ("pipe", False, False, "first")])
+def test_multi_tile_ragged_bce_three_parts(P, mode, sf, sg, ema_init):
+    """Several tiles + ragged widths (103 -> 70 -> 45 -> 13, none a multiple of 4), 3 layers,
+    3 partitions, multilabel BCE, dropout 0.3, Adam (3 steps)."""
+    g = gen_graph("yelp", seed=2, n=3001, nnz=40000, f0=103, classes=13)
+    widths = [103, 70, 45, 13]
+    params0 = glorot_params(widths, 5)
+    kw = dict(mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.7, ema_init=ema_init, dropout=0.3, loss="bce",
+              opt="adam", lr=0.01)
+    T = 3
+    gpu, _ = run_gpu(P, g, widths, 3, T, params0, **kw)
+    cfg = ModelCfg(widths=widths, dropout=0.3, lr=0.01, opt="adam", loss="bce", gamma=0.7)
+    ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, 3), params0, cfg, T, mode=mode, smooth_f=sf,
+                      smooth_g=sg, ema_init=ema_init)
+    check_against_oracle(gpu, ora, 3, 3, what=f"bce {mode} {ema_init}")
+
+
+def test_wide_rows_and_hidden_256(P):
+    """Reddit-like widths at small N: 602 -> 256 -> 41 (SpMM uses 32-lane groups x 5 float4 chunks)."""
+    g = gen_graph("reddit", seed=3, n=1500, nnz=60000, f0=602, classes=41)
+    widths = [602, 256, 41]
+    params0 = glorot_params(widths, 7)
+    kw = dict(mode="pipe", dropout=0.5, loss="ce", opt="sgd", lr=0.1)
+    gpu, _ = run_gpu(P, g, widths, 2, 3, params0, **kw)
+    cfg = ModelCfg(widths=widths, dropout=0.5, lr=0.1, opt="sgd", loss="ce")
+    ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, 2), params0, cfg, 3, mode="pipe")
+    check_against_oracle(gpu, ora, 2, 2, what="wide")
+
+
+def test_empty_partitions_and_one_partition(P):
+    """Degenerate cases: more partitions than nodes in some ranges (empty V_i), and n = 1."""
+    g = gen_graph("cora", seed=4, n=6, nnz=10, f0=5, classes=3, comm=2)
+    widths = [5, 4, 3]
+    params0 = glorot_params(widths, 1)
+    cfg = ModelCfg(widths=widths, dropout=0.0, lr=0.2, opt="sgd", loss="ce")
+    for n_parts in (1, 8):
+        gpu, _ = run_gpu(P, g, widths, n_parts, 3, params0, mode="pipe", loss="ce", opt="sgd", lr=0.2)
+        ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, n_parts), params0, cfg, 3, mode="pipe")
+        check_against_oracle(gpu, ora, 2, n_parts, what=f"degenerate n={n_parts}")
+
+
+def test_order_violations_poison_nothing(P):
+    import torch
+    g = gen_graph("cora", seed=1, n=200, nnz=800, f0=8, classes=3)
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 2)
+    cfg = P.make_config([8, 4, 3], n_global=g.n, n_train_global=g.n_train)
+    ctx = P.Context(part, cfg)
+    theta = torch.zeros(P.param_count(cfg), device="cuda")
+    with pytest.raises(P.PgcnError) as e:
+        ctx.layer_fwd(2, 1, theta)            # t must start at 1
+    assert e.value.code == P.ESTATE
+    with pytest.raises(P.PgcnError) as e:
+        ctx.layer_bwd(1, 2, theta)            # backward before forward
+    assert e.value.code == P.ESTATE
+    ctx.layer_fwd(1, 1, theta)                # the context is still usable
+    with pytest.raises(P.PgcnError) as e:
+        ctx.layer_fwd(1, 1, theta)            # layer 1 twice
+    assert e.value.code == P.ESTATE
+    ctx.layer_fwd(1, 2, theta)
+    ctx.loss(1)
+
+
+def test_launches_counted(P):
+    import torch
+    g = gen_graph("cora", seed=1, n=300, nnz=1200, f0=8, classes=3)
+    gpu, ctx = run_gpu(P, g, [8, 6, 3], 2, 2, glorot_params([8, 6, 3], 1), mode="pipe")
+    assert ctx.launch_count() > 20
