@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--parts", type=int, default=0, help="partitions (default max(2, N))")
     ap.add_argument("--mode", default="pipe", choices=["pipe", "vanilla"])
     ap.add_argument("--smooth", default="", help="'', 'f', 'g' or 'gf'")
-    ap.add_argument("--gemm", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "bf16"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -257,7 +257,7 @@ def main():
     pk = peaks()
     top = max(kern.items(), key=lambda kv: kv[1]["ms"])
     name, kd = top
-    if name.startswith("gemm") and args.gemm == "fp32":
+    if name.startswith("gemm") and args.gemm == "simt":
         # SIMT fp32: bound by FFMA issue, 148 SMs x 128 lanes x 2 flop x max SM clock
         peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         ach = kd["flops"] / (kd["ms"] / 1e3) / 1e12

@@ -133,7 +133,9 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *   dropout, seed       p and the mask seed: keep iff (SplitMix64(key ^ seed) >> 40) >=
  *                       floor(p*2^24 + 0.5), key = ((t(L+1)+l)N + gid)F_{l-1} + col, applied
  *                       to every layer's input after the exchange (App. F; R5).
- *   gemm                0 FP32 (SIMT, parity path), 1 BF16 tensor cores (tcgen05; 2e-2 tier).
+ *   gemm                0 fp32-grade on the tensor cores: tcgen05 kind::tf32 with the 3xTF32 split
+ *                       (hi/lo operands, 1e-4 tier; default); 1 BF16 tensor cores (2e-2 tier, not
+ *                       built yet); 2 fp32 SIMT CUDA-core GEMMs (reference kernels).
  *   loss                0 softmax cross-entropy (labels int32 [n_inner]), 1 sigmoid BCE
  *                       (labels uint8 [n_inner x F_L]); mean over the GLOBAL train set (R6).
  *   n_global            N (dropout keys); n_train_global: |train set| over the whole graph.

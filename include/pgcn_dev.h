@@ -1,0 +1,32 @@
+/*
+ * pgcn_dev.h -- diagnostics entry points of libpgcn.so (not needed to train; used by the GPU unit
+ * tests to check one kernel in isolation).  Same conventions as pgcn.h: 0 / negative PGCN_E*
+ * codes, message in pgcn_last_error(), device pointers, asynchronous on `stream`.
+ */
+#ifndef PGCN_DEV_H
+#define PGCN_DEV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* The three node-update GEMMs of a GraphSAGE layer (Alg. 1 l.14, l.18, l.20), with
+ * A_ext = [A0 | A1 | 1] ([M x (2F+1)], A0 / A1 row-major with row stride ldA) and
+ * W_ext = [W; b] ([(2F+1) x N] row-major, the layer's slice of theta):
+ *   op 0 (forward)  out[M x ld_out]      = act(A_ext W_ext), act = ReLU if relu; cols [N, ld_out) = 0
+ *   op 1 (dW)       out[(2F+1) x N]      = A_ext^T Mg            (Mg: [M x N], row stride ldM)
+ *   op 2 (dA)       out[M x 2 ld_out/2]  = [inv_deg o (Mg W_neigh^T) | Mg W_self^T], halves padded
+ * variant: 0 = tcgen05 3xTF32 tensor cores, 2 = fp32 SIMT.  scratch: device buffer of at least
+ * pgcn_dev_gemm_scratch_bytes(M, F, N) bytes (256-byte aligned).                                  */
+size_t pgcn_dev_gemm_scratch_bytes(int64_t M, int64_t F, int64_t N);
+int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1, int64_t ldA, int64_t M, int64_t F,
+                  const float* W_ext, int64_t N, const float* Mg, int64_t ldM, const float* inv_deg, float* out,
+                  int64_t ld_out, int32_t relu, void* scratch, size_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGCN_DEV_H */

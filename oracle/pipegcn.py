@@ -34,10 +34,15 @@ from .sage import Adam, loss_and_grad, sgd_update
 
 
 def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, gamma=None,
-        ema_init="first", seed=4, opt=None, keep_A=False):
+        ema_init="first", seed=4, opt=None, keep_A=False, relu_decision=None):
     """Train for t = 1..T.  Returns a list (one dict per t) with
     loss, H[l][i] (inner rows of layer l output), J[l][i] (inner J^(l) after accumulation),
-    halo[l][i] (boundary rows used as input of layer l), G_parts[i], G, params (after update)."""
+    halo[l][i] (boundary rows used as input of layer l), G_parts[i], G, params (after update).
+
+    relu_decision(t, l, i, Y) -> bool mask, optional: the sigma'(Y) = 1[Y > 0] decision used in
+    the backward (App. A.1).  Default Y > 0.  Parity tests pass a hook that adopts
+    the kernel's decision where |Y| is within the comparison tolerance of 0 (DESIGN.md reading
+    R25: a float-decided discrete choice is taken in the kernel's precision on both sides)."""
     assert mode in ("pipe", "vanilla")
     gamma = cfg.gamma if gamma is None else gamma
     n = len(parts)
@@ -127,7 +132,11 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
             J_in, J_halo = [], []
             for i in range(n):
                 A, Y, keep = saved[(l, i)]
-                M = J[i] * (Y > 0) if l < L else J[i]
+                if l < L:
+                    mask = (Y > 0) if relu_decision is None else relu_decision(t, l, i, Y)
+                    M = J[i] * mask
+                else:
+                    M = J[i]
                 G_parts[i][l - 1] = (A.T @ M, M.sum(0))                      # l.18
                 if l > 1:                                                    # l.20
                     dA = M @ W.T

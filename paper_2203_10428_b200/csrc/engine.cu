@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.h"
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "pgcn.h"
 
@@ -83,6 +84,12 @@ struct pgcn_ctx {
   cudaStream_t s = nullptr;
   float* dw_ws = nullptr;
   int64_t dw_ws_floats = 0;
+  // tensor-core operand prep per layer: W_ext^T and W (tf32 hi/lo splits, TMA-legal strides)
+  float* WT_hi[PGCN_MAX_LAYERS + 1] = {};
+  float* WT_lo[PGCN_MAX_LAYERS + 1] = {};
+  float* Wp_hi[PGCN_MAX_LAYERS + 1] = {};
+  float* Wp_lo[PGCN_MAX_LAYERS + 1] = {};
+  int64_t Fp[PGCN_MAX_LAYERS + 1] = {}, Kp[PGCN_MAX_LAYERS + 1] = {};
   float* part_loss = nullptr;
   int64_t exp_t = 1;
   int exp_kind = pgcn::K_FWD, exp_layer = 1;
@@ -106,7 +113,7 @@ int validate_cfg(const pgcn_config* c) {
     if (c->width[l] < 1) return fail(PGCN_EINVAL, "width[%d] < 1", l);
   if (c->mode != 0 && c->mode != 1) return fail(PGCN_EINVAL, "mode must be 0 (VANILLA) or 1 (PIPE)");
   if (!(c->dropout >= 0.0 && c->dropout < 1.0)) return fail(PGCN_EINVAL, "dropout must be in [0,1)");
-  if (c->gemm != 0) return fail(PGCN_EUNSUPPORTED, "gemm variant %d not built", c->gemm);
+  if (c->gemm != 0 && c->gemm != 2) return fail(PGCN_EUNSUPPORTED, "gemm variant %d not built", c->gemm);
   if (c->loss != 0 && c->loss != 1) return fail(PGCN_EINVAL, "loss must be 0 (CE) or 1 (BCE)");
   if (c->opt != 0 && c->opt != 1) return fail(PGCN_EINVAL, "opt must be 0 (SGD) or 1 (Adam)");
   if (c->n_train_global < 1) return fail(PGCN_EINVAL, "n_train_global < 1");
@@ -167,10 +174,22 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     for (int l = 1; l <= L; ++l) {
       int64_t w = gemm_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
       if (w > dw_need) dw_need = w;
+      w = tc_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
+      if (w > dw_need) dw_need = w;
     }
   }
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
+  if (C->cfg.gemm == 0) {
+    for (int l = 1; l <= L; ++l) {
+      C->Fp[l] = round_up(C->F[l - 1], 32);
+      C->Kp[l] = round_up(C->F[l], 4);
+      C->WT_hi[l] = A.take<float>(C->F[l] * 2 * C->Fp[l]);
+      C->WT_lo[l] = A.take<float>(C->F[l] * 2 * C->Fp[l]);
+      C->Wp_hi[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
+      C->Wp_lo[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
+    }
+  }
   C->part_loss = A.take<float>(n_local);
   return PGCN_OK;
 }
@@ -408,6 +427,13 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
+  const bool tcg = C->cfg.gemm == 0;
+  if (tcg) {
+    Scope sc(C, PGCN_K_GEMM_FWD, 0.0);
+    tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], C->WT_hi[l], C->WT_lo[l],
+             C->Wp_hi[l], C->Wp_lo[l], C->s);
+    ++C->launches;
+  }
   for (auto& p : C->parts) {
     float* Hin = layer_in(p, l, b);
     // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13; local transport = device gather)
@@ -454,7 +480,13 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     {
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * (2 * Fi + 1) * Fo,
                2.0 * p.n_in * (2 * Fi + 1) * Fo);
-      gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
+      if (tcg) {
+        if (gemm_fwd_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], C->WT_hi[l], C->WT_lo[l],
+                        Wext + 2 * C->F[l - 1] * C->F[l], C->F[l], out, ldo, l < C->L))
+          return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
+      } else {
+        gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
+      }
     }
   }
   rc = check_cuda(C, "pgcn_layer_fwd");
@@ -499,13 +531,25 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const float* D = C->cfg.dropout > 0.0 ? p.D[l] : layer_in(p, l, b);
     {
       Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (2 * Fi + Fo), 2.0 * p.n_in * (2 * Fi + 1) * Fo);
-      gemm_dw_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
-                  C->dw_ws_floats);
+      if (C->cfg.gemm == 0) {
+        if (gemm_dw_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
+                       C->dw_ws_floats))
+          return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
+      } else {
+        gemm_dw_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
+                    C->dw_ws_floats);
+      }
     }
     if (l >= 2) {
       {
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * 2 * Fi);
-        gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
+        if (C->cfg.gemm == 0) {
+          if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.inv_deg,
+                         p.dA, ldi))
+            return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
+        } else {
+          gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
+        }
       }
       Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);

@@ -1,0 +1,679 @@
+// Node-update GEMMs of the GraphSAGE layer (S4 fwd, S6 dW, S7 dA) on the 5th-generation tensor
+// cores: TMA-fed, tcgen05.mma with fp32 accumulators in TMEM, warp-specialised, persistent.
+//
+// Precision: "3xTF32" -- every fp32 operand x is split as hi = rna_tf32(x), lo = rna_tf32(x - hi)
+// and D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::tf32, fp32 accumulate).  The dropped A_lo B_lo
+// term and the tf32 rounding of lo are O(2^-22) relative, so the result is fp32-grade (the 1e-4
+// parity tier of the north_star) while running on the tensor pipe.
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer (one lane),
+// warps 2-3 = converters (split fp32 tiles into hi/lo in shared memory, in the UMMA layout),
+// warps 4-7 = epilogue (tcgen05.ld TMEM -> registers -> global).
+// Pipelines: full[s] (TMA -> converters), conv[s] (converters -> MMA), empty[s] (MMA commit ->
+// TMA), tfull[a] / tempty[a] (MMA <-> epilogue, two accumulator buffers in TMEM).
+//
+// Modes:
+//   FWD : Y[m, n]   = sum_k [Z | D][m, k] W[k, n] + b[n]  (ReLU)   A K-major (2 segments),
+//         B = W^T pre-split into hi/lo [N x 2Fp] K-major.
+//   DA  : dA[m, hF+c] = sum_j M[m, j] W[hF + c, j]  (h = 0 scaled by inv_deg[m])  A = M K-major,
+//         B = W pre-split [2F x Kp] K-major.
+//   DW  : part[z][segF + f, n] = sum_{r in split z} A_s[r, f] M[r, n]   both operands MN-major
+//         (row-major activations read "transposed"), both split by the converters.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "pgcn_dev.h"
+
+#include "common.h"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace pgcn {
+namespace tc {
+
+// ------------------------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// Bounded wait: a barrier that does not complete within ~2^32 cycles (seconds) means a pipeline
+// bug; report which wait and trap, so the launch fails loudly instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int tag) {
+  const uint32_t a = smem_u32(b);
+  long long t0 = 0;
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    const long long now = clock64();
+    if (t0 == 0) {
+      t0 = now;
+    } else if (now - t0 > (1ll << 32)) {
+      printf("pgcn tcgen05 watchdog: block %d thread %d wait tag %d parity %u timed out\n", blockIdx.x, threadIdx.x,
+             tag, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+#define TMEM_LD16(taddr, r)                                                                                          \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),    \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),         \
+                 "=r"(r[15])                                                                                        \
+               : "r"(taddr))
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor (sm100 version bits = 1).  layout 2 = SWIZZLE_128B (K-major
+// operands), layout 1 = SWIZZLE_128B_BASE32B (the only MN-major layout for tf32: 32-byte granules
+// permuted over 4-row atoms; TMA writes it with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout = 2) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
+}
+
+// ------------------------------------------------------------------------------------------------ kernel
+constexpr int kThreads = 256;
+constexpr int BM = 128;   // UMMA M (rows of A, TMEM lanes)
+constexpr int BK = 32;    // fp32 elements per k-block = one 128-byte swizzle row
+
+struct Tile {
+  int m0, n0, kb_begin, kb_end, z, seg, half;
+};
+
+__device__ __forceinline__ void decode(const TcParams& p, int t, Tile& T) {
+  if (p.mode == TC_DW) {
+    // t -> (z split, seg, f-tile, n-tile)
+    const int nt = t % p.n_ntiles;
+    int r = t / p.n_ntiles;
+    const int ft = r % p.n_ftiles;
+    r /= p.n_ftiles;
+    T.seg = r % p.n_seg;
+    T.z = r / p.n_seg;
+    T.m0 = ft * BM;
+    T.n0 = nt * p.BN;
+    T.kb_begin = T.z * p.kb_per_split;
+    T.kb_end = min(T.kb_begin + p.kb_per_split, p.kb_total);
+    T.half = 0;
+  } else {
+    const int nt = t % p.n_ntiles;
+    const int mt = t / p.n_ntiles;
+    T.m0 = mt * BM;
+    T.z = 0;
+    T.seg = 0;
+    if (p.mode == TC_DA) {
+      T.half = nt / p.n_ntiles_half;
+      T.n0 = (nt % p.n_ntiles_half) * p.BN;
+    } else {
+      T.half = 0;
+      T.n0 = nt * p.BN;
+    }
+    T.kb_begin = 0;
+    T.kb_end = p.kb_total;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant__ TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages;
+  const uint32_t a_bytes = BM * BK * 4;               // 16 KB
+  const uint32_t b_bytes = (uint32_t)p.BN * BK * 4;   // BN x 128 B
+  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  uint8_t* stA = smem;                                 // per stage: A(hi) | A_lo | B(hi) | B_lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* tfull = bars + 3 * S;
+  uint64_t* tempty = bars + 3 * S + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"((uint32_t)p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const bool split_b = p.mode == TC_DW;
+
+  if (warp == 0) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        Tile T;
+        decode(p, t, T);
+        for (int kb = T.kb_begin; kb < T.kb_end; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1, 1);
+          uint8_t* A = stA + (size_t)s * stage_bytes;
+          uint8_t* B = A + 2 * a_bytes;
+          uint8_t* Blo = B + b_bytes;
+          mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
+          if (p.mode == TC_DW) {
+            const CUtensorMap* am = T.seg == 0 ? &p.map_a0 : &p.map_a1;
+            const int r0 = kb * BK;
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, am, &full[s], T.m0 + 32 * j, r0);
+            for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 4096, &p.map_b, &full[s], T.n0 + 32 * j, r0);
+          } else if (p.mode == TC_FWD) {
+            const int seg = kb < p.kb_seg0 ? 0 : 1;
+            const int col = (kb - (seg ? p.kb_seg0 : 0)) * BK;
+            tma_load_2d(A, seg == 0 ? &p.map_a0 : &p.map_a1, &full[s], col, T.m0);
+            const int kcol = seg * p.kb_seg0 * BK + col;
+            tma_load_2d(B, &p.map_b, &full[s], kcol, T.n0);
+            tma_load_2d(Blo, &p.map_b_lo, &full[s], kcol, T.n0);
+          } else {  // TC_DA
+            tma_load_2d(A, &p.map_a0, &full[s], kb * BK, T.m0);
+            const int brow = T.half * p.F + T.n0;
+            tma_load_2d(B, &p.map_b, &full[s], kb * BK, brow);
+            tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * BK, brow);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (p.mode == TC_DW ? (1u << 15) | (1u << 16) : 0u) |
+                             ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        Tile T;
+        decode(p, t, T);
+        mbar_wait(&tempty[acc], acc_ph ^ 1, 2);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * p.BN);
+        uint32_t accum = 0;
+        for (int kb = T.kb_begin; kb < T.kb_end; ++kb) {
+          mbar_wait(&conv[s], ph, 3);
+          tc_fence_after();
+          const uint32_t A = smem_u32(stA + (size_t)s * stage_bytes);
+          const uint32_t Alo = A + a_bytes, B = A + 2 * a_bytes, Blo = B + b_bytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            uint64_t ah, al, bh, bl;
+            if (p.mode == TC_DW) {  // MN-major: MN atoms 4 KB apart (LBO), 4-row k-groups 512 B apart (SBO)
+              ah = make_desc(A + kk * 1024, 4096, 512, 1);
+              al = make_desc(Alo + kk * 1024, 4096, 512, 1);
+              bh = make_desc(B + kk * 1024, 4096, 512, 1);
+              bl = make_desc(Blo + kk * 1024, 4096, 512, 1);
+            } else {  // K-major: 8-row groups 1 KB apart (SBO); k-step = 32 bytes inside the swizzle row
+              ah = make_desc(A + kk * 32, 16, 1024);
+              al = make_desc(Alo + kk * 32, 16, 1024);
+              bh = make_desc(B + kk * 32, 16, 1024);
+              bl = make_desc(Blo + kk * 32, 16, 1024);
+            }
+            mma_tf32(d, ah, bh, idesc, accum);
+            mma_tf32(d, ah, bl, idesc, 1u);
+            mma_tf32(d, al, bh, idesc, 1u);
+            accum = 1u;
+          }
+          tc_commit(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp < 4) {
+    // ===================================================== converters: x -> (hi, lo)
+    const int ct = threadIdx.x - 64;  // 0..63
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      Tile T;
+      decode(p, t, T);
+      for (int kb = T.kb_begin; kb < T.kb_end; ++kb) {
+        mbar_wait(&full[s], ph, 4);
+        float4* A = reinterpret_cast<float4*>(stA + (size_t)s * stage_bytes);
+        float4* Alo = A + a_bytes / 16;
+        for (int i = ct; i < (int)(a_bytes / 16); i += 64) {
+          float4 x = A[i], h, l;
+          h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+          h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+          h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+          h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+          A[i] = h;
+          Alo[i] = l;
+        }
+        if (split_b) {
+          float4* B = A + 2 * (a_bytes / 16);
+          float4* Blo = B + b_bytes / 16;
+          for (int i = ct; i < (int)(b_bytes / 16); i += 64) {
+            float4 x = B[i], h, l;
+            h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+            h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+            h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+            h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+            B[i] = h;
+            Blo[i] = l;
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(&conv[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // ===================================================== epilogue: TMEM -> registers -> global
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      Tile T;
+      decode(p, t, T);
+      mbar_wait(&tfull[acc], acc_ph, 5);
+      __syncwarp();
+      tc_fence_after();
+      const int row = T.m0 + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.BN);
+      for (int c0 = 0; c0 < p.BN; c0 += 16) {
+        uint32_t r[16];
+        TMEM_LD16(tbase + c0, r);
+        tmem_ld_wait();
+        if (p.mode == TC_FWD) {
+          if (row < p.M) {
+            float* out = p.out + (int64_t)row * p.ld_out;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = T.n0 + c0 + i;
+              if (n < p.N) {
+                float v = __uint_as_float(r[i]) + p.bias[n];
+                out[n] = p.relu ? fmaxf(v, 0.f) : v;
+              } else if (n < p.ld_out) {
+                out[n] = 0.f;
+              }
+            }
+          }
+        } else if (p.mode == TC_DA) {
+          if (row < p.M) {
+            float* out = p.out + (int64_t)row * p.ld_out + (int64_t)T.half * p.ld_half;
+            const float sc = T.half == 0 ? p.inv_deg[row] : 1.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int c = T.n0 + c0 + i;
+              if (c < p.F) out[c] = __uint_as_float(r[i]) * sc;
+              else if (c < p.ld_half) out[c] = 0.f;
+            }
+          }
+        } else {  // TC_DW partial
+          if (row < p.F) {
+            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)T.seg * p.F + row) * p.N;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = T.n0 + c0 + i;
+              if (n < p.N) out[n] = __uint_as_float(r[i]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)p.tmem_cols));
+  }
+}
+
+// W prep: for layer weights W [2F x N] (+ bias), write the tf32 hi/lo splits in the two TMA
+// layouts used above: WT [N x 2Fp] (FWD operand B, K-major; cols [0,F) = W_neigh^T,
+// [Fp, Fp+F) = W_self^T) and Wp [2F x Kp] (DA operand B, K-major).
+__global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int Kp, float* WT_hi, float* WT_lo,
+                        float* Wp_hi, float* Wp_lo) {
+  const int64_t total_t = (int64_t)N * 2 * Fp, total_p = (int64_t)2 * F * Kp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x = 0.f;
+    if (i < total_t) {
+      const int64_t n = i / (2 * Fp), k = i % (2 * Fp);
+      const int seg = (int)(k / Fp), f = (int)(k % Fp);
+      if (f < F) x = W[((int64_t)seg * F + f) * N + n];
+      const float h = tf32_rna(x);
+      WT_hi[i] = h;
+      WT_lo[i] = tf32_rna(x - h);
+    } else {
+      const int64_t j = i - total_t, r = j / Kp, c = j % Kp;
+      if (c < N) x = W[r * N + c];
+      const float h = tf32_rna(x);
+      Wp_hi[j] = h;
+      Wp_lo[j] = tf32_rna(x - h);
+    }
+  }
+}
+
+// db partial: part[z][row_off + n] = sum_{r in split z} M[r, n]  (fixed order; the bias row of
+// the dW output, reduced over splits together with the tensor-core rows)
+__global__ void k_colsum(const float* __restrict__ Mg, int64_t M, int64_t ld, int N, int64_t rps,
+                         float* __restrict__ part, int64_t zstride, int64_t row_off) {
+  __shared__ float sh[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = r0 + rps < M ? r0 + rps : M;
+  float a = 0.f;
+  if (n < N)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) a += Mg[r * ld + n];
+  sh[threadIdx.y][threadIdx.x] = a;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float s = 0.f;
+    for (int y = 0; y < 8; ++y) s += sh[y][threadIdx.x];
+    part[(int64_t)blockIdx.y * zstride + row_off + n] = s;
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------------------------------------ host side
+namespace {
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  });
+  return fn;
+}
+}  // namespace
+
+bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
+               bool mn_major) {
+  EncodeFn f = encode_fn();
+  if (!f || cols <= 0 || rows <= 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int tc_stages(int BN) {
+  const int stage = 2 * tc::BM * tc::BK * 4 + 2 * BN * tc::BK * 4;
+  int S = (200 * 1024) / stage;
+  return S > 4 ? 4 : (S < 2 ? 2 : S);
+}
+
+size_t tc_smem_bytes(int BN, int S) {
+  const size_t stage = 2 * (size_t)tc::BM * tc::BK * 4 + 2 * (size_t)BN * tc::BK * 4;
+  return 1024 + S * stage + (3 * S + 4) * 8 + 16;
+}
+
+int tc_bn(int64_t N) {
+  int64_t bn = (N + 15) / 16 * 16;
+  if (bn > 256) bn = 256;
+  if (bn < 16) bn = 16;
+  return (int)bn;
+}
+
+int tc_tmem_cols(int BN) {
+  int need = 2 * BN, c = 32;
+  while (c < need) c *= 2;
+  return c;
+}
+
+cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms) {
+  static bool attr_set = false;
+  const size_t smem = tc_smem_bytes(p.BN, p.stages);
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc::k_umma_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  int grid = p.n_tiles < sms ? p.n_tiles : sms;
+  if (grid < 1) return cudaSuccess;
+  tc::k_umma_gemm<<<grid, tc::kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+void tc_wprep(const float* W, int F, int N, int Fp, int Kp, float* WT_hi, float* WT_lo, float* Wp_hi, float* Wp_lo,
+              cudaStream_t s) {
+  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 8) grid = 148 * 8;
+  tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, WT_hi, WT_lo, Wp_hi, Wp_lo);
+}
+
+// ---------------------------------------------------------------------------------------- mode wrappers
+static void tc_common(TcParams& p, int BN) {
+  p.BN = BN;
+  p.stages = tc_stages(BN);
+  p.tmem_cols = tc_tmem_cols(BN);
+}
+
+// dW reads Mg "transposed" (MN-major), whose swizzle atoms are 32 fp32 wide: N tiles are whole atoms.
+static int dw_bn(int64_t N) {
+  int64_t bn = (N + 31) / 32 * 32;
+  return (int)(bn > 256 ? 256 : bn);
+}
+
+static int dw_splits(int64_t M, int64_t F, int64_t N) {
+  const int BN = dw_bn(N);
+  const int64_t tiles = 2 * ((F + 127) / 128) * ((N + BN - 1) / BN);
+  int64_t Z = (2 * 148 + tiles - 1) / tiles;
+  const int64_t kb = (M + 31) / 32;
+  if (Z > kb) Z = kb;
+  if (Z < 1) Z = 1;
+  return (int)Z;
+}
+
+int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) { return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * N; }
+
+int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* WT_hi,
+                const float* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu) {
+  if (M <= 0) return 0;
+  TcParams p{};
+  const int BN = tc_bn(N);
+  tc_common(p, BN);
+  const int64_t Fp = (F + 31) / 32 * 32;
+  bool ok = tc_map_2d(&p.map_a0, Z, F, M, ldA, 32, 128) && tc_map_2d(&p.map_a1, D, F, M, ldA, 32, 128) &&
+            tc_map_2d(&p.map_b, WT_hi, 2 * Fp, N, 2 * Fp, 32, BN) && tc_map_2d(&p.map_b_lo, WT_lo, 2 * Fp, N, 2 * Fp, 32, BN);
+  if (!ok) return -1;
+  p.mode = TC_FWD;
+  p.n_ntiles = (int)((N + BN - 1) / BN);
+  p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
+  p.kb_seg0 = (int)(Fp / 32);
+  p.kb_total = 2 * p.kb_seg0;
+  p.M = (int)M;
+  p.N = (int)N;
+  p.F = (int)F;
+  p.ld_out = ldY;
+  p.out = Y;
+  p.bias = bias;
+  p.relu = relu;
+  if (L.count) *L.count += 1;
+  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+}
+
+int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* Wp_hi, const float* Wp_lo,
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld) {
+  if (M <= 0) return 0;
+  TcParams p{};
+  const int BN = tc_bn(F);
+  tc_common(p, BN);
+  bool ok = tc_map_2d(&p.map_a0, Mg, N, M, ldM, 32, 128) && tc_map_2d(&p.map_b, Wp_hi, N, 2 * F, Kp, 32, BN) &&
+            tc_map_2d(&p.map_b_lo, Wp_lo, N, 2 * F, Kp, 32, BN);
+  if (!ok) return -1;
+  p.mode = TC_DA;
+  p.n_ntiles_half = (int)((F + BN - 1) / BN);
+  p.n_ntiles = 2 * p.n_ntiles_half;
+  p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
+  p.kb_total = (int)((N + 31) / 32);
+  p.M = (int)M;
+  p.N = (int)N;
+  p.F = (int)F;
+  p.ld_out = 2 * ld;
+  p.ld_half = ld;
+  p.out = dA;
+  p.inv_deg = inv_deg;
+  if (L.count) *L.count += 1;
+  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+}
+
+int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats) {
+  const int64_t K = 2 * F + 1;
+  if (M <= 0) {
+    cudaMemsetAsync(G, 0, sizeof(float) * K * N, L.s);
+    return 0;
+  }
+  TcParams p{};
+  const int BN = dw_bn(N);
+  tc_common(p, BN);
+  const int Zs = dw_splits(M, F, N);
+  if ((int64_t)Zs * K * N > ws_floats) return -3;
+  bool ok = tc_map_2d(&p.map_a0, Z, F, M, ldA, 32, 32, true) && tc_map_2d(&p.map_a1, D, F, M, ldA, 32, 32, true) &&
+            tc_map_2d(&p.map_b, Mg, N, M, ldM, 32, 32, true);
+  if (!ok) return -1;
+  p.mode = TC_DW;
+  p.n_seg = 2;
+  p.n_ftiles = (int)((F + 127) / 128);
+  p.n_ntiles = (int)((N + BN - 1) / BN);
+  p.kb_total = (int)((M + 31) / 32);
+  p.kb_per_split = (p.kb_total + Zs - 1) / Zs;
+  const int Zeff = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.n_tiles = Zeff * p.n_seg * p.n_ftiles * p.n_ntiles;
+  p.M = (int)M;
+  p.N = (int)N;
+  p.F = (int)F;
+  p.K_out = (int)K;
+  p.out = ws;
+  if (tc_launch(p, L.s, 148) != cudaSuccess) return -2;
+  dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zeff);
+  tc::k_colsum<<<grid, block, 0, L.s>>>(Mg, M, ldM, (int)N, (int64_t)p.kb_per_split * 32, ws, K * N, 2 * F * N);
+  split_reduce(L, ws, Zeff, K * N, G);
+  if (L.count) *L.count += 2;
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace pgcn
+
+// ------------------------------------------------------------------------------------------------ diagnostics ABI
+namespace {
+int64_t r256(int64_t b) { return (b + 255) / 256 * 256; }
+}  // namespace
+
+extern "C" size_t pgcn_dev_gemm_scratch_bytes(int64_t M, int64_t F, int64_t N) {
+  const int64_t Fp = (F + 31) / 32 * 32, Kp = (N + 3) / 4 * 4;
+  int64_t ws = pgcn::tc_dw_ws_floats(M, F, N);
+  const int64_t ws2 = pgcn::gemm_dw_ws_floats(M, F, N);
+  if (ws2 > ws) ws = ws2;
+  return (size_t)(2 * r256(4 * N * 2 * Fp) + 2 * r256(4 * 2 * F * Kp) + r256(4 * ws));
+}
+
+extern "C" int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1, int64_t ldA, int64_t M,
+                             int64_t F, const float* W, int64_t N, const float* Mg, int64_t ldM, const float* inv_deg,
+                             float* out, int64_t ld_out, int32_t relu, void* scratch, size_t scratch_bytes,
+                             void* stream) {
+  using namespace pgcn;
+  if (op < 0 || op > 2 || (variant != 0 && variant != 2)) return fail(PGCN_EINVAL, "pgcn_dev_gemm: bad op/variant");
+  if (!out || !W || M < 0 || F < 1 || N < 1) return fail(PGCN_EINVAL, "pgcn_dev_gemm: bad shape/pointer");
+  if (scratch_bytes < pgcn_dev_gemm_scratch_bytes(M, F, N)) return fail(PGCN_ENOMEM, "pgcn_dev_gemm: scratch too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t Fp = (F + 31) / 32 * 32, Kp = (N + 3) / 4 * 4;
+  char* base = static_cast<char*>(scratch);
+  float* WT_hi = reinterpret_cast<float*>(base);
+  float* WT_lo = reinterpret_cast<float*>(base + r256(4 * N * 2 * Fp));
+  float* Wp_hi = reinterpret_cast<float*>(base + 2 * r256(4 * N * 2 * Fp));
+  float* Wp_lo = reinterpret_cast<float*>(base + 2 * r256(4 * N * 2 * Fp) + r256(4 * 2 * F * Kp));
+  float* ws = reinterpret_cast<float*>(base + 2 * r256(4 * N * 2 * Fp) + 2 * r256(4 * 2 * F * Kp));
+  const int64_t ws_floats = (int64_t)(scratch_bytes - (size_t)(2 * r256(4 * N * 2 * Fp) + 2 * r256(4 * 2 * F * Kp))) / 4;
+  Launch L{s, nullptr};
+  int rc = 0;
+  if (variant == 0) {
+    if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, WT_hi, WT_lo, Wp_hi, Wp_lo, s);
+    if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, WT_lo, W + 2 * F * N, N, out, ld_out, relu);
+    else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);
+    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2);
+  } else {
+    if (op == 0) gemm_fwd_f32(L, A0, A1, ldA, M, F, W, N, out, ld_out, relu);
+    else if (op == 1) gemm_dw_f32(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);
+    else gemm_da_f32(L, Mg, ldM, M, N, W, F, inv_deg, out, ld_out / 2);
+  }
+  if (rc) return fail(PGCN_ECUDA, "pgcn_dev_gemm: tensor-core path failed (%d)", rc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PGCN_ECUDA, "pgcn_dev_gemm: %s", cudaGetErrorString(e));
+  return PGCN_OK;
+}

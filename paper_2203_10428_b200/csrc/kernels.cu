@@ -86,128 +86,98 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 }
 
 // ---------------------------------------------------------------- SpMM forward (S3)
-// One group of G lanes per row; lane handles float4 columns lane + q*G (q < NC).  Neighbour
-// ids are loaded G at a time (coalesced) and broadcast with shuffles; U neighbour rows are in
-// flight per step.  Sums run in CSR order, then the row is scaled by inv_deg (reading R16).
-template <int G, int NC, int U>
-__global__ void __launch_bounds__(kThreads) k_spmm_fwd(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                                       const float* __restrict__ inv_deg, const float4* __restrict__ D,
-                                                       int64_t ld4, int64_t n_rows, int64_t n_valid, float4* __restrict__ Z) {
+// Work item = (row, chunk): a group of G lanes owns G float4 columns [chunk*G, chunk*G + G) of one
+// output row, so each lane keeps ONE float4 accumulator and U neighbour rows are in flight per
+// step (U*16 B outstanding per lane) -- wide rows (F = 602) become several independent items
+// instead of one register-heavy warp.  Neighbour ids are loaded G at a time (coalesced) and
+// broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
+template <int G, int U>
+__global__ void __launch_bounds__(kThreads, 4) k_spmm_fwd(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                          const float* __restrict__ inv_deg, const float4* __restrict__ D,
+                                                          int64_t ld4, int64_t n_rows, int64_t n_valid, int nchunk,
+                                                          float4* __restrict__ Z) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
+  const int64_t n_items = n_rows * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; row < n_rows; row += stride) {
-    float4 acc[NC];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
+    const int64_t row = it / nchunk;
+    const int64_t x = (it - row * nchunk) * G + lane;
+    const bool xin = x < ld4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = rp[row], end = rp[row + 1];
+    const float4* Dx = D + x;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
-        float4 v[U][NC];
+        float4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = __shfl_sync(gm, my, j + u, G);
-          const bool ok = c < n_valid;
-          const float4* src = D + (int64_t)c * ld4;
-#pragma unroll
-          for (int q = 0; q < NC; ++q) {
-            const int64_t x = lane + q * G;
-            v[u][q] = (ok && x < ld4) ? __ldg(src + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+          v[u] = (xin && c < n_valid) ? __ldg(Dx + (int64_t)c * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+        for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
       }
       for (; j < cnt; ++j) {
         const int c = __shfl_sync(gm, my, j, G);
-        if (c < n_valid) {
-          const float4* src = D + (int64_t)c * ld4;
-#pragma unroll
-          for (int q = 0; q < NC; ++q) {
-            const int64_t x = lane + q * G;
-            if (x < ld4) acc[q] = f4add(acc[q], __ldg(src + x));
-          }
-        }
+        if (xin && c < n_valid) acc = f4add(acc, __ldg(Dx + (int64_t)c * ld4));
       }
     }
-    const float s = inv_deg[row];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      const int64_t x = lane + q * G;
-      if (x < ld4) Z[row * ld4 + x] = f4scale(acc[q], s);
-    }
+    if (xin) Z[row * ld4 + x] = f4scale(acc, inv_deg[row]);
   }
 }
 
 // ---------------------------------------------------------------- transposed SpMM (S8)
-template <int G, int NC, int U>
-__global__ void __launch_bounds__(kThreads) k_spmm_bwd(const int64_t* __restrict__ trp, const int32_t* __restrict__ tcol,
-                                                       const float4* __restrict__ dZs, const float4* __restrict__ dDs,
-                                                       int64_t ldA4, int64_t n_in, int64_t n_all, float4* __restrict__ J,
-                                                       int64_t ld4, const int64_t* __restrict__ gid, DropSpec d) {
+template <int G, int U>
+__global__ void __launch_bounds__(kThreads, 4) k_spmm_bwd(const int64_t* __restrict__ trp, const int32_t* __restrict__ tcol,
+                                                          const float4* __restrict__ dZs, const float4* __restrict__ dDs,
+                                                          int64_t ldA4, int64_t n_in, int64_t n_all, int nchunk,
+                                                          float4* __restrict__ J, int64_t ld4,
+                                                          const int64_t* __restrict__ gid, DropSpec d) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
+  const int64_t n_items = n_all * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t u0 = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; u0 < n_all; u0 += stride) {
-    float4 acc[NC];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      const int64_t x = lane + q * G;
-      acc[q] = (u0 < n_in && x < ld4) ? dDs[u0 * ldA4 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
+    const int64_t u0 = it / nchunk;
+    const int64_t x = (it - u0 * nchunk) * G + lane;
+    const bool xin = x < ld4;
+    float4 acc = (u0 < n_in && xin) ? dDs[u0 * ldA4 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = trp[u0], end = trp[u0 + 1];
+    const float4* Sx = dZs + x;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
-        float4 v[U][NC];
+        float4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = __shfl_sync(gm, my, j + u, G);
-          const float4* src = dZs + (int64_t)c * ldA4;
-#pragma unroll
-          for (int q = 0; q < NC; ++q) {
-            const int64_t x = lane + q * G;
-            v[u][q] = x < ld4 ? __ldg(src + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+          v[u] = xin ? __ldg(Sx + (int64_t)c * ldA4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+        for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
       }
       for (; j < cnt; ++j) {
         const int c = __shfl_sync(gm, my, j, G);
-        const float4* src = dZs + (int64_t)c * ldA4;
-#pragma unroll
-        for (int q = 0; q < NC; ++q) {
-          const int64_t x = lane + q * G;
-          if (x < ld4) acc[q] = f4add(acc[q], __ldg(src + x));
-        }
+        if (xin) acc = f4add(acc, __ldg(Sx + (int64_t)c * ldA4));
       }
     }
+    if (!xin) continue;
     const int64_t g = gid[u0];
 #pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      const int64_t x = lane + q * G;
-      if (x >= ld4) continue;
-      float4 o = acc[q];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t c = 4 * x + j;
-        float val = comp(o, j);
-        if (c >= d.width) val = 0.f;
-        else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
-        set_comp(o, j, val);
-      }
-      J[u0 * ld4 + x] = o;
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = 4 * x + j;
+      float val = comp(acc, j);
+      if (c >= d.width) val = 0.f;
+      else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
+      set_comp(acc, j, val);
     }
+    J[u0 * ld4 + x] = acc;
   }
 }
 
@@ -550,31 +520,13 @@ __global__ void k_opt(const float* __restrict__ grads, int64_t P, float* __restr
 }
 
 // ---------------------------------------------------------------- SpMM dispatch
-struct Shape {
-  int G, NC;
-};
-Shape pick_shape(int64_t ld4) {
-  static const int Gs[] = {32, 16, 8, 4, 2};
-  static const int NCs[] = {1, 2, 3, 4, 5, 6, 8, 12, 16};
-  Shape best{32, 16};
-  int64_t best_waste = INT64_MAX;
-  for (int G : Gs) {
-    int64_t need = (ld4 + G - 1) / G;
-    int NC = -1;
-    for (int c : NCs)
-      if (c >= need) { NC = c; break; }
-    if (NC < 0) continue;
-    int64_t waste = (int64_t)G * NC - ld4;
-    if (waste < best_waste) { best_waste = waste; best = {G, NC}; }
-  }
-  return best;
+// Lanes per (row, chunk) item: 32 for rows of >= 24 float4, else the next power of two >= ld4.
+int pick_group(int64_t ld4) {
+  if (ld4 >= 24) return 32;
+  int g = 4;
+  while (g < ld4) g *= 2;
+  return g;
 }
-
-template <int G, int NC>
-constexpr int unroll_for() { return NC <= 1 ? 8 : NC <= 2 ? 4 : NC <= 4 ? 2 : 1; }
-
-#define PGCN_NC_LIST(X, G) X(G, 1) X(G, 2) X(G, 3) X(G, 4) X(G, 5) X(G, 6) X(G, 8) X(G, 12) X(G, 16)
-#define PGCN_G_LIST(X) PGCN_NC_LIST(X, 32) PGCN_NC_LIST(X, 16) PGCN_NC_LIST(X, 8) PGCN_NC_LIST(X, 4) PGCN_NC_LIST(X, 2)
 
 }  // namespace
 
@@ -595,18 +547,17 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
               int64_t n_rows, int64_t n_valid, float* Z) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
-  const Shape sh = pick_shape(ld4);
-  const int rows_per_block = kThreads / sh.G;
-  const int grid = grid_for(n_rows, rows_per_block, kSMs * 64);
+  const int G = pick_group(ld4);
+  const int nchunk = (int)((ld4 + G - 1) / G);
+  const int grid = grid_for(n_rows * nchunk, kThreads / G, kSMs * 64);
   auto D4 = reinterpret_cast<const float4*>(D);
   auto Z4 = reinterpret_cast<float4*>(Z);
-#define X(G_, NC_)                                                                                              \
-  if (sh.G == G_ && sh.NC == NC_) {                                                                            \
-    k_spmm_fwd<G_, NC_, unroll_for<G_, NC_>()><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, \
-                                                                           n_valid, Z4);                         \
-  } else
-  PGCN_G_LIST(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape\n"); }
-#undef X
+  switch (G) {
+    case 32: k_spmm_fwd<32, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
+    case 16: k_spmm_fwd<16, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
+    case 8: k_spmm_fwd<8, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
+    default: k_spmm_fwd<4, 4><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
+  }
   count(L);
 }
 
@@ -615,19 +566,19 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
               const DropSpec& d) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
-  const Shape sh = pick_shape(ld4);
-  const int rows_per_block = kThreads / sh.G;
-  const int grid = grid_for(n_all, rows_per_block, kSMs * 64);
+  const int G = pick_group(ld4);
+  const int nchunk = (int)((ld4 + G - 1) / G);
+  const int grid = grid_for(n_all * nchunk, kThreads / G, kSMs * 64);
   auto a = reinterpret_cast<const float4*>(dZs);
   auto b = reinterpret_cast<const float4*>(dDs);
   auto J4 = reinterpret_cast<float4*>(J);
-#define X(G_, NC_)                                                                                             \
-  if (sh.G == G_ && sh.NC == NC_) {                                                                           \
-    k_spmm_bwd<G_, NC_, unroll_for<G_, NC_>()><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, ld_dA / 4,  \
-                                                                           n_in, n_all, J4, ld4, gid, d);       \
-  } else
-  PGCN_G_LIST(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape\n"); }
-#undef X
+  const int64_t lda4 = ld_dA / 4;
+  switch (G) {
+    case 32: k_spmm_bwd<32, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
+    case 16: k_spmm_bwd<16, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
+    case 8: k_spmm_bwd<8, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
+    default: k_spmm_bwd<4, 4><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
+  }
   count(L);
 }
 
@@ -707,6 +658,11 @@ void gemm_dw_f32(Launch L, const float* Z, const float* D, int64_t ldA, int64_t 
   k_gemm_dw<<<grid, 256, 0, L.s>>>(Z, D, ldA, M, F, Mg, ldM, N, rps, ws);
   k_split_reduce<<<grid_for(K * N, kThreads), kThreads, 0, L.s>>>(ws, splits, K * N, G);
   count(L, 2);
+}
+
+void split_reduce(Launch L, const float* part, int64_t splits, int64_t len, float* G) {
+  k_split_reduce<<<grid_for(len, kThreads), kThreads, 0, L.s>>>(part, splits, len, G);
+  count(L);
 }
 
 void gemm_da_f32(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* W, int64_t F,

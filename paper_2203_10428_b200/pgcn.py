@@ -95,6 +95,10 @@ def lib():
         L.pgcn_timing_enable.argtypes = [vp, i32]
         L.pgcn_timing_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.pgcn_dev_gemm_scratch_bytes.argtypes = [i64, i64, i64]
+        L.pgcn_dev_gemm_scratch_bytes.restype = C.c_size_t
+        L.pgcn_dev_gemm.argtypes = [i32, i32, vp, vp, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, i32, vp,
+                                    C.c_size_t, vp]
         if hasattr(L, "pgcn_nccl_get_unique_id"):
             L.pgcn_nccl_get_unique_id.argtypes = [vp]
             L.pgcn_nccl_id_bytes.restype = i32
@@ -171,7 +175,7 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partit
 
 # ------------------------------------------------------------------------------------------- config
 def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
-                ema_init="first", dropout=0.0, seed=4, gemm="fp32", loss="ce", n_global=0, n_train_global=1,
+                ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
@@ -181,7 +185,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.smooth_f, c.smooth_g = int(bool(smooth_f)), int(bool(smooth_g))
     c.ema_init = {"first": 0, "zero": 1}[ema_init]
     c.gamma, c.dropout, c.seed = float(gamma), float(dropout), int(seed)
-    c.gemm = {"fp32": 0, "bf16": 1}[gemm]
+    c.gemm = {"tc": 0, "fp32": 0, "bf16": 1, "simt": 2}[gemm]
     c.loss = {"ce": 0, "bce": 1}[loss]
     c.n_global, c.n_train_global = int(n_global), int(n_train_global)
     c.opt = {"sgd": 0, "adam": 1}[opt]
@@ -289,3 +293,19 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------------------------------- diagnostics
+def dev_gemm(op, variant, A0, A1, M, F, W_ext, N, out, ld_out, Mg=None, inv_deg=None, relu=False, stream=None):
+    """pgcn_dev_gemm (include/pgcn_dev.h): one node-update GEMM on torch CUDA tensors."""
+    import torch
+    nb = int(lib().pgcn_dev_gemm_scratch_bytes(int(M), int(F), int(N)))
+    scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=out.device)
+    st = stream if stream is not None else torch.cuda.current_stream(out.device)
+    ldA = A0.stride(0) if A0 is not None else 0
+    ldM = Mg.stride(0) if Mg is not None else 0
+    variant = {"tc": 0, "simt": 2}.get(variant, variant)
+    _check(lib().pgcn_dev_gemm(int(op), int(variant), _ptr(A0), _ptr(A1), int(ldA), int(M), int(F), _ptr(W_ext),
+                               int(N), _ptr(Mg), int(ldM), _ptr(inv_deg), _ptr(out), int(ld_out), int(bool(relu)),
+                               scratch.data_ptr(), scratch.numel(), st.cuda_stream))
+    return scratch

@@ -1,0 +1,86 @@
+"""GPU unit tests of the node-update GEMMs (include/pgcn_dev.h) against float64 numpy matmul of the
+same fp32 inputs.  Tolerance: the fp32 tier, max|gpu - ref| <= 1e-4 * max|ref| (3xTF32 tensor
+cores and SIMT fp32 alike)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+SHAPES = [(300, 37, 16), (1000, 602, 256), (513, 256, 41), (700, 300, 512), (129, 16, 7), (4096, 128, 48)]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    from paper_2203_10428_b200 import build, pgcn
+    build.build()
+    return pgcn
+
+
+def ld(f):
+    return (f + 3) // 4 * 4
+
+
+def mk(M, F, N, seed):
+    rng = np.random.default_rng(seed)
+    A0 = np.zeros((M, ld(F)), np.float32)
+    A1 = np.zeros((M, ld(F)), np.float32)
+    A0[:, :F] = rng.standard_normal((M, F))
+    A1[:, :F] = rng.standard_normal((M, F))
+    W = rng.standard_normal((2 * F + 1, N)).astype(np.float32) * 0.1
+    Mg = np.zeros((M, ld(N)), np.float32)
+    Mg[:, :N] = rng.standard_normal((M, N))
+    inv = (1.0 / rng.integers(1, 50, M)).astype(np.float32)
+    return A0, A1, W, Mg, inv
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+@pytest.mark.parametrize("variant", ["tc", "simt"])
+@pytest.mark.parametrize("M,F,N", SHAPES)
+def test_forward(P, variant, M, F, N):
+    import torch
+    A0, A1, W, _, _ = mk(M, F, N, 1)
+    out = torch.full((M, ld(N)), 7.0, device="cuda")
+    t = [torch.tensor(x).cuda() for x in (A0, A1, W)]
+    P.dev_gemm(0, variant, t[0], t[1], M, F, t[2], N, out, ld(N), relu=True)
+    torch.cuda.synchronize()
+    A = np.hstack([A0[:, :F], A1[:, :F], np.ones((M, 1), np.float32)]).astype(np.float64)
+    ref = np.maximum(A @ W.astype(np.float64), 0)
+    got = out.cpu().numpy()
+    assert rel(got[:, :N], ref) <= 1e-4
+    assert (got[:, N:] == 0).all()
+
+
+@pytest.mark.parametrize("variant", ["tc", "simt"])
+@pytest.mark.parametrize("M,F,N", SHAPES)
+def test_weight_gradient(P, variant, M, F, N):
+    import torch
+    A0, A1, W, Mg, _ = mk(M, F, N, 2)
+    out = torch.zeros((2 * F + 1, N), device="cuda")
+    t = [torch.tensor(x).cuda() for x in (A0, A1, W, Mg)]
+    P.dev_gemm(1, variant, t[0], t[1], M, F, t[2], N, out, N, Mg=t[3])
+    torch.cuda.synchronize()
+    A = np.hstack([A0[:, :F], A1[:, :F], np.ones((M, 1), np.float32)]).astype(np.float64)
+    ref = A.T @ Mg[:, :N].astype(np.float64)
+    assert rel(out.cpu().numpy(), ref) <= 1e-4
+
+
+@pytest.mark.parametrize("variant", ["tc", "simt"])
+@pytest.mark.parametrize("M,F,N", SHAPES)
+def test_input_gradient(P, variant, M, F, N):
+    import torch
+    A0, A1, W, Mg, inv = mk(M, F, N, 3)
+    L = ld(F)
+    out = torch.full((M, 2 * L), 7.0, device="cuda")
+    t = [torch.tensor(x).cuda() for x in (W, Mg, inv)]
+    P.dev_gemm(2, variant, None, None, M, F, t[0], N, out, 2 * L, Mg=t[1], inv_deg=t[2])
+    torch.cuda.synchronize()
+    dA = Mg[:, :N].astype(np.float64) @ W[:2 * F].astype(np.float64).T
+    got = out.cpu().numpy()
+    assert rel(got[:, :F], dA[:, :F] * inv[:, None]) <= 1e-4
+    assert rel(got[:, L:L + F], dA[:, F:]) <= 1e-4
+    assert (got[:, F:L] == 0).all() and (got[:, L + F:] == 0).all()
