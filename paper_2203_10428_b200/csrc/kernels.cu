@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -86,98 +87,129 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 }
 
 // ---------------------------------------------------------------- SpMM forward (S3)
-// Work item = (row, chunk): a group of G lanes owns G float4 columns [chunk*G, chunk*G + G) of one
-// output row, so each lane keeps ONE float4 accumulator and U neighbour rows are in flight per
-// step (U*16 B outstanding per lane) -- wide rows (F = 602) become several independent items
-// instead of one register-heavy warp.  Neighbour ids are loaded G at a time (coalesced) and
-// broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
-template <int G, int U>
-__global__ void __launch_bounds__(kThreads, 4) k_spmm_fwd(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                                          const float* __restrict__ inv_deg, const float4* __restrict__ D,
-                                                          int64_t ld4, int64_t n_rows, int64_t n_valid, int nchunk,
-                                                          float4* __restrict__ Z) {
+// Work item = (row, chunk): a group of G lanes owns NC*G float4 columns of one output row (for
+// every width used here one chunk covers the whole row) and keeps NC float4 accumulators; U
+// neighbour rows are in flight per step, so each lane has NC*U 16-byte loads outstanding.  The
+// (G, NC, U) table in spmm_shape() was measured with tools/spmm_lab.py on B200 (whole row per
+// group, ~8 loads in flight).  Neighbour ids are loaded G at a time (coalesced)
+// and broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
+template <int G, int NC, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __restrict__ rp,
+                                                             const int32_t* __restrict__ col,
+                                                             const float* __restrict__ inv_deg,
+                                                             const float4* __restrict__ D, int64_t ld4, int64_t n_rows,
+                                                             int64_t n_valid, int nchunk, float4* __restrict__ Z) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
     const int64_t row = it / nchunk;
-    const int64_t x = (it - row * nchunk) * G + lane;
-    const bool xin = x < ld4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
+    float4 acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = rp[row], end = rp[row + 1];
-    const float4* Dx = D + x;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
-        float4 v[U];
+        float4 v[U][NC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = __shfl_sync(gm, my, j + u, G);
-          v[u] = (xin && c < n_valid) ? __ldg(Dx + (int64_t)c * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const bool ok = c < n_valid;
+          const float4* src = D + (int64_t)c * ld4 + x0;
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = (ok && x0 + q * G < ld4) ? __ldg(src + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
       }
       for (; j < cnt; ++j) {
         const int c = __shfl_sync(gm, my, j, G);
-        if (xin && c < n_valid) acc = f4add(acc, __ldg(Dx + (int64_t)c * ld4));
+        if (c < n_valid) {
+          const float4* src = D + (int64_t)c * ld4 + x0;
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            if (x0 + q * G < ld4) acc[q] = f4add(acc[q], __ldg(src + q * G));
+        }
       }
     }
-    if (xin) Z[row * ld4 + x] = f4scale(acc, inv_deg[row]);
+    const float s = inv_deg[row];
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (x0 + q * G < ld4) Z[row * ld4 + x0 + q * G] = f4scale(acc[q], s);
   }
 }
 
 // ---------------------------------------------------------------- transposed SpMM (S8)
-template <int G, int U>
-__global__ void __launch_bounds__(kThreads, 4) k_spmm_bwd(const int64_t* __restrict__ trp, const int32_t* __restrict__ tcol,
-                                                          const float4* __restrict__ dZs, const float4* __restrict__ dDs,
-                                                          int64_t ldA4, int64_t n_in, int64_t n_all, int nchunk,
-                                                          float4* __restrict__ J, int64_t ld4,
-                                                          const int64_t* __restrict__ gid, DropSpec d) {
+template <int G, int NC, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __restrict__ trp,
+                                                             const int32_t* __restrict__ tcol,
+                                                             const float4* __restrict__ dZs,
+                                                             const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
+                                                             int64_t n_all, int nchunk, float4* __restrict__ J,
+                                                             int64_t ld4, const int64_t* __restrict__ gid, DropSpec d) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
     const int64_t u0 = it / nchunk;
-    const int64_t x = (it - u0 * nchunk) * G + lane;
-    const bool xin = x < ld4;
-    float4 acc = (u0 < n_in && xin) ? dDs[u0 * ldA4 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
+    float4 acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      acc[q] = (u0 < n_in && x0 + q * G < ld4) ? dDs[u0 * ldA4 + x0 + q * G] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = trp[u0], end = trp[u0 + 1];
-    const float4* Sx = dZs + x;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
-        float4 v[U];
+        float4 v[U][NC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = __shfl_sync(gm, my, j + u, G);
-          v[u] = xin ? __ldg(Sx + (int64_t)c * ldA4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4* src = dZs + (int64_t)c * ldA4 + x0;
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = x0 + q * G < ld4 ? __ldg(src + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
       }
       for (; j < cnt; ++j) {
         const int c = __shfl_sync(gm, my, j, G);
-        if (xin) acc = f4add(acc, __ldg(Sx + (int64_t)c * ldA4));
+        const float4* src = dZs + (int64_t)c * ldA4 + x0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+          if (x0 + q * G < ld4) acc[q] = f4add(acc[q], __ldg(src + q * G));
       }
     }
-    if (!xin) continue;
     const int64_t g = gid[u0];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t c = 4 * x + j;
-      float val = comp(acc, j);
-      if (c >= d.width) val = 0.f;
-      else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
-      set_comp(acc, j, val);
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = x0 + q * G;
+      if (x >= ld4) continue;
+      float4 o = acc[q];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = 4 * x + j;
+        float val = comp(o, j);
+        if (c >= d.width) val = 0.f;
+        else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
+        set_comp(o, j, val);
+      }
+      J[u0 * ld4 + x] = o;
     }
-    J[u0 * ld4 + x] = acc;
   }
 }
 
@@ -520,12 +552,56 @@ __global__ void k_opt(const float* __restrict__ grads, int64_t P, float* __restr
 }
 
 // ---------------------------------------------------------------- SpMM dispatch
-// Lanes per (row, chunk) item: 32 for rows of >= 24 float4, else the next power of two >= ld4.
-int pick_group(int64_t ld4) {
-  if (ld4 >= 24) return 32;
-  int g = 4;
-  while (g < ld4) g *= 2;
-  return g;
+// (G, NC, U, min blocks/SM) per row width, measured in the full Reddit-shaped step on B200
+// (tools/spmm_sweep.sh; tools/spmm_lab.py for the isolated kernel): rows of <= 32 float4 use one
+// lane per float4 (G = next pow2, NC = 1, U = 8); wider rows use 32 lanes and NC = ceil(ld4/32)
+// float4 per lane, U ~ 8/NC rows in flight (whole row per warp); register caps chosen for 3-4
+// resident blocks (NC = 5: 3 blocks beat 2 by 15%; NC = 2: 4 blocks).
+struct SpmmShape {
+  int G, NC, U, MB, nchunk;
+};
+// Dev knob (not part of the ABI): PGCN_SPMM_TABLE="ld4=G,NC,U,MB;..." overrides the table for the
+// listed widths (used by the in-situ sweep in tools/; an unknown combination falls back).
+bool spmm_override(int64_t ld4, SpmmShape& s) {
+  const char* e = std::getenv("PGCN_SPMM_TABLE");
+  if (!e) return false;
+  const char* p = e;
+  while (*p) {
+    long long w;
+    int g, nc, u, mb, n = 0;
+    if (std::sscanf(p, "%lld=%d,%d,%d,%d%n", &w, &g, &nc, &u, &mb, &n) == 5) {
+      if (w == ld4) {
+        s = SpmmShape{g, nc, u, mb, (int)((ld4 + (int64_t)g * nc - 1) / ((int64_t)g * nc))};
+        return true;
+      }
+      p += n;
+    } else {
+      break;
+    }
+    while (*p == ';' || *p == ' ') ++p;
+  }
+  return false;
+}
+
+SpmmShape spmm_shape(int64_t ld4) {
+  SpmmShape s{32, 1, 8, 4, 1};
+  if (spmm_override(ld4, s)) return s;
+  if (ld4 <= 32) {
+    int g = 4;
+    while (g < ld4) g *= 2;
+    s.G = g;
+    return s;
+  }
+  int64_t nc = (ld4 + 31) / 32;
+  static const int NCs[] = {2, 3, 4, 5, 6, 8, 12, 16};
+  int pick = 16;
+  for (int c : NCs)
+    if (c >= nc) { pick = c; break; }
+  s.NC = pick;
+  s.U = pick == 2 ? 4 : (pick <= 4 ? 2 : 1);
+  s.MB = pick == 2 ? 4 : (pick <= 6 ? 3 : (pick <= 8 ? 2 : 1));
+  s.nchunk = (int)((ld4 + 32 * pick - 1) / (32 * pick));
+  return s;
 }
 
 }  // namespace
@@ -543,21 +619,26 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
   count(L);
 }
 
+#define PGCN_SPMM_CASES(X)                                                                                     \
+  X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
+  X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
+  X(32, 4, 2, 3)
+
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
-  const int G = pick_group(ld4);
-  const int nchunk = (int)((ld4 + G - 1) / G);
-  const int grid = grid_for(n_rows * nchunk, kThreads / G, kSMs * 64);
+  const SpmmShape sh = spmm_shape(ld4);
+  const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
   auto D4 = reinterpret_cast<const float4*>(D);
   auto Z4 = reinterpret_cast<float4*>(Z);
-  switch (G) {
-    case 32: k_spmm_fwd<32, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
-    case 16: k_spmm_fwd<16, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
-    case 8: k_spmm_fwd<8, 8><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
-    default: k_spmm_fwd<4, 4><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, nchunk, Z4); break;
-  }
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    k_spmm_fwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid,   \
+                                                             sh.nchunk, Z4);                                   \
+  } else
+  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); }
+#undef X
   count(L);
 }
 
@@ -566,19 +647,19 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
               const DropSpec& d) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
-  const int G = pick_group(ld4);
-  const int nchunk = (int)((ld4 + G - 1) / G);
-  const int grid = grid_for(n_all * nchunk, kThreads / G, kSMs * 64);
+  const SpmmShape sh = spmm_shape(ld4);
+  const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
   auto a = reinterpret_cast<const float4*>(dZs);
   auto b = reinterpret_cast<const float4*>(dDs);
   auto J4 = reinterpret_cast<float4*>(J);
   const int64_t lda4 = ld_dA / 4;
-  switch (G) {
-    case 32: k_spmm_bwd<32, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
-    case 16: k_spmm_bwd<16, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
-    case 8: k_spmm_bwd<8, 8><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
-    default: k_spmm_bwd<4, 4><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, nchunk, J4, ld4, gid, d); break;
-  }
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
+                                                             sh.nchunk, J4, ld4, gid, d);                      \
+  } else
+  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); }
+#undef X
   count(L);
 }
 
