@@ -100,6 +100,17 @@ def peaks():
                 "_fallback": True}
 
 
+def max_over_ranks(x, dist):
+    """Device-timed milliseconds -> the max over ranks (the slowest rank sets the epoch time)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def build_workload(name, n_parts):
     from synth.graphs import CONFIGS, gen_graph, glorot_params, model_for
     t0 = time.time()
@@ -173,11 +184,19 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1 or args.gpus > 1:
-        raise SystemExit("multi-GPU bench needs the NCCL transport (not built in this version)")
-    dev = 0
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = local_rank
     torch.cuda.set_device(dev)
-    parts = args.parts or max(2, args.gpus)
+    # N = 1: the configuration's partitions hosted on one GPU (local transport); N > 1: one
+    # partition per GPU (NCCL transport), n_parts = N.
+    parts = args.parts or (max(2, args.gpus) if world == 1 else world)
+    if world > 1 and parts != world:
+        raise SystemExit("multi-GPU runs host one partition per rank (--parts must equal WORLD_SIZE)")
     g, m, params0, t_gen = build_workload(args.config, parts)
     t0 = time.time()
     part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
@@ -186,9 +205,11 @@ def main():
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
                            n_train_global=g.n_train, gemm=args.gemm)
     stream = torch.cuda.Stream()
+    local_parts = list(range(parts)) if world == 1 else [rank]
+    comm = pgcn.nccl_comm(rank, world) if world > 1 else None
     with torch.cuda.stream(stream):
-        ctx = pgcn.Context(part, cfg, stream=stream)
-    views = [part.view(i) for i in range(parts)]
+        ctx = pgcn.Context(part, cfg, local_parts=local_parts, comm=comm, stream=stream)
+    views = [part.view(i) for i in local_parts]
     host = []
     for i, v in enumerate(views):
         gid = v["inner_gid"]
@@ -198,7 +219,8 @@ def main():
         host.append((X, lab, tm))
     dev_in = [tuple(a.cuda(non_blocking=True) for a in h) for h in host]
     torch.cuda.synchronize()
-    for i in range(parts):
+    nloc = len(local_parts)
+    for i in range(nloc):
         ctx.set_inputs(i, *dev_in[i])
     theta = torch.tensor(pgcn.flatten_params(params0), device="cuda")
     grads = torch.zeros_like(theta)
@@ -217,13 +239,18 @@ def main():
     ctx.timing_enable(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+        torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(K):
         t += 1
         ctx.step(t, theta, grads, opt, loss)
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms_total = ev0.elapsed_time(ev1)
+    if dist is not None:
+        dist.barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1), dist)
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
     kern = {name: ctx.timing_read(k) for k, name in enumerate(pgcn.KERNELS)}
@@ -242,7 +269,7 @@ def main():
         ev0.record(stream)
         for _ in range(K):
             t += 1
-            for i in range(parts):
+            for i in range(nloc):
                 ctx.set_inputs(i, *host[i])
             ctx.step(t, theta, grads, opt, loss)
             with torch.cuda.stream(stream):
@@ -250,7 +277,7 @@ def main():
             stream.synchronize()
         ev1.record(stream)
         torch.cuda.synchronize()
-        e_ms = ev0.elapsed_time(ev1) / K
+        e_ms = max_over_ranks(ev0.elapsed_time(ev1), dist) / K
         e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
                "ms_per_step": e_ms, "host_wall_ms_per_step": 1000.0 * (time.perf_counter() - e0) / K}
 
@@ -280,18 +307,22 @@ def main():
                      "TFLOPs": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None}
                  for k, v in kern.items() if v["launches"]}
     cpu = None
-    if not args.no_cpu and rank == 0:
+    if not args.no_cpu and world == 1:
         try:
             cpu = cpu_baseline(args.config, parts, args.mode, args.smooth)
         except Exception as e:  # noqa: BLE001
             cpu = {"error": str(e)}
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms,
+    if rank != 0:
+        return
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU (local transport), %s%s, "
-                                  "dropout %.1f, Adam" % (args.config, g.n, g.nnz, m.widths, parts, 1, args.mode,
+           "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU(s), %s%s, "
+                                  "dropout %.1f, Adam" % (args.config, g.n, g.nnz, m.widths, parts, world, args.mode,
                                                           ("-" + args.smooth.upper()) if args.smooth else "",
                                                           m.dropout),
-                      "global_batch": g.n, "parallelism": "partition x%d" % parts, "gemm": args.gemm,
+                      "global_batch": g.n,
+                      "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
+                      ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "breakdown": breakdown, "loss": loss_v,

@@ -170,6 +170,11 @@ typedef struct {
   const void* nccl_id_reduce;
 } pgcn_comm;
 
+/* NCCL bootstrap: size of an ncclUniqueId (0 if the library was built without NCCL) and a fresh
+ * id written to out (rank 0 calls it; the caller broadcasts the bytes to every rank).          */
+int pgcn_nccl_id_bytes(void);
+int pgcn_nccl_unique_id(void* out);
+
 typedef struct pgcn_ctx pgcn_ctx;
 
 /* Workspace bytes for hosting partitions local_parts[0..n_local) of p under cfg. */

@@ -25,6 +25,9 @@
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "pgcn.h"
+#ifdef PGCN_WITH_NCCL
+#include <nccl.h>
+#endif
 
 namespace pgcn {
 
@@ -97,9 +100,33 @@ struct pgcn_ctx {
   int64_t launches = 0;
   int timing = 0;
   pgcn::KTimer kt[PGCN_K_COUNT];
+  // ---- NCCL transport (one partition per rank)
+  int nccl = 0, rank = 0, nranks = 1;
+#ifdef PGCN_WITH_NCCL
+  ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
+#endif
+  cudaStream_t cs = nullptr;              // comm stream (high priority)
+  cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
+  cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][2] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][2] = {};
+  float* send_f[PGCN_MAX_LAYERS + 1] = {};     // packed S_{i,j} rows of the layer-l input
+  float* recv_f[PGCN_MAX_LAYERS + 1] = {};     // received boundary rows (EMA-F only)
+  float* recv_b[PGCN_MAX_LAYERS + 1][2] = {};  // received gradient rows, send order, parity
   ~pgcn_ctx() {
     for (auto& k : kt)
       for (auto e : k.ev) cudaEventDestroy(e);
+    for (int l = 0; l <= PGCN_MAX_LAYERS; ++l) {
+      if (ev_f_pack[l]) cudaEventDestroy(ev_f_pack[l]);
+      if (ev_b_ready[l]) cudaEventDestroy(ev_b_ready[l]);
+      for (int b = 0; b < 2; ++b) {
+        if (ev_f_done[l][b]) cudaEventDestroy(ev_f_done[l][b]);
+        if (ev_b_done[l][b]) cudaEventDestroy(ev_b_done[l][b]);
+      }
+    }
+#ifdef PGCN_WITH_NCCL
+    if (ch) ncclCommDestroy(ch);
+    if (cr) ncclCommDestroy(cr);
+#endif
+    if (cs) cudaStreamDestroy(cs);
   }
 };
 
@@ -180,6 +207,15 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   }
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
+  if (C->nccl && n_local == 1) {
+    const PartCtx& p = C->parts[0];
+    for (int l = 1; l <= L; ++l) {
+      C->send_f[l] = A.take<float>(p.n_send * C->ld[l - 1]);
+      if (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2) C->recv_f[l] = A.take<float>(p.n_bd * C->ld[l - 1]);
+      if (l >= 2)
+        for (int b = 0; b < 2; ++b) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
+    }
+  }
   if (C->cfg.gemm == 0) {
     for (int l = 1; l <= L; ++l) {
       C->Fp[l] = round_up(C->F[l - 1], 32);
@@ -195,7 +231,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
 }
 
 int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local,
-                    const pgcn_config* cfg) {
+                    const pgcn_config* cfg, const pgcn_comm* comm) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if (!part) return fail(PGCN_EINVAL, "partition is NULL");
@@ -203,10 +239,24 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   pgcn_part_view v0;
   rc = pgcn_partition_view(part, local[0], &v0);
   if (rc) return rc;
-  if (n_local != v0.n_parts)
-    return fail(PGCN_EUNSUPPORTED, "this build hosts all %d partitions in one context (got %d)", v0.n_parts, n_local);
-  for (int i = 0; i < n_local; ++i)
-    if (local[i] != i) return fail(PGCN_EINVAL, "local_parts must be 0..n_parts-1 in order");
+  if (comm && comm->nranks > 1) {
+#ifndef PGCN_WITH_NCCL
+    return fail(PGCN_EUNSUPPORTED, "library built without NCCL");
+#else
+    if (comm->nranks != v0.n_parts || n_local != 1 || local[0] != comm->rank || comm->rank < 0 ||
+        comm->rank >= comm->nranks)
+      return fail(PGCN_EUNSUPPORTED, "multi-process runs host exactly partition `rank` of n_parts == nranks");
+    if (!comm->nccl_id_halo || !comm->nccl_id_reduce) return fail(PGCN_EINVAL, "NCCL unique ids missing");
+    C->nccl = 1;
+    C->rank = comm->rank;
+    C->nranks = comm->nranks;
+#endif
+  } else {
+    if (n_local != v0.n_parts)
+      return fail(PGCN_EUNSUPPORTED, "a single-process context hosts all %d partitions (got %d)", v0.n_parts, n_local);
+    for (int i = 0; i < n_local; ++i)
+      if (local[i] != i) return fail(PGCN_EINVAL, "local_parts must be 0..n_parts-1 in order");
+  }
   if (cfg->n_global != pgcn_partition_n_nodes(part)) return fail(PGCN_EINVAL, "cfg.n_global != partition N");
   C->cfg = *cfg;
   C->L = cfg->n_layers;
@@ -305,6 +355,103 @@ struct Scope {
   }
 };
 
+#ifdef PGCN_WITH_NCCL
+int nccl_fail(pgcn_ctx* C, ncclResult_t r, const char* where) {
+  C->poisoned = 1;
+  return fail(PGCN_ENCCL, "%s: %s", where, ncclGetErrorString(r));
+}
+
+// Alg. 1 l.9-13 over NCCL (one partition per rank).  PIPE: wait for the exchange posted at t-1
+// (and smooth it, Sec. 3.4), then post this iteration's exchange, consumed at t+1; the receive
+// lands directly in the boundary rows of the next parity buffer.  VANILLA: post and wait.
+int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, const Launch& Lk, int64_t* n_valid) {
+  const bool pipe = C->cfg.mode == 1;
+  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int64_t ldi = C->ld[l - 1];
+  *n_valid = p.n_all;
+  if (pipe && t >= 2) {
+    if (l == 1) {
+      cudaStreamWaitEvent(C->s, C->ev_f_done[1][1], 0);  // X boundary rows, received at t = 1 (R10)
+    } else {
+      cudaStreamWaitEvent(C->s, C->ev_f_done[l][bp], 0);
+      if (C->cfg.smooth_f && p.n_bd > 0) {
+        SegTable src{};
+        src.n_seg = 1;
+        src.off[1] = p.n_bd;
+        src.base[0] = C->recv_f[l];
+        const bool first = C->cfg.ema_init == 0 && t == 2;
+        Scope sc(C, PGCN_K_GATHER, 12.0 * C->F[l - 1] * p.n_bd);
+        gather_rows(Lk, src, nullptr, p.n_bd, ldi, Hin + p.n_in * ldi, p.H[l - 1][bp] + p.n_in * ldi,
+                    (float)C->cfg.gamma, 1, first);
+      }
+    }
+  }
+  if (l == 1 ? t == 1 : true) {
+    if (p.n_send > 0) {
+      SegTable src{};
+      src.n_seg = 1;
+      src.off[1] = p.n_send;
+      src.base[0] = Hin;
+      Scope sc(C, PGCN_K_GATHER, 8.0 * C->F[l - 1] * p.n_send + 4.0 * p.n_send);
+      gather_rows(Lk, src, p.send_idx, p.n_send, ldi, C->send_f[l], nullptr, 0.f, 0, 0);
+    }
+    cudaEventRecord(C->ev_f_pack[l], C->s);
+    cudaStreamWaitEvent(C->cs, C->ev_f_pack[l], 0);
+    float* dst;
+    if (l == 1) dst = p.X + p.n_in * ldi;
+    else if (!pipe) dst = p.H[l - 1][b] + p.n_in * ldi;
+    else if (C->cfg.smooth_f) dst = C->recv_f[l];
+    else dst = p.H[l - 1][(t + 1) & 1] + p.n_in * ldi;
+    ncclResult_t r = ncclGroupStart();
+    for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
+      if (j == C->rank) continue;
+      const int64_t ns = p.v.send_off[j + 1] - p.v.send_off[j], nr = p.v.halo_off[j + 1] - p.v.halo_off[j];
+      if (ns) r = ncclSend(C->send_f[l] + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
+      if (nr && r == ncclSuccess)
+        r = ncclRecv(dst + p.v.halo_off[j] * ldi, (size_t)(nr * ldi), ncclFloat, j, C->ch, C->cs);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(C, r != ncclSuccess ? r : r2, "halo exchange (fwd)");
+    cudaEventRecord(C->ev_f_done[l][b], C->cs);
+    if (!pipe) cudaStreamWaitEvent(C->s, C->ev_f_done[l][b], 0);
+  }
+  if (pipe && l == 1 && t == 1) *n_valid = p.n_in;  // X boundary rows not installed yet: zero (l.6)
+  return PGCN_OK;
+}
+
+// Alg. 1 l.22-27 over NCCL: post the boundary-row gradients of J^(l-1) (parity t) to their owners
+// and return the message table to accumulate now (PIPE: the one received at t-1).
+int nccl_bwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, SegTable& msg, bool& have) {
+  const bool pipe = C->cfg.mode == 1;
+  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int64_t ldi = C->ld[l - 1];
+  const float* J = p.J[l - 1][b];
+  cudaEventRecord(C->ev_b_ready[l], C->s);
+  cudaStreamWaitEvent(C->cs, C->ev_b_ready[l], 0);
+  ncclResult_t r = ncclGroupStart();
+  for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
+    if (j == C->rank) continue;
+    const int64_t nh = p.v.halo_off[j + 1] - p.v.halo_off[j], ns = p.v.send_off[j + 1] - p.v.send_off[j];
+    if (nh) r = ncclSend(J + (p.n_in + p.v.halo_off[j]) * ldi, (size_t)(nh * ldi), ncclFloat, j, C->ch, C->cs);
+    if (ns && r == ncclSuccess)
+      r = ncclRecv(C->recv_b[l][b] + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(C, r != ncclSuccess ? r : r2, "halo exchange (bwd)");
+  cudaEventRecord(C->ev_b_done[l][b], C->cs);
+  msg = SegTable{};
+  have = p.n_send > 0 && (!pipe || t >= 2);
+  if (have) {
+    const int sb = pipe ? bp : b;
+    cudaStreamWaitEvent(C->s, C->ev_b_done[l][sb], 0);
+    msg.n_seg = 1;
+    msg.off[1] = p.n_send;
+    msg.base[0] = C->recv_b[l][sb];
+  }
+  return PGCN_OK;
+}
+#endif
+
 }  // namespace
 }  // namespace pgcn
 
@@ -316,7 +463,14 @@ extern "C" int pgcn_workspace_bytes(const pgcn_partitioning* part, const int32_t
                                     const pgcn_config* cfg, size_t* bytes) {
   if (!bytes) return fail(PGCN_EINVAL, "bytes is NULL");
   pgcn_ctx C;
-  int rc = init_ctx_shapes(&C, part, local, n_local, cfg);
+  int rc = init_ctx_shapes(&C, part, local, n_local, cfg, nullptr);
+  if (rc == PGCN_EUNSUPPORTED && n_local == 1) {  // one partition of a multi-process run
+    pgcn_part_view v0;
+    if (pgcn_partition_view(part, local[0], &v0) == PGCN_OK && v0.n_parts > 1) {
+      pgcn_comm cm{local[0], v0.n_parts, "x", "x"};
+      rc = init_ctx_shapes(&C, part, local, n_local, cfg, &cm);
+    }
+  }
   if (rc) return rc;
   Arena A;
   rc = layout(&C, part, local, n_local, A);
@@ -330,10 +484,9 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
                                void* stream, pgcn_ctx** out) {
   if (!out) return fail(PGCN_EINVAL, "out is NULL");
   *out = nullptr;
-  if (comm && comm->nranks > 1) return fail(PGCN_EUNSUPPORTED, "NCCL transport not built in this library");
   pgcn_ctx* C = new (std::nothrow) pgcn_ctx();
   if (!C) return fail(PGCN_ENOMEM, "host allocation failed");
-  int rc = init_ctx_shapes(C, part, local, n_local, cfg);
+  int rc = init_ctx_shapes(C, part, local, n_local, cfg, comm);
   if (rc) { delete C; return rc; }
   Arena dry;
   rc = layout(C, part, local, n_local, dry);
@@ -387,6 +540,36 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
       return fail(PGCN_ECUDA, "pgcn_ctx_create upload: %s", cudaGetErrorString(e));
     }
   }
+  if (C->nccl) {
+#ifdef PGCN_WITH_NCCL
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&C->cs, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      delete C;
+      return fail(PGCN_ECUDA, "comm stream creation failed");
+    }
+    for (int l = 1; l <= C->L; ++l) {
+      cudaEventCreateWithFlags(&C->ev_f_pack[l], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&C->ev_b_ready[l], cudaEventDisableTiming);
+      for (int b = 0; b < 2; ++b) {
+        cudaEventCreateWithFlags(&C->ev_f_done[l][b], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&C->ev_b_done[l][b], cudaEventDisableTiming);
+      }
+    }
+    ncclUniqueId ih, ir;
+    std::memcpy(&ih, comm->nccl_id_halo, sizeof(ih));
+    std::memcpy(&ir, comm->nccl_id_reduce, sizeof(ir));
+    ncclResult_t nr = ncclGroupStart();
+    if (nr == ncclSuccess) nr = ncclCommInitRank(&C->ch, C->nranks, ih, C->rank);
+    if (nr == ncclSuccess) nr = ncclCommInitRank(&C->cr, C->nranks, ir, C->rank);
+    ncclResult_t ne = ncclGroupEnd();
+    if (nr != ncclSuccess || ne != ncclSuccess) {
+      const char* msg = ncclGetErrorString(nr != ncclSuccess ? nr : ne);
+      delete C;
+      return fail(PGCN_ENCCL, "ncclCommInitRank: %s", msg);
+    }
+#endif
+  }
   rc = check_cuda(C, "pgcn_ctx_create");
   if (rc) { delete C; return rc; }
   *out = C;
@@ -436,8 +619,13 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   }
   for (auto& p : C->parts) {
     float* Hin = layer_in(p, l, b);
-    // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13; local transport = device gather)
-    if (C->n_parts > 1 && p.n_bd > 0) {
+    // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13)
+    int64_t n_valid = p.n_all;
+    if (C->nccl) {
+#ifdef PGCN_WITH_NCCL
+      if ((rc = nccl_fwd_exchange(C, p, t, l, Hin, Lk, &n_valid))) return rc;
+#endif
+    } else if (C->n_parts > 1 && p.n_bd > 0) {  // local transport: device gather from the owners
       bool do_install = false, ema = false, first = false;
       const float* prev = nullptr;
       SegTable src{};
@@ -468,12 +656,12 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const float* D = Hin;
     if (C->cfg.dropout > 0.0) {
       Scope sc(C, PGCN_K_DROPOUT, 8.0 * Fi * p.n_all + 8.0 * p.n_all);
-      dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, p.n_all, p.gid, drop_spec(C, t, l));
+      dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, n_valid, p.gid, drop_spec(C, t, l));
       D = p.D[l];
     }
     {
       Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, p.n_all, p.Z[l]);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l]);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     float* out = l < C->L ? p.H[l][b] : p.logits;
@@ -563,8 +751,18 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       SegTable msg{};
       msg.n_seg = 0;
       bool use_ema = false, first = false;
-      const bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t >= 2);
-      if (have) {
+      bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t >= 2);
+      const int32_t* row_map = p.msg_map;
+      if (C->nccl) {
+#ifdef PGCN_WITH_NCCL
+        if ((rc = nccl_bwd_exchange(C, p, t, l, msg, have))) return rc;
+        row_map = nullptr;
+        if (have && pipe && C->cfg.smooth_g) {
+          use_ema = true;
+          first = C->cfg.ema_init == 0 && t == 2;
+        }
+#endif
+      } else if (have) {
         msg.n_seg = C->n_parts;
         const int sb = pipe ? bp : b;
         for (int j = 0; j <= C->n_parts; ++j) msg.off[j] = p.v.send_off[j];
@@ -577,7 +775,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       const double Fi = (double)C->F[l - 1];
       Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j) + 8.0 * p.n_in +
                                           (msg.n_seg ? (4.0 * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
-      grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, p.msg_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
+      grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, row_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
                   p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi);
     }
   }
@@ -599,6 +797,12 @@ extern "C" int pgcn_update(pgcn_ctx* C, int64_t t, float* params, float* grads, 
   for (int i = 0; i < G.n; ++i) G.p[i] = C->parts[i].G;
   Scope sc(C, PGCN_K_UPDATE, 4.0 * C->P * (G.n + 2 + (C->cfg.opt == 1 ? 4 : 1)));
   sum_grads(Lk, G, C->P, grads);
+#ifdef PGCN_WITH_NCCL
+  if (C->nccl) {  // l.31: G = AllReduce(G_i), SUM (R6), on the compute stream (consumed right away)
+    ncclResult_t r = ncclAllReduce(grads, grads, (size_t)C->P, ncclFloat, ncclSum, C->cr, C->s);
+    if (r != ncclSuccess) return nccl_fail(C, r, "pgcn_update all-reduce");
+  }
+#endif
   OptSpec o{};
   o.adam = C->cfg.opt == 1;
   o.lr = (float)C->cfg.lr;
@@ -689,4 +893,26 @@ extern "C" int pgcn_timing_read(pgcn_ctx* C, int32_t kind, double* ms, int64_t* 
   if (bytes) *bytes = k.bytes;
   if (flops) *flops = k.flops;
   return PGCN_OK;
+}
+
+extern "C" int pgcn_nccl_id_bytes(void) {
+#ifdef PGCN_WITH_NCCL
+  return (int)sizeof(ncclUniqueId);
+#else
+  return 0;
+#endif
+}
+
+extern "C" int pgcn_nccl_unique_id(void* out) {
+#ifdef PGCN_WITH_NCCL
+  if (!out) return fail(PGCN_EINVAL, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(PGCN_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(out, &id, sizeof(id));
+  return PGCN_OK;
+#else
+  (void)out;
+  return fail(PGCN_EUNSUPPORTED, "library built without NCCL");
+#endif
 }

@@ -99,9 +99,8 @@ def lib():
         L.pgcn_dev_gemm_scratch_bytes.restype = C.c_size_t
         L.pgcn_dev_gemm.argtypes = [i32, i32, vp, vp, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, i32, vp,
                                     C.c_size_t, vp]
-        if hasattr(L, "pgcn_nccl_get_unique_id"):
-            L.pgcn_nccl_get_unique_id.argtypes = [vp]
-            L.pgcn_nccl_id_bytes.restype = i32
+        L.pgcn_nccl_unique_id.argtypes = [vp]
+        L.pgcn_nccl_id_bytes.restype = i32
         _lib = L
     return _lib
 
@@ -213,6 +212,34 @@ def unflatten_params(theta, widths):
         o += fo
         out.append((W, b))
     return out
+
+
+# ------------------------------------------------------------------------------------------- NCCL bootstrap
+def nccl_comm(rank: int, nranks: int, group=None) -> Comm:
+    """pgcn_comm for a multi-process run: rank 0 draws two ncclUniqueIds (halo exchange and
+    gradient all-reduce communicators) and torch.distributed broadcasts their bytes."""
+    import torch
+    import torch.distributed as dist
+    nb = int(lib().pgcn_nccl_id_bytes())
+    if nb <= 0:
+        raise RuntimeError("libpgcn.so was built without NCCL")
+    buf = np.zeros(2 * nb, dtype=np.uint8)
+    if rank == 0:
+        for k in range(2):
+            tmp = (C.c_uint8 * nb)()
+            _check(lib().pgcn_nccl_unique_id(C.addressof(tmp)))
+            buf[k * nb:(k + 1) * nb] = np.frombuffer(bytes(tmp), dtype=np.uint8)
+    t = torch.from_numpy(buf)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=0, group=group)
+    ids = t.cpu().numpy().copy()
+    cm = Comm()
+    cm.rank, cm.nranks = int(rank), int(nranks)
+    cm._ids = (C.c_uint8 * (2 * nb)).from_buffer_copy(ids.tobytes())
+    cm.nccl_id_halo = C.addressof(cm._ids)
+    cm.nccl_id_reduce = C.addressof(cm._ids) + nb
+    return cm
 
 
 # ------------------------------------------------------------------------------------------- context
