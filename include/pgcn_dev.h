@@ -26,6 +26,16 @@ int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1,
                   const float* W_ext, int64_t N, const float* Mg, int64_t ldM, const float* inv_deg, float* out,
                   int64_t ld_out, int32_t relu, void* scratch, size_t scratch_bytes, void* stream);
 
+/* The aggregation kernel of S3 (Eq. 3): Z[v] = inv_deg[v] * sum_{e in row v} D[col[e]] for rows
+ * [0, n_rows), neighbours >= n_valid contributing 0; D, Z row stride ld (multiple of 4).       */
+int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
+                  int64_t n_rows, int64_t n_valid, float* Z, void* stream);
+
+/* L2 streaming-read microbenchmark (roofline denominator for L2-served kernels): every thread reads
+ * float4s of buf[0 .. bytes) grid-stride, `reps` passes, and writes one checksum per block to
+ * out[gridDim] (148 x 8 blocks of 256 threads).  Keep `bytes` well below the 126 MB L2.        */
+int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

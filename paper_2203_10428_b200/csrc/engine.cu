@@ -94,6 +94,7 @@ struct pgcn_ctx {
   float* Wp_lo[PGCN_MAX_LAYERS + 1] = {};
   int64_t Fp[PGCN_MAX_LAYERS + 1] = {}, Kp[PGCN_MAX_LAYERS + 1] = {};
   float* part_loss = nullptr;
+  unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
   int64_t exp_t = 1;
   int exp_kind = pgcn::K_FWD, exp_layer = 1;
   int poisoned = 0;
@@ -227,6 +228,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     }
   }
   C->part_loss = A.take<float>(n_local);
+  C->work = A.take<unsigned long long>(4);
   return PGCN_OK;
 }
 
@@ -661,7 +663,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
     {
       Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l]);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     float* out = l < C->L ? p.H[l][b] : p.logits;
@@ -742,7 +744,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l));
+               drop_spec(C, t, l), C->work);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "pgcn_dev.h"
 
 namespace pgcn {
 namespace {
@@ -93,17 +94,32 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 // (G, NC, U) table in spmm_shape() was measured with tools/spmm_lab.py on B200 (whole row per
 // group, ~8 loads in flight).  Neighbour ids are loaded G at a time (coalesced)
 // and broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
+// Work distribution: static grid-stride, or (work != nullptr) dynamic -- each group takes the
+// next item from a per-launch atomic counter, so heavy-tailed degrees do not leave a tail of
+// groups still busy with their statically assigned long rows.
+template <int G>
+__device__ __forceinline__ int64_t next_item(unsigned long long* work, int lane, unsigned gm, int64_t cur,
+                                             int64_t stride) {
+  if (!work) return cur + stride;
+  unsigned long long v = 0;
+  if (lane == 0) v = atomicAdd(work, 1ull);
+  return (int64_t)__shfl_sync(gm, v, 0, G);
+}
+
 template <int G, int NC, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __restrict__ rp,
                                                              const int32_t* __restrict__ col,
                                                              const float* __restrict__ inv_deg,
                                                              const float4* __restrict__ D, int64_t ld4, int64_t n_rows,
-                                                             int64_t n_valid, int nchunk, float4* __restrict__ Z) {
+                                                             int64_t n_valid, int nchunk, float4* __restrict__ Z,
+                                                             unsigned long long* work) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
+  int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+  if (work) first = next_item<G>(work, lane, gm, 0, 0);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
     const int64_t row = it / nchunk;
     const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
     float4 acc[NC];
@@ -154,12 +170,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              const float4* __restrict__ dZs,
                                                              const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
-                                                             int64_t ld4, const int64_t* __restrict__ gid, DropSpec d) {
+                                                             int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
+                                                             unsigned long long* work) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t it = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; it < n_items; it += stride) {
+  int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+  if (work) first = next_item<G>(work, lane, gm, 0, 0);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
     const int64_t u0 = it / nchunk;
     const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
     float4 acc[NC];
@@ -624,18 +643,29 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
   X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
   X(32, 4, 2, 3)
 
+static bool dyn_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PGCN_SPMM_DYN");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
-              int64_t n_rows, int64_t n_valid, float* Z) {
+              int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
   const SpmmShape sh = spmm_shape(ld4);
+  if (!dyn_enabled()) work = nullptr;
+  if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
   const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
   auto D4 = reinterpret_cast<const float4*>(D);
   auto Z4 = reinterpret_cast<float4*>(Z);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_fwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid,   \
-                                                             sh.nchunk, Z4);                                   \
+                                                             sh.nchunk, Z4, work);                             \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); }
 #undef X
@@ -644,10 +674,12 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
-              const DropSpec& d) {
+              const DropSpec& d, unsigned long long* work) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
   const SpmmShape sh = spmm_shape(ld4);
+  if (!dyn_enabled()) work = nullptr;
+  if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
   const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
   auto a = reinterpret_cast<const float4*>(dZs);
   auto b = reinterpret_cast<const float4*>(dDs);
@@ -656,7 +688,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
-                                                             sh.nchunk, J4, ld4, gid, d);                      \
+                                                             sh.nchunk, J4, ld4, gid, d, work);                \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); }
 #undef X
@@ -764,4 +796,46 @@ void opt_update(Launch L, const float* grads, int64_t P, float* params, float* m
   count(L);
 }
 
+namespace {
+__global__ void __launch_bounds__(256) k_l2_read(const float4* __restrict__ buf, int64_t n4, int reps,
+                                                 float* __restrict__ out) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  for (int r = 0; r < reps; ++r) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    for (; i + st < n4; i += 2 * st) {
+      const float4 x = __ldcg(buf + i), y = __ldcg(buf + i + st);
+      a = f4add(a, x);
+      b = f4add(b, y);
+    }
+    if (i < n4) a = f4add(a, __ldcg(buf + i));
+  }
+  float s = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ float sh[8];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += sh[w];
+    out[blockIdx.x] = t;
+  }
+}
+}  // namespace
 }  // namespace pgcn
+
+extern "C" int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D,
+                             int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, void* stream) {
+  if (!row_ptr || !col || !inv_deg || !D || !Z || ld % 4 || n_rows < 0) return -1;
+  pgcn::spmm_fwd(pgcn::Launch{static_cast<cudaStream_t>(stream), nullptr}, row_ptr, col, inv_deg, D, ld, n_rows,
+                 n_valid, Z, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+extern "C" int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, float* out, void* stream) {
+  if (!buf || !out || bytes < 16 || reps < 1) return -1;
+  pgcn::k_l2_read<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const float4*>(buf), bytes / 16,
+                                                                       reps, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

@@ -37,14 +37,16 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
                  const int64_t* gid, const DropSpec& d);
 
 // S3: Z[v] = inv_deg[v] * sum_{e in row v} D[col[e]]   (neighbours >= n_valid contribute 0)
+// work: per-launch atomic item counter (8 bytes of device scratch) for dynamic row scheduling,
+// or nullptr for static grid-stride.
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
-              const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z);
+              const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work);
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
-              const int64_t* gid, const DropSpec& d);
+              const int64_t* gid, const DropSpec& d, unsigned long long* work);
 
 // S1 / S2: dst[r] = src(r) (copy) or EMA: dst[r] = first ? src : gamma*prev[r] + (1-gamma)*src.
 void gather_rows(Launch, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld,

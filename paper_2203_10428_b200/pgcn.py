@@ -99,6 +99,8 @@ def lib():
         L.pgcn_dev_gemm_scratch_bytes.restype = C.c_size_t
         L.pgcn_dev_gemm.argtypes = [i32, i32, vp, vp, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, i32, vp,
                                     C.c_size_t, vp]
+        L.pgcn_dev_spmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
+        L.pgcn_dev_l2_read.argtypes = [vp, i64, i32, vp, vp]
         L.pgcn_nccl_unique_id.argtypes = [vp]
         L.pgcn_nccl_id_bytes.restype = i32
         _lib = L

@@ -22,7 +22,8 @@ def P():
 
 
 def header_functions():
-    src = open(os.path.join(ROOT, "include", "pgcn.h")).read()
+    import glob
+    src = "\n".join(open(f).read() for f in sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(pgcn_[a-z0-9_]+)\s*\(", src)))
 
