@@ -579,8 +579,31 @@ __global__ void k_opt(const float* __restrict__ grads, int64_t P, float* __restr
 struct SpmmShape {
   int G, NC, U, MB, nchunk;
 };
+#define PGCN_SPMM_CASES(X)                                                                                     \
+  X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
+  X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
+  X(32, 4, 2, 3)
+
+static bool dyn_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PGCN_SPMM_DYN");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+bool spmm_instantiated(int G, int NC, int U, int MB) {
+#define X(G_, NC_, U_, MB_) \
+  if (G == G_ && NC == NC_ && U == U_ && MB == MB_) return true;
+  PGCN_SPMM_CASES(X)
+#undef X
+  return false;
+}
+
 // Dev knob (not part of the ABI): PGCN_SPMM_TABLE="ld4=G,NC,U,MB;..." overrides the table for the
-// listed widths (used by the in-situ sweep in tools/; an unknown combination falls back).
+// listed widths (used by the in-situ sweep in tools/); combinations that are not instantiated are
+// ignored (the default shape is used), so a kernel is never skipped.
 bool spmm_override(int64_t ld4, SpmmShape& s) {
   const char* e = std::getenv("PGCN_SPMM_TABLE");
   if (!e) return false;
@@ -589,7 +612,7 @@ bool spmm_override(int64_t ld4, SpmmShape& s) {
     long long w;
     int g, nc, u, mb, n = 0;
     if (std::sscanf(p, "%lld=%d,%d,%d,%d%n", &w, &g, &nc, &u, &mb, &n) == 5) {
-      if (w == ld4) {
+      if (w == ld4 && spmm_instantiated(g, nc, u, mb)) {
         s = SpmmShape{g, nc, u, mb, (int)((ld4 + (int64_t)g * nc - 1) / ((int64_t)g * nc))};
         return true;
       }
@@ -638,20 +661,6 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
   count(L);
 }
 
-#define PGCN_SPMM_CASES(X)                                                                                     \
-  X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
-  X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
-  X(32, 4, 2, 3)
-
-static bool dyn_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PGCN_SPMM_DYN");
-    v = e ? std::atoi(e) : 1;
-  }
-  return v != 0;
-}
-
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work) {
   if (n_rows <= 0) return;
@@ -667,7 +676,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     k_spmm_fwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid,   \
                                                              sh.nchunk, Z4, work);                             \
   } else
-  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); }
+  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
   count(L);
 }
@@ -690,7 +699,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
                                                              sh.nchunk, J4, ld4, gid, d, work);                \
   } else
-  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); }
+  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
   count(L);
 }
