@@ -298,27 +298,54 @@ def main():
     value = 1000.0 / ms
     loss_v = float(loss.item())
 
-    # end to end through the public API: pinned host inputs copied in every step, loss read back
+    # End to end through the public API: every step's inputs are copied from pinned host memory
+    # (H2D over PCIe on a copy stream into a double-buffered device staging area, prefetched one
+    # step ahead so the copy overlaps the previous step's compute), installed with pgcn_set_inputs
+    # (device-to-device into the padded layout) and the step's loss is read back to the host.
     e2e = None
     if not args.no_e2e:
         loss_h = torch.zeros(1).pin_memory()
         h2d = sum(sum(a.numel() * a.element_size() for a in h) for h in host)
+        copy_s = torch.cuda.Stream()
+        stage = [[tuple(torch.empty_like(a, device="cuda") for a in h) for h in host] for _ in range(2)]
+        ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_used = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def issue_copy(k):
+            buf = stage[k % 2]
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(ev_used[k % 2])
+                for i in range(nloc):
+                    for dst, src in zip(buf[i], host[i]):
+                        dst.copy_(src, non_blocking=True)
+                ev_copied[k % 2].record(copy_s)
+
         torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         e0 = time.perf_counter()
         ev0.record(stream)
-        for _ in range(K):
+        issue_copy(0)
+        for k in range(K):
             t += 1
+            stream.wait_event(ev_copied[k % 2])
             for i in range(nloc):
-                ctx.set_inputs(i, *host[i])
+                ctx.set_inputs(i, *stage[k % 2][i])
+            ev_used[k % 2].record(stream)
+            if k + 1 < K:
+                issue_copy(k + 1)
             ctx.step(t, theta, grads, opt, loss)
             with torch.cuda.stream(stream):
                 loss_h.copy_(loss, non_blocking=True)
             stream.synchronize()
+            _ = float(loss_h.item())
         ev1.record(stream)
         torch.cuda.synchronize()
         e_ms = max_over_ranks(ev0.elapsed_time(ev1), dist) / K
         e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
-               "ms_per_step": e_ms, "host_wall_ms_per_step": 1000.0 * (time.perf_counter() - e0) / K}
+               "ms_per_step": e_ms, "host_wall_ms_per_step": 1000.0 * (time.perf_counter() - e0) / K,
+               "note": "pinned host -> device copy of every step's X, labels, train mask (prefetched one step "
+                       "ahead on a copy stream), pgcn_set_inputs, pgcn_step, loss read back each step"}
 
     pk = peaks()
     top = max(kern.items(), key=lambda kv: kv[1]["ms"])
