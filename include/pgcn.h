@@ -141,6 +141,10 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *   n_global            N (dropout keys); n_train_global: |train set| over the whole graph.
  *   opt                 0 SGD (Alg. 1 l.32), 1 Adam (Table 3; PyTorch defaults, R7).
  *   dump_j              1: also store the accumulated J^(l) inner rows (parity checks only).
+ *   transform_first     0: aggregate then transform everywhere (Eq. 3 then the update, as written);
+ *                       1 (auto): per layer, compute P(D W_neigh) instead of (P D) W_neigh where that
+ *                       gathers fewer bytes -- layer 1 if 2 F_1 < F_0, layers >= 2 if F_l < F_{l-1}
+ *                       (same mathematics, fp32 reassociation only).  Tensor-core GEMMs only.
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -158,6 +162,7 @@ typedef struct {
   int32_t opt;
   int32_t dump_j;
   double lr, beta1, beta2, eps;
+  int32_t transform_first;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

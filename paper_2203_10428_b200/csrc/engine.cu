@@ -44,6 +44,8 @@ struct PartCtx {
   float* logits = nullptr;
   float* D[PGCN_MAX_LAYERS + 1] = {};
   float* Z[PGCN_MAX_LAYERS + 1] = {};
+  float* T[PGCN_MAX_LAYERS + 1] = {};
+  int64_t n_valid[PGCN_MAX_LAYERS + 1] = {};  // rows of the layer input valid this iteration
   float* M = nullptr;
   float* dA = nullptr;
   float* J[PGCN_MAX_LAYERS + 1][2] = {};
@@ -92,7 +94,11 @@ struct pgcn_ctx {
   float* WT_lo[PGCN_MAX_LAYERS + 1] = {};
   float* Wp_hi[PGCN_MAX_LAYERS + 1] = {};
   float* Wp_lo[PGCN_MAX_LAYERS + 1] = {};
-  int64_t Fp[PGCN_MAX_LAYERS + 1] = {}, Kp[PGCN_MAX_LAYERS + 1] = {};
+  float* WJ_hi[PGCN_MAX_LAYERS + 1] = {};
+  float* WJ_lo[PGCN_MAX_LAYERS + 1] = {};
+  int64_t Fp[PGCN_MAX_LAYERS + 1] = {}, Kp[PGCN_MAX_LAYERS + 1] = {}, Kq[PGCN_MAX_LAYERS + 1] = {};
+  // N1 transform-before-aggregate per layer: Y = P(D W_neigh) + D W_self + b instead of (PD) W_neigh
+  int tf[PGCN_MAX_LAYERS + 1] = {};
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
   int64_t exp_t = 1;
@@ -187,7 +193,8 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.logits = A.take<float>(p.n_in * C->ld[L]);
     for (int l = 1; l <= L; ++l) {
       if (C->cfg.dropout > 0.0) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
-      p.Z[l] = A.take<float>(p.n_in * C->ld[l - 1]);
+      p.Z[l] = A.take<float>(p.n_in * (C->tf[l] ? C->ld[l] : C->ld[l - 1]));   // Z, or S = inv_deg P T
+      if (C->tf[l]) p.T[l] = A.take<float>(p.n_all * C->ld[l]);                 // T = D W_neigh, then Q
     }
     p.M = A.take<float>(p.n_in * C->ldmax);
     if (L > 1) p.dA = A.take<float>(p.n_in * 2 * C->ldmax);
@@ -202,7 +209,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     for (int l = 1; l <= L; ++l) {
       int64_t w = gemm_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
       if (w > dw_need) dw_need = w;
-      w = tc_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
+      w = tc_dw_ws_floats(C->tf[l] ? p.n_all : p.n_in, C->F[l - 1], C->F[l]);
       if (w > dw_need) dw_need = w;
     }
   }
@@ -225,6 +232,11 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       C->WT_lo[l] = A.take<float>(C->F[l] * 2 * C->Fp[l]);
       C->Wp_hi[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
       C->Wp_lo[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
+      if (C->tf[l]) {
+        C->Kq[l] = round_up(C->F[l], 32);
+        C->WJ_hi[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
+        C->WJ_lo[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
+      }
     }
   }
   C->part_loss = A.take<float>(n_local);
@@ -271,6 +283,12 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   }
   C->woff[1] = 0;
   for (int l = 1; l <= C->L; ++l) C->woff[l + 1] = C->woff[l] + (2 * C->F[l - 1] + 1) * C->F[l];
+  // N1 traffic rule (gathered row widths per iteration): layer 1 aggregates F_0 forward only
+  // (no J^(0), R11) vs F_1 forward + F_1 backward; layers >= 2 aggregate F_in both ways vs F_out.
+  for (int l = 1; l <= C->L; ++l) {
+    const int64_t fi = C->ld[l - 1], fo = C->ld[l];
+    C->tf[l] = (cfg->transform_first == 1 && cfg->gemm == 0) ? (l == 1 ? 2 * fo < fi : fo < fi) : 0;
+  }
   C->P = C->woff[C->L + 1];
   return PGCN_OK;
 }
@@ -615,8 +633,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const bool tcg = C->cfg.gemm == 0;
   if (tcg) {
     Scope sc(C, PGCN_K_GEMM_FWD, 0.0);
-    tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], C->WT_hi[l], C->WT_lo[l],
-             C->Wp_hi[l], C->Wp_lo[l], C->s);
+    tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
+             C->WT_lo[l], C->Wp_hi[l], C->Wp_lo[l], C->WJ_hi[l], C->WJ_lo[l], C->s);
     ++C->launches;
   }
   for (auto& p : C->parts) {
@@ -661,18 +679,40 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, n_valid, p.gid, drop_spec(C, t, l));
       D = p.D[l];
     }
+    p.n_valid[l] = n_valid;
+    float* out = l < C->L ? p.H[l][b] : p.logits;
+    const float* bias = Wext + 2 * C->F[l - 1] * C->F[l];
+    if (C->tf[l]) {
+      // N1: T = D W_neigh (all valid local rows), S = inv_deg o P_i T, Y = D_in W_self + S + b
+      {
+        Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * n_valid * (Fi + Fo), 2.0 * n_valid * Fi * Fo);
+        if (tc_fwd_1seg(Lk, D, n_valid, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], 2 * C->Fp[l], 0, C->F[l],
+                        p.T[l], ldo, nullptr, nullptr, 0, 0))
+          return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
+      }
+      {
+        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fo * p.n_in);
+        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work);
+      }
+      {
+        Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
+        if (tc_fwd_1seg(Lk, D, p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], 2 * C->Fp[l],
+                        (int)(C->Fp[l] / 32), C->F[l], out, ldo, bias, p.Z[l], ldo, l < C->L))
+          return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (self) failed (layer %d)", l);
+      }
+      continue;
+    }
     {
       Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
-    float* out = l < C->L ? p.H[l][b] : p.logits;
     {
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * (2 * Fi + 1) * Fo,
                2.0 * p.n_in * (2 * Fi + 1) * Fo);
       if (tcg) {
-        if (gemm_fwd_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], C->WT_hi[l], C->WT_lo[l],
-                        Wext + 2 * C->F[l - 1] * C->F[l], C->F[l], out, ldo, l < C->L))
+        if (gemm_fwd_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], bias, C->F[l], out, ldo,
+                        l < C->L))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
       } else {
         gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
@@ -719,6 +759,33 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
     const float* D = C->cfg.dropout > 0.0 ? p.D[l] : layer_in(p, l, b);
+    if (C->tf[l]) {
+      // N1 backward: Q = P_i^T (inv_deg o M) over inner + boundary rows (width F_out);
+      // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
+      const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
+      {
+        Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fo * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
+                                         4.0 * Fo * p.n_all);
+        scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
+        DropSpec none{};
+        none.width = (int32_t)C->F[l];
+        spmm_bwd(Lk, p.trp, p.tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work);
+      }
+      {
+        Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
+        if (tc_dw_general(Lk, D, p.T[l], nv, D, p.M, p.n_in, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
+                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats))
+          return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
+      }
+      if (l >= 2) {
+        Scope sc(C, PGCN_K_GEMM_DA, 4.0 * (p.n_all + p.n_in) * Fo + 4.0 * p.n_all * Fi,
+                 2.0 * (p.n_all + p.n_in) * Fo * Fi);
+        if (tc_fwd_mask(Lk, p.T[l], p.n_all, p.M, p.n_in, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
+                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l)))
+          return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
+      }
+      continue;
+    }
     {
       Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (2 * Fi + Fo), 2.0 * p.n_in * (2 * Fi + 1) * Fo);
       if (C->cfg.gemm == 0) {
@@ -847,9 +914,9 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
       if (!lok) break;
       *o = {(void*)layer_in(p, l, b), p.n_all, C->F[l - 1], C->ld[l - 1]};
       return PGCN_OK;
-    case PGCN_T_Z:
+    case PGCN_T_Z:  // Z = inv_deg P D (width F_{l-1}); transform-first layers: S = inv_deg P (D W_neigh)
       if (!lok) break;
-      *o = {(void*)p.Z[l], p.n_in, C->F[l - 1], C->ld[l - 1]};
+      *o = {(void*)p.Z[l], p.n_in, C->tf[l] ? C->F[l] : C->F[l - 1], C->tf[l] ? C->ld[l] : C->ld[l - 1]};
       return PGCN_OK;
     case PGCN_T_J:
       if (l < 1 || l >= C->L) break;

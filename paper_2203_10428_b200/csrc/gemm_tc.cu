@@ -131,19 +131,22 @@ struct Tile {
   int m0, n0, kb_begin, kb_end, z, seg, half;
 };
 
+// FWD/DA: tile = (m-tile, n-tile), K loop over the A segments (FWD) or F_out (DA).
+// DW: tile = (segment, split z, f-tile, n-tile); K loop = the split's row blocks of that segment.
 __device__ __forceinline__ void decode(const TcParams& p, int t, Tile& T) {
   if (p.mode == TC_DW) {
-    // t -> (z split, seg, f-tile, n-tile)
-    const int nt = t % p.n_ntiles;
-    int r = t / p.n_ntiles;
+    const int per_seg = p.Z * p.n_ftiles * p.n_ntiles;
+    T.seg = t / per_seg;
+    int r = t - T.seg * per_seg;
+    const int nt = r % p.n_ntiles;
+    r /= p.n_ntiles;
     const int ft = r % p.n_ftiles;
-    r /= p.n_ftiles;
-    T.seg = r % p.n_seg;
-    T.z = r / p.n_seg;
+    T.z = r / p.n_ftiles;
     T.m0 = ft * BM;
     T.n0 = nt * p.BN;
-    T.kb_begin = T.z * p.kb_per_split;
-    T.kb_end = min(T.kb_begin + p.kb_per_split, p.kb_total);
+    T.kb_begin = T.z * p.kb_per_split[T.seg];
+    T.kb_end = min(T.kb_begin + p.kb_per_split[T.seg], p.kb_seg[T.seg]);
+    if (T.kb_end < T.kb_begin) T.kb_end = T.kb_begin;
     T.half = 0;
   } else {
     const int nt = t % p.n_ntiles;
@@ -159,8 +162,15 @@ __device__ __forceinline__ void decode(const TcParams& p, int t, Tile& T) {
       T.n0 = nt * p.BN;
     }
     T.kb_begin = 0;
-    T.kb_end = p.kb_total;
+    T.kb_end = p.kb_seg[0] + (p.nseg > 1 ? p.kb_seg[1] : 0);
   }
+}
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 (dropout mask, reading R5)
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant__ TcParams p) {
@@ -218,21 +228,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           uint8_t* Blo = B + b_bytes;
           mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
           if (p.mode == TC_DW) {
-            const CUtensorMap* am = T.seg == 0 ? &p.map_a0 : &p.map_a1;
             const int r0 = kb * BK;
-            for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, am, &full[s], T.m0 + 32 * j, r0);
-            for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 4096, &p.map_b, &full[s], T.n0 + 32 * j, r0);
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+            for (int j = 0; j < p.BN / 32; ++j)
+              tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
           } else if (p.mode == TC_FWD) {
-            const int seg = kb < p.kb_seg0 ? 0 : 1;
-            const int col = (kb - (seg ? p.kb_seg0 : 0)) * BK;
-            tma_load_2d(A, seg == 0 ? &p.map_a0 : &p.map_a1, &full[s], col, T.m0);
-            const int kcol = seg * p.kb_seg0 * BK + col;
-            tma_load_2d(B, &p.map_b, &full[s], kcol, T.n0);
+            const int seg = kb < p.kb_seg[0] ? 0 : 1;
+            const int kl = kb - (seg ? p.kb_seg[0] : 0);
+            tma_load_2d(A, &p.map_a[seg], &full[s], kl * BK, T.m0);
+            const int kcol = (p.kb_off_b[seg] + kl) * BK;
+            tma_load_2d(B, &p.map_b[0], &full[s], kcol, T.n0);
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kcol, T.n0);
           } else {  // TC_DA
-            tma_load_2d(A, &p.map_a0, &full[s], kb * BK, T.m0);
+            tma_load_2d(A, &p.map_a[0], &full[s], kb * BK, T.m0);
             const int brow = T.half * p.F + T.n0;
-            tma_load_2d(B, &p.map_b, &full[s], kb * BK, brow);
+            tma_load_2d(B, &p.map_b[0], &full[s], kb * BK, brow);
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * BK, brow);
           }
           if (++s == S) { s = 0; ph ^= 1; }
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           tc_commit(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        tc_commit(&tfull[acc]);  // also for an empty K range: the epilogue then writes zeros
         if (++acc == 2) { acc = 0; acc_ph ^= 1; }
       }
     }
@@ -336,27 +346,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
       mbar_wait(&tfull[acc], acc_ph, 5);
       __syncwarp();
       tc_fence_after();
+      const bool empty_k = T.kb_end <= T.kb_begin;
       const int row = T.m0 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 16) {
         uint32_t r[16];
         TMEM_LD16(tbase + c0, r);
         tmem_ld_wait();
-        if (p.mode == TC_FWD) {
+        if (empty_k) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = 0u;
+        }
+        if (p.epi == EPI_ACT) {
           if (row < p.M) {
             float* out = p.out + (int64_t)row * p.ld_out;
+            const float* add = p.addend ? p.addend + (int64_t)row * p.ld_add : nullptr;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int n = T.n0 + c0 + i;
               if (n < p.N) {
-                float v = __uint_as_float(r[i]) + p.bias[n];
+                float v = __uint_as_float(r[i]);
+                if (add) v += add[n];
+                if (p.bias) v += p.bias[n];
                 out[n] = p.relu ? fmaxf(v, 0.f) : v;
               } else if (n < p.ld_out) {
                 out[n] = 0.f;
               }
             }
           }
-        } else if (p.mode == TC_DA) {
+        } else if (p.epi == EPI_MASK) {  // dropout backward of the layer input (R5)
+          if (row < p.M) {
+            float* out = p.out + (int64_t)row * p.ld_out;
+            const uint64_t g = (uint64_t)p.gid[row];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = T.n0 + c0 + i;
+              if (n < p.N) {
+                float v = __uint_as_float(r[i]);
+                if (p.mask_on) {
+                  const uint64_t key = (p.key_base + g) * (uint64_t)p.width + (uint64_t)n;
+                  v = (uint32_t)(smix(key ^ p.seed) >> 40) >= p.thr ? v * p.scale : 0.f;
+                }
+                out[n] = v;
+              } else if (n < p.ld_out) {
+                out[n] = 0.f;
+              }
+            }
+          }
+        } else if (p.epi == EPI_DA) {
           if (row < p.M) {
             float* out = p.out + (int64_t)row * p.ld_out + (int64_t)T.half * p.ld_half;
             const float sc = T.half == 0 ? p.inv_deg[row] : 1.f;
@@ -367,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
               else if (c < p.ld_half) out[c] = 0.f;
             }
           }
-        } else {  // TC_DW partial
+        } else {  // EPI_PART: dW partial of split z
           if (row < p.F) {
-            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)T.seg * p.F + row) * p.N;
+            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)p.out_row_off[T.seg] + row) * p.N;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int n = T.n0 + c0 + i;
@@ -394,13 +431,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
 // W prep: for layer weights W [2F x N] (+ bias), write the tf32 hi/lo splits in the two TMA
 // layouts used above: WT [N x 2Fp] (FWD operand B, K-major; cols [0,F) = W_neigh^T,
 // [Fp, Fp+F) = W_self^T) and Wp [2F x Kp] (DA operand B, K-major).
-__global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int Kp, float* WT_hi, float* WT_lo,
-                        float* Wp_hi, float* Wp_lo) {
+// WJ [F x 2Kq] (Kq = round_up(N, 32)): row f = [W_neigh[f, :] | W_self[f, :]], the B operand of the
+// transform-first input gradient J = [Q | M] [W_neigh | W_self]^T (null to skip).
+__global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo,
+                        float* Wp_hi, float* Wp_lo, float* WJ_hi, float* WJ_lo) {
   const int64_t total_t = (int64_t)N * 2 * Fp, total_p = (int64_t)2 * F * Kp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p;
+  const int64_t total_j = WJ_hi ? (int64_t)F * 2 * Kq : 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p + total_j;
        i += (int64_t)gridDim.x * blockDim.x) {
     float x = 0.f;
-    if (i < total_t) {
+    if (i >= total_t + total_p) {
+      const int64_t j = i - total_t - total_p, f = j / (2 * Kq), k = j % (2 * Kq);
+      const int seg = (int)(k / Kq), c = (int)(k % Kq);
+      if (c < N) x = W[((int64_t)seg * F + f) * N + c];
+      const float h = tf32_rna(x);
+      WJ_hi[j] = h;
+      WJ_lo[j] = tf32_rna(x - h);
+    } else if (i < total_t) {
       const int64_t n = i / (2 * Fp), k = i % (2 * Fp);
       const int seg = (int)(k / Fp), f = (int)(k % Fp);
       if (f < F) x = W[((int64_t)seg * F + f) * N + n];
@@ -508,12 +555,12 @@ cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms) {
   return cudaGetLastError();
 }
 
-void tc_wprep(const float* W, int F, int N, int Fp, int Kp, float* WT_hi, float* WT_lo, float* Wp_hi, float* Wp_lo,
-              cudaStream_t s) {
-  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp;
+void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo, float* Wp_hi,
+              float* Wp_lo, float* WJ_hi, float* WJ_lo, cudaStream_t s) {
+  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp + (WJ_hi ? (int64_t)F * 2 * Kq : 0);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 8) grid = 148 * 8;
-  tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, WT_hi, WT_lo, Wp_hi, Wp_lo);
+  tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, WT_hi, WT_lo, Wp_hi, Wp_lo, WJ_hi, WJ_lo);
 }
 
 // ---------------------------------------------------------------------------------------- mode wrappers
@@ -541,30 +588,83 @@ static int dw_splits(int64_t M, int64_t F, int64_t N) {
 
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) { return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * N; }
 
+// FWD-mode launch with 1 or 2 K-major A segments sharing one pre-split B operand copy.
+static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* rowsA, int64_t ldA, int64_t K,
+                      const float* B_hi, const float* B_lo, int64_t ldB, const int* kb_off, int64_t M, int64_t N,
+                      TcParams& p) {
+  const int BN = tc_bn(N);
+  tc_common(p, BN);
+  bool ok = tc_map_2d(&p.map_b[0], B_hi, ldB, N, ldB, 32, BN) && tc_map_2d(&p.map_b_lo, B_lo, ldB, N, ldB, 32, BN);
+  for (int s = 0; s < nseg && ok; ++s) ok = tc_map_2d(&p.map_a[s], A[s], K, rowsA[s] > 0 ? rowsA[s] : 1, ldA, 32, 128);
+  if (!ok) return -1;
+  p.mode = TC_FWD;
+  p.nseg = nseg;
+  for (int s = 0; s < nseg; ++s) {
+    p.kb_seg[s] = (int)((K + 31) / 32);
+    p.kb_off_b[s] = kb_off[s];
+  }
+  p.n_ntiles = (int)((N + BN - 1) / BN);
+  p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
+  p.M = (int)M;
+  p.N = (int)N;
+  if (L.count) *L.count += 1;
+  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+}
+
 int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* WT_hi,
                 const float* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu) {
   if (M <= 0) return 0;
   TcParams p{};
-  const int BN = tc_bn(N);
-  tc_common(p, BN);
   const int64_t Fp = (F + 31) / 32 * 32;
-  bool ok = tc_map_2d(&p.map_a0, Z, F, M, ldA, 32, 128) && tc_map_2d(&p.map_a1, D, F, M, ldA, 32, 128) &&
-            tc_map_2d(&p.map_b, WT_hi, 2 * Fp, N, 2 * Fp, 32, BN) && tc_map_2d(&p.map_b_lo, WT_lo, 2 * Fp, N, 2 * Fp, 32, BN);
-  if (!ok) return -1;
-  p.mode = TC_FWD;
-  p.n_ntiles = (int)((N + BN - 1) / BN);
-  p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
-  p.kb_seg0 = (int)(Fp / 32);
-  p.kb_total = 2 * p.kb_seg0;
-  p.M = (int)M;
-  p.N = (int)N;
-  p.F = (int)F;
+  const float* A[2] = {Z, D};
+  const int64_t rows[2] = {M, M};
+  const int off[2] = {0, (int)(Fp / 32)};
+  p.epi = EPI_ACT;
   p.ld_out = ldY;
   p.out = Y;
   p.bias = bias;
   p.relu = relu;
-  if (L.count) *L.count += 1;
-  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+  return launch_fwd(L, 2, A, rows, ldA, F, WT_hi, WT_lo, 2 * Fp, off, M, N, p);
+}
+
+int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const float* WT_hi, const float* WT_lo,
+                int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
+                const float* addend, int64_t ld_add, int relu) {
+  if (M <= 0) return 0;
+  TcParams p{};
+  const float* As[1] = {A};
+  const int64_t rows[1] = {M};
+  const int off[1] = {kb_off};
+  p.epi = EPI_ACT;
+  p.ld_out = ld_out;
+  p.out = out;
+  p.bias = bias;
+  p.addend = addend;
+  p.ld_add = ld_add;
+  p.relu = relu;
+  return launch_fwd(L, 1, As, rows, ldA, K, WT_hi, WT_lo, ldB, off, M, N, p);
+}
+
+int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
+                const float* WJ_hi, const float* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
+                const int64_t* gid, const DropSpec& d) {
+  if (M <= 0) return 0;
+  TcParams p{};
+  const float* A[2] = {Q, Mg};
+  const int64_t rows[2] = {M, M_inner};
+  const int off[2] = {0, (int)(Kq / 32)};
+  p.epi = EPI_MASK;
+  p.ld_out = ldJ;
+  p.out = J;
+  p.gid = gid;
+  p.seed = d.seed;
+  p.key_base = d.key_base;
+  p.thr = d.thr;
+  p.scale = d.scale;
+  p.width = d.width;
+  p.mask_on = d.on;
+  if (M_inner <= 0) return launch_fwd(L, 1, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p);
+  return launch_fwd(L, 2, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p);
 }
 
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* Wp_hi, const float* Wp_lo,
@@ -573,14 +673,16 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   TcParams p{};
   const int BN = tc_bn(F);
   tc_common(p, BN);
-  bool ok = tc_map_2d(&p.map_a0, Mg, N, M, ldM, 32, 128) && tc_map_2d(&p.map_b, Wp_hi, N, 2 * F, Kp, 32, BN) &&
+  bool ok = tc_map_2d(&p.map_a[0], Mg, N, M, ldM, 32, 128) && tc_map_2d(&p.map_b[0], Wp_hi, N, 2 * F, Kp, 32, BN) &&
             tc_map_2d(&p.map_b_lo, Wp_lo, N, 2 * F, Kp, 32, BN);
   if (!ok) return -1;
   p.mode = TC_DA;
+  p.epi = EPI_DA;
+  p.nseg = 1;
   p.n_ntiles_half = (int)((F + BN - 1) / BN);
   p.n_ntiles = 2 * p.n_ntiles_half;
   p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
-  p.kb_total = (int)((N + 31) / 32);
+  p.kb_seg[0] = (int)((N + 31) / 32);
   p.M = (int)M;
   p.N = (int)N;
   p.F = (int)F;
@@ -592,40 +694,64 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
 }
 
-int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
-               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats) {
+int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
+                  int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
+                  float* G, float* ws, int64_t ws_floats) {
   const int64_t K = 2 * F + 1;
-  if (M <= 0) {
+  const int64_t rmax = rows0 > rows1 ? rows0 : rows1;
+  if (rmax <= 0) {
     cudaMemsetAsync(G, 0, sizeof(float) * K * N, L.s);
     return 0;
   }
   TcParams p{};
   const int BN = dw_bn(N);
   tc_common(p, BN);
-  const int Zs = dw_splits(M, F, N);
+  const int Zs = dw_splits(rmax, F, N);
   if ((int64_t)Zs * K * N > ws_floats) return -3;
-  bool ok = tc_map_2d(&p.map_a0, Z, F, M, ldA, 32, 32, true) && tc_map_2d(&p.map_a1, D, F, M, ldA, 32, 32, true) &&
-            tc_map_2d(&p.map_b, Mg, N, M, ldM, 32, 32, true);
+  const float* As[2] = {A0, A1};
+  const float* Bs[2] = {B0, B1};
+  const int64_t rows[2] = {rows0, rows1};
+  bool ok = true;
+  for (int s = 0; s < 2 && ok; ++s)
+    ok = tc_map_2d(&p.map_a[s], As[s], F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, true) &&
+         tc_map_2d(&p.map_b[s], Bs[s], N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, true);
   if (!ok) return -1;
   p.mode = TC_DW;
-  p.n_seg = 2;
+  p.epi = EPI_PART;
+  p.nseg = 2;
+  p.Z = Zs;
+  for (int s = 0; s < 2; ++s) {
+    p.kb_seg[s] = (int)((rows[s] + 31) / 32);
+    p.kb_per_split[s] = (p.kb_seg[s] + Zs - 1) / Zs;
+    if (p.kb_per_split[s] < 1) p.kb_per_split[s] = 1;
+    p.out_row_off[s] = (int)(s * F);
+  }
   p.n_ftiles = (int)((F + 127) / 128);
   p.n_ntiles = (int)((N + BN - 1) / BN);
-  p.kb_total = (int)((M + 31) / 32);
-  p.kb_per_split = (p.kb_total + Zs - 1) / Zs;
-  const int Zeff = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
-  p.n_tiles = Zeff * p.n_seg * p.n_ftiles * p.n_ntiles;
-  p.M = (int)M;
+  p.n_tiles = 2 * Zs * p.n_ftiles * p.n_ntiles;
+  p.M = (int)rmax;
   p.N = (int)N;
   p.F = (int)F;
   p.K_out = (int)K;
   p.out = ws;
   if (tc_launch(p, L.s, 148) != cudaSuccess) return -2;
-  dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zeff);
-  tc::k_colsum<<<grid, block, 0, L.s>>>(Mg, M, ldM, (int)N, (int64_t)p.kb_per_split * 32, ws, K * N, 2 * F * N);
-  split_reduce(L, ws, Zeff, K * N, G);
+  // bias row: colsum of Mb in the same Z splits (rows per split = a multiple of 32)
+  const int64_t kbb = (rowsMb + 31) / 32;
+  const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
+  dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
+  if (rowsMb > 0) {
+    tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * N, 2 * F * N);
+  } else {
+    for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * N + 2 * F * N, 0, sizeof(float) * N, L.s);
+  }
+  split_reduce(L, ws, Zs, K * N, G);
   if (L.count) *L.count += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats) {
+  return tc_dw_general(L, Z, Mg, M, D, Mg, M, ldA, ldM, F, N, Mg, M, G, ws, ws_floats);
 }
 
 }  // namespace pgcn
@@ -663,7 +789,7 @@ extern "C" int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const
   Launch L{s, nullptr};
   int rc = 0;
   if (variant == 0) {
-    if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, WT_hi, WT_lo, Wp_hi, Wp_lo, s);
+    if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, 0, WT_hi, WT_lo, Wp_hi, Wp_lo, nullptr, nullptr, s);
     if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, WT_lo, W + 2 * F * N, N, out, ld_out, relu);
     else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);
     else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2);

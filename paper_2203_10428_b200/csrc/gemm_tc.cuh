@@ -8,18 +8,26 @@
 namespace pgcn {
 
 enum { TC_FWD = 0, TC_DA = 1, TC_DW = 2 };
+enum { EPI_ACT = 0, EPI_DA = 1, EPI_MASK = 2, EPI_PART = 3 };
 
 struct alignas(64) TcParams {
-  CUtensorMap map_a0, map_a1, map_b, map_b_lo;
-  int mode, BN, stages, tmem_cols;
-  int n_tiles, n_ntiles, n_ntiles_half, n_ftiles, n_seg;
-  int kb_total, kb_seg0, kb_per_split;
+  CUtensorMap map_a[2], map_b[2], map_b_lo;
+  int mode, epi, BN, stages, tmem_cols;
+  int nseg, kb_seg[2], kb_off_b[2], kb_per_split[2];
+  int n_tiles, n_ntiles, n_ntiles_half, n_ftiles, Z;
   int M, N, F, K_out;
-  int64_t ld_out, ld_half;
+  int out_row_off[2];
+  int64_t ld_out, ld_half, ld_add;
   float* out;
   const float* bias;
   const float* inv_deg;
+  const float* addend;
   int relu;
+  const int64_t* gid;
+  uint64_t seed, key_base;
+  uint32_t thr;
+  float scale;
+  int width, mask_on;
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
@@ -29,9 +37,12 @@ size_t tc_smem_bytes(int BN, int S);
 int tc_bn(int64_t N);
 int tc_tmem_cols(int BN);
 cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms);
-void tc_wprep(const float* W, int F, int N, int Fp, int Kp, float* WT_hi, float* WT_lo, float* Wp_hi, float* Wp_lo,
-              cudaStream_t s);
+// W [2F x N] -> tf32 hi/lo operand copies: WT [N x 2Fp] (FWD B), Wp [2F x Kp] (DA B), optionally
+// WJ [F x 2Kq] (transform-first input-gradient B; null to skip).
+void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo, float* Wp_hi,
+              float* Wp_lo, float* WJ_hi, float* WJ_lo, cudaStream_t s);
 struct Launch;
+struct DropSpec;
 // Mode wrappers (return 0 on success, < 0 if the shape could not be mapped / launched).
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N);
 int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* WT_hi,
@@ -40,5 +51,21 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
                int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld);
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
                int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats);
+
+// Transform-before-aggregate pieces (N1: P(DW) = (PD)W for F_out < F_in):
+//   out[M x N] = act(A[M x K] W_seg^T + addend + bias), W_seg = W_neigh (kb_off 0) or W_self
+//   (kb_off = Fp/32) read from the WT operand copy (ldB = 2Fp columns).
+int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const float* WT_hi, const float* WT_lo,
+                int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
+                const float* addend, int64_t ld_add, int relu);
+//   J[M x F] = mask o s o ([Q | Mg] [W_neigh | W_self]^T), Q rows M, Mg rows M_inner (rows beyond
+//   are zero), B = WJ [F x 2Kq]; mask / gid / key per DropSpec (R5).
+int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
+                const float* WJ_hi, const float* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
+                const int64_t* gid, const DropSpec& d);
+//   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts.
+int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
+                  int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
+                  float* G, float* ws, int64_t ws_floats);
 
 }  // namespace pgcn

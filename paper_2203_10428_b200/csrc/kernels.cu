@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     float4 acc[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q)
-      acc[q] = (u0 < n_in && x0 + q * G < ld4) ? dDs[u0 * ldA4 + x0 + q * G] : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = (dDs && u0 < n_in && x0 + q * G < ld4) ? dDs[u0 * ldA4 + x0 + q * G] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -545,6 +545,14 @@ __global__ void __launch_bounds__(256) k_gemm_da(const float* __restrict__ Mg, i
   }
 }
 
+// out[v] = s[v] * M[v] (row scaling, e.g. inv_deg o M before the transposed aggregation)
+__global__ void k_scale_rows(const float4* __restrict__ M, const float* __restrict__ sc, int64_t n, int64_t ld4,
+                             float4* __restrict__ out) {
+  const int64_t total = n * ld4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = f4scale(M[i], sc[i / ld4]);
+}
+
 // ---------------------------------------------------------------- optimiser (S11, S12)
 __global__ void k_sum_grads(const __grid_constant__ PtrList G, int64_t P, float* __restrict__ grads) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
@@ -792,6 +800,13 @@ void gemm_da_f32(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, c
   if (M <= 0) return;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((2 * ld + BN - 1) / BN));
   k_gemm_da<<<grid, 256, 0, L.s>>>(Mg, ldM, M, N, W, F, inv_deg, dA, ld);
+  count(L);
+}
+
+void scale_rows(Launch L, const float* M, const float* s, int64_t n, int64_t ld, float* out) {
+  if (n <= 0) return;
+  k_scale_rows<<<grid_for(n * (ld / 4), kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(M), s, n,
+                                                                      ld / 4, reinterpret_cast<float4*>(out));
   count(L);
 }
 

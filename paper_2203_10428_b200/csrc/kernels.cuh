@@ -48,6 +48,9 @@ void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const floa
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work);
 
+// out[v] = s[v] * M[v] over n rows of stride ld
+void scale_rows(Launch, const float* M, const float* s, int64_t n, int64_t ld, float* out);
+
 // S1 / S2: dst[r] = src(r) (copy) or EMA: dst[r] = first ? src : gamma*prev[r] + (1-gamma)*src.
 void gather_rows(Launch, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld,
                  float* dst, const float* prev, float gamma, int ema, int first);

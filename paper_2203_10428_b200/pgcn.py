@@ -48,7 +48,7 @@ class Config(C.Structure):
                 ("gamma", C.c_double), ("dropout", C.c_double), ("seed", C.c_uint64), ("gemm", C.c_int32),
                 ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
-                ("eps", C.c_double)]
+                ("eps", C.c_double), ("transform_first", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -177,7 +177,8 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partit
 # ------------------------------------------------------------------------------------------- config
 def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
-                opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False) -> Config:
+                opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
+                transform_first=True) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -192,6 +193,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.opt = {"sgd": 0, "adam": 1}[opt]
     c.dump_j = int(bool(dump_j))
     c.lr, c.beta1, c.beta2, c.eps = float(lr), float(beta1), float(beta2), float(eps)
+    c.transform_first = int(bool(transform_first))
     return c
 
 

@@ -62,12 +62,15 @@ def row_oracle(g, P, v_local, t, W, b, p, seed, L, halo_zero):
     return Z, np.maximum(Y, 0.0)
 
 
-def test_sampled_layer1_rows_full_size(setup):
+@pytest.mark.parametrize("tf", [True, False])
+def test_sampled_layer1_rows_full_size(setup, tf):
+    """tf: bench's default transform-before-aggregate on layer 1 (the Z view then holds
+    S = inv_deg P (D W_neigh), checked as Z_v W_neigh) or aggregate-first (Z itself)."""
     import torch
     P, g, m = setup
     part = P.partition(g.n, g.row_ptr, g.col_idx, 2)
     cfg = P.make_config(m.widths, mode="pipe", dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
-                        n_train_global=g.n_train, seed=4)
+                        n_train_global=g.n_train, seed=4, transform_first=tf)
     ctx = P.Context(part, cfg)
     views = [part.view(i) for i in range(2)]
     keep = []
@@ -95,12 +98,15 @@ def test_sampled_layer1_rows_full_size(setup):
             assert abs(lv - np.log(41) * g.n_train / g.n_train) < 1.0     # ~ log C at init
         assert torch.isfinite(grads).all()
         for i, v in enumerate(views):
-            Zg = ctx.tensor(i, P.T_Z, 1, t)[:, :F0].cpu().numpy()
+            zt = ctx.tensor(i, P.T_Z, 1, t)
+            Zg = zt[:, :zt.shape[1]].cpu().numpy()
             Hg = ctx.tensor(i, P.T_H, 1, t)[:, :F1].cpu().numpy()
             rows = rng.choice(v["n_inner"], 24, replace=False)
             W, b = W_by_t[t]
             Zr, Hr = zip(*[row_oracle(g, v, r, t, W, b, m.dropout, 4, L, halo_zero=(t == 1)) for r in rows])
             Zr, Hr = np.array(Zr), np.array(Hr)
+            if Zg.shape[1] == F1:                     # transform-first: S_v = Z_v W_neigh
+                Zr = Zr @ W[:F0].astype(np.float64)
             ez = np.abs(Zg[rows] - Zr).max() / max(np.abs(Zr).max(), 1e-30)
             eh = np.abs(Hg[rows] - Hr).max() / max(np.abs(Hr).max(), 1e-30)
             assert ez <= 1e-4, (t, i, ez)

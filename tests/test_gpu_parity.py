@@ -120,12 +120,15 @@ MODES = [("vanilla", False, False), ("pipe", False, False), ("pipe", True, False
 
 @pytest.mark.parametrize("mode,sf,sg", MODES)
 @pytest.mark.parametrize("p", [0.0, 0.5])
-def test_cora_two_partitions(P, mode, sf, sg, p):
-    """BASELINE configs[0]: Cora-shaped graph, 2-layer GraphSAGE hidden 16, 2 partitions on 1 GPU."""
+@pytest.mark.parametrize("tf", [True, False])
+def test_cora_two_partitions(P, mode, sf, sg, p, tf):
+    """BASELINE configs[0]: Cora-shaped graph, 2-layer GraphSAGE hidden 16, 2 partitions on 1 GPU;
+    tf = transform-before-aggregate on both layers (N1) or aggregate-first as written (Eq. 3)."""
     g = gen_graph("cora", seed=1)
     widths = [1433, 16, 7]
     params0 = glorot_params(widths, 3)
-    kw = dict(mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.95, dropout=p, loss="ce", opt="sgd", lr=0.5)
+    kw = dict(mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.95, dropout=p, loss="ce", opt="sgd", lr=0.5,
+              transform_first=tf)
     T = 4
     gpu, _ = run_gpu(P, g, widths, 2, T, params0, **kw)
     cfg = ModelCfg(widths=widths, dropout=p, lr=0.5, opt="sgd", loss="ce", gamma=0.95)
