@@ -6,9 +6,9 @@
 // term and the tf32 rounding of lo are O(2^-22) relative, so the result is fp32-grade (the 1e-4
 // parity tier of the north_star) while running on the tensor pipe.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer (one lane),
-// warps 2-3 = converters (split fp32 tiles into hi/lo in shared memory, in the UMMA layout),
-// warps 4-7 = epilogue (tcgen05.ld TMEM -> registers -> global).
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer (one lane),
+// warps 2-7 = converters (split fp32 tiles into hi/lo in shared memory, in the UMMA layout),
+// warps 8-11 = epilogue (tcgen05.ld TMEM -> registers -> global; warp % 4 = its TMEM lane quarter).
 // Pipelines: full[s] (TMA -> converters), conv[s] (converters -> MMA), empty[s] (MMA commit ->
 // TMA), tfull[a] / tempty[a] (MMA <-> epilogue, two accumulator buffers in TMEM).
 //
@@ -123,7 +123,9 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
 }
 
 // ------------------------------------------------------------------------------------------------ kernel
-constexpr int kThreads = 256;
+constexpr int kConvWarps = 6;                       // warps 2..7 split fp32 tiles into tf32 hi/lo
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kThreads = 64 + kConvThreads + 128;   // + TMA warp, MMA warp, 4 epilogue warps
 constexpr int BM = 128;   // UMMA M (rows of A, TMEM lanes)
 constexpr int BK = 32;    // fp32 elements per k-block = one 128-byte swizzle row
 
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 64);
+      mbar_init(&conv[s], kConvThreads);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -296,9 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         if (++acc == 2) { acc = 0; acc_ph ^= 1; }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 2 + kConvWarps) {
     // ===================================================== converters: x -> (hi, lo)
-    const int ct = threadIdx.x - 64;  // 0..63
+    const int ct = threadIdx.x - 64;
     int s = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         mbar_wait(&full[s], ph, 4);
         float4* A = reinterpret_cast<float4*>(stA + (size_t)s * stage_bytes);
         float4* Alo = A + a_bytes / 16;
-        for (int i = ct; i < (int)(a_bytes / 16); i += 64) {
+        for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
           float4 x = A[i], h, l;
           h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
           h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         if (split_b) {
           float4* B = A + 2 * (a_bytes / 16);
           float4* Blo = B + b_bytes / 16;
-          for (int i = ct; i < (int)(b_bytes / 16); i += 64) {
+          for (int i = ct; i < (int)(b_bytes / 16); i += kConvThreads) {
             float4 x = B[i], h, l;
             h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
             h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
@@ -357,21 +359,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 16; ++i) r[i] = 0u;
         }
+        // 16 accumulator columns of this thread's row -> four float4 groups (16-byte aligned:
+        // every output stride is a multiple of 4 floats and n0 + c0 a multiple of 16).
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
         if (p.epi == EPI_ACT) {
           if (row < p.M) {
             float* out = p.out + (int64_t)row * p.ld_out;
             const float* add = p.addend ? p.addend + (int64_t)row * p.ld_add : nullptr;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = T.n0 + c0 + i;
-              if (n < p.N) {
-                float v = __uint_as_float(r[i]);
-                if (add) v += add[n];
-                if (p.bias) v += p.bias[n];
-                out[n] = p.relu ? fmaxf(v, 0.f) : v;
-              } else if (n < p.ld_out) {
-                out[n] = 0.f;
+            for (int g4 = 0; g4 < 4; ++g4) {
+              const int n = T.n0 + c0 + 4 * g4;
+              if (n >= p.ld_out) break;
+              float4 o = make_float4(v[4 * g4], v[4 * g4 + 1], v[4 * g4 + 2], v[4 * g4 + 3]);
+              if (n + 3 < p.N) {
+                if (add) {
+                  const float4 a4 = *reinterpret_cast<const float4*>(add + n);
+                  o.x += a4.x; o.y += a4.y; o.z += a4.z; o.w += a4.w;
+                }
+                if (p.bias) {
+                  o.x += p.bias[n]; o.y += p.bias[n + 1]; o.z += p.bias[n + 2]; o.w += p.bias[n + 3];
+                }
+                if (p.relu) {
+                  o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                }
+              } else {
+                float e[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (n + j < p.N) {
+                    if (add) e[j] += add[n + j];
+                    if (p.bias) e[j] += p.bias[n + j];
+                    if (p.relu) e[j] = fmaxf(e[j], 0.f);
+                  } else {
+                    e[j] = 0.f;
+                  }
+                }
+                o = make_float4(e[0], e[1], e[2], e[3]);
               }
+              *reinterpret_cast<float4*>(out + n) = o;
             }
           }
         } else if (p.epi == EPI_MASK) {  // dropout backward of the layer input (R5)
@@ -379,18 +406,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             float* out = p.out + (int64_t)row * p.ld_out;
             const uint64_t g = (uint64_t)p.gid[row];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = T.n0 + c0 + i;
-              if (n < p.N) {
-                float v = __uint_as_float(r[i]);
-                if (p.mask_on) {
-                  const uint64_t key = (p.key_base + g) * (uint64_t)p.width + (uint64_t)n;
-                  v = (uint32_t)(smix(key ^ p.seed) >> 40) >= p.thr ? v * p.scale : 0.f;
+            for (int g4 = 0; g4 < 4; ++g4) {
+              const int n = T.n0 + c0 + 4 * g4;
+              if (n >= p.ld_out) break;
+              float e[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float x = v[4 * g4 + j];
+                if (n + j >= p.N) {
+                  x = 0.f;
+                } else if (p.mask_on) {
+                  const uint64_t key = (p.key_base + g) * (uint64_t)p.width + (uint64_t)(n + j);
+                  x = (uint32_t)(smix(key ^ p.seed) >> 40) >= p.thr ? x * p.scale : 0.f;
                 }
-                out[n] = v;
-              } else if (n < p.ld_out) {
-                out[n] = 0.f;
+                e[j] = x;
               }
+              *reinterpret_cast<float4*>(out + n) = make_float4(e[0], e[1], e[2], e[3]);
             }
           }
         } else if (p.epi == EPI_DA) {
@@ -398,19 +429,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             float* out = p.out + (int64_t)row * p.ld_out + (int64_t)T.half * p.ld_half;
             const float sc = T.half == 0 ? p.inv_deg[row] : 1.f;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int c = T.n0 + c0 + i;
-              if (c < p.F) out[c] = __uint_as_float(r[i]) * sc;
-              else if (c < p.ld_half) out[c] = 0.f;
+            for (int g4 = 0; g4 < 4; ++g4) {
+              const int c = T.n0 + c0 + 4 * g4;
+              if (c >= p.ld_half) break;
+              float e[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) e[j] = (c + j < p.F) ? v[4 * g4 + j] * sc : 0.f;
+              *reinterpret_cast<float4*>(out + c) = make_float4(e[0], e[1], e[2], e[3]);
             }
           }
-        } else {  // EPI_PART: dW partial of split z
+        } else {  // EPI_PART: dW partial of split z, row stride ld_out = round_up(N, 4)
           if (row < p.F) {
-            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)p.out_row_off[T.seg] + row) * p.N;
+            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)p.out_row_off[T.seg] + row) * p.ld_out;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = T.n0 + c0 + i;
-              if (n < p.N) out[n] = __uint_as_float(r[i]);
+            for (int g4 = 0; g4 < 4; ++g4) {
+              const int n = T.n0 + c0 + 4 * g4;
+              if (n >= p.ld_out) break;
+              *reinterpret_cast<float4*>(out + n) =
+                  make_float4(v[4 * g4], v[4 * g4 + 1], v[4 * g4 + 2], v[4 * g4 + 3]);
             }
           }
         }
@@ -586,7 +622,9 @@ static int dw_splits(int64_t M, int64_t F, int64_t N) {
   return (int)Z;
 }
 
-int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) { return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * N; }
+int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
+  return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * ((N + 3) / 4 * 4);
+}
 
 // FWD-mode launch with 1 or 2 K-major A segments sharing one pre-split B operand copy.
 static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* rowsA, int64_t ldA, int64_t K,
@@ -707,7 +745,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int BN = dw_bn(N);
   tc_common(p, BN);
   const int Zs = dw_splits(rmax, F, N);
-  if ((int64_t)Zs * K * N > ws_floats) return -3;
+  const int64_t NP = (N + 3) / 4 * 4;  // partial row stride (16-byte aligned epilogue stores)
+  if ((int64_t)Zs * K * NP > ws_floats) return -3;
   const float* As[2] = {A0, A1};
   const float* Bs[2] = {B0, B1};
   const int64_t rows[2] = {rows0, rows1};
@@ -733,6 +772,7 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.N = (int)N;
   p.F = (int)F;
   p.K_out = (int)K;
+  p.ld_out = NP;
   p.out = ws;
   if (tc_launch(p, L.s, 148) != cudaSuccess) return -2;
   // bias row: colsum of Mb in the same Z splits (rows per split = a multiple of 32)
@@ -740,11 +780,11 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
   dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
   if (rowsMb > 0) {
-    tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * N, 2 * F * N);
+    tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * NP, 2 * F * NP);
   } else {
-    for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * N + 2 * F * N, 0, sizeof(float) * N, L.s);
+    for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * NP + 2 * F * NP, 0, sizeof(float) * N, L.s);
   }
-  split_reduce(L, ws, Zs, K * N, G);
+  split_reduce_strided(L, ws, Zs, K, N, NP, G);
   if (L.count) *L.count += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

@@ -478,6 +478,18 @@ __global__ void __launch_bounds__(256) k_gemm_dw(const float* __restrict__ Z, co
   }
 }
 
+// G[r * N + c] = sum_s part[s][r * NP + c]  (ascending s)
+__global__ void k_split_reduce_strided(const float* __restrict__ part, int64_t splits, int64_t rows, int64_t N,
+                                       int64_t NP, float* __restrict__ G) {
+  const int64_t len = rows * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i - r * N;
+    float a = 0.f;
+    for (int64_t s = 0; s < splits; ++s) a += part[s * rows * NP + r * NP + c];
+    G[i] = a;
+  }
+}
+
 __global__ void k_split_reduce(const float* __restrict__ part, int64_t splits, int64_t len, float* __restrict__ G) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
     float a = 0.f;
@@ -792,6 +804,12 @@ void gemm_dw_f32(Launch L, const float* Z, const float* D, int64_t ldA, int64_t 
 
 void split_reduce(Launch L, const float* part, int64_t splits, int64_t len, float* G) {
   k_split_reduce<<<grid_for(len, kThreads), kThreads, 0, L.s>>>(part, splits, len, G);
+  count(L);
+}
+
+void split_reduce_strided(Launch L, const float* part, int64_t splits, int64_t rows, int64_t N, int64_t NP,
+                          float* G) {
+  k_split_reduce_strided<<<grid_for(rows * N, kThreads), kThreads, 0, L.s>>>(part, splits, rows, N, NP, G);
   count(L);
 }
 

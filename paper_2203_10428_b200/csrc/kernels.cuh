@@ -78,6 +78,8 @@ void gemm_dw_f32(Launch, const float* Z, const float* D, int64_t ldA, int64_t M,
 int64_t gemm_dw_ws_floats(int64_t M, int64_t F, int64_t N);
 // G[i] = sum_{s < splits} part[s * len + i]  (ascending s)
 void split_reduce(Launch, const float* part, int64_t splits, int64_t len, float* G);
+// G[r * N + c] = sum_s part[s][r * NP + c] over rows x N (partials with row stride NP)
+void split_reduce_strided(Launch, const float* part, int64_t splits, int64_t rows, int64_t N, int64_t NP, float* G);
 // dA = Mg W^T ([M x 2F]); first half scaled by inv_deg[row] (dZ' of S7), into dA (ld_dA = 2 ld)
 void gemm_da_f32(Launch, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* W, int64_t F,
                  const float* inv_deg, float* dA, int64_t ld);
