@@ -52,7 +52,10 @@ def launches(path):
             continue
         d = dict(zip(hdr, r))
         k = kind_of(d["Kernel Name"])
-        val = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
+        try:
+            val = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
+        except ValueError:
+            continue
         agg[k][d["Metric Name"]] += val
         if d["Metric Name"] == "gpu__time_duration.sum":
             cnt[k] += 1
@@ -79,6 +82,8 @@ def raw(rep):
 
 def main():
     tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    if not reps:
+        reps = []
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     agg, cnt = launches(lcsv)
     # one step = launches of the last (timed) step; ncu saw warm-up + timed steps: report shares
