@@ -147,7 +147,7 @@ int validate_cfg(const pgcn_config* c) {
     if (c->width[l] < 1) return fail(PGCN_EINVAL, "width[%d] < 1", l);
   if (c->mode != 0 && c->mode != 1) return fail(PGCN_EINVAL, "mode must be 0 (VANILLA) or 1 (PIPE)");
   if (!(c->dropout >= 0.0 && c->dropout < 1.0)) return fail(PGCN_EINVAL, "dropout must be in [0,1)");
-  if (c->gemm != 0 && c->gemm != 2) return fail(PGCN_EUNSUPPORTED, "gemm variant %d not built", c->gemm);
+  if (c->gemm < 0 || c->gemm > 2) return fail(PGCN_EINVAL, "gemm must be 0 (3xTF32), 1 (bf16) or 2 (SIMT)");
   if (c->loss != 0 && c->loss != 1) return fail(PGCN_EINVAL, "loss must be 0 (CE) or 1 (BCE)");
   if (c->opt != 0 && c->opt != 1) return fail(PGCN_EINVAL, "opt must be 0 (SGD) or 1 (Adam)");
   if (c->n_train_global < 1) return fail(PGCN_EINVAL, "n_train_global < 1");
@@ -224,7 +224,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         for (int b = 0; b < 2; ++b) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
     }
   }
-  if (C->cfg.gemm == 0) {
+  if (C->cfg.gemm == 0) {  // 3xTF32 operand copies: fp32 hi/lo, k-blocks of 32
     for (int l = 1; l <= L; ++l) {
       C->Fp[l] = round_up(C->F[l - 1], 32);
       C->Kp[l] = round_up(C->F[l], 4);
@@ -236,6 +236,17 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         C->Kq[l] = round_up(C->F[l], 32);
         C->WJ_hi[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
         C->WJ_lo[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
+      }
+    }
+  } else if (C->cfg.gemm == 1) {  // bf16 operand copies, k-blocks of 64 (stored in the *_hi slots)
+    for (int l = 1; l <= L; ++l) {
+      C->Fp[l] = round_up(C->F[l - 1], 64);
+      C->Kp[l] = round_up(C->F[l], 8);
+      C->WT_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l] * 2 * C->Fp[l]));
+      C->Wp_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(2 * C->F[l - 1] * C->Kp[l]));
+      if (C->tf[l]) {
+        C->Kq[l] = round_up(C->F[l], 64);
+        C->WJ_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l - 1] * 2 * C->Kq[l]));
       }
     }
   }
@@ -287,7 +298,7 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   // (no J^(0), R11) vs F_1 forward + F_1 backward; layers >= 2 aggregate F_in both ways vs F_out.
   for (int l = 1; l <= C->L; ++l) {
     const int64_t fi = C->ld[l - 1], fo = C->ld[l];
-    C->tf[l] = (cfg->transform_first == 1 && cfg->gemm == 0) ? (l == 1 ? 2 * fo < fi : fo < fi) : 0;
+    C->tf[l] = (cfg->transform_first == 1 && cfg->gemm != 2) ? (l == 1 ? 2 * fo < fi : fo < fi) : 0;
   }
   C->P = C->woff[C->L + 1];
   return PGCN_OK;
@@ -630,11 +641,17 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
-  const bool tcg = C->cfg.gemm == 0;
+  const bool tcg = C->cfg.gemm != 2;
+  const int bf = C->cfg.gemm == 1;
+  const int kbk = bf ? 64 : 32;
   if (tcg) {
     Scope sc(C, PGCN_K_GEMM_FWD, 0.0);
-    tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
-             C->WT_lo[l], C->Wp_hi[l], C->Wp_lo[l], C->WJ_hi[l], C->WJ_lo[l], C->s);
+    if (bf)
+      tc_wprep_bf16(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
+                    C->Wp_hi[l], C->WJ_hi[l], C->s);
+    else
+      tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
+               C->WT_lo[l], C->Wp_hi[l], C->Wp_lo[l], C->WJ_hi[l], C->WJ_lo[l], C->s);
     ++C->launches;
   }
   for (auto& p : C->parts) {
@@ -687,7 +704,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * n_valid * (Fi + Fo), 2.0 * n_valid * Fi * Fo);
         if (tc_fwd_1seg(Lk, D, n_valid, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], 2 * C->Fp[l], 0, C->F[l],
-                        p.T[l], ldo, nullptr, nullptr, 0, 0))
+                        p.T[l], ldo, nullptr, nullptr, 0, 0, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
       }
       {
@@ -697,7 +714,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
         if (tc_fwd_1seg(Lk, D, p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], 2 * C->Fp[l],
-                        (int)(C->Fp[l] / 32), C->F[l], out, ldo, bias, p.Z[l], ldo, l < C->L))
+                        (int)(C->Fp[l] / kbk), C->F[l], out, ldo, bias, p.Z[l], ldo, l < C->L, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (self) failed (layer %d)", l);
       }
       continue;
@@ -712,7 +729,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                2.0 * p.n_in * (2 * Fi + 1) * Fo);
       if (tcg) {
         if (gemm_fwd_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], bias, C->F[l], out, ldo,
-                        l < C->L))
+                        l < C->L, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
       } else {
         gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
@@ -755,6 +772,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
+  const int bf = C->cfg.gemm == 1;
   // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
@@ -774,23 +792,23 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
         if (tc_dw_general(Lk, D, p.T[l], nv, D, p.M, p.n_in, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
-                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats))
+                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       }
       if (l >= 2) {
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * (p.n_all + p.n_in) * Fo + 4.0 * p.n_all * Fi,
                  2.0 * (p.n_all + p.n_in) * Fo * Fi);
         if (tc_fwd_mask(Lk, p.T[l], p.n_all, p.M, p.n_in, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
-                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l)))
+                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
       }
       continue;
     }
     {
       Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (2 * Fi + Fo), 2.0 * p.n_in * (2 * Fi + 1) * Fo);
-      if (C->cfg.gemm == 0) {
+      if (C->cfg.gemm != 2) {
         if (gemm_dw_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
-                       C->dw_ws_floats))
+                       C->dw_ws_floats, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       } else {
         gemm_dw_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
@@ -800,9 +818,9 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     if (l >= 2) {
       {
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * 2 * Fi);
-        if (C->cfg.gemm == 0) {
+        if (C->cfg.gemm != 2) {
           if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.inv_deg,
-                         p.dA, ldi))
+                         p.dA, ldi, bf))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         } else {
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);

@@ -20,6 +20,7 @@
 //   DW  : part[z][segF + f, n] = sum_{r in split z} A_s[r, f] M[r, n]   both operands MN-major
 //         (row-major activations read "transposed"), both split by the converters.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -100,6 +101,22 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -132,6 +149,34 @@ constexpr int BK = 32;    // fp32 elements per k-block = one 128-byte swizzle ro
 struct Tile {
   int m0, n0, kb_begin, kb_end, z, seg, half;
 };
+
+// Per-stage shared-memory geometry.  tf32 (BF = 0): A | A_lo | B | B_lo, k-block = 32 elements
+// (FWD/DA) or 32 rows (DW).  bf16 (BF = 1): A_raw (fp32 as loaded) | A_bf16 | B (bf16 weights, or
+// raw fp32 for DW) | B_bf16 (DW only); k-block = 64 elements (FWD/DA) or 32 rows (DW).
+struct Geo {
+  uint32_t a_raw, a_cvt, b_raw, b_cvt;
+  __host__ __device__ uint32_t stage() const { return a_raw + a_cvt + b_raw + b_cvt; }
+};
+__host__ __device__ inline Geo geometry(int bf, int mode, int BN) {
+  Geo g;
+  if (!bf) {
+    g.a_raw = BM * BK * 4;
+    g.a_cvt = BM * BK * 4;
+    g.b_raw = (uint32_t)BN * BK * 4;
+    g.b_cvt = (uint32_t)BN * BK * 4;
+  } else if (mode == TC_DW) {
+    g.a_raw = BM * 32 * 4;           // 128 features x 32 rows fp32
+    g.a_cvt = BM * 32 * 2;           // bf16 MN-major
+    g.b_raw = (uint32_t)BN * 32 * 4;
+    g.b_cvt = (uint32_t)BN * 32 * 2;
+  } else {
+    g.a_raw = BM * 64 * 4;           // 128 rows x 64 k fp32 (two boxes)
+    g.a_cvt = BM * 64 * 2;           // bf16 K-major, 128-byte rows
+    g.b_raw = (uint32_t)BN * 64 * 2; // bf16 weights straight from TMA
+    g.b_cvt = 0;
+  }
+  return g;
+}
 
 // FWD/DA: tile = (m-tile, n-tile), K loop over the A segments (FWD) or F_out (DA).
 // DW: tile = (segment, split z, f-tile, n-tile); K loop = the split's row blocks of that segment.
@@ -175,14 +220,16 @@ __device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 (dropout m
   return z ^ (z >> 31);
 }
 
+template <int BF>
 __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant__ TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  const uint32_t a_bytes = BM * BK * 4;               // 16 KB
-  const uint32_t b_bytes = (uint32_t)p.BN * BK * 4;   // BN x 128 B
-  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  uint8_t* stA = smem;                                 // per stage: A(hi) | A_lo | B(hi) | B_lo
+  const Geo geo = geometry(BF, p.mode, p.BN);
+  const uint32_t a_bytes = geo.a_raw;
+  const uint32_t b_bytes = geo.b_raw;
+  const uint32_t stage_bytes = geo.stage();
+  uint8_t* stA = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
   uint64_t* full = bars;
   uint64_t* conv = bars + S;
@@ -226,8 +273,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         for (int kb = T.kb_begin; kb < T.kb_end; ++kb) {
           mbar_wait(&empty[s], ph ^ 1, 1);
           uint8_t* A = stA + (size_t)s * stage_bytes;
-          uint8_t* B = A + 2 * a_bytes;
-          uint8_t* Blo = B + b_bytes;
+          uint8_t* B = A + geo.a_raw + geo.a_cvt;
+          uint8_t* Blo = B + geo.b_raw;
+          if (BF) {
+            mbar_expect_tx(&full[s], geo.a_raw + geo.b_raw);
+            if (p.mode == TC_DW) {
+              const int r0 = kb * 32;
+              for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+              for (int j = 0; j < p.BN / 32; ++j)
+                tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
+            } else if (p.mode == TC_FWD) {
+              const int seg = kb < p.kb_seg[0] ? 0 : 1;
+              const int kl = kb - (seg ? p.kb_seg[0] : 0);
+              tma_load_2d(A, &p.map_a[seg], &full[s], kl * 64, T.m0);
+              tma_load_2d(A + BM * 128, &p.map_a[seg], &full[s], kl * 64 + 32, T.m0);
+              tma_load_2d(B, &p.map_b[0], &full[s], (p.kb_off_b[seg] + kl) * 64, T.n0);
+            } else {  // TC_DA
+              tma_load_2d(A, &p.map_a[0], &full[s], kb * 64, T.m0);
+              tma_load_2d(A + BM * 128, &p.map_a[0], &full[s], kb * 64 + 32, T.m0);
+              tma_load_2d(B, &p.map_b[0], &full[s], kb * 64, T.half * p.F + T.n0);
+            }
+          } else {
           mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
           if (p.mode == TC_DW) {
             const int r0 = kb * BK;
@@ -247,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             tma_load_2d(B, &p.map_b[0], &full[s], kb * BK, brow);
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * BK, brow);
           }
+          }
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -254,7 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
   } else if (warp == 1) {
     // ===================================================== MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (p.mode == TC_DW ? (1u << 15) | (1u << 16) : 0u) |
+      const uint32_t fmt = BF ? 1u : 2u;  // BF16 (kind::f16) or TF32 (kind::tf32) operands, F32 accumulators
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (p.mode == TC_DW ? (1u << 15) | (1u << 16) : 0u) |
                              ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       int s = 0;
       uint32_t ph = 0;
@@ -271,6 +339,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           mbar_wait(&conv[s], ph, 3);
           tc_fence_after();
           const uint32_t A = smem_u32(stA + (size_t)s * stage_bytes);
+          if (BF) {
+            const uint32_t Ab = A + geo.a_raw, Bb = A + geo.a_raw + geo.a_cvt;
+            if (p.mode == TC_DW) {  // bf16 MN-major SW128: 64-wide atoms 4 KB apart, 8-row groups 1 KB apart
+              const uint32_t Bc = Bb + geo.b_raw;
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                mma_bf16(d, make_desc(Ab + kk * 2048, 4096, 1024), make_desc(Bc + kk * 2048, 4096, 1024), idesc,
+                         accum);
+                accum = 1u;
+              }
+            } else {  // bf16 K-major SW128: k-step of 16 elements = 32 bytes
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                mma_bf16(d, make_desc(Ab + kk * 32, 16, 1024), make_desc(Bb + kk * 32, 16, 1024), idesc, accum);
+                accum = 1u;
+              }
+            }
+            tc_commit(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
+            continue;
+          }
           const uint32_t Alo = A + a_bytes, B = A + 2 * a_bytes, Blo = B + b_bytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
@@ -308,6 +397,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
       decode(p, t, T);
       for (int kb = T.kb_begin; kb < T.kb_end; ++kb) {
         mbar_wait(&full[s], ph, 4);
+        if (BF) {
+          uint8_t* base = stA + (size_t)s * stage_bytes;
+          if (p.mode == TC_DW) {
+            // raw fp32 box jb (32 features x 32 rows, 128-byte rows, no swizzle) -> bf16 MN-major SW128:
+            // chunk (atom a, row r, h) = features 64a + 8h .. +7 at a*4096 + r*128 + ((h ^ (r & 7)) << 4)
+            for (int part = 0; part < 2; ++part) {
+              const uint8_t* raw = part == 0 ? base : base + geo.a_raw + geo.a_cvt;
+              uint8_t* cvt = part == 0 ? base + geo.a_raw : base + geo.a_raw + geo.a_cvt + geo.b_raw;
+              const int nf = part == 0 ? BM : p.BN;
+              const int items = (nf / 8) * 32;
+              for (int i = ct; i < items; i += kConvThreads) {
+                const int r = i & 31, hc = i >> 5;  // hc: 8-feature chunk index
+                const float4* src = reinterpret_cast<const float4*>(raw + (hc >> 2) * 4096 + r * 128 + (hc & 3) * 32);
+                const float4 x = src[0], y = src[1];
+                uint4 o;
+                o.x = pack_bf16(x.x, x.y); o.y = pack_bf16(x.z, x.w); o.z = pack_bf16(y.x, y.y); o.w = pack_bf16(y.z, y.w);
+                const int a = hc >> 3, h = hc & 7;
+                *reinterpret_cast<uint4*>(cvt + a * 4096 + r * 128 + ((h ^ (r & 7)) << 4)) = o;
+              }
+            }
+          } else {
+            // raw fp32 (two 32-column boxes, 128-byte rows, no swizzle) -> bf16 K-major SW128 rows
+            const uint8_t* raw = base;
+            uint8_t* cvt = base + geo.a_raw;
+            for (int i = ct; i < BM * 8; i += kConvThreads) {
+              const int r = i >> 3, j = i & 7;
+              const float4* src = reinterpret_cast<const float4*>(raw + (j >> 2) * (BM * 128) + r * 128 + (j & 3) * 32);
+              const float4 x = src[0], y = src[1];
+              uint4 o;
+              o.x = pack_bf16(x.x, x.y); o.y = pack_bf16(x.z, x.w); o.z = pack_bf16(y.x, y.y); o.w = pack_bf16(y.z, y.w);
+              *reinterpret_cast<uint4*>(cvt + r * 128 + ((j ^ (r & 7)) << 4)) = o;
+            }
+          }
+          fence_async_smem();
+          mbar_arrive(&conv[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         float4* A = reinterpret_cast<float4*>(stA + (size_t)s * stage_bytes);
         float4* Alo = A + a_bytes / 16;
         for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
@@ -500,6 +627,33 @@ __global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int K
   }
 }
 
+// bf16 operand copies of W [2F x N] (RNE): WT [N x 2Fp] (FWD B), Wp [2F x Kp] (DA B) and optionally
+// WJ [F x 2Kq] (transform-first J), Fp/Kq multiples of 64 elements, Kp of 8.
+__global__ void k_wprep_bf16(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, __nv_bfloat16* WT,
+                             __nv_bfloat16* Wp, __nv_bfloat16* WJ) {
+  const int64_t total_t = (int64_t)N * 2 * Fp, total_p = (int64_t)2 * F * Kp;
+  const int64_t total_j = WJ ? (int64_t)F * 2 * Kq : 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p + total_j;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x = 0.f;
+    if (i >= total_t + total_p) {
+      const int64_t j = i - total_t - total_p, f = j / (2 * Kq), k = j % (2 * Kq);
+      const int seg = (int)(k / Kq), c = (int)(k % Kq);
+      if (c < N) x = W[((int64_t)seg * F + f) * N + c];
+      WJ[j] = __float2bfloat16_rn(x);
+    } else if (i < total_t) {
+      const int64_t n = i / (2 * Fp), k = i % (2 * Fp);
+      const int seg = (int)(k / Fp), f = (int)(k % Fp);
+      if (f < F) x = W[((int64_t)seg * F + f) * N + n];
+      WT[i] = __float2bfloat16_rn(x);
+    } else {
+      const int64_t j = i - total_t, r = j / Kp, c = j % Kp;
+      if (c < N) x = W[r * N + c];
+      Wp[j] = __float2bfloat16_rn(x);
+    }
+  }
+}
+
 // db partial: part[z][row_off + n] = sum_{r in split z} M[r, n]  (fixed order; the bias row of
 // the dW output, reduced over splits together with the tensor-core rows)
 __global__ void k_colsum(const float* __restrict__ Mg, int64_t M, int64_t ld, int N, int64_t rps,
@@ -540,28 +694,36 @@ EncodeFn encode_fn() {
 }
 }  // namespace
 
-bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
-               bool mn_major) {
+// swz: 0 none, 1 128B (K-major UMMA operands), 2 128B_ATOM_32B (tf32 MN-major operands).
+static bool tc_map(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int64_t rows, int64_t ld, int box_cols,
+                   int box_rows, int swz) {
   EncodeFn f = encode_fn();
   if (!f || cols <= 0 || rows <= 0) return false;
+  const size_t es_b = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es_b};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
-  return f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUtensorMapSwizzle sw = swz == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                         : (swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  return f(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int tc_stages(int BN) {
-  const int stage = 2 * tc::BM * tc::BK * 4 + 2 * BN * tc::BK * 4;
+bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
+               bool mn_major) {
+  return tc_map(m, base, false, cols, rows, ld, box_cols, box_rows, mn_major ? 2 : 1);
+}
+
+int tc_stages(int BN, int bf, int mode) {
+  const int stage = (int)tc::geometry(bf, mode, BN).stage();
   int S = (200 * 1024) / stage;
   return S > 4 ? 4 : (S < 2 ? 2 : S);
 }
 
-size_t tc_smem_bytes(int BN, int S) {
-  const size_t stage = 2 * (size_t)tc::BM * tc::BK * 4 + 2 * (size_t)BN * tc::BK * 4;
+size_t tc_smem_bytes(int BN, int S, int bf, int mode) {
+  const size_t stage = tc::geometry(bf, mode, BN).stage();
   return 1024 + S * stage + (3 * S + 4) * 8 + 16;
 }
 
@@ -580,15 +742,25 @@ int tc_tmem_cols(int BN) {
 
 cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms) {
   static bool attr_set = false;
-  const size_t smem = tc_smem_bytes(p.BN, p.stages);
+  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode);
   if (!attr_set) {
-    cudaFuncSetAttribute(tc::k_umma_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tc::k_umma_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tc::k_umma_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   int grid = p.n_tiles < sms ? p.n_tiles : sms;
   if (grid < 1) return cudaSuccess;
-  tc::k_umma_gemm<<<grid, tc::kThreads, smem, s>>>(p);
+  if (p.bf) tc::k_umma_gemm<1><<<grid, tc::kThreads, smem, s>>>(p);
+  else tc::k_umma_gemm<0><<<grid, tc::kThreads, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, void* WT, void* Wp, void* WJ, cudaStream_t s) {
+  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp + (WJ ? (int64_t)F * 2 * Kq : 0);
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 8) grid = 148 * 8;
+  tc::k_wprep_bf16<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, static_cast<__nv_bfloat16*>(WT),
+                                        static_cast<__nv_bfloat16*>(Wp), static_cast<__nv_bfloat16*>(WJ));
 }
 
 void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo, float* Wp_hi,
@@ -600,20 +772,23 @@ void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi
 }
 
 // ---------------------------------------------------------------------------------------- mode wrappers
-static void tc_common(TcParams& p, int BN) {
+// bf = 1: bf16 operands (kind::f16; k-block 64 elements; B = bf16 weight copy, SW128); bf = 0: 3xTF32.
+static void tc_common(TcParams& p, int BN, int bf, int mode) {
   p.BN = BN;
-  p.stages = tc_stages(BN);
+  p.bf = bf;
+  p.stages = tc_stages(BN, bf, mode);
   p.tmem_cols = tc_tmem_cols(BN);
 }
 
-// dW reads Mg "transposed" (MN-major), whose swizzle atoms are 32 fp32 wide: N tiles are whole atoms.
-static int dw_bn(int64_t N) {
-  int64_t bn = (N + 31) / 32 * 32;
+// dW reads activations "transposed" (MN-major): N tiles are whole swizzle atoms (32 fp32 / 64 bf16).
+static int dw_bn(int64_t N, int bf) {
+  const int64_t atom = bf ? 64 : 32;
+  int64_t bn = (N + atom - 1) / atom * atom;
   return (int)(bn > 256 ? 256 : bn);
 }
 
 static int dw_splits(int64_t M, int64_t F, int64_t N) {
-  const int BN = dw_bn(N);
+  const int BN = dw_bn(N, 0);
   const int64_t tiles = 2 * ((F + 127) / 128) * ((N + BN - 1) / BN);
   int64_t Z = (2 * 148 + tiles - 1) / tiles;
   const int64_t kb = (M + 31) / 32;
@@ -626,19 +801,25 @@ int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
   return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * ((N + 3) / 4 * 4);
 }
 
-// FWD-mode launch with 1 or 2 K-major A segments sharing one pre-split B operand copy.
+// FWD-mode launch with 1 or 2 K-major A segments sharing one pre-converted B operand copy
+// (tf32: hi/lo fp32 [N x ldB]; bf16: [N x ldB] bf16).  kb_off in k-blocks of the variant.
 static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* rowsA, int64_t ldA, int64_t K,
-                      const float* B_hi, const float* B_lo, int64_t ldB, const int* kb_off, int64_t M, int64_t N,
-                      TcParams& p) {
+                      const void* B_hi, const void* B_lo, int64_t ldB, const int* kb_off, int64_t M, int64_t N,
+                      TcParams& p, int bf) {
   const int BN = tc_bn(N);
-  tc_common(p, BN);
-  bool ok = tc_map_2d(&p.map_b[0], B_hi, ldB, N, ldB, 32, BN) && tc_map_2d(&p.map_b_lo, B_lo, ldB, N, ldB, 32, BN);
-  for (int s = 0; s < nseg && ok; ++s) ok = tc_map_2d(&p.map_a[s], A[s], K, rowsA[s] > 0 ? rowsA[s] : 1, ldA, 32, 128);
+  tc_common(p, BN, bf, TC_FWD);
+  bool ok;
+  if (bf) ok = tc_map(&p.map_b[0], B_hi, true, ldB, N, ldB, 64, BN, 1);
+  else
+    ok = tc_map(&p.map_b[0], B_hi, false, ldB, N, ldB, 32, BN, 1) && tc_map(&p.map_b_lo, B_lo, false, ldB, N, ldB, 32, BN, 1);
+  for (int s = 0; s < nseg && ok; ++s)
+    ok = tc_map(&p.map_a[s], A[s], false, K, rowsA[s] > 0 ? rowsA[s] : 1, ldA, 32, 128, bf ? 0 : 1);
   if (!ok) return -1;
+  const int kbk = bf ? 64 : 32;
   p.mode = TC_FWD;
   p.nseg = nseg;
   for (int s = 0; s < nseg; ++s) {
-    p.kb_seg[s] = (int)((K + 31) / 32);
+    p.kb_seg[s] = (int)((K + kbk - 1) / kbk);
     p.kb_off_b[s] = kb_off[s];
   }
   p.n_ntiles = (int)((N + BN - 1) / BN);
@@ -649,25 +830,27 @@ static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* 
   return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
 }
 
-int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* WT_hi,
-                const float* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu) {
+int64_t tc_kpad(int64_t K, int bf) { return bf ? (K + 63) / 64 * 64 : (K + 31) / 32 * 32; }
+
+int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const void* WT_hi,
+                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf) {
   if (M <= 0) return 0;
   TcParams p{};
-  const int64_t Fp = (F + 31) / 32 * 32;
+  const int64_t Fp = tc_kpad(F, bf);
   const float* A[2] = {Z, D};
   const int64_t rows[2] = {M, M};
-  const int off[2] = {0, (int)(Fp / 32)};
+  const int off[2] = {0, (int)(Fp / (bf ? 64 : 32))};
   p.epi = EPI_ACT;
   p.ld_out = ldY;
   p.out = Y;
   p.bias = bias;
   p.relu = relu;
-  return launch_fwd(L, 2, A, rows, ldA, F, WT_hi, WT_lo, 2 * Fp, off, M, N, p);
+  return launch_fwd(L, 2, A, rows, ldA, F, WT_hi, WT_lo, 2 * Fp, off, M, N, p, bf);
 }
 
-int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const float* WT_hi, const float* WT_lo,
+int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const void* WT_hi, const void* WT_lo,
                 int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
-                const float* addend, int64_t ld_add, int relu) {
+                const float* addend, int64_t ld_add, int relu, int bf) {
   if (M <= 0) return 0;
   TcParams p{};
   const float* As[1] = {A};
@@ -680,17 +863,17 @@ int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, con
   p.addend = addend;
   p.ld_add = ld_add;
   p.relu = relu;
-  return launch_fwd(L, 1, As, rows, ldA, K, WT_hi, WT_lo, ldB, off, M, N, p);
+  return launch_fwd(L, 1, As, rows, ldA, K, WT_hi, WT_lo, ldB, off, M, N, p, bf);
 }
 
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
-                const float* WJ_hi, const float* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d) {
+                const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
+                const int64_t* gid, const DropSpec& d, int bf) {
   if (M <= 0) return 0;
   TcParams p{};
   const float* A[2] = {Q, Mg};
   const int64_t rows[2] = {M, M_inner};
-  const int off[2] = {0, (int)(Kq / 32)};
+  const int off[2] = {0, (int)(Kq / (bf ? 64 : 32))};
   p.epi = EPI_MASK;
   p.ld_out = ldJ;
   p.out = J;
@@ -701,18 +884,21 @@ int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_
   p.scale = d.scale;
   p.width = d.width;
   p.mask_on = d.on;
-  if (M_inner <= 0) return launch_fwd(L, 1, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p);
-  return launch_fwd(L, 2, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p);
+  if (M_inner <= 0) return launch_fwd(L, 1, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p, bf);
+  return launch_fwd(L, 2, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p, bf);
 }
 
-int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* Wp_hi, const float* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld) {
+int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf) {
   if (M <= 0) return 0;
   TcParams p{};
   const int BN = tc_bn(F);
-  tc_common(p, BN);
-  bool ok = tc_map_2d(&p.map_a[0], Mg, N, M, ldM, 32, 128) && tc_map_2d(&p.map_b[0], Wp_hi, N, 2 * F, Kp, 32, BN) &&
-            tc_map_2d(&p.map_b_lo, Wp_lo, N, 2 * F, Kp, 32, BN);
+  tc_common(p, BN, bf, TC_DA);
+  bool ok = tc_map(&p.map_a[0], Mg, false, N, M, ldM, 32, 128, bf ? 0 : 1);
+  if (bf) ok = ok && tc_map(&p.map_b[0], Wp_hi, true, N, 2 * F, Kp, 64, BN, 1);
+  else
+    ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, 2 * F, Kp, 32, BN, 1) &&
+         tc_map(&p.map_b_lo, Wp_lo, false, N, 2 * F, Kp, 32, BN, 1);
   if (!ok) return -1;
   p.mode = TC_DA;
   p.epi = EPI_DA;
@@ -720,7 +906,7 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   p.n_ntiles_half = (int)((F + BN - 1) / BN);
   p.n_ntiles = 2 * p.n_ntiles_half;
   p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
-  p.kb_seg[0] = (int)((N + 31) / 32);
+  p.kb_seg[0] = (int)((N + (bf ? 63 : 31)) / (bf ? 64 : 32));
   p.M = (int)M;
   p.N = (int)N;
   p.F = (int)F;
@@ -734,7 +920,7 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
 
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
-                  float* G, float* ws, int64_t ws_floats) {
+                  float* G, float* ws, int64_t ws_floats, int bf) {
   const int64_t K = 2 * F + 1;
   const int64_t rmax = rows0 > rows1 ? rows0 : rows1;
   if (rmax <= 0) {
@@ -742,8 +928,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
     return 0;
   }
   TcParams p{};
-  const int BN = dw_bn(N);
-  tc_common(p, BN);
+  const int BN = dw_bn(N, bf);
+  tc_common(p, BN, bf, TC_DW);
   const int Zs = dw_splits(rmax, F, N);
   const int64_t NP = (N + 3) / 4 * 4;  // partial row stride (16-byte aligned epilogue stores)
   if ((int64_t)Zs * K * NP > ws_floats) return -3;
@@ -752,8 +938,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int64_t rows[2] = {rows0, rows1};
   bool ok = true;
   for (int s = 0; s < 2 && ok; ++s)
-    ok = tc_map_2d(&p.map_a[s], As[s], F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, true) &&
-         tc_map_2d(&p.map_b[s], Bs[s], N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, true);
+    ok = tc_map(&p.map_a[s], As[s], false, F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, bf ? 0 : 2) &&
+         tc_map(&p.map_b[s], Bs[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, bf ? 0 : 2);
   if (!ok) return -1;
   p.mode = TC_DW;
   p.epi = EPI_PART;
@@ -790,8 +976,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
 }
 
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
-               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats) {
-  return tc_dw_general(L, Z, Mg, M, D, Mg, M, ldA, ldM, F, N, Mg, M, G, ws, ws_floats);
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf) {
+  return tc_dw_general(L, Z, Mg, M, D, Mg, M, ldA, ldM, F, N, Mg, M, G, ws, ws_floats, bf);
 }
 
 }  // namespace pgcn
@@ -802,7 +988,7 @@ int64_t r256(int64_t b) { return (b + 255) / 256 * 256; }
 }  // namespace
 
 extern "C" size_t pgcn_dev_gemm_scratch_bytes(int64_t M, int64_t F, int64_t N) {
-  const int64_t Fp = (F + 31) / 32 * 32, Kp = (N + 3) / 4 * 4;
+  const int64_t Fp = (F + 63) / 64 * 64, Kp = (N + 7) / 8 * 8;  // covers the tf32 and bf16 layouts
   int64_t ws = pgcn::tc_dw_ws_floats(M, F, N);
   const int64_t ws2 = pgcn::gemm_dw_ws_floats(M, F, N);
   if (ws2 > ws) ws = ws2;
@@ -814,7 +1000,7 @@ extern "C" int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const
                              float* out, int64_t ld_out, int32_t relu, void* scratch, size_t scratch_bytes,
                              void* stream) {
   using namespace pgcn;
-  if (op < 0 || op > 2 || (variant != 0 && variant != 2)) return fail(PGCN_EINVAL, "pgcn_dev_gemm: bad op/variant");
+  if (op < 0 || op > 2 || variant < 0 || variant > 2) return fail(PGCN_EINVAL, "pgcn_dev_gemm: bad op/variant");
   if (!out || !W || M < 0 || F < 1 || N < 1) return fail(PGCN_EINVAL, "pgcn_dev_gemm: bad shape/pointer");
   if (scratch_bytes < pgcn_dev_gemm_scratch_bytes(M, F, N)) return fail(PGCN_ENOMEM, "pgcn_dev_gemm: scratch too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -830,9 +1016,15 @@ extern "C" int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const
   int rc = 0;
   if (variant == 0) {
     if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, 0, WT_hi, WT_lo, Wp_hi, Wp_lo, nullptr, nullptr, s);
-    if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, WT_lo, W + 2 * F * N, N, out, ld_out, relu);
-    else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);
-    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2);
+    if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, WT_lo, W + 2 * F * N, N, out, ld_out, relu, 0);
+    else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats, 0);
+    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2, 0);
+  } else if (variant == 1) {
+    const int64_t Fb = (F + 63) / 64 * 64, Kb = (N + 7) / 8 * 8;
+    if (op != 1) tc_wprep_bf16(W, (int)F, (int)N, (int)Fb, (int)Kb, 0, WT_hi, Wp_hi, nullptr, s);
+    if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, nullptr, W + 2 * F * N, N, out, ld_out, relu, 1);
+    else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats, 1);
+    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, nullptr, Kb, F, inv_deg, out, ld_out / 2, 1);
   } else {
     if (op == 0) gemm_fwd_f32(L, A0, A1, ldA, M, F, W, N, out, ld_out, relu);
     else if (op == 1) gemm_dw_f32(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);

@@ -28,12 +28,14 @@ struct alignas(64) TcParams {
   uint32_t thr;
   float scale;
   int width, mask_on;
+  int bf;  // 1: bf16 operands (kind::f16), 0: 3xTF32 (kind::tf32)
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
                bool mn_major = false);
-int tc_stages(int BN);
-size_t tc_smem_bytes(int BN, int S);
+int tc_stages(int BN, int bf, int mode);
+size_t tc_smem_bytes(int BN, int S, int bf, int mode);
+void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, void* WT, void* Wp, void* WJ, cudaStream_t s);
 int tc_bn(int64_t N);
 int tc_tmem_cols(int BN);
 cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms);
@@ -45,27 +47,30 @@ struct Launch;
 struct DropSpec;
 // Mode wrappers (return 0 on success, < 0 if the shape could not be mapped / launched).
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N);
-int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* WT_hi,
-                const float* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu);
-int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* Wp_hi, const float* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld);
+// K padded to whole k-blocks of the variant (32 for 3xTF32, 64 for bf16)
+int64_t tc_kpad(int64_t K, int bf);
+// Node-update GEMMs; bf = 0: 3xTF32 (B operand copies are tf32 hi/lo fp32 arrays), bf = 1: bf16
+// (B operand copy is bf16, *_lo unused).  Return 0 on success, < 0 on mapping / launch failure.
+int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const void* WT_hi,
+                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf);
+int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf);
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
-               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats);
-
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf);
 // Transform-before-aggregate pieces (N1: P(DW) = (PD)W for F_out < F_in):
 //   out[M x N] = act(A[M x K] W_seg^T + addend + bias), W_seg = W_neigh (kb_off 0) or W_self
-//   (kb_off = Fp/32) read from the WT operand copy (ldB = 2Fp columns).
-int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const float* WT_hi, const float* WT_lo,
+//   (kb_off = Fp / k-block) read from the WT operand copy (ldB = 2Fp columns).
+int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const void* WT_hi, const void* WT_lo,
                 int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
-                const float* addend, int64_t ld_add, int relu);
+                const float* addend, int64_t ld_add, int relu, int bf);
 //   J[M x F] = mask o s o ([Q | Mg] [W_neigh | W_self]^T), Q rows M, Mg rows M_inner (rows beyond
 //   are zero), B = WJ [F x 2Kq]; mask / gid / key per DropSpec (R5).
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
-                const float* WJ_hi, const float* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d);
+                const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
+                const int64_t* gid, const DropSpec& d, int bf);
 //   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts.
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
-                  float* G, float* ws, int64_t ws_floats);
+                  float* G, float* ws, int64_t ws_floats, int bf);
 
 }  // namespace pgcn

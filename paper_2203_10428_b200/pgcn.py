@@ -335,7 +335,7 @@ def dev_gemm(op, variant, A0, A1, M, F, W_ext, N, out, ld_out, Mg=None, inv_deg=
     st = stream if stream is not None else torch.cuda.current_stream(out.device)
     ldA = A0.stride(0) if A0 is not None else 0
     ldM = Mg.stride(0) if Mg is not None else 0
-    variant = {"tc": 0, "simt": 2}.get(variant, variant)
+    variant = {"tc": 0, "bf16": 1, "simt": 2}.get(variant, variant)
     _check(lib().pgcn_dev_gemm(int(op), int(variant), _ptr(A0), _ptr(A1), int(ldA), int(M), int(F), _ptr(W_ext),
                                int(N), _ptr(Mg), int(ldM), _ptr(inv_deg), _ptr(out), int(ld_out), int(bool(relu)),
                                scratch.data_ptr(), scratch.numel(), st.cuda_stream))

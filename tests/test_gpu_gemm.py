@@ -1,6 +1,6 @@
 """GPU unit tests of the node-update GEMMs (include/pgcn_dev.h) against float64 numpy matmul of the
-same fp32 inputs.  Tolerance: the fp32 tier, max|gpu - ref| <= 1e-4 * max|ref| (3xTF32 tensor
-cores and SIMT fp32 alike)."""
+same fp32 inputs.  Tolerance: max|gpu - ref| <= tol * max|ref| with tol = 1e-4 for the fp32 tier
+(3xTF32 tensor cores, SIMT fp32) and 2e-2 for the bf16 tensor-core variant (north_star)."""
 import numpy as np
 import pytest
 
@@ -39,7 +39,11 @@ def rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
 
 
-@pytest.mark.parametrize("variant", ["tc", "simt"])
+TOLS = {"tc": 1e-4, "simt": 1e-4, "bf16": 2e-2}
+VARIANTS = ["tc", "simt", "bf16"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("M,F,N", SHAPES)
 def test_forward(P, variant, M, F, N):
     import torch
@@ -51,11 +55,11 @@ def test_forward(P, variant, M, F, N):
     A = np.hstack([A0[:, :F], A1[:, :F], np.ones((M, 1), np.float32)]).astype(np.float64)
     ref = np.maximum(A @ W.astype(np.float64), 0)
     got = out.cpu().numpy()
-    assert rel(got[:, :N], ref) <= 1e-4
+    assert rel(got[:, :N], ref) <= TOLS[variant]
     assert (got[:, N:] == 0).all()
 
 
-@pytest.mark.parametrize("variant", ["tc", "simt"])
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("M,F,N", SHAPES)
 def test_weight_gradient(P, variant, M, F, N):
     import torch
@@ -66,10 +70,10 @@ def test_weight_gradient(P, variant, M, F, N):
     torch.cuda.synchronize()
     A = np.hstack([A0[:, :F], A1[:, :F], np.ones((M, 1), np.float32)]).astype(np.float64)
     ref = A.T @ Mg[:, :N].astype(np.float64)
-    assert rel(out.cpu().numpy(), ref) <= 1e-4
+    assert rel(out.cpu().numpy(), ref) <= TOLS[variant]
 
 
-@pytest.mark.parametrize("variant", ["tc", "simt"])
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("M,F,N", SHAPES)
 def test_input_gradient(P, variant, M, F, N):
     import torch
@@ -81,6 +85,6 @@ def test_input_gradient(P, variant, M, F, N):
     torch.cuda.synchronize()
     dA = Mg[:, :N].astype(np.float64) @ W[:2 * F].astype(np.float64).T
     got = out.cpu().numpy()
-    assert rel(got[:, :F], dA[:, :F] * inv[:, None]) <= 1e-4
-    assert rel(got[:, L:L + F], dA[:, F:]) <= 1e-4
+    assert rel(got[:, :F], dA[:, :F] * inv[:, None]) <= TOLS[variant]
+    assert rel(got[:, L:L + F], dA[:, F:]) <= TOLS[variant]
     assert (got[:, F:L] == 0).all() and (got[:, L + F:] == 0).all()

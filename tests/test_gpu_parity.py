@@ -67,7 +67,7 @@ def run_gpu(P, g, widths, n_parts, T, params0, part_of=None, **kw):
     return recs, ctx
 
 
-def kernel_relu_decision(gpu, tol=TOL):
+def kernel_relu_decision(gpu, tol=TOL):  # noqa: D401
     """sigma' hook for the oracle (reading R25): where |Y| <= tol * max|Y| the sign of Y is not
     resolved by the fp32 kernel's precision, so the oracle takes the kernel's decision (H > 0);
     everywhere else it keeps its own."""
@@ -87,8 +87,8 @@ def kernel_relu_decision(gpu, tol=TOL):
     return decide
 
 
-def oracle_run(gpu, g, n_parts, params0, cfg, T, **kw):
-    dec = kernel_relu_decision(gpu)
+def oracle_run(gpu, g, n_parts, params0, cfg, T, tol=TOL, **kw):
+    dec = kernel_relu_decision(gpu, tol)
     ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, n_parts), params0, cfg, T, relu_decision=dec,
                       **kw)
     return ora
@@ -260,3 +260,30 @@ def test_launches_counted(P):
     g = gen_graph("cora", seed=1, n=300, nnz=1200, f0=8, classes=3)
     gpu, ctx = run_gpu(P, g, [8, 6, 3], 2, 2, glorot_params([8, 6, 3], 1), mode="pipe")
     assert ctx.launch_count() > 20
+
+
+@pytest.mark.parametrize("case", ["cora", "wide", "yelp"])
+@pytest.mark.parametrize("tf", [True, False])
+def test_bf16_tensor_core_variant(P, case, tf):
+    """gemm = bf16 (kind::f16 tcgen05, fp32 accumulation) against the fp64 oracle at the north_star's
+    2e-2 tier, PIPE with smoothing and dropout, both aggregation orders, 2 iterations (SGD)."""
+    tol = 2e-2
+    if case == "cora":
+        g = gen_graph("cora", seed=1)
+        widths = [1433, 16, 7]
+        loss = "ce"
+    elif case == "wide":
+        g = gen_graph("reddit", seed=3, n=1500, nnz=60000, f0=602, classes=41)
+        widths = [602, 256, 41]
+        loss = "ce"
+    else:
+        g = gen_graph("yelp", seed=5, n=2500, nnz=30000, f0=300, classes=100)
+        widths = [300, 512, 100]
+        loss = "bce"
+    params0 = glorot_params(widths, 3)
+    kw = dict(mode="pipe", smooth_f=True, smooth_g=True, dropout=0.3, loss=loss, opt="sgd", lr=0.5, gemm="bf16",
+              transform_first=tf)
+    gpu, _ = run_gpu(P, g, widths, 2, 2, params0, **kw)
+    cfg = ModelCfg(widths=widths, dropout=0.3, lr=0.5, opt="sgd", loss=loss)
+    ora = oracle_run(gpu, g, 2, params0, cfg, 2, tol=tol, mode="pipe", smooth_f=True, smooth_g=True)
+    check_against_oracle(gpu, ora, 2, 2, tol=tol, what="bf16 %s tf%s" % (case, tf))

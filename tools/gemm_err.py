@@ -17,7 +17,7 @@ for (M, F, N) in [(2000, 300, 512), (100000, 256, 256), (100000, 602, 256)]:
     A = np.hstack([A0[:, :F], A1[:, :F], np.ones((M, 1))]).astype(np.float64)
     refs = {0: A @ W.astype(np.float64), 1: A.T @ Mg[:, :N].astype(np.float64),
             2: Mg[:, :N].astype(np.float64) @ W[:2 * F].astype(np.float64).T}
-    for v in ("tc", "simt"):
+    for v in ("tc", "bf16", "simt"):
         out = torch.zeros((M, ld(N)), device="cuda"); P.dev_gemm(0, v, t["A0"], t["A1"], M, F, t["W"], N, out, ld(N))
         e0 = rel(out.cpu().numpy()[:, :N], refs[0])
         out = torch.zeros((2 * F + 1, N), device="cuda"); P.dev_gemm(1, v, t["A0"], t["A1"], M, F, t["W"], N, out, N, Mg=t["Mg"])
