@@ -145,6 +145,8 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       1 (auto): per layer, compute P(D W_neigh) instead of (P D) W_neigh where that
  *                       gathers fewer bytes -- layer 1 if 2 F_1 < F_0, layers >= 2 if F_l < F_{l-1}
  *                       (same mathematics, fp32 reassociation only).  Tensor-core GEMMs only.
+ *   staleness_stats     1: measure the staleness errors of Fig. 5/7 (see pgcn_staleness); local
+ *                       transport only (adds one reduction kernel per layer and direction).
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -163,6 +165,7 @@ typedef struct {
   int32_t dump_j;
   double lr, beta1, beta2, eps;
   int32_t transform_first;
+  int32_t staleness_stats;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this
@@ -240,6 +243,13 @@ typedef struct {
 } pgcn_tensor_desc;
 int pgcn_tensor(pgcn_ctx* ctx, int32_t local, int32_t kind, int32_t layer, int64_t t,
                 pgcn_tensor_desc* out);
+
+/* Fig. 5/7 staleness errors of the last completed iteration for `layer` (1..L):
+ *   feat_err = ||boundary rows of the layer-l input used - the owners' fresh rows||_F (before dropout)
+ *   grad_err = ||feature-gradient messages accumulated into J^(l-1) - the fresh ones||_F
+ * summed over the hosted partitions ("used" = 0 when nothing was received, t = 1; the smoothed
+ * value under EMA).  Needs cfg.staleness_stats and the local transport.  Synchronises.          */
+int pgcn_staleness(pgcn_ctx* ctx, int32_t layer, double* feat_err, double* grad_err);
 
 /* Number of kernels this library launched on the context so far (counted at launch). */
 int64_t pgcn_launch_count(const pgcn_ctx* ctx);

@@ -37,7 +37,10 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
         ema_init="first", seed=4, opt=None, keep_A=False, relu_decision=None):
     """Train for t = 1..T.  Returns a list (one dict per t) with
     loss, H[l][i] (inner rows of layer l output), J[l][i] (inner J^(l) after accumulation),
-    halo[l][i] (boundary rows used as input of layer l), G_parts[i], G, params (after update).
+    halo[l][i] (boundary rows used as input of layer l), G_parts[i], G, params (after update),
+    err_f[l] / err_g[l] (Fig. 5/7: Frobenius norm of the boundary features /
+    received feature-gradient messages actually used minus the fresh ones of the same iteration;
+    0 when nothing is used, e.g. t = 1).
 
     relu_decision(t, l, i, Y) -> bool mask, optional: the sigma'(Y) = 1[Y > 0] decision used in
     the backward (App. A.1).  Default Y > 0.  Parity tests pass a hook that adopts
@@ -67,7 +70,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
     ema_b = {l: [None] * n for l in range(1, L + 1)}
     recs = []
     for t in range(1, T + 1):
-        rec = dict(t=t, H={}, J={}, halo={}, A={}, Y={})
+        rec = dict(t=t, H={}, J={}, halo={}, A={}, Y={}, err_f={}, err_g={})
         H_in = [X[P["inner_gid"]] for P in parts]
         saved = {}
         # ---------------- forward (Alg. 1 l.8-15)
@@ -109,6 +112,8 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                 H_out.append(np.maximum(Y, 0.0) if l < L else Y)
                 saved[(l, i)] = (A, Y, keep)
             rec["halo"][l] = halos
+            # Fig. 5/7: Frobenius norm of (boundary features used - fresh ones)
+            rec["err_f"][l] = float(np.sqrt(sum(((h - a) ** 2).sum() for h, a in zip(halos, arrived))))
             rec["H"][l] = H_out
             if keep_A:
                 rec["A"][l] = [saved[(l, i)][0] for i in range(n)]
@@ -150,6 +155,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
             # message from i to owner j: i's boundary rows owned by j (aligned with S_{j,i})
             cur = [[J_halo[i][parts[i]["halo_off"][j]:parts[i]["halo_off"][j + 1]] for i in range(n)]
                    for j in range(n)]
+            esq = 0.0
             for j in range(n):
                 if mode == "vanilla":
                     contrib = cur[j]
@@ -165,6 +171,9 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                             ema_b[l][j] = [gamma * e + (1.0 - gamma) * c
                                            for e, c in zip(ema_b[l][j], contrib)]
                         contrib = ema_b[l][j]
+                # used minus fresh; nothing received (t = 1) means 0 was used (R9)
+                esq += sum((((c if contrib is not None else 0.0) - f) ** 2).sum()
+                           for c, f in zip(contrib if contrib is not None else cur[j], cur[j]))
                 if contrib is not None:
                     P = parts[j]
                     for i in range(n):                                       # l.23-25
@@ -174,6 +183,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                     recv_b[l][j] = cur[j]                                    # l.27, used at t + 1
             J = J_in
             rec["J"][l - 1] = J
+            rec["err_g"][l] = float(np.sqrt(esq))  # gradient messages used vs fresh (Fig. 5/7)
         # ---------------- l.31-32
         G = []
         for l in range(L):

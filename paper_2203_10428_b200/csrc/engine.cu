@@ -101,6 +101,7 @@ struct pgcn_ctx {
   int tf[PGCN_MAX_LAYERS + 1] = {};
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
+  double* diag = nullptr;              // N4: [2][L+1] squared staleness errors of the current iteration
   int64_t exp_t = 1;
   int exp_kind = pgcn::K_FWD, exp_layer = 1;
   int poisoned = 0;
@@ -252,6 +253,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   }
   C->part_loss = A.take<float>(n_local);
   C->work = A.take<unsigned long long>(4);
+  C->diag = A.take<double>(2 * (PGCN_MAX_LAYERS + 1));
   return PGCN_OK;
 }
 
@@ -641,6 +643,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
+  if (l == 1 && C->cfg.staleness_stats)
+    cudaMemsetAsync(C->diag, 0, sizeof(double) * 2 * (PGCN_MAX_LAYERS + 1), C->s);
   const bool tcg = C->cfg.gemm != 2;
   const int bf = C->cfg.gemm == 1;
   const int kbk = bf ? 64 : 32;
@@ -687,6 +691,14 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_GATHER, (8.0 + (ema ? 4.0 : 0.0)) * F * p.n_bd + 4.0 * p.n_bd);
         gather_rows(Lk, src, p.halo_map, p.n_bd, ldi, Hin + p.n_in * ldi, prev, (float)C->cfg.gamma, ema, first);
       }
+    }
+    // N4: ||boundary rows used - owners' fresh rows||^2 (local transport only)
+    if (C->cfg.staleness_stats && !C->nccl && C->n_parts > 1 && p.n_bd > 0) {
+      SegTable fresh{};
+      fresh.n_seg = C->n_parts;
+      for (int j = 0; j <= C->n_parts; ++j) fresh.off[j] = p.v.halo_off[j];
+      for (int j = 0; j < C->n_parts; ++j) fresh.base[j] = l == 1 ? C->parts[j].X : C->parts[j].H[l - 1][b];
+      stale_err(Lk, fresh, p.halo_map, nullptr, nullptr, Hin + p.n_in * ldi, p.n_bd, ldi, C->F[l - 1], C->diag + l);
     }
     // S3: dropout after the exchange (App. F), aggregation
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
@@ -864,6 +876,20 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                                           (msg.n_seg ? (4.0 * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
       grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, row_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
                   p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi);
+      if (C->cfg.staleness_stats && !C->nccl && C->n_parts > 1 && p.n_send > 0) {
+        // N4: ||gradient messages used - fresh ones||^2 (fresh = peers' boundary rows of this iteration;
+        // used = the smoothed state, the stale messages, or 0 when nothing was received)
+        SegTable fresh{};
+        fresh.n_seg = C->n_parts;
+        for (int j = 0; j <= C->n_parts; ++j) fresh.off[j] = p.v.send_off[j];
+        for (int j = 0; j < C->n_parts; ++j) fresh.base[j] = C->parts[j].J[l - 1][b];
+        if (use_ema)
+          stale_err(Lk, fresh, p.msg_map, nullptr, nullptr, p.emaG[l - 1], p.n_send, ldi, C->F[l - 1],
+                    C->diag + PGCN_MAX_LAYERS + 1 + l);
+        else
+          stale_err(Lk, fresh, p.msg_map, msg.n_seg ? &msg : nullptr, row_map, nullptr, p.n_send, ldi, C->F[l - 1],
+                    C->diag + PGCN_MAX_LAYERS + 1 + l);
+      }
     }
   }
   rc = check_cuda(C, "pgcn_layer_bwd");
@@ -950,6 +976,19 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
 }
 
 extern "C" int64_t pgcn_launch_count(const pgcn_ctx* C) { return C ? C->launches : -1; }
+
+extern "C" int pgcn_staleness(pgcn_ctx* C, int32_t layer, double* feat_err, double* grad_err) {
+  if (!C || layer < 1 || layer > C->L) return fail(PGCN_EINVAL, "pgcn_staleness: bad argument");
+  if (!C->cfg.staleness_stats) return fail(PGCN_ESTATE, "pgcn_staleness: context created without staleness_stats");
+  if (C->nccl) return fail(PGCN_EUNSUPPORTED, "pgcn_staleness: local transport only");
+  double h[2];
+  cudaStreamSynchronize(C->s);
+  cudaMemcpy(&h[0], C->diag + layer, sizeof(double), cudaMemcpyDeviceToHost);
+  cudaMemcpy(&h[1], C->diag + PGCN_MAX_LAYERS + 1 + layer, sizeof(double), cudaMemcpyDeviceToHost);
+  if (feat_err) *feat_err = std::sqrt(h[0]);
+  if (grad_err) *grad_err = std::sqrt(h[1]);
+  return check_cuda(C, "pgcn_staleness");
+}
 
 extern "C" int pgcn_timing_enable(pgcn_ctx* C, int32_t on) {
   if (!C) return fail(PGCN_EINVAL, "ctx is NULL");

@@ -565,6 +565,41 @@ __global__ void k_scale_rows(const float4* __restrict__ M, const float* __restri
     out[i] = f4scale(M[i], sc[i / ld4]);
 }
 
+// ---------------------------------------------------------------- staleness diagnostics (N4)
+// out += sum over rows r, cols c < F of (used(r) - fresh(r))^2, where used(r) is used + r*ld (or 0 if
+// used is null, or the second table `ustab` row) and fresh(r) comes from the segment table `ftab`.
+__global__ void k_stale_err(const __grid_constant__ SegTable ftab, const int32_t* __restrict__ fmap,
+                            const __grid_constant__ SegTable utab, const int32_t* __restrict__ umap,
+                            const float* __restrict__ used, int use_tab, int64_t n_rows, int64_t ld, int64_t F,
+                            double* out) {
+  double a = 0.0;
+  const int64_t total = n_rows * F;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, c = i - r * F;
+    const int s = find_seg(ftab, r);
+    const int64_t fr = fmap ? (int64_t)fmap[r] : r - ftab.off[s];
+    const float f = ftab.base[s][fr * ld + c];
+    float u = 0.f;
+    if (use_tab) {
+      const int su = find_seg(utab, r);
+      const int64_t ur = umap ? (int64_t)umap[r] : r - utab.off[su];
+      u = utab.base[su][ur * ld + c];
+    } else if (used) {
+      u = used[r * ld + c];
+    }
+    const double d = (double)u - (double)f;
+    a += d * d;
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicAdd(out, sh[0]);
+}
+
 // ---------------------------------------------------------------- optimiser (S11, S12)
 __global__ void k_sum_grads(const __grid_constant__ PtrList G, int64_t P, float* __restrict__ grads) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
@@ -818,6 +853,15 @@ void gemm_da_f32(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, c
   if (M <= 0) return;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((2 * ld + BN - 1) / BN));
   k_gemm_da<<<grid, 256, 0, L.s>>>(Mg, ldM, M, N, W, F, inv_deg, dA, ld);
+  count(L);
+}
+
+void stale_err(Launch L, const SegTable& fresh, const int32_t* fmap, const SegTable* used_tab, const int32_t* umap,
+               const float* used, int64_t n_rows, int64_t ld, int64_t F, double* out) {
+  if (n_rows <= 0) return;
+  SegTable none{};
+  k_stale_err<<<grid_for(n_rows * F, 256, kSMs * 4), 256, 0, L.s>>>(fresh, fmap, used_tab ? *used_tab : none, umap, used,
+                                                                    used_tab ? 1 : 0, n_rows, ld, F, out);
   count(L);
 }
 

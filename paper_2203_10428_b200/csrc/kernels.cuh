@@ -48,6 +48,11 @@ void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const floa
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work);
 
+// N4 diagnostics: out[0] += sum_{r < n_rows, c < F} (used(r, c) - fresh(r, c))^2 with fresh rows from a
+// segment table (row_map fmap) and used rows from a segment table (umap), a plain array, or 0.
+void stale_err(Launch, const SegTable& fresh, const int32_t* fmap, const SegTable* used_tab, const int32_t* umap,
+               const float* used, int64_t n_rows, int64_t ld, int64_t F, double* out);
+
 // out[v] = s[v] * M[v] over n rows of stride ld
 void scale_rows(Launch, const float* M, const float* s, int64_t n, int64_t ld, float* out);
 

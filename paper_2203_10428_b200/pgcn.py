@@ -48,7 +48,7 @@ class Config(C.Structure):
                 ("gamma", C.c_double), ("dropout", C.c_double), ("seed", C.c_uint64), ("gemm", C.c_int32),
                 ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
-                ("eps", C.c_double), ("transform_first", C.c_int32)]
+                ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -99,6 +99,7 @@ def lib():
         L.pgcn_dev_gemm_scratch_bytes.restype = C.c_size_t
         L.pgcn_dev_gemm.argtypes = [i32, i32, vp, vp, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, i32, vp,
                                     C.c_size_t, vp]
+        L.pgcn_staleness.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pgcn_dev_spmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
         L.pgcn_dev_l2_read.argtypes = [vp, i64, i32, vp, vp]
         L.pgcn_nccl_unique_id.argtypes = [vp]
@@ -178,7 +179,7 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partit
 def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
-                transform_first=True) -> Config:
+                transform_first=True, staleness_stats=False) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -194,6 +195,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.dump_j = int(bool(dump_j))
     c.lr, c.beta1, c.beta2, c.eps = float(lr), float(beta1), float(beta2), float(eps)
     c.transform_first = int(bool(transform_first))
+    c.staleness_stats = int(bool(staleness_stats))
     return c
 
 
@@ -310,6 +312,12 @@ class Context:
         ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         _check(lib().pgcn_timing_read(self.handle, int(kind), C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
         return dict(ms=ms.value, launches=n.value, bytes=by.value, flops=fl.value)
+
+    def staleness(self, layer):
+        """(feature error, gradient error) of the last iteration for `layer` (Fig. 5/7)."""
+        f, g = C.c_double(), C.c_double()
+        _check(lib().pgcn_staleness(self.handle, int(layer), C.byref(f), C.byref(g)))
+        return f.value, g.value
 
     def launch_count(self) -> int:
         return int(lib().pgcn_launch_count(self.handle))

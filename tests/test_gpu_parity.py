@@ -287,3 +287,43 @@ def test_bf16_tensor_core_variant(P, case, tf):
     cfg = ModelCfg(widths=widths, dropout=0.3, lr=0.5, opt="sgd", loss=loss)
     ora = oracle_run(gpu, g, 2, params0, cfg, 2, tol=tol, mode="pipe", smooth_f=True, smooth_g=True)
     check_against_oracle(gpu, ora, 2, 2, tol=tol, what="bf16 %s tf%s" % (case, tf))
+
+
+@pytest.mark.parametrize("mode,sf,sg", [("pipe", False, False), ("pipe", True, True), ("vanilla", False, False)])
+def test_staleness_errors_match_oracle(P, mode, sf, sg):
+    """N4 / Fig. 5-7: per-layer ||used - fresh||_F of boundary features and gradient
+    messages, GPU (pgcn_staleness) vs the oracle's err_f / err_g.  A norm of differences of fp32
+    quantities: tolerance 1e-3 of the value plus 1e-6 of the fresh magnitude scale."""
+    import torch
+    g = gen_graph("yelp", seed=2, n=3001, nnz=40000, f0=103, classes=13)
+    widths = [103, 70, 45, 13]
+    params0 = glorot_params(widths, 5)
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 3)
+    cfg = P.make_config(widths, mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.7, dropout=0.3, loss="bce",
+                        opt="sgd", lr=2.0, n_global=g.n, n_train_global=g.n_train, staleness_stats=True)
+    ctx = P.Context(part, cfg)
+    keep = []
+    for i in range(3):
+        gid = part.view(i)["inner_gid"]
+        a = (torch.tensor(g.X[gid]).cuda(), torch.tensor(g.labels[gid]).cuda(), torch.tensor(g.train_mask[gid]).cuda())
+        keep.append(a)
+        ctx.set_inputs(i, *a)
+    theta = torch.tensor(P.flatten_params(params0)).cuda()
+    grads = torch.zeros_like(theta)
+    T = 3
+    got = []
+    for t in range(1, T + 1):
+        ctx.step(t, theta, grads, None, None)
+        got.append({l: ctx.staleness(l) for l in range(1, 4)})
+    ora = pipegcn.run(g, oracle_partition(g.n, g.row_ptr, g.col_idx, 3), params0,
+                      ModelCfg(widths=widths, dropout=0.3, lr=2.0, opt="sgd", loss="bce", gamma=0.7), T, mode=mode,
+                      smooth_f=sf, smooth_g=sg)
+    for t in range(T):
+        for l in range(1, 4):
+            f_gpu, g_gpu = got[t][l]
+            f_ora = ora[t]["err_f"][l]
+            g_ora = ora[t]["err_g"].get(l, 0.0)
+            assert abs(f_gpu - f_ora) <= 1e-3 * f_ora + 1e-6, (t, l, f_gpu, f_ora)
+            assert abs(g_gpu - g_ora) <= 1e-3 * g_ora + 1e-9, (t, l, g_gpu, g_ora)
+    if mode == "vanilla":
+        assert all(v == (0.0, 0.0) for d in got for v in d.values())

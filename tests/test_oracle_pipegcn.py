@@ -240,3 +240,33 @@ def test_layer1_exact_for_t_ge_2():
     for t in range(2, 6):
         ref = sage.forward_backward(g, Ws[t - 1], t, c)
         assert close(assemble(parts, recs[t - 1]["H"][1], g.n, 8), ref["H"][1], 1e-12)
+
+
+def test_staleness_error_definition():
+    """Fig. 5/7: err = ||used - fresh||_F.  Vanilla uses fresh values (0); at t = 1
+    PIPE uses zero boundary rows, so err_f equals the norm of the owners' fresh rows (recomputed
+    here from the recorded layer outputs by gid); with eta = 0, p = 0 both errors vanish once the
+    pipeline has filled (t >= 2L); gamma = 0 smoothing gives the unsmoothed errors exactly."""
+    g = small_graph(seed=8)
+    widths = [9, 8, 7, 4]
+    params = glorot_params(widths, 3)
+    parts = partition(g.n, g.row_ptr, g.col_idx, 3)
+    c = cfg(widths, p=0.0, lr=0.2)
+    van = pipegcn.run(g, parts, params, c, 3, mode="vanilla")
+    assert all(v == 0.0 for r in van for v in list(r["err_f"].values()) + list(r["err_g"].values()))
+    pip = pipegcn.run(g, parts, params, c, 3, mode="pipe")
+    H1 = assemble(parts, pip[0]["H"][1], g.n, widths[1])
+    fresh = np.concatenate([H1[P["halo_gid"]] for P in parts])
+    assert np.isclose(pip[0]["err_f"][2], np.linalg.norm(fresh), rtol=1e-13)
+    c0 = cfg(widths, p=0.0, lr=0.0)
+    L = 3
+    z = pipegcn.run(g, parts, params, c0, 2 * L + 1, mode="pipe")
+    assert z[0]["err_f"][2] > 0 and z[0]["err_g"][2] > 0
+    for t in range(2 * L, 2 * L + 1):
+        for l in range(1, L + 1):
+            assert z[t - 1]["err_f"][l] <= 1e-12 * max(1.0, z[0]["err_f"][2])
+        for l in range(2, L + 1):
+            assert z[t - 1]["err_g"][l] <= 1e-12 * max(1.0, z[0]["err_g"][2])
+    s0 = pipegcn.run(g, parts, params, c, 3, mode="pipe", smooth_f=True, smooth_g=True, gamma=0.0)
+    for a, b in zip(pip, s0):
+        assert a["err_f"] == b["err_f"] and a["err_g"] == b["err_g"]
