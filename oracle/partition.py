@@ -85,15 +85,27 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None):
         inv_ptr = np.zeros(n_in + 1, dtype=np.int64)
         np.cumsum(np.bincount(si, minlength=n_in), out=inv_ptr[1:])
         P.update(n_inner=n_in, n_halo=n_bd, nnz=int(rp[-1]), n_send=int(si.size),
+                 deg=deg[np.concatenate([inner, halo])].astype(np.int64),
                  row_ptr=rp, col_idx=lc.astype(np.int32), inv_deg=inv,
                  t_row_ptr=t_rp, t_col_idx=rows_of[order].astype(np.int32),
                  inv_ptr=inv_ptr, inv_pos=iorder.astype(np.int32))
     return parts
 
 
-def local_P(P):
-    """scipy CSR of P_i (n_inner x (n_inner + n_halo)) with values inv_deg[v] (Eq. 3)."""
+def local_P(P, model="sage"):
+    """scipy CSR of P_i (n_inner x (n_inner + n_halo)).
+    sage: values inv_deg[v] (mean aggregator, Eq. 3).
+    gcn:  P = D~^-1/2 (A + I) D~^-1/2 (App. A.1), D~ = d + 1 (full-graph degrees of
+          both endpoints, incl. boundary nodes): P_i[v, u] = 1/sqrt((d_v+1)(d_u+1)) for u in N(v) and
+          the self loop u = v."""
     import scipy.sparse as sp
     n_in, n_all = P["n_inner"], P["n_inner"] + P["n_halo"]
-    vals = np.repeat(P["inv_deg"], np.diff(P["row_ptr"]))
-    return sp.csr_matrix((vals, P["col_idx"].astype(np.int64), P["row_ptr"]), shape=(n_in, n_all))
+    if model == "sage":
+        vals = np.repeat(P["inv_deg"], np.diff(P["row_ptr"]))
+        return sp.csr_matrix((vals, P["col_idx"].astype(np.int64), P["row_ptr"]), shape=(n_in, n_all))
+    s = 1.0 / np.sqrt(P["deg"].astype(np.float64) + 1.0)
+    rows = np.repeat(np.arange(n_in), np.diff(P["row_ptr"]))
+    cols = P["col_idx"].astype(np.int64)
+    r = np.concatenate([rows, np.arange(n_in)])
+    c = np.concatenate([cols, np.arange(n_in)])
+    return sp.csr_matrix((s[r] * s[c], (r, c)), shape=(n_in, n_all))

@@ -53,7 +53,8 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
     N = g.n
     p = cfg.dropout
     s = 1.0 / (1.0 - p) if p > 0 else 1.0
-    Ps = [local_P(P) for P in parts]
+    model = getattr(cfg, "model", "sage")
+    Ps = [local_P(P, model) for P in parts]
     PTs = [Pm.T.tocsr() for Pm in Ps]
     gids = [np.concatenate([P["inner_gid"], P["halo_gid"]]) for P in parts]
     X = np.asarray(g.X, dtype=np.float64)
@@ -107,7 +108,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                 full = np.vstack([H_in[i], halos[i]])
                 D, keep = dropout(full, t, l, L, N, gids[i], seed, p)
                 Z = Ps[i] @ D
-                A = np.hstack([Z, D[:parts[i]["n_inner"]]])
+                A = np.hstack([Z, D[:parts[i]["n_inner"]]]) if model == "sage" else Z
                 Y = A @ W + b
                 H_out.append(np.maximum(Y, 0.0) if l < L else Y)
                 saved[(l, i)] = (A, Y, keep)
@@ -133,7 +134,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
         G_parts = [[None] * L for _ in range(n)]
         for l in range(L, 0, -1):
             W, b = params[l - 1]
-            F = W.shape[0] // 2
+            F = W.shape[0] // 2 if model == "sage" else W.shape[0]
             J_in, J_halo = [], []
             for i in range(n):
                 A, Y, keep = saved[(l, i)]
@@ -145,8 +146,11 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                 G_parts[i][l - 1] = (A.T @ M, M.sum(0))                      # l.18
                 if l > 1:                                                    # l.20
                     dA = M @ W.T
-                    dD = PTs[i] @ dA[:, :F]
-                    dD[:parts[i]["n_inner"]] += dA[:, F:]
+                    if model == "sage":
+                        dD = PTs[i] @ dA[:, :F]
+                        dD[:parts[i]["n_inner"]] += dA[:, F:]
+                    else:
+                        dD = PTs[i] @ dA
                     Jf = dD * keep * s
                     J_in.append(Jf[:parts[i]["n_inner"]].copy())
                     J_halo.append(Jf[parts[i]["n_inner"]:])

@@ -26,9 +26,20 @@ import scipy.sparse as sp
 from .hashmask import dropout
 
 
-def prop_matrix(n, row_ptr, col_idx, inv_deg=None):
+def prop_matrix(n, row_ptr, col_idx, inv_deg=None, model="sage", deg_full=None):
+    """sage: P[v, u] = inv_deg[v] for u in N(v) (Eq. 3).
+    gcn:  P = D~^-1/2 (A + I) D~^-1/2 (App. A.1, PAPER.md:637) with D~ = deg_full + 1 (deg_full
+          defaults to the row lengths; overridden to pin Alg. 1 l.6 with full-graph degrees)."""
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
     deg = np.diff(row_ptr)
+    if model == "gcn":
+        d = deg if deg_full is None else np.asarray(deg_full)
+        s = 1.0 / np.sqrt(d.astype(np.float64) + 1.0)
+        rows = np.repeat(np.arange(n), deg)
+        cols = np.asarray(col_idx, dtype=np.int64)
+        r = np.concatenate([rows, np.arange(n)])
+        c = np.concatenate([cols, np.arange(n)])
+        return sp.csr_matrix((s[r] * s[c], (r, c)), shape=(n, n))
     if inv_deg is None:
         inv_deg = np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
     vals = np.repeat(np.asarray(inv_deg, dtype=np.float64), deg)
@@ -66,12 +77,15 @@ def loss_and_grad(Y, labels, train_mask, n_train, kind):
     return float(loss), J
 
 
-def forward_backward(g, params, t, cfg, seed=4, inv_deg=None, n_train=None):
+def forward_backward(g, params, t, cfg, seed=4, inv_deg=None, n_train=None, deg_full=None):
     """One full-graph iteration t: returns dict(H, A, Y, loss, J, grads).
-    g: synth.Graph-like (n, row_ptr, col_idx, X, labels, train_mask); params: [(W, b)]."""
+    g: synth.Graph-like (n, row_ptr, col_idx, X, labels, train_mask); params: [(W, b)].
+    cfg.model "sage" (default, A = [PD | D], W = [W_neigh; W_self]) or "gcn" (A = P D, App. A.1
+    PAPER.md:637-647 with the bias of reading R26)."""
     n = g.n
     L = len(params)
-    P = prop_matrix(n, g.row_ptr, g.col_idx, inv_deg)
+    model = getattr(cfg, "model", "sage")
+    P = prop_matrix(n, g.row_ptr, g.col_idx, inv_deg, model, deg_full)
     gids = np.arange(n)
     p = cfg.dropout
     H = np.asarray(g.X, dtype=np.float64)
@@ -80,7 +94,7 @@ def forward_backward(g, params, t, cfg, seed=4, inv_deg=None, n_train=None):
         W, b = (np.asarray(a, dtype=np.float64) for a in params[l - 1])
         D, keep = dropout(H, t, l, L, n, gids, seed, p)
         Z = P @ D
-        A = np.hstack([Z, D])
+        A = np.hstack([Z, D]) if model == "sage" else Z
         Y = A @ W + b
         H = np.maximum(Y, 0.0) if l < L else Y
         out["A"].append(A)
@@ -94,14 +108,16 @@ def forward_backward(g, params, t, cfg, seed=4, inv_deg=None, n_train=None):
     grads = [None] * L
     for l in range(L, 0, -1):
         W = np.asarray(params[l - 1][0], dtype=np.float64)
-        F = W.shape[0] // 2
         M = J * (out["Y"][l - 1] > 0) if l < L else J
         grads[l - 1] = (out["A"][l - 1].T @ M, M.sum(0))
         if l > 1:
             dA = M @ W.T
-            dZ, dD = dA[:, :F], dA[:, F:]
             s = 1.0 / (1.0 - p) if p > 0 else 1.0
-            J = (P.T @ dZ + dD) * out["keep"][l - 1] * s
+            if model == "sage":
+                F = W.shape[0] // 2
+                J = (P.T @ dA[:, :F] + dA[:, F:]) * out["keep"][l - 1] * s
+            else:
+                J = (P.T @ dA) * out["keep"][l - 1] * s
             Js[l - 1] = J
     out["J"] = Js
     out["grads"] = grads

@@ -58,6 +58,7 @@ class ModelCfg:
     opt: str                # "adam" | "sgd"
     loss: str               # "ce" | "bce"
     gamma: float = 0.95     # default smoothing decay
+    model: str = "sage"     # "sage" (GraphSAGE-mean, CONCAT) or "gcn" (App. A.1 propagation)
 
     @property
     def n_layers(self) -> int:
@@ -181,14 +182,15 @@ def gen_graph(name: str, seed: int = 1, n: Optional[int] = None, nnz: Optional[i
                  multilabel=bool(c["multilabel"]))
 
 
-def glorot_params(widths, seed: int = 3):
-    """Per-layer (W [2F_in x F_out] float32, b [F_out] float32); W rows 0..F_in-1 multiply
-    the aggregated z, rows F_in..2F_in-1 the node's own h (CONCAT(z, h))."""
+def glorot_params(widths, seed: int = 3, model: str = "sage"):
+    """Per-layer (W, b float32).  sage: W [2F_in x F_out], rows 0..F_in-1 multiply the aggregated
+    z, rows F_in..2F_in-1 the node's own h (CONCAT(z, h)).  gcn: W [F_in x F_out]."""
     rng = np.random.default_rng(seed)
     out = []
+    k = 2 if model == "sage" else 1
     for fi, fo in zip(widths[:-1], widths[1:]):
-        a = np.sqrt(6.0 / (2 * fi + fo))
-        W = rng.uniform(-a, a, (2 * fi, fo)).astype(np.float32)
+        a = np.sqrt(6.0 / (k * fi + fo))
+        W = rng.uniform(-a, a, (k * fi, fo)).astype(np.float32)
         out.append((W, np.zeros(fo, dtype=np.float32)))
     return out
 
