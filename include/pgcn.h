@@ -98,7 +98,10 @@ int pgcn_partition(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col_i
  *                            with u in N(v), ascending v
  *   inv_ptr [n_inner+1], inv_pos [n_send]
  *                            inverse send map: positions k with send_idx[k] == v, ascending k
- *                            (Alg. 1 l.23-25 accumulation)                                  */
+ *                            (Alg. 1 l.23-25 accumulation)
+ *   deg [n_inner+n_halo]     full-graph degree d_u of every local row (inner then boundary);
+ *                            the GCN-sym weights 1/sqrt((d_v+1)(d_u+1)) of App. A.1
+ *                            need it for boundary columns too (reading R26)                  */
 typedef struct {
   int32_t part, n_parts;
   int64_t n_inner, n_halo, nnz, n_send;
@@ -114,6 +117,7 @@ typedef struct {
   const int32_t* t_col_idx;
   const int64_t* inv_ptr;
   const int32_t* inv_pos;
+  const int64_t* deg;
 } pgcn_part_view;
 
 int pgcn_partition_view(const pgcn_partitioning* p, int32_t part, pgcn_part_view* out);
@@ -147,6 +151,9 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       (same mathematics, fp32 reassociation only).  Tensor-core GEMMs only.
  *   staleness_stats     1: measure the staleness errors of Fig. 5/7 (see pgcn_staleness); local
  *                       transport only (adds one reduction kernel per layer and direction).
+ *   model               0 GraphSAGE-mean (above); 1 GCN-sym (SURVEY N3, App. A.1 PAPER.md:637-647,
+ *                       reading R26): Y = P D W + b with P = D~^-1/2 (A + I) D~^-1/2, D~ = d + 1
+ *                       (full-graph degrees), W [F_{l-1} x F_l]; tensor-core GEMMs only (gemm 0/1).
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -166,6 +173,7 @@ typedef struct {
   double lr, beta1, beta2, eps;
   int32_t transform_first;
   int32_t staleness_stats;
+  int32_t model;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this
@@ -205,7 +213,8 @@ int pgcn_set_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* la
 
 /* Flat parameter vector theta = vec[W^(1), b^(1), ..., W^(L), b^(L)], fp32,
  * unpadded: W^(l) is [2F_{l-1} x F_l] row-major (rows 0..F_{l-1}-1 multiply z, the rest h;
- * CONCAT(z_v, h_v) PAPER.md:44, reading R3), b^(l) is [F_l].                               */
+ * CONCAT(z_v, h_v) PAPER.md:44, reading R3), b^(l) is [F_l].  GCN-sym (cfg.model 1): W^(l) is
+ * [F_{l-1} x F_l].                                                                          */
 int64_t pgcn_param_count(const pgcn_config* cfg);
 
 /* (3) Alg. 1 l.9-14 for layer `layer` (1..L) of every hosted partition, iteration t.
@@ -232,7 +241,8 @@ int pgcn_step(pgcn_ctx* ctx, int64_t t, float* params, float* grads, float* opt_
 /* Device views of internal buffers for parity checks and diagnostics (not needed to train).
  * kind: PGCN_T_H   layer-l output H^(l) (l = 1..L; l = L: logits), inner rows, parity of t
  *       PGCN_T_HIN layer-l input buffer [inner; boundary] rows (l = 1..L)
- *       PGCN_T_Z   aggregated Z of layer l (inner rows)
+ *       PGCN_T_Z   aggregated Z of layer l (inner rows); with transform-first S = P_i (D W_neigh)
+ *                  (GraphSAGE) -- not kept for GCN-sym transform-first layers (PGCN_EINVAL)
  *       PGCN_T_J   accumulated J^(l) inner rows (needs cfg.dump_j; l = 1..L-1), t's parity
  *       PGCN_T_G   this partition's G_i, flat like theta
  * The returned pointer is valid until the next call that writes that buffer.               */

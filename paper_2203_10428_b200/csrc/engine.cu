@@ -39,6 +39,7 @@ struct PartCtx {
   int32_t *col = nullptr, *tcol = nullptr, *halo_map = nullptr, *msg_map = nullptr, *send_idx = nullptr,
           *inv_pos = nullptr;
   float* inv_deg = nullptr;
+  float* sym = nullptr;  // GCN-sym: d~_u^-1/2 = 1/sqrt(d_u + 1) of inner then boundary rows (R26)
   float* X = nullptr;
   float* H[PGCN_MAX_LAYERS + 1][2] = {};
   float* logits = nullptr;
@@ -99,6 +100,7 @@ struct pgcn_ctx {
   int64_t Fp[PGCN_MAX_LAYERS + 1] = {}, Kp[PGCN_MAX_LAYERS + 1] = {}, Kq[PGCN_MAX_LAYERS + 1] = {};
   // N1 transform-before-aggregate per layer: Y = P(D W_neigh) + D W_self + b instead of (PD) W_neigh
   int tf[PGCN_MAX_LAYERS + 1] = {};
+  int gcn = 0, ns = 2;  // cfg.model == 1 (GCN-sym, R26); weight row segments
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
   double* diag = nullptr;              // N4: [2][L+1] squared staleness errors of the current iteration
@@ -153,12 +155,15 @@ int validate_cfg(const pgcn_config* c) {
   if (c->opt != 0 && c->opt != 1) return fail(PGCN_EINVAL, "opt must be 0 (SGD) or 1 (Adam)");
   if (c->n_train_global < 1) return fail(PGCN_EINVAL, "n_train_global < 1");
   if (!(c->gamma >= 0.0 && c->gamma <= 1.0)) return fail(PGCN_EINVAL, "gamma out of [0,1]");
+  if (c->model != 0 && c->model != 1) return fail(PGCN_EINVAL, "model must be 0 (GraphSAGE) or 1 (GCN-sym)");
+  if (c->model == 1 && c->gemm == 2) return fail(PGCN_EUNSUPPORTED, "GCN-sym needs the tensor-core GEMMs (gemm 0/1)");
   return PGCN_OK;
 }
 
 int64_t param_count(const pgcn_config* c) {
   int64_t P = 0;
-  for (int l = 1; l <= c->n_layers; ++l) P += (2 * (int64_t)c->width[l - 1] + 1) * c->width[l];
+  const int64_t k = c->model == 1 ? 1 : 2;
+  for (int l = 1; l <= c->n_layers; ++l) P += (k * (int64_t)c->width[l - 1] + 1) * c->width[l];
   return P;
 }
 
@@ -180,6 +185,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.rp = A.take<int64_t>(p.n_in + 1);
     p.col = A.take<int32_t>(p.nnz);
     p.inv_deg = A.take<float>(p.n_in);
+    if (C->cfg.model == 1) p.sym = A.take<float>(p.n_all);
     p.trp = A.take<int64_t>(p.n_all + 1);
     p.tcol = A.take<int32_t>(p.nnz);
     p.gid = A.take<int64_t>(p.n_all);
@@ -193,7 +199,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       for (int b = 0; b < 2; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
     p.logits = A.take<float>(p.n_in * C->ld[L]);
     for (int l = 1; l <= L; ++l) {
-      if (C->cfg.dropout > 0.0) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
+      if (C->cfg.dropout > 0.0 || C->cfg.model == 1) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
       p.Z[l] = A.take<float>(p.n_in * (C->tf[l] ? C->ld[l] : C->ld[l - 1]));   // Z, or S = inv_deg P T
       if (C->tf[l]) p.T[l] = A.take<float>(p.n_all * C->ld[l]);                 // T = D W_neigh, then Q
     }
@@ -225,29 +231,30 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         for (int b = 0; b < 2; ++b) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
     }
   }
-  if (C->cfg.gemm == 0) {  // 3xTF32 operand copies: fp32 hi/lo, k-blocks of 32
+  const int64_t ns = C->ns;  // weight row segments: 2 GraphSAGE [W_neigh; W_self], 1 GCN-sym
+  if (C->cfg.gemm == 0) {     // 3xTF32 operand copies: fp32 hi/lo, k-blocks of 32
     for (int l = 1; l <= L; ++l) {
       C->Fp[l] = round_up(C->F[l - 1], 32);
       C->Kp[l] = round_up(C->F[l], 4);
-      C->WT_hi[l] = A.take<float>(C->F[l] * 2 * C->Fp[l]);
-      C->WT_lo[l] = A.take<float>(C->F[l] * 2 * C->Fp[l]);
-      C->Wp_hi[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
-      C->Wp_lo[l] = A.take<float>(2 * C->F[l - 1] * C->Kp[l]);
+      C->WT_hi[l] = A.take<float>(C->F[l] * ns * C->Fp[l]);
+      C->WT_lo[l] = A.take<float>(C->F[l] * ns * C->Fp[l]);
+      C->Wp_hi[l] = A.take<float>(ns * C->F[l - 1] * C->Kp[l]);
+      C->Wp_lo[l] = A.take<float>(ns * C->F[l - 1] * C->Kp[l]);
       if (C->tf[l]) {
         C->Kq[l] = round_up(C->F[l], 32);
-        C->WJ_hi[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
-        C->WJ_lo[l] = A.take<float>(C->F[l - 1] * 2 * C->Kq[l]);
+        C->WJ_hi[l] = A.take<float>(C->F[l - 1] * ns * C->Kq[l]);
+        C->WJ_lo[l] = A.take<float>(C->F[l - 1] * ns * C->Kq[l]);
       }
     }
   } else if (C->cfg.gemm == 1) {  // bf16 operand copies, k-blocks of 64 (stored in the *_hi slots)
     for (int l = 1; l <= L; ++l) {
       C->Fp[l] = round_up(C->F[l - 1], 64);
       C->Kp[l] = round_up(C->F[l], 8);
-      C->WT_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l] * 2 * C->Fp[l]));
-      C->Wp_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(2 * C->F[l - 1] * C->Kp[l]));
+      C->WT_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l] * ns * C->Fp[l]));
+      C->Wp_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(ns * C->F[l - 1] * C->Kp[l]));
       if (C->tf[l]) {
         C->Kq[l] = round_up(C->F[l], 64);
-        C->WJ_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l - 1] * 2 * C->Kq[l]));
+        C->WJ_hi[l] = reinterpret_cast<float*>(A.take<uint16_t>(C->F[l - 1] * ns * C->Kq[l]));
       }
     }
   }
@@ -294,8 +301,10 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
     C->ld[l] = ld_of(cfg->width[l]);
     if (C->ld[l] > C->ldmax) C->ldmax = C->ld[l];
   }
+  C->gcn = cfg->model == 1;
+  C->ns = C->gcn ? 1 : 2;
   C->woff[1] = 0;
-  for (int l = 1; l <= C->L; ++l) C->woff[l + 1] = C->woff[l] + (2 * C->F[l - 1] + 1) * C->F[l];
+  for (int l = 1; l <= C->L; ++l) C->woff[l + 1] = C->woff[l] + (C->ns * C->F[l - 1] + 1) * C->F[l];
   // N1 traffic rule (gathered row widths per iteration): layer 1 aggregates F_0 forward only
   // (no J^(0), R11) vs F_1 forward + F_1 backward; layers >= 2 aggregate F_in both ways vs F_out.
   for (int l = 1; l <= C->L; ++l) {
@@ -559,6 +568,12 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     cudaMemcpyAsync(p.rp, v.row_ptr, sizeof(int64_t) * (p.n_in + 1), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.col, v.col_idx, sizeof(int32_t) * p.nnz, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.inv_deg, v.inv_deg, sizeof(float) * p.n_in, cudaMemcpyHostToDevice, s);
+    std::vector<float> sym;
+    if (p.sym) {  // d~^-1/2 = 1/sqrt(d + 1), correctly rounded from double (App. A.1, R26)
+      sym.resize(p.n_all);
+      for (int64_t r = 0; r < p.n_all; ++r) sym[r] = (float)(1.0 / std::sqrt((double)v.deg[r] + 1.0));
+      cudaMemcpyAsync(p.sym, sym.data(), sizeof(float) * p.n_all, cudaMemcpyHostToDevice, s);
+    }
     cudaMemcpyAsync(p.trp, v.t_row_ptr, sizeof(int64_t) * (p.n_all + 1), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.tcol, v.t_col_idx, sizeof(int32_t) * p.nnz, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.gid, gid.data(), sizeof(int64_t) * p.n_all, cudaMemcpyHostToDevice, s);
@@ -651,10 +666,10 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   if (tcg) {
     Scope sc(C, PGCN_K_GEMM_FWD, 0.0);
     if (bf)
-      tc_wprep_bf16(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
-                    C->Wp_hi[l], C->WJ_hi[l], C->s);
+      tc_wprep_bf16(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->ns,
+                    C->WT_hi[l], C->Wp_hi[l], C->WJ_hi[l], C->s);
     else
-      tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->WT_hi[l],
+      tc_wprep(Wext, (int)C->F[l - 1], (int)C->F[l], (int)C->Fp[l], (int)C->Kp[l], (int)C->Kq[l], C->ns, C->WT_hi[l],
                C->WT_lo[l], C->Wp_hi[l], C->Wp_lo[l], C->WJ_hi[l], C->WJ_lo[l], C->s);
     ++C->launches;
   }
@@ -703,14 +718,39 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     // S3: dropout after the exchange (App. F), aggregation
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
     const float* D = Hin;
-    if (C->cfg.dropout > 0.0) {
-      Scope sc(C, PGCN_K_DROPOUT, 8.0 * Fi * p.n_all + 8.0 * p.n_all);
-      dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, n_valid, p.gid, drop_spec(C, t, l));
+    if (C->cfg.dropout > 0.0 || C->gcn) {  // GCN-sym: D' = d~^-1/2 o dropout(H) (the right factor of P)
+      Scope sc(C, PGCN_K_DROPOUT, 8.0 * Fi * p.n_all + 8.0 * p.n_all + (C->gcn ? 4.0 * p.n_all : 0.0));
+      dropout_fwd(Lk, Hin, p.D[l], ldi, p.n_all, n_valid, p.gid, drop_spec(C, t, l), p.sym);
       D = p.D[l];
     }
     p.n_valid[l] = n_valid;
     float* out = l < C->L ? p.H[l][b] : p.logits;
-    const float* bias = Wext + 2 * C->F[l - 1] * C->F[l];
+    const float* bias = Wext + C->ns * C->F[l - 1] * C->F[l];
+    if (C->gcn) {
+      // GCN-sym (App. A.1, R26): Y = d~^-1/2 o (A + I) D' W + b
+      if (C->tf[l]) {  // N1: T = D' W over the valid local rows, then H = act(d~^-1/2 o (A + I) T + b)
+        {
+          Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * n_valid * (Fi + Fo), 2.0 * n_valid * Fi * Fo);
+          if (tc_fwd_1seg(Lk, D, n_valid, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], p.T[l],
+                          ldo, nullptr, nullptr, 0, 0, bf))
+            return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
+        }
+        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
+                                         4.0 * Fo * p.n_in);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, p.n_in, n_valid, out, C->work, 1, bias, C->F[l], l < C->L);
+        continue;
+      }
+      {
+        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
+                                         4.0 * Fi * p.n_in);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1);
+      }
+      Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
+      if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
+                      bias, nullptr, 0, l < C->L, bf))
+        return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
+      continue;
+    }
     if (C->tf[l]) {
       // N1: T = D W_neigh (all valid local rows), S = inv_deg o P_i T, Y = D_in W_self + S + b
       {
@@ -788,7 +828,55 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
-    const float* D = C->cfg.dropout > 0.0 ? p.D[l] : layer_in(p, l, b);
+    const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
+    if (C->gcn) {
+      // GCN-sym backward (App. A.1 PAPER.md:651-657 with P = S (A + I) S, S = diag(d~^-1/2), R26)
+      if (C->tf[l]) {
+        // Q = (A + I)^T (S M) over inner + boundary rows; G = [D'^T Q ; colsum M]; J = mask o s o S (Q W^T)
+        const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
+        {
+          Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fo * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+                                           8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all);
+          scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
+          DropSpec none{};
+          none.width = (int32_t)C->F[l];
+          spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work);
+        }
+        {
+          Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
+          if (tc_dw_general(Lk, D, p.T[l], nv, nullptr, nullptr, 0, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
+                            p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf))
+            return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
+        }
+        if (l >= 2) {
+          Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_all * (Fo + Fi), 2.0 * p.n_all * Fo * Fi);
+          if (tc_fwd_mask(Lk, p.T[l], p.n_all, nullptr, 0, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
+                          C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, p.sym))
+            return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
+        }
+        continue;
+      }
+      {
+        Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (Fi + Fo), 2.0 * p.n_in * (Fi + 1) * Fo);
+        if (tc_dw_general(Lk, p.Z[l], p.M, p.n_in, nullptr, nullptr, 0, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
+                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf))
+          return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
+      }
+      if (l >= 2) {
+        {  // dZs = S (M W^T)
+          Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * Fi);
+          if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.sym, p.dA,
+                         ldi, bf, 1))
+            return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
+        }
+        // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
+        Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+                                         4.0 * Fi * p.n_all + 12.0 * p.n_all);
+        spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
+                 C->work, p.sym);
+      }
+      continue;
+    }
     if (C->tf[l]) {
       // N1 backward: Q = P_i^T (inv_deg o M) over inner + boundary rows (width F_out);
       // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
@@ -811,7 +899,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * (p.n_all + p.n_in) * Fo + 4.0 * p.n_all * Fi,
                  2.0 * (p.n_all + p.n_in) * Fo * Fi);
         if (tc_fwd_mask(Lk, p.T[l], p.n_all, p.M, p.n_in, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
-                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf))
+                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, nullptr))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
       }
       continue;
@@ -832,7 +920,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * 2 * Fi);
         if (C->cfg.gemm != 2) {
           if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.inv_deg,
-                         p.dA, ldi, bf))
+                         p.dA, ldi, bf, 2))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         } else {
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
@@ -959,7 +1047,7 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
       *o = {(void*)layer_in(p, l, b), p.n_all, C->F[l - 1], C->ld[l - 1]};
       return PGCN_OK;
     case PGCN_T_Z:  // Z = inv_deg P D (width F_{l-1}); transform-first layers: S = inv_deg P (D W_neigh)
-      if (!lok) break;
+      if (!lok || (C->gcn && C->tf[l])) break;
       *o = {(void*)p.Z[l], p.n_in, C->tf[l] ? C->F[l] : C->F[l - 1], C->tf[l] ? C->ld[l] : C->ld[l - 1]};
       return PGCN_OK;
     case PGCN_T_J:

@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           if (row < p.M) {
             float* out = p.out + (int64_t)row * p.ld_out;
             const uint64_t g = (uint64_t)p.gid[row];
+            const float rs = p.rscale ? p.rscale[row] : 1.f;  // GCN-sym: d~_u^-1/2 (R26)
 #pragma unroll
             for (int g4 = 0; g4 < 4; ++g4) {
               const int n = T.n0 + c0 + 4 * g4;
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
               float e[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                float x = v[4 * g4 + j];
+                float x = v[4 * g4 + j] * rs;
                 if (n + j >= p.N) {
                   x = 0.f;
                 } else if (p.mask_on) {
@@ -591,27 +592,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
   }
 }
 
-// W prep: for layer weights W [2F x N] (+ bias), write the tf32 hi/lo splits in the two TMA
-// layouts used above: WT [N x 2Fp] (FWD operand B, K-major; cols [0,F) = W_neigh^T,
-// [Fp, Fp+F) = W_self^T) and Wp [2F x Kp] (DA operand B, K-major).
-// WJ [F x 2Kq] (Kq = round_up(N, 32)): row f = [W_neigh[f, :] | W_self[f, :]], the B operand of the
-// transform-first input gradient J = [Q | M] [W_neigh | W_self]^T (null to skip).
-__global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo,
-                        float* Wp_hi, float* Wp_lo, float* WJ_hi, float* WJ_lo) {
-  const int64_t total_t = (int64_t)N * 2 * Fp, total_p = (int64_t)2 * F * Kp;
-  const int64_t total_j = WJ_hi ? (int64_t)F * 2 * Kq : 0;
+// W prep: for layer weights W [ns F x N] (ns = 2 GraphSAGE [W_neigh; W_self], ns = 1 GCN-sym), write
+// the tf32 hi/lo splits in the two TMA layouts used above: WT [N x ns Fp] (FWD operand B, K-major;
+// segment s = cols [s Fp, s Fp + F)) and Wp [ns F x Kp] (DA operand B, K-major).
+// WJ [F x ns Kq] (Kq = round_up(N, 32)): row f = [W_neigh[f, :] | W_self[f, :]] (GCN: W[f, :]), the
+// B operand of the transform-first input gradient J = [Q | M] [W_neigh | W_self]^T (null to skip).
+__global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, int ns, float* WT_hi,
+                        float* WT_lo, float* Wp_hi, float* Wp_lo, float* WJ_hi, float* WJ_lo) {
+  const int64_t total_t = (int64_t)N * ns * Fp, total_p = (int64_t)ns * F * Kp;
+  const int64_t total_j = WJ_hi ? (int64_t)F * ns * Kq : 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p + total_j;
        i += (int64_t)gridDim.x * blockDim.x) {
     float x = 0.f;
     if (i >= total_t + total_p) {
-      const int64_t j = i - total_t - total_p, f = j / (2 * Kq), k = j % (2 * Kq);
+      const int64_t j = i - total_t - total_p, f = j / (ns * Kq), k = j % (ns * Kq);
       const int seg = (int)(k / Kq), c = (int)(k % Kq);
       if (c < N) x = W[((int64_t)seg * F + f) * N + c];
       const float h = tf32_rna(x);
       WJ_hi[j] = h;
       WJ_lo[j] = tf32_rna(x - h);
     } else if (i < total_t) {
-      const int64_t n = i / (2 * Fp), k = i % (2 * Fp);
+      const int64_t n = i / (ns * Fp), k = i % (ns * Fp);
       const int seg = (int)(k / Fp), f = (int)(k % Fp);
       if (f < F) x = W[((int64_t)seg * F + f) * N + n];
       const float h = tf32_rna(x);
@@ -627,22 +628,22 @@ __global__ void k_wprep(const float* __restrict__ W, int F, int N, int Fp, int K
   }
 }
 
-// bf16 operand copies of W [2F x N] (RNE): WT [N x 2Fp] (FWD B), Wp [2F x Kp] (DA B) and optionally
-// WJ [F x 2Kq] (transform-first J), Fp/Kq multiples of 64 elements, Kp of 8.
-__global__ void k_wprep_bf16(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, __nv_bfloat16* WT,
-                             __nv_bfloat16* Wp, __nv_bfloat16* WJ) {
-  const int64_t total_t = (int64_t)N * 2 * Fp, total_p = (int64_t)2 * F * Kp;
-  const int64_t total_j = WJ ? (int64_t)F * 2 * Kq : 0;
+// bf16 operand copies of W [ns F x N] (RNE): WT [N x ns Fp] (FWD B), Wp [ns F x Kp] (DA B) and
+// optionally WJ [F x ns Kq] (transform-first J), Fp/Kq multiples of 64 elements, Kp of 8.
+__global__ void k_wprep_bf16(const float* __restrict__ W, int F, int N, int Fp, int Kp, int Kq, int ns,
+                             __nv_bfloat16* WT, __nv_bfloat16* Wp, __nv_bfloat16* WJ) {
+  const int64_t total_t = (int64_t)N * ns * Fp, total_p = (int64_t)ns * F * Kp;
+  const int64_t total_j = WJ ? (int64_t)F * ns * Kq : 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_t + total_p + total_j;
        i += (int64_t)gridDim.x * blockDim.x) {
     float x = 0.f;
     if (i >= total_t + total_p) {
-      const int64_t j = i - total_t - total_p, f = j / (2 * Kq), k = j % (2 * Kq);
+      const int64_t j = i - total_t - total_p, f = j / (ns * Kq), k = j % (ns * Kq);
       const int seg = (int)(k / Kq), c = (int)(k % Kq);
       if (c < N) x = W[((int64_t)seg * F + f) * N + c];
       WJ[j] = __float2bfloat16_rn(x);
     } else if (i < total_t) {
-      const int64_t n = i / (2 * Fp), k = i % (2 * Fp);
+      const int64_t n = i / (ns * Fp), k = i % (ns * Fp);
       const int seg = (int)(k / Fp), f = (int)(k % Fp);
       if (f < F) x = W[((int64_t)seg * F + f) * N + n];
       WT[i] = __float2bfloat16_rn(x);
@@ -755,20 +756,21 @@ cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms) {
   return cudaGetLastError();
 }
 
-void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, void* WT, void* Wp, void* WJ, cudaStream_t s) {
-  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp + (WJ ? (int64_t)F * 2 * Kq : 0);
+void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, void* WT, void* Wp, void* WJ,
+                   cudaStream_t s) {
+  const int64_t total = (int64_t)N * ns * Fp + (int64_t)ns * F * Kp + (WJ ? (int64_t)F * ns * Kq : 0);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 8) grid = 148 * 8;
-  tc::k_wprep_bf16<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, static_cast<__nv_bfloat16*>(WT),
+  tc::k_wprep_bf16<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, ns, static_cast<__nv_bfloat16*>(WT),
                                         static_cast<__nv_bfloat16*>(Wp), static_cast<__nv_bfloat16*>(WJ));
 }
 
-void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo, float* Wp_hi,
+void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, float* WT_hi, float* WT_lo, float* Wp_hi,
               float* Wp_lo, float* WJ_hi, float* WJ_lo, cudaStream_t s) {
-  const int64_t total = (int64_t)N * 2 * Fp + (int64_t)2 * F * Kp + (WJ_hi ? (int64_t)F * 2 * Kq : 0);
+  const int64_t total = (int64_t)N * ns * Fp + (int64_t)ns * F * Kp + (WJ_hi ? (int64_t)F * ns * Kq : 0);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 8) grid = 148 * 8;
-  tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, WT_hi, WT_lo, Wp_hi, Wp_lo, WJ_hi, WJ_lo);
+  tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, ns, WT_hi, WT_lo, Wp_hi, Wp_lo, WJ_hi, WJ_lo);
 }
 
 // ---------------------------------------------------------------------------------------- mode wrappers
@@ -868,7 +870,7 @@ int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, con
 
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
                 const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d, int bf) {
+                const int64_t* gid, const DropSpec& d, int bf, const float* rscale) {
   if (M <= 0) return 0;
   TcParams p{};
   const float* A[2] = {Q, Mg};
@@ -884,33 +886,36 @@ int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_
   p.scale = d.scale;
   p.width = d.width;
   p.mask_on = d.on;
-  if (M_inner <= 0) return launch_fwd(L, 1, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p, bf);
-  return launch_fwd(L, 2, A, rows, ld, K, WJ_hi, WJ_lo, 2 * Kq, off, M, F, p, bf);
+  p.rscale = rscale;
+  const int64_t ldB = Mg ? 2 * Kq : Kq;  // GCN-sym: one segment (Mg == nullptr), B = WJ [F x Kq]
+  if (M_inner <= 0 || !Mg) return launch_fwd(L, 1, A, rows, ld, K, WJ_hi, WJ_lo, ldB, off, M, F, p, bf);
+  return launch_fwd(L, 2, A, rows, ld, K, WJ_hi, WJ_lo, ldB, off, M, F, p, bf);
 }
 
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf) {
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves) {
   if (M <= 0) return 0;
+  if (halves != 1 && halves != 2) return -1;
   TcParams p{};
   const int BN = tc_bn(F);
   tc_common(p, BN, bf, TC_DA);
   bool ok = tc_map(&p.map_a[0], Mg, false, N, M, ldM, 32, 128, bf ? 0 : 1);
-  if (bf) ok = ok && tc_map(&p.map_b[0], Wp_hi, true, N, 2 * F, Kp, 64, BN, 1);
+  if (bf) ok = ok && tc_map(&p.map_b[0], Wp_hi, true, N, halves * F, Kp, 64, BN, 1);
   else
-    ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, 2 * F, Kp, 32, BN, 1) &&
-         tc_map(&p.map_b_lo, Wp_lo, false, N, 2 * F, Kp, 32, BN, 1);
+    ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, halves * F, Kp, 32, BN, 1) &&
+         tc_map(&p.map_b_lo, Wp_lo, false, N, halves * F, Kp, 32, BN, 1);
   if (!ok) return -1;
   p.mode = TC_DA;
   p.epi = EPI_DA;
   p.nseg = 1;
   p.n_ntiles_half = (int)((F + BN - 1) / BN);
-  p.n_ntiles = 2 * p.n_ntiles_half;
+  p.n_ntiles = halves * p.n_ntiles_half;
   p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
   p.kb_seg[0] = (int)((N + (bf ? 63 : 31)) / (bf ? 64 : 32));
   p.M = (int)M;
   p.N = (int)N;
   p.F = (int)F;
-  p.ld_out = 2 * ld;
+  p.ld_out = halves * ld;
   p.ld_half = ld;
   p.out = dA;
   p.inv_deg = inv_deg;
@@ -921,7 +926,9 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
                   float* G, float* ws, int64_t ws_floats, int bf) {
-  const int64_t K = 2 * F + 1;
+  const int nseg = A1 ? 2 : 1;  // GCN-sym: G = [A0^T B0 ; colsum(Mb)]
+  if (!A1) rows1 = 0;
+  const int64_t K = nseg * F + 1;
   const int64_t rmax = rows0 > rows1 ? rows0 : rows1;
   if (rmax <= 0) {
     cudaMemsetAsync(G, 0, sizeof(float) * K * N, L.s);
@@ -937,15 +944,15 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const float* Bs[2] = {B0, B1};
   const int64_t rows[2] = {rows0, rows1};
   bool ok = true;
-  for (int s = 0; s < 2 && ok; ++s)
+  for (int s = 0; s < nseg && ok; ++s)
     ok = tc_map(&p.map_a[s], As[s], false, F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, bf ? 0 : 2) &&
          tc_map(&p.map_b[s], Bs[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, bf ? 0 : 2);
   if (!ok) return -1;
   p.mode = TC_DW;
   p.epi = EPI_PART;
-  p.nseg = 2;
+  p.nseg = nseg;
   p.Z = Zs;
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < nseg; ++s) {
     p.kb_seg[s] = (int)((rows[s] + 31) / 32);
     p.kb_per_split[s] = (p.kb_seg[s] + Zs - 1) / Zs;
     if (p.kb_per_split[s] < 1) p.kb_per_split[s] = 1;
@@ -953,7 +960,7 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   }
   p.n_ftiles = (int)((F + 127) / 128);
   p.n_ntiles = (int)((N + BN - 1) / BN);
-  p.n_tiles = 2 * Zs * p.n_ftiles * p.n_ntiles;
+  p.n_tiles = nseg * Zs * p.n_ftiles * p.n_ntiles;
   p.M = (int)rmax;
   p.N = (int)N;
   p.F = (int)F;
@@ -966,9 +973,9 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
   dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
   if (rowsMb > 0) {
-    tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * NP, 2 * F * NP);
+    tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * NP, nseg * F * NP);
   } else {
-    for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * NP + 2 * F * NP, 0, sizeof(float) * N, L.s);
+    for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * NP + nseg * F * NP, 0, sizeof(float) * N, L.s);
   }
   split_reduce_strided(L, ws, Zs, K, N, NP, G);
   if (L.count) *L.count += 2;
@@ -1015,16 +1022,16 @@ extern "C" int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const
   Launch L{s, nullptr};
   int rc = 0;
   if (variant == 0) {
-    if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, 0, WT_hi, WT_lo, Wp_hi, Wp_lo, nullptr, nullptr, s);
+    if (op != 1) tc_wprep(W, (int)F, (int)N, (int)Fp, (int)Kp, 0, 2, WT_hi, WT_lo, Wp_hi, Wp_lo, nullptr, nullptr, s);
     if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, WT_lo, W + 2 * F * N, N, out, ld_out, relu, 0);
     else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats, 0);
-    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2, 0);
+    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, Wp_lo, Kp, F, inv_deg, out, ld_out / 2, 0, 2);
   } else if (variant == 1) {
     const int64_t Fb = (F + 63) / 64 * 64, Kb = (N + 7) / 8 * 8;
-    if (op != 1) tc_wprep_bf16(W, (int)F, (int)N, (int)Fb, (int)Kb, 0, WT_hi, Wp_hi, nullptr, s);
+    if (op != 1) tc_wprep_bf16(W, (int)F, (int)N, (int)Fb, (int)Kb, 0, 2, WT_hi, Wp_hi, nullptr, s);
     if (op == 0) rc = gemm_fwd_tc(L, A0, A1, ldA, M, F, WT_hi, nullptr, W + 2 * F * N, N, out, ld_out, relu, 1);
     else if (op == 1) rc = gemm_dw_tc(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats, 1);
-    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, nullptr, Kb, F, inv_deg, out, ld_out / 2, 1);
+    else rc = gemm_da_tc(L, Mg, ldM, M, N, Wp_hi, nullptr, Kb, F, inv_deg, out, ld_out / 2, 1, 2);
   } else {
     if (op == 0) gemm_fwd_f32(L, A0, A1, ldA, M, F, W, N, out, ld_out, relu);
     else if (op == 1) gemm_dw_f32(L, A0, A1, ldA, M, F, Mg, ldM, N, out, ws, ws_floats);

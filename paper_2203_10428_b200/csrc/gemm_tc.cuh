@@ -28,6 +28,7 @@ struct alignas(64) TcParams {
   uint32_t thr;
   float scale;
   int width, mask_on;
+  const float* rscale;  // EPI_MASK: optional per-row scale (GCN-sym d~^-1/2)
   int bf;  // 1: bf16 operands (kind::f16), 0: 3xTF32 (kind::tf32)
 };
 
@@ -35,13 +36,14 @@ bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, in
                bool mn_major = false);
 int tc_stages(int BN, int bf, int mode);
 size_t tc_smem_bytes(int BN, int S, int bf, int mode);
-void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, void* WT, void* Wp, void* WJ, cudaStream_t s);
+void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, void* WT, void* Wp, void* WJ,
+                   cudaStream_t s);
 int tc_bn(int64_t N);
 int tc_tmem_cols(int BN);
 cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms);
-// W [2F x N] -> tf32 hi/lo operand copies: WT [N x 2Fp] (FWD B), Wp [2F x Kp] (DA B), optionally
-// WJ [F x 2Kq] (transform-first input-gradient B; null to skip).
-void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, float* WT_hi, float* WT_lo, float* Wp_hi,
+// W [ns F x N] (ns = 2 GraphSAGE, 1 GCN-sym) -> tf32 hi/lo operand copies: WT [N x ns Fp] (FWD B),
+// Wp [ns F x Kp] (DA B), optionally WJ [F x ns Kq] (transform-first input-gradient B; null to skip).
+void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, float* WT_hi, float* WT_lo, float* Wp_hi,
               float* Wp_lo, float* WJ_hi, float* WJ_lo, cudaStream_t s);
 struct Launch;
 struct DropSpec;
@@ -53,8 +55,10 @@ int64_t tc_kpad(int64_t K, int bf);
 // (B operand copy is bf16, *_lo unused).  Return 0 on success, < 0 on mapping / launch failure.
 int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const void* WT_hi,
                 const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf);
+// dA = Mg W^T; halves = 2: [dZ' | dD] (GraphSAGE, first half scaled by inv_deg, row stride 2 ld),
+// halves = 1: inv_deg o (Mg W^T) (GCN-sym, row stride ld).
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf);
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves);
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
                int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf);
 // Transform-before-aggregate pieces (N1: P(DW) = (PD)W for F_out < F_in):
@@ -63,12 +67,14 @@ int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M,
 int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const void* WT_hi, const void* WT_lo,
                 int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
                 const float* addend, int64_t ld_add, int relu, int bf);
-//   J[M x F] = mask o s o ([Q | Mg] [W_neigh | W_self]^T), Q rows M, Mg rows M_inner (rows beyond
-//   are zero), B = WJ [F x 2Kq]; mask / gid / key per DropSpec (R5).
+//   J[M x F] = mask o s o rscale o ([Q | Mg] [W_neigh | W_self]^T), Q rows M, Mg rows M_inner (rows
+//   beyond are zero), B = WJ [F x 2Kq]; mask / gid / key per DropSpec (R5).  GCN-sym: Mg = nullptr,
+//   J = mask o s o rscale o (Q W^T) with B = WJ [F x Kq]; rscale (per row) may be null.
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
                 const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d, int bf);
-//   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts.
+                const int64_t* gid, const DropSpec& d, int bf, const float* rscale);
+//   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts;
+//   A1 == nullptr: G[(F+1) x N] = [A0^T B0 ; colsum(Mb)] (GCN-sym).
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
                   float* G, float* ws, int64_t ws_floats, int bf);

@@ -67,7 +67,7 @@ __device__ __forceinline__ int find_seg(const SegTable& t, int64_t r) {
 
 // ---------------------------------------------------------------- dropout (S3 prologue, R5)
 __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, int64_t ld4, int64_t n_rows,
-                          int64_t n_valid, const int64_t* __restrict__ gid, DropSpec d) {
+                          int64_t n_valid, const int64_t* __restrict__ gid, DropSpec d, const float* __restrict__ rs) {
   const int64_t total = n_rows * ld4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / ld4, x = i - r * ld4;
@@ -75,11 +75,12 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
     if (r < n_valid) {
       const float4 h = H[i];
       const int64_t g = gid[r];
+      const float sr = rs ? rs[r] : 1.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t c = 4 * x + j;
         float v = 0.f;
-        if (c < d.width && keep_el(d, g, c)) v = comp(h, j) * d.scale;
+        if (c < d.width && (!d.on || keep_el(d, g, c))) v = comp(h, j) * d.scale * sr;
         set_comp(out, j, v);
       }
     }
@@ -112,7 +113,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              const float* __restrict__ inv_deg,
                                                              const float4* __restrict__ D, int64_t ld4, int64_t n_rows,
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
-                                                             unsigned long long* work) {
+                                                             unsigned long long* work, int self,
+                                                             const float* __restrict__ bias, int64_t n_bias, int relu) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -124,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
     const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
     float4 acc[NC];
 #pragma unroll
-    for (int q = 0; q < NC; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < NC; ++q)  // GCN-sym self loop (A + I, R26): the row's own (inner) input
+      acc[q] = (self && x0 + q * G < ld4) ? __ldg(D + row * ld4 + x0 + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -158,8 +161,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
     }
     const float s = inv_deg[row];
 #pragma unroll
-    for (int q = 0; q < NC; ++q)
-      if (x0 + q * G < ld4) Z[row * ld4 + x0 + q * G] = f4scale(acc[q], s);
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = x0 + q * G;
+      if (x >= ld4) continue;
+      float4 o = f4scale(acc[q], s);
+      if (bias) {  // fused node-update epilogue (GCN-sym transform-first: H = act(P (D W) + b))
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float v = comp(o, j) + (4 * x + j < n_bias ? bias[4 * x + j] : 0.f);
+          set_comp(o, j, relu ? fmaxf(v, 0.f) : v);
+        }
+      }
+      Z[row * ld4 + x] = o;
+    }
   }
 }
 
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
-                                                             unsigned long long* work) {
+                                                             unsigned long long* work, const float* __restrict__ rs) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -214,11 +228,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
       }
     }
     const int64_t g = gid[u0];
+    const float sr = rs ? rs[u0] : 1.f;  // GCN-sym: d~_u^-1/2 of the (inner or boundary) row u (R26)
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
-      float4 o = acc[q];
+      float4 o = rs ? f4scale(acc[q], sr) : acc[q];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t c = 4 * x + j;
@@ -708,16 +723,17 @@ static void count(const Launch& L, int64_t n = 1) {
 }
 
 void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows, int64_t n_valid,
-                 const int64_t* gid, const DropSpec& d) {
+                 const int64_t* gid, const DropSpec& d, const float* rs) {
   const int64_t ld4 = ld / 4;
   if (n_rows <= 0) return;
   k_dropout<<<grid_for(n_rows * ld4, kThreads), kThreads, 0, L.s>>>(
-      reinterpret_cast<const float4*>(H), reinterpret_cast<float4*>(D), ld4, n_rows, n_valid, gid, d);
+      reinterpret_cast<const float4*>(H), reinterpret_cast<float4*>(D), ld4, n_rows, n_valid, gid, d, rs);
   count(L);
 }
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
-              int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work) {
+              int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
+              int64_t n_bias, int relu) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
   const SpmmShape sh = spmm_shape(ld4);
@@ -729,7 +745,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_fwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid,   \
-                                                             sh.nchunk, Z4, work);                             \
+                                                             sh.nchunk, Z4, work, self, bias, n_bias, relu);   \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -738,7 +754,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
-              const DropSpec& d, unsigned long long* work) {
+              const DropSpec& d, unsigned long long* work, const float* rs) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
   const SpmmShape sh = spmm_shape(ld4);
@@ -752,7 +768,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
-                                                             sh.nchunk, J4, ld4, gid, d, work);                \
+                                                             sh.nchunk, J4, ld4, gid, d, work, rs);            \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X

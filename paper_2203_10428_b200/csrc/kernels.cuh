@@ -33,20 +33,28 @@ struct Launch {
 };
 
 // S3 prologue: D = dropout(H) over rows [0, n_rows); rows >= n_valid are written as 0.
+// rs (optional, per row): D[r] *= rs[r] (GCN-sym prescale by d~^-1/2, R26); with d.on == 0 a plain
+// (row-scaled) copy.
 void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, int64_t n_valid,
-                 const int64_t* gid, const DropSpec& d);
+                 const int64_t* gid, const DropSpec& d, const float* rs = nullptr);
 
 // S3: Z[v] = inv_deg[v] * sum_{e in row v} D[col[e]]   (neighbours >= n_valid contribute 0)
 // work: per-launch atomic item counter (8 bytes of device scratch) for dynamic row scheduling,
 // or nullptr for static grid-stride.
+// GCN-sym (R26): self = 1 adds the row's own D[v] (A + I); inv_deg then holds d~_v^-1/2.
+// bias (optional, n_bias entries): Z = act(Z + b) epilogue (relu = ReLU), fusing the node update of
+// a transform-first GCN layer.
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
-              const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work);
+              const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
+              int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0);
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
+//     rs (optional, GCN-sym R26): the sum is scaled by rs[u] = d~_u^-1/2 before the mask (dDs = dZs
+//     then realises the self loop).
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
-              const int64_t* gid, const DropSpec& d, unsigned long long* work);
+              const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr);
 
 // N4 diagnostics: out[0] += sum_{r < n_rows, c < F} (used(r, c) - fresh(r, c))^2 with fresh rows from a
 // segment table (row_map fmap) and used rows from a segment table (umap), a plain array, or 0.

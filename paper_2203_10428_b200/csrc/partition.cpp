@@ -27,6 +27,7 @@ struct PartArrays {
   std::vector<int64_t> inner_gid, halo_gid, halo_off, send_off, row_ptr, t_row_ptr, inv_ptr;
   std::vector<int32_t> send_idx, col_idx, t_col_idx, inv_pos;
   std::vector<float> inv_deg;
+  std::vector<int64_t> deg;  // full-graph degree of inner then boundary rows (GCN-sym, R26)
 };
 
 struct pgcn_partitioning {
@@ -172,6 +173,9 @@ extern "C" int pgcn_partition(int64_t n, const int64_t* row_ptr, const int32_t* 
         A.row_ptr[r + 1] = A.row_ptr[r] + d;
         A.inv_deg[r] = d > 0 ? 1.0f / (float)d : 0.0f;
       }
+      A.deg.resize(n_in + n_bd);
+      for (int64_t r = 0; r < n_in; ++r) A.deg[r] = A.row_ptr[r + 1] - A.row_ptr[r];
+      for (int64_t k = 0; k < n_bd; ++k) A.deg[n_in + k] = row_ptr[A.halo_gid[k] + 1] - row_ptr[A.halo_gid[k]];
       A.col_idx.resize(A.row_ptr[n_in]);
       std::vector<int64_t> tcount(n_in + n_bd + 1, 0);
       for (int64_t r = 0; r < n_in; ++r) {
@@ -221,6 +225,7 @@ extern "C" int pgcn_partition_view(const pgcn_partitioning* p, int32_t part, pgc
   o->t_col_idx = A.t_col_idx.data();
   o->inv_ptr = A.inv_ptr.data();
   o->inv_pos = A.inv_pos.data();
+  o->deg = A.deg.data();
   return PGCN_OK;
 }
 

@@ -39,7 +39,8 @@ class PartView(C.Structure):
                 ("send_idx", C.POINTER(C.c_int32)), ("row_ptr", C.POINTER(C.c_int64)),
                 ("col_idx", C.POINTER(C.c_int32)), ("inv_deg", C.POINTER(C.c_float)),
                 ("t_row_ptr", C.POINTER(C.c_int64)), ("t_col_idx", C.POINTER(C.c_int32)),
-                ("inv_ptr", C.POINTER(C.c_int64)), ("inv_pos", C.POINTER(C.c_int32))]
+                ("inv_ptr", C.POINTER(C.c_int64)), ("inv_pos", C.POINTER(C.c_int32)),
+                ("deg", C.POINTER(C.c_int64))]
 
 
 class Config(C.Structure):
@@ -48,7 +49,8 @@ class Config(C.Structure):
                 ("gamma", C.c_double), ("dropout", C.c_double), ("seed", C.c_uint64), ("gemm", C.c_int32),
                 ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
-                ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32)]
+                ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
+                ("model", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -157,7 +159,8 @@ class Partitioning:
                     send_idx=arr(v.send_idx, ns, np.int32), row_ptr=arr(v.row_ptr, n_in + 1, np.int64),
                     col_idx=arr(v.col_idx, nnz, np.int32), inv_deg=arr(v.inv_deg, n_in, np.float32),
                     t_row_ptr=arr(v.t_row_ptr, n_in + n_bd + 1, np.int64), t_col_idx=arr(v.t_col_idx, nnz, np.int32),
-                    inv_ptr=arr(v.inv_ptr, n_in + 1, np.int64), inv_pos=arr(v.inv_pos, ns, np.int32))
+                    inv_ptr=arr(v.inv_ptr, n_in + 1, np.int64), inv_pos=arr(v.inv_pos, ns, np.int32),
+                    deg=arr(v.deg, n_in + n_bd, np.int64))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -179,7 +182,7 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partit
 def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
-                transform_first=True, staleness_stats=False) -> Config:
+                transform_first=True, staleness_stats=False, model="sage") -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -196,6 +199,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.lr, c.beta1, c.beta2, c.eps = float(lr), float(beta1), float(beta2), float(eps)
     c.transform_first = int(bool(transform_first))
     c.staleness_stats = int(bool(staleness_stats))
+    c.model = {"sage": 0, "gcn": 1}[model]
     return c
 
 
@@ -209,11 +213,12 @@ def flatten_params(layers) -> np.ndarray:
                            for W, b in layers]).astype(np.float32)
 
 
-def unflatten_params(theta, widths):
+def unflatten_params(theta, widths, model="sage"):
     out, o = [], 0
+    k = 2 if model == "sage" else 1
     for fi, fo in zip(widths[:-1], widths[1:]):
-        W = theta[o:o + 2 * fi * fo].reshape(2 * fi, fo)
-        o += 2 * fi * fo
+        W = theta[o:o + k * fi * fo].reshape(k * fi, fo)
+        o += k * fi * fo
         b = theta[o:o + fo]
         o += fo
         out.append((W, b))

@@ -38,7 +38,7 @@ def test_exports_every_declared_symbol(P):
 
 
 ARRAYS = ["inner_gid", "halo_gid", "halo_off", "send_off", "send_idx", "row_ptr", "col_idx", "t_row_ptr",
-          "t_col_idx", "inv_ptr", "inv_pos"]
+          "t_col_idx", "inv_ptr", "inv_pos", "deg"]
 
 
 def compare(pv, ov):
