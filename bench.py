@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--mode", default="pipe", choices=["pipe", "vanilla"])
     ap.add_argument("--smooth", default="", help="'', 'f', 'g' or 'gf'")
     ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "bf16"])
+    ap.add_argument("--model", default="sage", choices=["sage", "gcn"],
+                    help="GraphSAGE-mean (the paper's benchmark model) or GCN-sym (App. A.1, SURVEY N3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -150,16 +152,18 @@ def max_over_ranks(x, dist):
     return float(t.item())
 
 
-def build_workload(name, n_parts):
+def build_workload(name, n_parts, model="sage"):
+    import dataclasses
+
     from synth.graphs import CONFIGS, gen_graph, glorot_params, model_for
     t0 = time.time()
     g = gen_graph(name, seed=1)
-    m = model_for(name)
-    params0 = glorot_params(m.widths, 3)
+    m = dataclasses.replace(model_for(name), model=model)
+    params0 = glorot_params(m.widths, 3, model=model)
     return g, m, params0, time.time() - t0
 
 
-def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2):
+def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2, model="sage"):
     """The oracle (oracle/, numpy/scipy fp64) as it stands, on a bounded sample of the same workload:
     the same generator recipe, degree, widths, dropout and partition count at N = sample_n, timed
     for `iters` PipeGCN iterations; per-epoch time extrapolated linearly in N (every term of the
@@ -170,8 +174,9 @@ def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2):
     c = CONFIGS[name]
     deg = c["nnz"] / c["n"]
     g = gen_graph(name, seed=1, n=sample_n, nnz=int(sample_n * deg))
-    m = model_for(name)
-    params0 = glorot_params(m.widths, 3)
+    import dataclasses
+    m = dataclasses.replace(model_for(name), model=model)
+    params0 = glorot_params(m.widths, 3, model=model)
     parts_o = opart(g.n, g.row_ptr, g.col_idx, parts)
     t0 = time.time()
     pipegcn.run(g, parts_o, params0, m, iters, mode=mode, smooth_f="f" in smooth, smooth_g="g" in smooth)
@@ -180,9 +185,9 @@ def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2):
     epoch_s = dt * scale
     cores = len(os.sched_getaffinity(0))
     return {"value": 1.0 / epoch_s, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "oracle PipeGCN (%s) %d iterations on a %s-recipe graph with N=%d (nnz=%d, same degree, widths, "
-                      "dropout, %d partitions); %.2f s/iteration x N_full/N_sample=%.1f" % (
-                          mode, iters, name, sample_n, g.nnz, parts, dt, scale)}
+            "sample": "oracle PipeGCN (%s, %s) %d iterations on a %s-recipe graph with N=%d (nnz=%d, same degree, "
+                      "widths, dropout, %d partitions); %.2f s/iteration x N_full/N_sample=%.1f" % (
+                          mode, model, iters, name, sample_n, g.nnz, parts, dt, scale)}
 
 
 def run_reference(args):
@@ -192,11 +197,11 @@ def run_reference(args):
     parts = args.parts or max(2, args.gpus)
     vals = []
     for _ in range(args.warmup):
-        cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1)
+        cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1, model=args.model)
     info = None
     t0 = time.time()
     for _ in range(args.steps):
-        info = cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1)
+        info = cpu_baseline(args.config, parts, args.mode, args.smooth, iters=1, model=args.model)
         vals.append(1.0 / info["value"])
     wall = time.time() - t0
     ms = 1000.0 * sum(vals) / len(vals)
@@ -204,7 +209,8 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "%s-synthetic, %d partitions, %s" % (args.config, parts, args.mode)},
+           "config": {"workload": "%s-synthetic, %d partitions, %s%s" % (
+               args.config, parts, args.mode, "" if args.model == "sage" else ", GCN-sym")},
            "cpu_baseline": dict(info, value=v),
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": wall}
@@ -236,13 +242,13 @@ def main():
     parts = args.parts or (max(2, args.gpus) if world == 1 else world)
     if world > 1 and parts != world:
         raise SystemExit("multi-GPU runs host one partition per rank (--parts must equal WORLD_SIZE)")
-    g, m, params0, t_gen = build_workload(args.config, parts)
+    g, m, params0, t_gen = build_workload(args.config, parts, args.model)
     t0 = time.time()
     part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
     t_part = time.time() - t0
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
-                           n_train_global=g.n_train, gemm=args.gemm)
+                           n_train_global=g.n_train, gemm=args.gemm, model=args.model)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
@@ -385,7 +391,7 @@ def main():
     cpu = None
     if not args.no_cpu and world == 1:
         try:
-            cpu = cpu_baseline(args.config, parts, args.mode, args.smooth)
+            cpu = cpu_baseline(args.config, parts, args.mode, args.smooth, model=args.model)
         except Exception as e:  # noqa: BLE001
             cpu = {"error": str(e)}
     if rank != 0:
@@ -393,9 +399,9 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU(s), %s%s, "
-                                  "dropout %.1f, Adam" % (args.config, g.n, g.nnz, m.widths, parts, world, args.mode,
-                                                          ("-" + args.smooth.upper()) if args.smooth else "",
-                                                          m.dropout),
+                                  "dropout %.1f, Adam%s" % (args.config, g.n, g.nnz, m.widths, parts, world, args.mode,
+                                                            ("-" + args.smooth.upper()) if args.smooth else "",
+                                                            m.dropout, "" if args.model == "sage" else ", GCN-sym"),
                       "global_batch": g.n,
                       "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
                       ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
@@ -182,9 +183,9 @@ __host__ __device__ inline Geo geometry(int bf, int mode, int BN) {
 // DW: tile = (segment, split z, f-tile, n-tile); K loop = the split's row blocks of that segment.
 __device__ __forceinline__ void decode(const TcParams& p, int t, Tile& T) {
   if (p.mode == TC_DW) {
-    const int per_seg = p.Z * p.n_ftiles * p.n_ntiles;
-    T.seg = t / per_seg;
-    int r = t - T.seg * per_seg;
+    const int seg0 = p.Zseg[0] * p.n_ftiles * p.n_ntiles;  // segment-major, per-segment split counts
+    T.seg = t < seg0 ? 0 : 1;
+    int r = t - (T.seg ? seg0 : 0);
     const int nt = r % p.n_ntiles;
     r /= p.n_ntiles;
     const int ft = r % p.n_ftiles;
@@ -213,11 +214,13 @@ __device__ __forceinline__ void decode(const TcParams& p, int t, Tile& T) {
   }
 }
 
-__device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 (dropout mask, reading R5)
+// Bits 40..63 of SplitMix64(z) (dropout mask, reading R5); the output xorshift z ^ (z >> 31) does not
+// touch them and is skipped.
+__device__ __forceinline__ uint32_t smix_top24(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+  return (uint32_t)(z >> 40);
 }
 
 template <int BF>
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         } else if (p.epi == EPI_MASK) {  // dropout backward of the layer input (R5)
           if (row < p.M) {
             float* out = p.out + (int64_t)row * p.ld_out;
-            const uint64_t g = (uint64_t)p.gid[row];
+            const uint64_t kr = ((uint64_t)p.key_base + (uint64_t)p.gid[row]) * (uint64_t)p.width;
             const float rs = p.rscale ? p.rscale[row] : 1.f;  // GCN-sym: d~_u^-1/2 (R26)
 #pragma unroll
             for (int g4 = 0; g4 < 4; ++g4) {
@@ -544,8 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
                 if (n + j >= p.N) {
                   x = 0.f;
                 } else if (p.mask_on) {
-                  const uint64_t key = (p.key_base + g) * (uint64_t)p.width + (uint64_t)(n + j);
-                  x = (uint32_t)(smix(key ^ p.seed) >> 40) >= p.thr ? x * p.scale : 0.f;
+                  x = smix_top24((kr + (uint64_t)(n + j)) ^ p.seed) >= p.thr ? x * p.scale : 0.f;
                 }
                 e[j] = x;
               }
@@ -789,18 +791,43 @@ static int dw_bn(int64_t N, int bf) {
   return (int)(bn > 256 ? 256 : bn);
 }
 
-static int dw_splits(int64_t M, int64_t F, int64_t N) {
-  const int BN = dw_bn(N, 0);
-  const int64_t tiles = 2 * ((F + 127) / 128) * ((N + BN - 1) / BN);
-  int64_t Z = (2 * 148 + tiles - 1) / tiles;
-  const int64_t kb = (M + 31) / 32;
-  if (Z > kb) Z = kb;
-  if (Z < 1) Z = 1;
-  return (int)Z;
+// Split-K plan of the dW GEMM: each of the n_seg segments (row counts kb_s k-blocks of 32 rows) is cut
+// into Z_s splits so that every tile (segment, split, f-tile, n-tile) carries about the same number of
+// k-blocks and the tile count fits W whole waves of the 148-CTA persistent grid (W = 1..3, the cheapest
+// by "W x largest tile + per-tile overhead").  Balancing per segment matters for transform-first layers,
+// whose two segments have n_all and n_in rows.
+constexpr int kDwMaxWaves = 3;
+static int dw_base(int64_t F, int64_t N) { return (int)(((F + 127) / 128) * ((N + dw_bn(N, 0) - 1) / dw_bn(N, 0))); }
+static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
+  const int64_t ovh = 6;  // per-tile fill / drain, in k-block units
+  int64_t best = INT64_MAX;
+  Z[0] = 1;
+  Z[1] = nseg > 1 ? 1 : 0;
+  for (int W = 1; W <= kDwMaxWaves; ++W) {
+    const int slots = W * 148 / base;
+    if (slots < nseg) continue;
+    const int lo = 1, hi = nseg > 1 ? slots - 1 : slots;
+    for (int z0 = lo; z0 <= hi; ++z0) {
+      int64_t a = z0 < kb0 ? z0 : (kb0 > 0 ? kb0 : 1);
+      int64_t b = nseg > 1 ? (slots - z0 < kb1 ? slots - z0 : (kb1 > 0 ? kb1 : 1)) : 0;
+      const int64_t kpt = std::max((kb0 + a - 1) / a, nseg > 1 ? (kb1 + b - 1) / b : (int64_t)0);
+      const int64_t waves = ((a + b) * base + 147) / 148;
+      const int64_t cost = waves * (kpt + ovh);
+      if (cost < best) {
+        best = cost;
+        Z[0] = (int)a;
+        Z[1] = (int)b;
+      }
+    }
+  }
 }
 
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
-  return (int64_t)dw_splits(M, F, N) * (2 * F + 1) * ((N + 3) / 4 * 4);
+  int64_t Z = kDwMaxWaves * 148 / dw_base(F, N);
+  const int64_t kb = (M + 31) / 32;
+  if (Z > kb) Z = kb;
+  if (Z < 1) Z = 1;
+  return Z * (2 * F + 1) * ((N + 3) / 4 * 4);
 }
 
 // FWD-mode launch with 1 or 2 K-major A segments sharing one pre-converted B operand copy
@@ -937,7 +964,9 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   TcParams p{};
   const int BN = dw_bn(N, bf);
   tc_common(p, BN, bf, TC_DW);
-  const int Zs = dw_splits(rmax, F, N);
+  int Zseg[2];
+  dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg);
+  const int Zs = std::max(Zseg[0], Zseg[1]);
   const int64_t NP = (N + 3) / 4 * 4;  // partial row stride (16-byte aligned epilogue stores)
   if ((int64_t)Zs * K * NP > ws_floats) return -3;
   const float* As[2] = {A0, A1};
@@ -953,14 +982,15 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.nseg = nseg;
   p.Z = Zs;
   for (int s = 0; s < nseg; ++s) {
+    p.Zseg[s] = Zseg[s];
     p.kb_seg[s] = (int)((rows[s] + 31) / 32);
-    p.kb_per_split[s] = (p.kb_seg[s] + Zs - 1) / Zs;
+    p.kb_per_split[s] = (p.kb_seg[s] + Zseg[s] - 1) / Zseg[s];
     if (p.kb_per_split[s] < 1) p.kb_per_split[s] = 1;
     p.out_row_off[s] = (int)(s * F);
   }
   p.n_ftiles = (int)((F + 127) / 128);
   p.n_ntiles = (int)((N + BN - 1) / BN);
-  p.n_tiles = nseg * Zs * p.n_ftiles * p.n_ntiles;
+  p.n_tiles = (Zseg[0] + (nseg > 1 ? Zseg[1] : 0)) * p.n_ftiles * p.n_ntiles;
   p.M = (int)rmax;
   p.N = (int)N;
   p.F = (int)F;
@@ -977,7 +1007,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   } else {
     for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * NP + nseg * F * NP, 0, sizeof(float) * N, L.s);
   }
-  split_reduce_strided(L, ws, Zs, K, N, NP, G);
+  const int64_t zc[3] = {Zseg[0], nseg > 1 ? Zseg[1] : 0, Zs};  // splits of rows [0,F), [F,2F), bias row
+  split_reduce_dw(L, ws, zc, F, nseg, N, NP, G);
   if (L.count) *L.count += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

@@ -13,7 +13,7 @@ enum { EPI_ACT = 0, EPI_DA = 1, EPI_MASK = 2, EPI_PART = 3 };
 struct alignas(64) TcParams {
   CUtensorMap map_a[2], map_b[2], map_b_lo;
   int mode, epi, BN, stages, tmem_cols;
-  int nseg, kb_seg[2], kb_off_b[2], kb_per_split[2];
+  int nseg, kb_seg[2], kb_off_b[2], kb_per_split[2], Zseg[2];
   int n_tiles, n_ntiles, n_ntiles_half, n_ftiles, Z;
   int M, N, F, K_out;
   int out_row_off[2];

@@ -24,16 +24,21 @@ inline int grid_for(int64_t work, int per_block, int max_blocks = kSMs * 16) {
   return (int)b;
 }
 
-__device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 output for state z
+// Bits 40..63 of SplitMix64(z) (reading R5 keeps an element iff they are >= thr).  The output
+// xorshift z ^ (z >> 31) only changes bits 0..32, so it is skipped: same bits, fewer instructions.
+__device__ __forceinline__ uint32_t smix_top24(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+  return (uint32_t)(z >> 40);
 }
 
-__device__ __forceinline__ bool keep_el(const DropSpec& d, int64_t gid, int64_t c) {
-  uint64_t key = ((uint64_t)d.key_base + (uint64_t)gid) * (uint64_t)d.width + (uint64_t)c;
-  return (uint32_t)(smix(key ^ d.seed) >> 40) >= d.thr;
+// key = ((t(L+1)+l)N + gid) F + col: the row part kr = (key_base + gid) F is hoisted per row.
+__device__ __forceinline__ uint64_t row_key(const DropSpec& d, int64_t gid) {
+  return ((uint64_t)d.key_base + (uint64_t)gid) * (uint64_t)d.width;
+}
+__device__ __forceinline__ bool keep_at(const DropSpec& d, uint64_t kr, int64_t c) {
+  return smix_top24((kr + (uint64_t)c) ^ d.seed) >= d.thr;
 }
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
@@ -74,13 +79,13 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
     float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < n_valid) {
       const float4 h = H[i];
-      const int64_t g = gid[r];
+      const uint64_t kr = row_key(d, gid[r]);
       const float sr = rs ? rs[r] : 1.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t c = 4 * x + j;
         float v = 0.f;
-        if (c < d.width && (!d.on || keep_el(d, g, c))) v = comp(h, j) * d.scale * sr;
+        if (c < d.width && (!d.on || keep_at(d, kr, c))) v = comp(h, j) * d.scale * sr;
         set_comp(out, j, v);
       }
     }
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
           if (x0 + q * G < ld4) acc[q] = f4add(acc[q], __ldg(src + q * G));
       }
     }
-    const int64_t g = gid[u0];
+    const uint64_t kr = row_key(d, gid[u0]);
     const float sr = rs ? rs[u0] : 1.f;  // GCN-sym: d~_u^-1/2 of the (inner or boundary) row u (R26)
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
         const int64_t c = 4 * x + j;
         float val = comp(o, j);
         if (c >= d.width) val = 0.f;
-        else if (d.on) val = keep_el(d, g, c) ? val * d.scale : 0.f;
+        else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
         set_comp(o, j, val);
       }
       J[u0 * ld4 + x] = o;
@@ -499,6 +504,20 @@ __global__ void k_split_reduce_strided(const float* __restrict__ part, int64_t s
   const int64_t len = rows * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / N, c = i - r * N;
+    float a = 0.f;
+    for (int64_t s = 0; s < splits; ++s) a += part[s * rows * NP + r * NP + c];
+    G[i] = a;
+  }
+}
+
+// dW partial reduce with per-row-range split counts: rows [0, F) sum zc[0] splits, [F, 2F) zc[1]
+// (nseg == 2), the bias row zc[2]; partial z holds (nseg F + 1) rows of stride NP.
+__global__ void k_split_reduce_dw(const float* __restrict__ part, int64_t z0, int64_t z1, int64_t zb, int64_t F,
+                                  int64_t rows, int64_t N, int64_t NP, float* __restrict__ G) {
+  const int64_t len = rows * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i - r * N;
+    const int64_t splits = r == rows - 1 ? zb : (r < F ? z0 : z1);
     float a = 0.f;
     for (int64_t s = 0; s < splits; ++s) a += part[s * rows * NP + r * NP + c];
     G[i] = a;
@@ -861,6 +880,13 @@ void split_reduce(Launch L, const float* part, int64_t splits, int64_t len, floa
 void split_reduce_strided(Launch L, const float* part, int64_t splits, int64_t rows, int64_t N, int64_t NP,
                           float* G) {
   k_split_reduce_strided<<<grid_for(rows * N, kThreads), kThreads, 0, L.s>>>(part, splits, rows, N, NP, G);
+  count(L);
+}
+
+void split_reduce_dw(Launch L, const float* part, const int64_t zc[3], int64_t F, int nseg, int64_t N, int64_t NP,
+                     float* G) {
+  const int64_t rows = nseg * F + 1;
+  k_split_reduce_dw<<<grid_for(rows * N, kThreads), kThreads, 0, L.s>>>(part, zc[0], zc[1], zc[2], F, rows, N, NP, G);
   count(L);
 }
 

@@ -93,6 +93,9 @@ int64_t gemm_dw_ws_floats(int64_t M, int64_t F, int64_t N);
 void split_reduce(Launch, const float* part, int64_t splits, int64_t len, float* G);
 // G[r * N + c] = sum_s part[s][r * NP + c] over rows x N (partials with row stride NP)
 void split_reduce_strided(Launch, const float* part, int64_t splits, int64_t rows, int64_t N, int64_t NP, float* G);
+// dW partials (tc_dw_general): rows [0, F) reduce zc[0] splits, [F, 2F) zc[1] (nseg 2), bias row zc[2]
+void split_reduce_dw(Launch, const float* part, const int64_t zc[3], int64_t F, int nseg, int64_t N, int64_t NP,
+                     float* G);
 // dA = Mg W^T ([M x 2F]); first half scaled by inv_deg[row] (dZ' of S7), into dA (ld_dA = 2 ld)
 void gemm_da_f32(Launch, const float* Mg, int64_t ldM, int64_t M, int64_t N, const float* W, int64_t F,
                  const float* inv_deg, float* dA, int64_t ld);

@@ -111,3 +111,60 @@ def test_sampled_layer1_rows_full_size(setup, tf):
             eh = np.abs(Hg[rows] - Hr).max() / max(np.abs(Hr).max(), 1e-30)
             assert ez <= 1e-4, (t, i, ez)
             assert eh <= 1e-4, (t, i, eh)
+
+
+def row_oracle_gcn(g, P, v_local, t, W, b, p, seed, L, halo_zero):
+    """H^(1) of local inner row v under GCN-sym (App. A.1, R26), one row, float64:
+    H_v = ReLU(s_v (s_v D_v + sum_{u in N(v)} s_u D_u) W + b), s_u = (d_u + 1)^-1/2 with full-graph
+    degrees; boundary neighbours contribute 0 at t = 1 (Alg. 1 l.6)."""
+    N = g.n
+    gv = int(P["inner_gid"][v_local])
+    nb = g.col_idx[g.row_ptr[gv]:g.row_ptr[gv + 1]].astype(np.int64)
+    F = g.X.shape[1]
+    use = nb
+    if halo_zero:
+        lo, hi = P["inner_gid"][0], P["inner_gid"][-1]
+        use = nb[(nb >= lo) & (nb <= hi)]
+    s_of = lambda u: 1.0 / np.sqrt(np.diff(g.row_ptr)[u].astype(np.float64) + 1.0)  # noqa: E731
+    Du = g.X[use].astype(np.float64) * keep_mask(t, 1, L, N, use, F, seed, p) / (1.0 - p)
+    Dv = g.X[gv].astype(np.float64) * keep_mask(t, 1, L, N, [gv], F, seed, p)[0] / (1.0 - p)
+    sv = s_of(np.array([gv]))[0]
+    Z = sv * (sv * Dv + (s_of(use)[:, None] * Du).sum(0))
+    return np.maximum(Z @ W.astype(np.float64) + b.astype(np.float64), 0.0)
+
+
+def test_sampled_layer1_rows_full_size_gcn(setup):
+    """GCN-sym (N3) at the full Reddit size in bench.py --model gcn's configuration (layer 1
+    transform-first): sampled H^(1) rows at t = 1, 2 against the one-row oracle."""
+    import torch
+    P, g, m = setup
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 2)
+    cfg = P.make_config(m.widths, mode="pipe", dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
+                        n_train_global=g.n_train, seed=4, model="gcn")
+    ctx = P.Context(part, cfg)
+    views = [part.view(i) for i in range(2)]
+    keep = []
+    for i, v in enumerate(views):
+        gid = v["inner_gid"]
+        a = tuple(torch.tensor(x).cuda() for x in (g.X[gid], g.labels[gid], g.train_mask[gid]))
+        keep.append(a)
+        ctx.set_inputs(i, *a)
+    params0 = glorot_params(m.widths, 3, model="gcn")
+    theta = torch.tensor(P.flatten_params(params0)).cuda()
+    grads = torch.zeros_like(theta)
+    opt = torch.zeros(2 * theta.numel(), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    L = len(m.widths) - 1
+    F1 = m.widths[1]
+    rng = np.random.default_rng(12)
+    for t in (1, 2):
+        W, b = P.unflatten_params(theta.cpu().numpy().copy(), m.widths, model="gcn")[0]
+        ctx.step(t, theta, grads, opt, loss)
+        torch.cuda.synchronize()
+        assert np.isfinite(float(loss.item())) and torch.isfinite(grads).all()
+        for i, v in enumerate(views):
+            Hg = ctx.tensor(i, P.T_H, 1, t)[:, :F1].cpu().numpy()
+            rows = rng.choice(v["n_inner"], 24, replace=False)
+            Hr = np.array([row_oracle_gcn(g, v, r, t, W, b, m.dropout, 4, L, halo_zero=(t == 1)) for r in rows])
+            eh = np.abs(Hg[rows] - Hr).max() / max(np.abs(Hr).max(), 1e-30)
+            assert eh <= 1e-4, (t, i, eh)
