@@ -25,6 +25,9 @@ Smoothing (Sec. 3.4): `smooth_f` -- EMA of installed boundary features for layer
 (reading R14); `smooth_g` -- EMA of each received gradient message before the sum
 (reading R13).  `ema_init` "first" (reading R12) or "zero".
 Dropout is applied after install (App. F) with the gid-keyed mask.
+Pipeline depth (`depth` = s, reading R27; the future work of App. C: "using two
+iterations of compute to hide one iteration of communication"): an exchange sent at t is consumed
+at t + s (s = 1 is Alg. 1); for t <= s boundary rows are 0 and no gradient is accumulated.
 """
 import numpy as np
 
@@ -34,7 +37,7 @@ from .sage import Adam, loss_and_grad, sgd_update
 
 
 def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, gamma=None,
-        ema_init="first", seed=4, opt=None, keep_A=False, relu_decision=None):
+        ema_init="first", seed=4, opt=None, keep_A=False, relu_decision=None, depth=1):
     """Train for t = 1..T.  Returns a list (one dict per t) with
     loss, H[l][i] (inner rows of layer l output), J[l][i] (inner J^(l) after accumulation),
     halo[l][i] (boundary rows used as input of layer l), G_parts[i], G, params (after update),
@@ -46,7 +49,7 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
     the backward (App. A.1).  Default Y > 0.  Parity tests pass a hook that adopts
     the kernel's decision where |Y| is within the comparison tolerance of 0 (DESIGN.md reading
     R25: a float-decided discrete choice is taken in the kernel's precision on both sides)."""
-    assert mode in ("pipe", "vanilla")
+    assert mode in ("pipe", "vanilla") and depth >= 1
     gamma = cfg.gamma if gamma is None else gamma
     n = len(parts)
     L = len(params0)
@@ -65,9 +68,9 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
     opt = opt or cfg.opt
     adam = Adam(cfg.lr) if opt == "adam" else None
 
-    recv_f = {l: [None] * n for l in range(1, L + 1)}      # B^(l) received at t-1, per receiver
+    recv_f = {l: {} for l in range(1, L + 1)}      # recv_f[l][t'] = B^(l) sent at t', per receiver
     ema_f = {l: [None] * n for l in range(1, L + 1)}
-    recv_b = {l: [None] * n for l in range(1, L + 1)}      # C^(l) received at t-1, per owner: list per peer
+    recv_b = {l: {} for l in range(1, L + 1)}      # recv_b[l][t'][owner] = C^(l) sent at t', list per peer
     ema_b = {l: [None] * n for l in range(1, L + 1)}
     recs = []
     for t in range(1, T + 1):
@@ -88,10 +91,10 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
             for i in range(n):
                 if mode == "vanilla":
                     halo = arrived[i]
-                elif t == 1:
-                    halo = np.zeros((parts[i]["n_halo"], F))                 # l.6 / R8
+                elif t <= depth:
+                    halo = np.zeros((parts[i]["n_halo"], F))                 # l.6 / R8 (R27)
                 else:
-                    halo = recv_f[l][i]                                      # l.9-11
+                    halo = recv_f[l][t - depth][i]                           # l.9-11
                     if smooth_f and l >= 2:
                         if ema_f[l][i] is None:
                             ema_f[l][i] = halo.copy() if ema_init == "first" else \
@@ -101,8 +104,8 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                         halo = ema_f[l][i]
                 halos.append(halo)
             if mode == "pipe":
-                for i in range(n):
-                    recv_f[l][i] = arrived[i]                                # consumed at t + 1
+                recv_f[l][t] = arrived                                       # consumed at t + depth
+                recv_f[l].pop(t - depth, None)
             H_out = []
             for i in range(n):
                 full = np.vstack([H_in[i], halos[i]])
@@ -163,10 +166,10 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
             for j in range(n):
                 if mode == "vanilla":
                     contrib = cur[j]
-                elif t == 1:
-                    contrib = None                                           # R9
+                elif t <= depth:
+                    contrib = None                                           # R9 (R27)
                 else:
-                    contrib = recv_b[l][j]                                   # l.22
+                    contrib = recv_b[l][t - depth][j]                        # l.22
                     if smooth_g:
                         if ema_b[l][j] is None:
                             ema_b[l][j] = [c.copy() if ema_init == "first" else (1.0 - gamma) * c
@@ -184,7 +187,8 @@ def run(g, parts, params0, cfg, T, mode="pipe", smooth_f=False, smooth_g=False, 
                         seg = P["send_idx"][P["send_off"][i]:P["send_off"][i + 1]]
                         np.add.at(J_in[j], seg, contrib[i])
                 if mode == "pipe":
-                    recv_b[l][j] = cur[j]                                    # l.27, used at t + 1
+                    recv_b[l].setdefault(t, [None] * n)[j] = cur[j]          # l.27, used at t + depth
+            recv_b[l].pop(t - depth, None)
             J = J_in
             rec["J"][l - 1] = J
             rec["err_g"][l] = float(np.sqrt(esq))  # gradient messages used vs fresh (Fig. 5/7)

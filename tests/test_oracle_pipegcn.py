@@ -270,3 +270,86 @@ def test_staleness_error_definition():
     s0 = pipegcn.run(g, parts, params, c, 3, mode="pipe", smooth_f=True, smooth_g=True, gamma=0.0)
     for a, b in zip(pip, s0):
         assert a["err_f"] == b["err_f"] and a["err_g"] == b["err_g"]
+
+
+# ---------------------------------------------------------------- pipeline depth s (reading R27)
+@pytest.mark.parametrize("n_parts,depth", [(2, 2), (3, 3)])
+def test_depth_matrix_form(n_parts, depth):
+    """App. A.1's matrix form with the one-iteration delay replaced by s:
+    Z^(t) = P_in H^(t) + P_bd H^(t-s) for t > s;  J^(t,l-1) = P_in^T M^(t) W^(t)T_neigh +
+    P_bd^T M^(t-s) W^(t-s)T_neigh + M^(t) W^(t)T_self (sender's weights of iteration t - s)."""
+    g = small_graph(seed=9, n=150)
+    widths = [9, 8, 7, 4]
+    c = cfg(widths, p=0.0, lr=0.3)
+    params0 = glorot_params(widths, 5)
+    part_of = contiguous_map(g.n, n_parts)
+    parts = partition(g.n, g.row_ptr, g.col_idx, n_parts, part_of)
+    T = depth + 4
+    recs = pipegcn.run(g, parts, params0, c, T, mode="pipe", depth=depth)
+    deg = np.diff(g.row_ptr)
+    rows = np.repeat(np.arange(g.n), deg)
+    inv = np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0.0)
+    same = part_of[rows] == part_of[g.col_idx]
+    P_in = sp.csr_matrix((inv[rows] * same, (rows, g.col_idx)), shape=(g.n, g.n))
+    P_bd = sp.csr_matrix((inv[rows] * ~same, (rows, g.col_idx)), shape=(g.n, g.n))
+    L = 3
+    Ws = [[(np.asarray(W, float), np.asarray(b, float)) for W, b in params0]] + [r["params"] for r in recs]
+    X = g.X.astype(np.float64)
+
+    def Hf(t, l):
+        return X if l == 0 else assemble(parts, recs[t - 1]["H"][l], g.n, widths[l])
+
+    def Mf(t, l):
+        J = assemble(parts, recs[t - 1]["J"][l], g.n, widths[l])
+        Y = assemble(parts, recs[t - 1]["Y"][l], g.n, widths[l])
+        return J * (Y > 0) if l < L else J
+
+    for t in range(1, T + 1):
+        for l in range(1, L + 1):
+            W, b = Ws[t - 1][l - 1]
+            Hold = Hf(t - depth, l - 1) if t > depth else np.zeros_like(Hf(t, l - 1))
+            Y = np.hstack([P_in @ Hf(t, l - 1) + P_bd @ Hold, Hf(t, l - 1)]) @ W + b
+            assert close(Hf(t, l), np.maximum(Y, 0) if l < L else Y, 1e-11), (t, l)
+        for l in range(L, 1, -1):
+            F = widths[l - 1]
+            Wt = Ws[t - 1][l - 1][0]
+            J = P_in.T @ (Mf(t, l) @ Wt[:F].T) + Mf(t, l) @ Wt[F:].T
+            if t > depth:
+                J = J + P_bd.T @ (Mf(t - depth, l) @ Ws[t - 1 - depth][l - 1][0][:F].T)
+            assert close(assemble(parts, recs[t - 1]["J"][l - 1], g.n, F), J, 1e-11), (t, l)
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_depth_eta0_converges_to_vanilla(depth):
+    """eta = 0, p = 0: with an s-deep pipeline every stale value is exact once the pipeline has
+    filled (t >= 2 s L), and not before (t = s + 1 still sees stale gradients)."""
+    L = 3
+    g = small_graph(seed=10)
+    widths = [9, 8, 7, 4]
+    c = cfg(widths, p=0.0, lr=0.0)
+    params = glorot_params(widths, 3)
+    parts = partition(g.n, g.row_ptr, g.col_idx, 3)
+    T = 2 * depth * L + 1
+    van = pipegcn.run(g, parts, params, c, 1, mode="vanilla")
+    pip = pipegcn.run(g, parts, params, c, T, mode="pipe", depth=depth)
+
+    def gerr(t):
+        return max(np.abs(a - x).max() for (a, _), (x, _) in zip(pip[t - 1]["G"], van[0]["G"]))
+    scale = max(np.abs(x).max() for x, _ in van[0]["G"])
+    assert gerr(depth + 1) > 1e-6 * scale
+    for t in range(2 * depth * L, T + 1):
+        assert gerr(t) <= 1e-13 * scale, t
+    # depth s at t <= s is the t = 1 computation with the weights of t (here unchanged): identical
+    for t in range(2, depth + 1):
+        assert pip[t - 1]["loss"] == pip[0]["loss"]
+
+
+def test_depth_ema_gamma0_is_identity():
+    g = small_graph(seed=11)
+    c = cfg([9, 8, 7, 4], p=0.5, lr=0.1)
+    params = glorot_params(c.widths, 3)
+    parts = partition(g.n, g.row_ptr, g.col_idx, 3)
+    a = pipegcn.run(g, parts, params, c, 5, mode="pipe", depth=2)
+    b = pipegcn.run(g, parts, params, c, 5, mode="pipe", depth=2, smooth_f=True, smooth_g=True, gamma=0.0)
+    for ra, rb in zip(a, b):
+        assert ra["loss"] == rb["loss"]
