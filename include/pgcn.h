@@ -57,6 +57,7 @@ enum {
 
 #define PGCN_MAX_LAYERS 16
 #define PGCN_MAX_PARTS 64
+#define PGCN_MAX_DEPTH 3
 
 const char* pgcn_last_error(void);
 int pgcn_version(void); /* 100 * major + minor */
@@ -151,6 +152,11 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       (same mathematics, fp32 reassociation only).  Tensor-core GEMMs only.
  *   staleness_stats     1: measure the staleness errors of Fig. 5/7 (see pgcn_staleness); local
  *                       transport only (adds one reduction kernel per layer and direction).
+ *   depth               pipeline depth s of PIPE (0 or 1: Alg. 1; 2..PGCN_MAX_DEPTH: App. C's "two
+ *                       iterations of compute to hide one iteration of communication", PAPER.md:923,
+ *                       reading R27): the exchange posted at t is consumed at t + s; boundary rows
+ *                       are 0 and no gradient is accumulated for t <= s.  Activation / gradient
+ *                       buffers rotate over s + 1 slots.
  *   model               0 GraphSAGE-mean (above); 1 GCN-sym (SURVEY N3, App. A.1 PAPER.md:637-647,
  *                       reading R26): Y = P D W + b with P = D~^-1/2 (A + I) D~^-1/2, D~ = d + 1
  *                       (full-graph degrees), W [F_{l-1} x F_l]; tensor-core GEMMs only (gemm 0/1).
@@ -174,6 +180,7 @@ typedef struct {
   int32_t transform_first;
   int32_t staleness_stats;
   int32_t model;
+  int32_t depth;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

@@ -2,14 +2,15 @@
 //
 // Data layout in the caller's workspace, per hosted partition i:
 //   X        [n_all x ld0]         layer-1 input; rows [0,n_in) = X_i, [n_in,n_all) = boundary
-//   H[l][b]  [n_all x ld_l]        layer-l output / layer-(l+1) input, b = t & 1 (parity
-//                                  double buffer: the PIPE install at t reads owners' b(t-1))
+//   H[l][b]  [n_all x ld_l]        layer-l output / layer-(l+1) input, b = t mod (s + 1) for
+//                                  pipeline depth s (R27; s = 1: parity double buffer -- the
+//                                  PIPE install at t reads owners' buffer of t - s)
 //   logits   [n_in  x ld_L]
 //   D[l]     [n_all x ld_{l-1}]    dropout(layer-l input) (absent when p = 0: D = input)
 //   Z[l]     [n_in  x ld_{l-1}]    aggregated neighbours (S3)
 //   M        [n_in  x max ld]      J o sigma' of the layer being back-propagated
 //   dA       [n_in  x 2 max ld]    [inv_deg * dZ | dD_self] (S7)
-//   J[l][b]  [n_all x ld_l]        J^(l) for inner + boundary rows (S8), parity double buffer
+//   J[l][b]  [n_all x ld_l]        J^(l) for inner + boundary rows (S8), s + 1 rotating buffers
 //   emaG[l]  [n_send x ld_l]       EMA-G state per received gradient row (Sec. 3.4)
 //   G        [P]                   this partition's G_i, laid out like theta
 // ld_l = round_up(F_l, 4).  Boundary rows start at 0 (workspace zero-filled; Alg. 1 l.6).
@@ -31,6 +32,8 @@
 
 namespace pgcn {
 
+constexpr int kMaxBuf = PGCN_MAX_DEPTH + 1;  // rotating activation / gradient buffers (depth s + 1)
+
 struct PartCtx {
   int32_t part = 0;
   pgcn_part_view v{};
@@ -41,7 +44,7 @@ struct PartCtx {
   float* inv_deg = nullptr;
   float* sym = nullptr;  // GCN-sym: d~_u^-1/2 = 1/sqrt(d_u + 1) of inner then boundary rows (R26)
   float* X = nullptr;
-  float* H[PGCN_MAX_LAYERS + 1][2] = {};
+  float* H[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};
   float* logits = nullptr;
   float* D[PGCN_MAX_LAYERS + 1] = {};
   float* Z[PGCN_MAX_LAYERS + 1] = {};
@@ -49,7 +52,7 @@ struct PartCtx {
   int64_t n_valid[PGCN_MAX_LAYERS + 1] = {};  // rows of the layer input valid this iteration
   float* M = nullptr;
   float* dA = nullptr;
-  float* J[PGCN_MAX_LAYERS + 1][2] = {};
+  float* J[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};
   float* emaG[PGCN_MAX_LAYERS + 1] = {};
   void* labels = nullptr;
   uint8_t* train = nullptr;
@@ -101,6 +104,7 @@ struct pgcn_ctx {
   // N1 transform-before-aggregate per layer: Y = P(D W_neigh) + D W_self + b instead of (PD) W_neigh
   int tf[PGCN_MAX_LAYERS + 1] = {};
   int gcn = 0, ns = 2;  // cfg.model == 1 (GCN-sym, R26); weight row segments
+  int64_t depth = 1;    // pipeline depth s (R27): an exchange posted at t is consumed at t + s
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
   double* diag = nullptr;              // N4: [2][L+1] squared staleness errors of the current iteration
@@ -117,17 +121,19 @@ struct pgcn_ctx {
 #endif
   cudaStream_t cs = nullptr;              // comm stream (high priority)
   cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
-  cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][2] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][2] = {};
-  float* send_f[PGCN_MAX_LAYERS + 1] = {};     // packed S_{i,j} rows of the layer-l input
-  float* recv_f[PGCN_MAX_LAYERS + 1] = {};     // received boundary rows (EMA-F only)
-  float* recv_b[PGCN_MAX_LAYERS + 1][2] = {};  // received gradient rows, send order, parity
+  cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};
+  float* send_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // packed S_{i,j} rows of the layer-l input
+  float* recv_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // received boundary rows (EMA-F only)
+  float* recv_b[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // received gradient rows, send order
+  int nb = 2;                                              // buffers in rotation = depth + 1
+  int bi(int64_t t) const { return (int)(((t % nb) + nb) % nb); }
   ~pgcn_ctx() {
     for (auto& k : kt)
       for (auto e : k.ev) cudaEventDestroy(e);
     for (int l = 0; l <= PGCN_MAX_LAYERS; ++l) {
       if (ev_f_pack[l]) cudaEventDestroy(ev_f_pack[l]);
       if (ev_b_ready[l]) cudaEventDestroy(ev_b_ready[l]);
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < pgcn::kMaxBuf; ++b) {
         if (ev_f_done[l][b]) cudaEventDestroy(ev_f_done[l][b]);
         if (ev_b_done[l][b]) cudaEventDestroy(ev_b_done[l][b]);
       }
@@ -157,6 +163,7 @@ int validate_cfg(const pgcn_config* c) {
   if (!(c->gamma >= 0.0 && c->gamma <= 1.0)) return fail(PGCN_EINVAL, "gamma out of [0,1]");
   if (c->model != 0 && c->model != 1) return fail(PGCN_EINVAL, "model must be 0 (GraphSAGE) or 1 (GCN-sym)");
   if (c->model == 1 && c->gemm == 2) return fail(PGCN_EUNSUPPORTED, "GCN-sym needs the tensor-core GEMMs (gemm 0/1)");
+  if (c->depth < 0 || c->depth > PGCN_MAX_DEPTH) return fail(PGCN_EINVAL, "depth must be in 0..%d", PGCN_MAX_DEPTH);
   return PGCN_OK;
 }
 
@@ -196,7 +203,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.msg_map = A.take<int32_t>(p.n_send);
     p.X = A.take<float>(p.n_all * C->ld[0]);
     for (int l = 1; l < L; ++l)
-      for (int b = 0; b < 2; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
+      for (int b = 0; b < C->nb; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
     p.logits = A.take<float>(p.n_in * C->ld[L]);
     for (int l = 1; l <= L; ++l) {
       if (C->cfg.dropout > 0.0 || C->cfg.model == 1) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
@@ -206,7 +213,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.M = A.take<float>(p.n_in * C->ldmax);
     if (L > 1) p.dA = A.take<float>(p.n_in * 2 * C->ldmax);
     for (int l = 1; l < L; ++l) {
-      for (int b = 0; b < 2; ++b) p.J[l][b] = A.take<float>(p.n_all * C->ld[l]);
+      for (int b = 0; b < C->nb; ++b) p.J[l][b] = A.take<float>(p.n_all * C->ld[l]);
       if (C->cfg.smooth_g) p.emaG[l] = A.take<float>(p.n_send * C->ld[l]);
     }
     p.labels = C->cfg.loss == 0 ? (void*)A.take<int32_t>(p.n_in) : (void*)A.take<uint8_t>(p.n_in * C->F[L]);
@@ -224,12 +231,12 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   C->dw_ws = A.take<float>(dw_need);
   if (C->nccl && n_local == 1) {
     const PartCtx& p = C->parts[0];
-    for (int l = 1; l <= L; ++l) {
-      C->send_f[l] = A.take<float>(p.n_send * C->ld[l - 1]);
-      if (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2) C->recv_f[l] = A.take<float>(p.n_bd * C->ld[l - 1]);
-      if (l >= 2)
-        for (int b = 0; b < 2; ++b) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
-    }
+    for (int l = 1; l <= L; ++l)
+      for (int b = 0; b < (l == 1 ? 1 : C->nb); ++b) {
+        C->send_f[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
+        if (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2) C->recv_f[l][b] = A.take<float>(p.n_bd * C->ld[l - 1]);
+        if (l >= 2) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
+      }
   }
   const int64_t ns = C->ns;  // weight row segments: 2 GraphSAGE [W_neigh; W_self], 1 GCN-sym
   if (C->cfg.gemm == 0) {     // 3xTF32 operand copies: fp32 hi/lo, k-blocks of 32
@@ -303,6 +310,8 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   }
   C->gcn = cfg->model == 1;
   C->ns = C->gcn ? 1 : 2;
+  C->depth = cfg->depth > 1 ? cfg->depth : 1;
+  C->nb = (int)C->depth + 1;
   C->woff[1] = 0;
   for (int l = 1; l <= C->L; ++l) C->woff[l + 1] = C->woff[l] + (C->ns * C->F[l - 1] + 1) * C->F[l];
   // N1 traffic rule (gathered row widths per iteration): layer 1 aggregates F_0 forward only
@@ -406,22 +415,24 @@ int nccl_fail(pgcn_ctx* C, ncclResult_t r, const char* where) {
 // Alg. 1 l.9-13 over NCCL (one partition per rank).  PIPE: wait for the exchange posted at t-1
 // (and smooth it, Sec. 3.4), then post this iteration's exchange, consumed at t+1; the receive
 // lands directly in the boundary rows of the next parity buffer.  VANILLA: post and wait.
+// Depth s (R27): the exchange posted at t is consumed at t + s; buffers rotate over s + 1 slots.
 int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, const Launch& Lk, int64_t* n_valid) {
   const bool pipe = C->cfg.mode == 1;
-  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int64_t s = C->depth;
+  const int b = C->bi(t), bp = C->bi(t - 1), bs = C->bi(t - s);
   const int64_t ldi = C->ld[l - 1];
   *n_valid = p.n_all;
-  if (pipe && t >= 2) {
+  if (pipe && t > s) {
     if (l == 1) {
-      cudaStreamWaitEvent(C->s, C->ev_f_done[1][1], 0);  // X boundary rows, received at t = 1 (R10)
+      cudaStreamWaitEvent(C->s, C->ev_f_done[1][C->bi(1)], 0);  // X boundary rows, received at t = 1 (R10)
     } else {
-      cudaStreamWaitEvent(C->s, C->ev_f_done[l][bp], 0);
+      cudaStreamWaitEvent(C->s, C->ev_f_done[l][bs], 0);
       if (C->cfg.smooth_f && p.n_bd > 0) {
         SegTable src{};
         src.n_seg = 1;
         src.off[1] = p.n_bd;
-        src.base[0] = C->recv_f[l];
-        const bool first = C->cfg.ema_init == 0 && t == 2;
+        src.base[0] = C->recv_f[l][bs];
+        const bool first = C->cfg.ema_init == 0 && t == s + 1;
         Scope sc(C, PGCN_K_GATHER, 12.0 * C->F[l - 1] * p.n_bd);
         gather_rows(Lk, src, nullptr, p.n_bd, ldi, Hin + p.n_in * ldi, p.H[l - 1][bp] + p.n_in * ldi,
                     (float)C->cfg.gamma, 1, first);
@@ -435,20 +446,21 @@ int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, con
       src.off[1] = p.n_send;
       src.base[0] = Hin;
       Scope sc(C, PGCN_K_GATHER, 8.0 * C->F[l - 1] * p.n_send + 4.0 * p.n_send);
-      gather_rows(Lk, src, p.send_idx, p.n_send, ldi, C->send_f[l], nullptr, 0.f, 0, 0);
+      gather_rows(Lk, src, p.send_idx, p.n_send, ldi, C->send_f[l][l == 1 ? 0 : b], nullptr, 0.f, 0, 0);
     }
     cudaEventRecord(C->ev_f_pack[l], C->s);
     cudaStreamWaitEvent(C->cs, C->ev_f_pack[l], 0);
     float* dst;
     if (l == 1) dst = p.X + p.n_in * ldi;
     else if (!pipe) dst = p.H[l - 1][b] + p.n_in * ldi;
-    else if (C->cfg.smooth_f) dst = C->recv_f[l];
-    else dst = p.H[l - 1][(t + 1) & 1] + p.n_in * ldi;
+    else if (C->cfg.smooth_f) dst = C->recv_f[l][b];
+    else dst = p.H[l - 1][C->bi(t + s)] + p.n_in * ldi;  // lands in the buffer read at t + s
+    const float* sendb = C->send_f[l][l == 1 ? 0 : b];
     ncclResult_t r = ncclGroupStart();
     for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
       if (j == C->rank) continue;
       const int64_t ns = p.v.send_off[j + 1] - p.v.send_off[j], nr = p.v.halo_off[j + 1] - p.v.halo_off[j];
-      if (ns) r = ncclSend(C->send_f[l] + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
+      if (ns) r = ncclSend(sendb + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
       if (nr && r == ncclSuccess)
         r = ncclRecv(dst + p.v.halo_off[j] * ldi, (size_t)(nr * ldi), ncclFloat, j, C->ch, C->cs);
     }
@@ -457,7 +469,7 @@ int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, con
     cudaEventRecord(C->ev_f_done[l][b], C->cs);
     if (!pipe) cudaStreamWaitEvent(C->s, C->ev_f_done[l][b], 0);
   }
-  if (pipe && l == 1 && t == 1) *n_valid = p.n_in;  // X boundary rows not installed yet: zero (l.6)
+  if (pipe && l == 1 && t <= s) *n_valid = p.n_in;  // X boundary rows not installed yet: zero (l.6)
   return PGCN_OK;
 }
 
@@ -465,7 +477,8 @@ int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, con
 // and return the message table to accumulate now (PIPE: the one received at t-1).
 int nccl_bwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, SegTable& msg, bool& have) {
   const bool pipe = C->cfg.mode == 1;
-  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int64_t s = C->depth;
+  const int b = C->bi(t), bs = C->bi(t - s);
   const int64_t ldi = C->ld[l - 1];
   const float* J = p.J[l - 1][b];
   cudaEventRecord(C->ev_b_ready[l], C->s);
@@ -482,9 +495,9 @@ int nccl_bwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, SegTable& msg, 
   if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(C, r != ncclSuccess ? r : r2, "halo exchange (bwd)");
   cudaEventRecord(C->ev_b_done[l][b], C->cs);
   msg = SegTable{};
-  have = p.n_send > 0 && (!pipe || t >= 2);
+  have = p.n_send > 0 && (!pipe || t > s);
   if (have) {
-    const int sb = pipe ? bp : b;
+    const int sb = pipe ? bs : b;
     cudaStreamWaitEvent(C->s, C->ev_b_done[l][sb], 0);
     msg.n_seg = 1;
     msg.off[1] = p.n_send;
@@ -599,7 +612,7 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     for (int l = 1; l <= C->L; ++l) {
       cudaEventCreateWithFlags(&C->ev_f_pack[l], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&C->ev_b_ready[l], cudaEventDisableTiming);
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < C->nb; ++b) {
         cudaEventCreateWithFlags(&C->ev_f_done[l][b], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&C->ev_b_done[l][b], cudaEventDisableTiming);
       }
@@ -654,7 +667,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   if (rc) return rc;
   if (!params) return fail(PGCN_EINVAL, "params is NULL");
   const Launch Lk{C->s, &C->launches};
-  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int b = C->bi(t), bp = C->bi(t - 1), bs = C->bi(t - C->depth);
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
@@ -688,16 +701,16 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       src.n_seg = C->n_parts;
       for (int j = 0; j <= C->n_parts; ++j) src.off[j] = p.v.halo_off[j];
       if (l == 1) {
-        // X is constant: one exchange at t = 1, consumed at t = 1 (VANILLA) or t = 2 (PIPE) (R10)
-        do_install = pipe ? t == 2 : t == 1;
+        // X is constant: one exchange at t = 1, consumed at t = 1 (VANILLA) or t = 1 + s (PIPE) (R10)
+        do_install = pipe ? t == 1 + C->depth : t == 1;
         for (int j = 0; j < C->n_parts; ++j) src.base[j] = C->parts[j].X;
       } else {
-        const int sb = pipe ? bp : b;
-        do_install = pipe ? t >= 2 : true;
+        const int sb = pipe ? bs : b;  // owners' layer output of t - s (PIPE) or t (VANILLA)
+        do_install = pipe ? t > C->depth : true;
         for (int j = 0; j < C->n_parts; ++j) src.base[j] = C->parts[j].H[l - 1][sb];
         if (pipe && C->cfg.smooth_f) {
           ema = true;
-          first = C->cfg.ema_init == 0 && t == 2;
+          first = C->cfg.ema_init == 0 && t == C->depth + 1;
           prev = p.H[l - 1][bp] + p.n_in * ldi;
         }
       }
@@ -820,7 +833,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   if (rc) return rc;
   if (!params) return fail(PGCN_EINVAL, "params is NULL");
   const Launch Lk{C->s, &C->launches};
-  const int b = (int)(t & 1), bp = (int)((t - 1) & 1);
+  const int b = C->bi(t), bs = C->bi(t - C->depth);
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
@@ -938,7 +951,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       SegTable msg{};
       msg.n_seg = 0;
       bool use_ema = false, first = false;
-      bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t >= 2);
+      bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t > C->depth);
       const int32_t* row_map = p.msg_map;
       if (C->nccl) {
 #ifdef PGCN_WITH_NCCL
@@ -946,17 +959,17 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         row_map = nullptr;
         if (have && pipe && C->cfg.smooth_g) {
           use_ema = true;
-          first = C->cfg.ema_init == 0 && t == 2;
+          first = C->cfg.ema_init == 0 && t == C->depth + 1;
         }
 #endif
       } else if (have) {
         msg.n_seg = C->n_parts;
-        const int sb = pipe ? bp : b;
+        const int sb = pipe ? bs : b;  // peers' boundary-row gradients of t - s (PIPE) or t (VANILLA)
         for (int j = 0; j <= C->n_parts; ++j) msg.off[j] = p.v.send_off[j];
         for (int j = 0; j < C->n_parts; ++j) msg.base[j] = C->parts[j].J[l - 1][sb];
         if (pipe && C->cfg.smooth_g) {
           use_ema = true;
-          first = C->cfg.ema_init == 0 && t == 2;
+          first = C->cfg.ema_init == 0 && t == C->depth + 1;
         }
       }
       const double Fi = (double)C->F[l - 1];
@@ -1035,7 +1048,7 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
   if (!C || !o) return fail(PGCN_EINVAL, "null argument");
   if (local < 0 || local >= (int)C->parts.size()) return fail(PGCN_EINVAL, "local index out of range");
   PartCtx& p = C->parts[local];
-  const int b = (int)(t & 1);
+  const int b = C->bi(t);
   const bool lok = l >= 1 && l <= C->L;
   switch (kind) {
     case PGCN_T_H:

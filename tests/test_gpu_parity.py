@@ -327,3 +327,21 @@ def test_staleness_errors_match_oracle(P, mode, sf, sg):
             assert abs(g_gpu - g_ora) <= 1e-3 * g_ora + 1e-9, (t, l, g_gpu, g_ora)
     if mode == "vanilla":
         assert all(v == (0.0, 0.0) for d in got for v in d.values())
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+@pytest.mark.parametrize("sf,sg", [(False, False), (True, True)])
+@pytest.mark.parametrize("model", ["sage", "gcn"])
+def test_pipeline_depth(P, depth, sf, sg, model):
+    """Depth-s pipeline (R27, App. C future work PAPER.md:923): exchanges consumed s iterations
+    later, s + 1 rotating buffers; 3 layers, 3 partitions, dropout, over 2 s + 2 iterations so the
+    zero-halo start (t <= s), the first receipt (EMA init) and steady state are all covered."""
+    g = gen_graph("reddit", seed=6, n=2500, nnz=30000, f0=37, classes=5)
+    widths = [37, 30, 22, 5]
+    params0 = glorot_params(widths, 4, model=model)
+    T = 2 * depth + 2
+    kw = dict(mode="pipe", smooth_f=sf, smooth_g=sg, gamma=0.8, dropout=0.2, loss="ce", opt="sgd", lr=0.5)
+    gpu, _ = run_gpu(P, g, widths, 3, T, params0, depth=depth, model=model, **kw)
+    cfg = ModelCfg(widths=widths, dropout=0.2, lr=0.5, opt="sgd", loss="ce", gamma=0.8, model=model)
+    ora = oracle_run(gpu, g, 3, params0, cfg, T, mode="pipe", smooth_f=sf, smooth_g=sg, depth=depth)
+    check_against_oracle(gpu, ora, 3, 3, what=f"depth {depth} {model} F{sf} G{sg}")

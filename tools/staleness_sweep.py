@@ -1,7 +1,8 @@
 """N4: Fig. 4/5/7-style study on the Reddit-shaped graph (2 partitions on one GPU, Adam lr 0.01,
 dropout 0.5, Table 3): training loss and per-layer staleness errors ||used - fresh||_F of boundary
-features and gradient messages, for VANILLA, PIPE, PIPE-F/-G/-GF and a gamma sweep.
-Writes profiles/r1_staleness.md."""
+features and gradient messages, for VANILLA, PIPE, PIPE-F/-G/-GF, a gamma sweep and the deeper
+pipeline of App. C (depth 2, 3; reading R27).  Writes gpurun_out/r1_staleness.md (copied to
+profiles/ by hand: gpurun only brings gpurun_out/ back)."""
 import os
 import sys
 
@@ -21,14 +22,17 @@ views = [part.view(i) for i in range(2)]
 inputs = [tuple(torch.tensor(x).cuda() for x in (g.X[v["inner_gid"]], g.labels[v["inner_gid"]],
                                                  g.train_mask[v["inner_gid"]])) for v in views]
 L = len(m.widths) - 1
-runs = [("GCN (vanilla)", "vanilla", False, False, 0.95), ("PipeGCN", "pipe", False, False, 0.95),
-        ("PipeGCN-F", "pipe", True, False, 0.95), ("PipeGCN-G", "pipe", False, True, 0.95),
-        ("PipeGCN-GF", "pipe", True, True, 0.95), ("PipeGCN-GF g=0.7", "pipe", True, True, 0.7),
-        ("PipeGCN-GF g=0.5", "pipe", True, True, 0.5)]
+runs = [("GCN (vanilla)", "vanilla", False, False, 0.95, 1), ("PipeGCN", "pipe", False, False, 0.95, 1),
+        ("PipeGCN-F", "pipe", True, False, 0.95, 1), ("PipeGCN-G", "pipe", False, True, 0.95, 1),
+        ("PipeGCN-GF", "pipe", True, True, 0.95, 1), ("PipeGCN-GF g=0.7", "pipe", True, True, 0.7, 1),
+        ("PipeGCN-GF g=0.5", "pipe", True, True, 0.5, 1), ("PipeGCN-GF g=0", "pipe", True, True, 0.0, 1),
+        ("PipeGCN depth 2", "pipe", False, False, 0.95, 2), ("PipeGCN-GF depth 2", "pipe", True, True, 0.95, 2),
+        ("PipeGCN depth 3", "pipe", False, False, 0.95, 3)]
 rows = []
-for name, mode, sf, sg, gam in runs:
+for name, mode, sf, sg, gam, depth in runs:
     cfg = pgcn.make_config(m.widths, mode=mode, smooth_f=sf, smooth_g=sg, gamma=gam, dropout=m.dropout, loss=m.loss,
-                           opt="adam", lr=m.lr, n_global=g.n, n_train_global=g.n_train, staleness_stats=True)
+                           opt="adam", lr=m.lr, n_global=g.n, n_train_global=g.n_train, staleness_stats=True,
+                           depth=depth)
     ctx = pgcn.Context(part, cfg)
     for i in range(2):
         ctx.set_inputs(i, *inputs[i])
@@ -58,6 +62,8 @@ lines = ["# r1: staleness study (N4; paper Fig. 4, 5, 7 analogue)", "",
 for name, l0, l1, l2, l3, f, gg in rows:
     lines.append("| %s | %.4f | %.4f | %.4f | %.4f | %s | %s |" % (
         name, l0, l1, l2, l3, " / ".join("%.3g" % x for x in f[1:]), " / ".join("%.3g" % x for x in gg[1:])))
-lines += ["", "Layer-1 feature errors are 0 for t >= 2 (X is constant, R10); VANILLA errors are 0 by construction."]
-open(os.path.join(ROOT, "profiles", "r1_staleness.md"), "w").write("\n".join(lines) + "\n")
+lines += ["", "Layer-1 feature errors are 0 for t > depth (X is constant, R10); VANILLA errors are 0 by construction.",
+          "Depth s (R27): boundary values are s iterations old (compare the depth rows with PipeGCN / PipeGCN-GF)."]
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+open(os.path.join(ROOT, "gpurun_out", "r1_staleness.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
