@@ -27,7 +27,8 @@ int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1,
                   int64_t ld_out, int32_t relu, void* scratch, size_t scratch_bytes, void* stream);
 
 /* The aggregation kernel of S3 (Eq. 3): Z[v] = inv_deg[v] * sum_{e in row v} D[col[e]] for rows
- * [0, n_rows), neighbours >= n_valid contributing 0; D, Z row stride ld (multiple of 4).       */
+ * [0, n_rows); D holds n_valid rows and every column id must be < n_valid (the unchecked product
+ * variant, as in a step where every boundary row is installed); D, Z row stride ld (multiple of 4). */
 int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
                   int64_t n_rows, int64_t n_valid, float* Z, void* stream);
 

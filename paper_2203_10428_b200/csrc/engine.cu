@@ -750,13 +750,14 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         }
         Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
                                          4.0 * Fo * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, p.n_in, n_valid, out, C->work, 1, bias, C->F[l], l < C->L);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, p.n_in, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
+                 p.n_all);
         continue;
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
                                          4.0 * Fi * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -774,7 +775,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fo * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work);
+        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -786,7 +787,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
     {
       Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {

@@ -1,10 +1,12 @@
 // Node-update GEMMs of the GraphSAGE layer (S4 fwd, S6 dW, S7 dA) on the 5th-generation tensor
 // cores: TMA-fed, tcgen05.mma with fp32 accumulators in TMEM, warp-specialised, persistent.
 //
-// Precision: "3xTF32" -- every fp32 operand x is split as hi = rna_tf32(x), lo = rna_tf32(x - hi)
-// and D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::tf32, fp32 accumulate).  The dropped A_lo B_lo
-// term and the tf32 rounding of lo are O(2^-22) relative, so the result is fp32-grade (the 1e-4
-// parity tier of the north_star) while running on the tensor pipe.
+// Precision: "3xTF32" -- every fp32 operand x is split as x = hi + lo with hi = x truncated to
+// tf32 (the raw fp32 word: kind::tf32 reads its top 19 bits) and lo = x - hi (exact), and
+// D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::tf32, fp32 accumulate).  The dropped A_lo B_lo
+// term and the truncation of lo are O(2^-20) relative, so the result is fp32-grade (the 1e-4
+// parity tier of the north_star) while running on the tensor pipe.  Weights are pre-split
+// (hi = rna_tf32(W), lo = rna_tf32(W - hi)) by k_wprep.
 //
 // Roles (384 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer (one lane),
 // warps 2-7 = converters (split fp32 tiles into hi/lo in shared memory, in the UMMA layout),
@@ -122,6 +124,15 @@ __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+// hi = the fp32 word itself (kind::tf32 reads only the top 19 bits, i.e. truncates), lo = the exact
+// remainder x - trunc_tf32(x) (|lo| < 2^-10 |x|; its own truncation costs <= 2^-21 |x|).  The
+// converter then writes only lo: half the shared-memory stores of an explicit rna hi/lo split.
+#ifndef PGCN_TF32_TRUNC_HI
+#define PGCN_TF32_TRUNC_HI 1
+#endif
+__device__ __forceinline__ float tf32_lo_trunc(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 #define TMEM_LD16(taddr, r)                                                                                          \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
@@ -440,6 +451,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         }
         float4* A = reinterpret_cast<float4*>(stA + (size_t)s * stage_bytes);
         float4* Alo = A + a_bytes / 16;
+#if PGCN_TF32_TRUNC_HI
+        for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
+          const float4 x = A[i];
+          Alo[i] = make_float4(tf32_lo_trunc(x.x), tf32_lo_trunc(x.y), tf32_lo_trunc(x.z), tf32_lo_trunc(x.w));
+        }
+        if (split_b) {
+          const float4* B = A + 2 * (a_bytes / 16);
+          float4* Blo = A + 2 * (a_bytes / 16) + b_bytes / 16;
+          for (int i = ct; i < (int)(b_bytes / 16); i += kConvThreads) {
+            const float4 x = B[i];
+            Blo[i] = make_float4(tf32_lo_trunc(x.x), tf32_lo_trunc(x.y), tf32_lo_trunc(x.z), tf32_lo_trunc(x.w));
+          }
+        }
+#else
         for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
           float4 x = A[i], h, l;
           h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
@@ -462,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             Blo[i] = l;
           }
         }
+#endif
         fence_async_smem();
         mbar_arrive(&conv[s]);
         if (++s == S) { s = 0; ph ^= 1; }

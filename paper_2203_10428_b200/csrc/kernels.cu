@@ -44,6 +44,21 @@ __device__ __forceinline__ bool keep_at(const DropSpec& d, uint64_t kr, int64_t 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
+// Neighbour row c's float4 at lane base bq: one IMAD.WIDE.U32 with a 64-bit addend.
+__device__ __forceinline__ const float4* nbr(const char* bq, uint32_t c, uint32_t row_bytes) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(c), "r"(row_bytes), "l"(reinterpret_cast<uint64_t>(bq)));
+  return reinterpret_cast<const float4*>(r);
+}
+// Same sums as f4add (round-to-nearest per component) on the packed fp32x2 pipe (FADD2): half
+// the add instructions of the SpMM inner loops.
+__device__ __forceinline__ void f4acc(float4& a, const float4& b) {
+  asm("{\n\t.reg .b64 p, q;\n\t"
+      "mov.b64 p, {%0, %1};\n\tmov.b64 q, {%4, %5};\n\tadd.rn.f32x2 p, p, q;\n\tmov.b64 {%0, %1}, p;\n\t"
+      "mov.b64 p, {%2, %3};\n\tmov.b64 q, {%6, %7};\n\tadd.rn.f32x2 p, p, q;\n\tmov.b64 {%2, %3}, p;\n\t}"
+      : "+f"(a.x), "+f"(a.y), "+f"(a.z), "+f"(a.w)
+      : "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w));
+}
 __device__ __forceinline__ float4 f4scale(float4 a, float s) {
   return make_float4(a.x * s, a.y * s, a.z * s, a.w * s);
 }
@@ -56,9 +71,12 @@ __device__ __forceinline__ void set_comp(float4& v, int j, float x) {
 
 template <int G>
 __device__ __forceinline__ unsigned group_mask() {
-  if (G == 32) return 0xffffffffu;
-  const unsigned lane = threadIdx.x & 31u;
-  return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+  if constexpr (G == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+  }
 }
 
 __device__ __forceinline__ int find_seg(const SegTable& t, int64_t r) {
@@ -112,7 +130,7 @@ __device__ __forceinline__ int64_t next_item(unsigned long long* work, int lane,
   return (int64_t)__shfl_sync(gm, v, 0, G);
 }
 
-template <int G, int NC, int U, int MINB>
+template <int G, int NC, int U, int MINB, bool CHK>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __restrict__ rp,
                                                              const int32_t* __restrict__ col,
                                                              const float* __restrict__ inv_deg,
@@ -124,15 +142,28 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  // Hot-loop addressing is 32-bit: neighbour row c sits at lane_base + c * row_bytes (one
+  // IMAD.WIDE per edge; the launcher guarantees ld4 * 16 < 2^32 and ids < 2^31).
+  const uint32_t row_bytes = (uint32_t)ld4 * 16u;
+  const uint32_t nv = (uint32_t)n_valid;
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
   if (work) first = next_item<G>(work, lane, gm, 0, 0);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
     const int64_t row = it / nchunk;
     const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
+    // Lanes past the row end gather a clamped in-row column (same sectors as their neighbours,
+    // no extra traffic) and never store, so the loop carries no column predicates.
+    int xq[NC];
+    const char* bq[NC];  // lane column base per chunk: neighbour c's float4 is at bq + c * row_bytes
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      xq[q] = (int)(x0 + q * G < ld4 ? x0 + q * G : ld4 - 1);
+      bq[q] = reinterpret_cast<const char*>(D + xq[q]);
+    }
     float4 acc[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q)  // GCN-sym self loop (A + I, R26): the row's own (inner) input
-      acc[q] = (self && x0 + q * G < ld4) ? __ldg(D + row * ld4 + x0 + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -142,25 +173,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
         float4 v[U][NC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = __shfl_sync(gm, my, j + u, G);
-          const bool ok = c < n_valid;
-          const float4* src = D + (int64_t)c * ld4 + x0;
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u, G);
 #pragma unroll
           for (int q = 0; q < NC; ++q)
-            v[u][q] = (ok && x0 + q * G < ld4) ? __ldg(src + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][q] = (!CHK || c < nv) ? __ldg(nbr(bq[q], c, row_bytes))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+          for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
       for (; j < cnt; ++j) {
-        const int c = __shfl_sync(gm, my, j, G);
-        if (c < n_valid) {
-          const float4* src = D + (int64_t)c * ld4 + x0;
+        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
+        if (!CHK || c < nv) {
 #pragma unroll
           for (int q = 0; q < NC; ++q)
-            if (x0 + q * G < ld4) acc[q] = f4add(acc[q], __ldg(src + q * G));
+            f4acc(acc[q], __ldg(nbr(bq[q], c, row_bytes)));
         }
       }
     }
@@ -195,15 +224,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  const uint32_t row_bytes = (uint32_t)ldA4 * 16u;  // 32-bit hot-loop addressing (see k_spmm_fwd)
+  const char* base = reinterpret_cast<const char*>(dZs);
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
   if (work) first = next_item<G>(work, lane, gm, 0, 0);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
     const int64_t u0 = it / nchunk;
     const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
+    int xq[NC];
+    const char* bq[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      xq[q] = (int)(x0 + q * G < ld4 ? x0 + q * G : ld4 - 1);
+      bq[q] = base + (size_t)xq[q] * 16;
+    }
     float4 acc[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q)
-      acc[q] = (dDs && u0 < n_in && x0 + q * G < ld4) ? dDs[u0 * ldA4 + x0 + q * G] : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[q] = (dDs && u0 < n_in) ? dDs[u0 * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -213,23 +251,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
         float4 v[U][NC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = __shfl_sync(gm, my, j + u, G);
-          const float4* src = dZs + (int64_t)c * ldA4 + x0;
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u, G);
 #pragma unroll
-          for (int q = 0; q < NC; ++q)
-            v[u][q] = x0 + q * G < ld4 ? __ldg(src + q * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < NC; ++q) v[u][q] = __ldg(nbr(bq[q], c, row_bytes));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int q = 0; q < NC; ++q) acc[q] = f4add(acc[q], v[u][q]);
+          for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
       for (; j < cnt; ++j) {
-        const int c = __shfl_sync(gm, my, j, G);
-        const float4* src = dZs + (int64_t)c * ldA4 + x0;
+        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
 #pragma unroll
         for (int q = 0; q < NC; ++q)
-          if (x0 + q * G < ld4) acc[q] = f4add(acc[q], __ldg(src + q * G));
+          f4acc(acc[q], __ldg(nbr(bq[q], c, row_bytes)));
       }
     }
     const uint64_t kr = row_key(d, gid[u0]);
@@ -752,9 +787,14 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
-              int64_t n_bias, int relu) {
+              int64_t n_bias, int relu, int64_t n_cols) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
+  if (ld4 * 16 >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
+    std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
+    std::abort();
+  }
+  const bool chk = n_cols < 0 || n_valid < n_cols;  // some neighbour rows are not valid yet
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;
   if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
@@ -763,8 +803,14 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
   auto Z4 = reinterpret_cast<float4*>(Z);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
-    k_spmm_fwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid,   \
-                                                             sh.nchunk, Z4, work, self, bias, n_bias, relu);   \
+    if (chk)                                                                                                   \
+      k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
+                                                                     n_valid, sh.nchunk, Z4, work, self, bias,  \
+                                                                     n_bias, relu);                             \
+    else                                                                                                       \
+      k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,    \
+                                                                      n_valid, sh.nchunk, Z4, work, self, bias, \
+                                                                      n_bias, relu);                            \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -776,6 +822,10 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
               const DropSpec& d, unsigned long long* work, const float* rs) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
+  if (ld_dA * 4 >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
+    std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
+    std::abort();
+  }
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;
   if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
@@ -957,7 +1007,7 @@ extern "C" int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const f
                              int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, void* stream) {
   if (!row_ptr || !col || !inv_deg || !D || !Z || ld % 4 || n_rows < 0) return -1;
   pgcn::spmm_fwd(pgcn::Launch{static_cast<cudaStream_t>(stream), nullptr}, row_ptr, col, inv_deg, D, ld, n_rows,
-                 n_valid, Z, nullptr);
+                 n_valid, Z, nullptr, 0, nullptr, 0, 0, n_valid);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -43,10 +43,11 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 // or nullptr for static grid-stride.
 // GCN-sym (R26): self = 1 adds the row's own D[v] (A + I); inv_deg then holds d~_v^-1/2.
 // bias (optional, n_bias entries): Z = act(Z + b) epilogue (relu = ReLU), fusing the node update of
-// a transform-first GCN layer.
+// a transform-first GCN layer.  n_cols: rows of D (neighbour ids < n_cols); -1 = unknown (ids are
+// then checked against n_valid on every edge).
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
-              int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0);
+              int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1);
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpgcn.so")
+LIB_PATH = os.environ.get("PGCN_LIB") or os.path.join(HERE, "libpgcn.so")  # PGCN_LIB: dev A/B builds
 MAX_LAYERS = 16
 MAX_PARTS = 64
 
