@@ -706,7 +706,7 @@ struct SpmmShape {
 #define PGCN_SPMM_CASES(X)                                                                                     \
   X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
   X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
-  X(32, 4, 2, 3)
+  X(32, 4, 2, 3) X(32, 2, 8, 2)
 
 static bool dyn_enabled() {
   static int v = -1;
@@ -764,8 +764,10 @@ SpmmShape spmm_shape(int64_t ld4) {
   for (int c : NCs)
     if (c >= nc) { pick = c; break; }
   s.NC = pick;
-  s.U = pick == 2 ? 4 : (pick <= 4 ? 2 : 1);
-  s.MB = pick == 2 ? 4 : (pick <= 6 ? 3 : (pick <= 8 ? 2 : 1));
+  // 256-wide rows (pick 2): 8 neighbours in flight x 2 float4 per lane, 2 blocks/SM (in-situ sweep
+  // after the 32-bit-addressing rewrite, tools/spmm_sweep5.sh: Reddit step 49.0 -> 46.5 ms).
+  s.U = pick == 2 ? 8 : (pick <= 4 ? 2 : 1);
+  s.MB = pick == 2 ? 2 : (pick <= 6 ? 3 : (pick <= 8 ? 2 : 1));
   s.nchunk = (int)((ld4 + 32 * pick - 1) / (32 * pick));
   return s;
 }
