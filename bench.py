@@ -115,13 +115,16 @@ def l2_ceilings(pgcn, torch, g_rp, n_rows, stream):
     buf = torch.ones(nbytes // 4, device="cuda")
     out = torch.empty(148 * 8, device="cuda")
     reps = 50
-    with torch.cuda.stream(stream):
-        L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, 2, out.data_ptr(), s)
-        e0.record(stream)
-        L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, reps, out.data_ptr(), s)
-        e1.record(stream)
-    torch.cuda.synchronize()
-    res = {"l2_read_GBps": nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9}
+    best = 0.0
+    for variant in (0, 1, 2):
+        with torch.cuda.stream(stream):
+            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | 2, out.data_ptr(), s)
+            e0.record(stream)
+            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | reps, out.data_ptr(), s)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    res = {"l2_read_GBps": best}
     rp = torch.tensor(g_rp, device="cuda")
     nnz = int(g_rp[-1])
     col = torch.randint(0, 30000, (nnz,), device="cuda", dtype=torch.int32)

@@ -32,9 +32,11 @@ int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1,
 int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
                   int64_t n_rows, int64_t n_valid, float* Z, void* stream);
 
-/* L2 streaming-read microbenchmark (roofline denominator for L2-served kernels): every thread reads
- * float4s of buf[0 .. bytes) grid-stride, `reps` passes, and writes one checksum per block to
- * out[gridDim] (148 x 8 blocks of 256 threads).  Keep `bytes` well below the 126 MB L2.        */
+/* L2 streaming-read microbenchmark (roofline denominator for L2-served kernels): warps stream
+ * contiguous chunks of buf[0 .. bytes) with __ldcg, `reps` passes (low 24 bits of reps), and write
+ * one checksum per block to out[] (up to 148 x 8 blocks of 256 threads).  reps bits 24..31 pick the
+ * variant (0: 4 loads in flight per lane, 8 blocks/SM; 1: 8 loads, 8 blocks/SM; 2: 8 loads, 4
+ * blocks/SM).  Keep `bytes` well below the 126 MB L2.                                          */
 int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, float* out, void* stream);
 
 #ifdef __cplusplus

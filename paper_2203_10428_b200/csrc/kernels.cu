@@ -88,12 +88,32 @@ __device__ __forceinline__ int find_seg(const SegTable& t, int64_t r) {
   return lo;
 }
 
+// Division-free grid-stride walk over the float4 elements (r, x) of an n_rows x ld4 array: one
+// 64-bit division per thread at the start, then (r, x) advances by the grid size with a carry.
+struct RowCursor {
+  int64_t r;
+  int x, dx;
+  int64_t dr;
+  __device__ __forceinline__ RowCursor(int64_t ld4) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    r = g / ld4;
+    x = (int)(g - r * ld4);
+    dr = T / ld4;
+    dx = (int)(T - dr * ld4);
+  }
+  __device__ __forceinline__ void next(int ld4) {
+    r += dr;
+    x += dx;
+    if (x >= ld4) { x -= ld4; ++r; }
+  }
+};
+
 // ---------------------------------------------------------------- dropout (S3 prologue, R5)
 __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, int64_t ld4, int64_t n_rows,
                           int64_t n_valid, const int64_t* __restrict__ gid, DropSpec d, const float* __restrict__ rs) {
-  const int64_t total = n_rows * ld4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / ld4, x = i - r * ld4;
+  for (RowCursor rc(ld4); rc.r < n_rows; rc.next((int)ld4)) {
+    const int64_t r = rc.r, x = rc.x, i = r * ld4 + x;
     float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < n_valid) {
       const float4 h = H[i];
@@ -291,9 +311,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
 __global__ void k_gather(const __grid_constant__ SegTable t, const int32_t* __restrict__ row_map, int64_t n_rows,
                          int64_t ld4, float4* __restrict__ dst, const float4* __restrict__ prev, float gamma, int ema,
                          int first) {
-  const int64_t total = n_rows * ld4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / ld4, x = i - r * ld4;
+  for (RowCursor rc(ld4); rc.r < n_rows; rc.next((int)ld4)) {
+    const int64_t r = rc.r, x = rc.x, i = r * ld4 + x;
     const int s = find_seg(t, r);
     const int64_t srow = row_map ? (int64_t)row_map[r] : r - t.off[s];
     float4 v = __ldg(reinterpret_cast<const float4*>(t.base[s]) + srow * ld4 + x);
@@ -629,9 +648,10 @@ __global__ void __launch_bounds__(256) k_gemm_da(const float* __restrict__ Mg, i
 // out[v] = s[v] * M[v] (row scaling, e.g. inv_deg o M before the transposed aggregation)
 __global__ void k_scale_rows(const float4* __restrict__ M, const float* __restrict__ sc, int64_t n, int64_t ld4,
                              float4* __restrict__ out) {
-  const int64_t total = n * ld4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = f4scale(M[i], sc[i / ld4]);
+  for (RowCursor rc(ld4); rc.r < n; rc.next((int)ld4)) {
+    const int64_t i = rc.r * ld4 + rc.x;
+    out[i] = f4scale(M[i], sc[rc.r]);
+  }
 }
 
 // ---------------------------------------------------------------- staleness diagnostics (N4)
@@ -977,18 +997,27 @@ void opt_update(Launch L, const float* grads, int64_t P, float* params, float* m
 }
 
 namespace {
+template <int U>
 __global__ void __launch_bounds__(256) k_l2_read(const float4* __restrict__ buf, int64_t n4, int reps,
                                                  float* __restrict__ out) {
+  // Each warp streams contiguous 512*U-byte chunks (U independent 512-byte LDG.128 per lane in
+  // flight), chunks handed out grid-stride over warps; 32-bit indexing.
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t n_chunks = (uint32_t)(n4 / (32 * U));
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int r = 0; r < reps; ++r) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t st = (int64_t)gridDim.x * blockDim.x;
-    for (; i + st < n4; i += 2 * st) {
-      const float4 x = __ldcg(buf + i), y = __ldcg(buf + i + st);
-      a = f4add(a, x);
-      b = f4add(b, y);
+    for (uint32_t c = w0; c < n_chunks; c += nw) {
+      const float4* p = buf + (size_t)c * (32 * U) + lane;
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(p + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        f4acc(a, v[u]);
+        if (u + 1 < U) f4acc(b, v[u + 1]);
+      }
     }
-    if (i < n4) a = f4add(a, __ldcg(buf + i));
   }
   float s = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
 #pragma unroll
@@ -1015,7 +1044,14 @@ extern "C" int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const f
 
 extern "C" int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, float* out, void* stream) {
   if (!buf || !out || bytes < 16 || reps < 1) return -1;
-  pgcn::k_l2_read<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const float4*>(buf), bytes / 16,
-                                                                       reps, out);
+  // variant (reps' high byte): 0 = 4 x 512 B in flight per warp, 8 blocks/SM; 1 = 8 x 512 B,
+  // 8 blocks/SM; 2 = 8 x 512 B, 4 blocks/SM.  The caller takes the best as the L2 read peak.
+  const int variant = (reps >> 24) & 0xff;
+  reps &= 0xffffff;
+  auto s = static_cast<cudaStream_t>(stream);
+  auto b4 = static_cast<const float4*>(buf);
+  if (variant == 0) pgcn::k_l2_read<4><<<148 * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
+  else if (variant == 1) pgcn::k_l2_read<8><<<148 * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
+  else pgcn::k_l2_read<8><<<148 * 4, 256, 0, s>>>(b4, bytes / 16, reps, out);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
