@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--mode", default="pipe", choices=["pipe", "vanilla"])
     ap.add_argument("--smooth", default="", help="'', 'f', 'g' or 'gf'")
     ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "bf16"])
+    ap.add_argument("--gather", default="f32", choices=["f32", "bf16"],
+                    help="bf16: the bf16 gather tier (SpMM tables rounded to bf16, 2e-2 tier; SURVEY N1(iv))")
     ap.add_argument("--model", default="sage", choices=["sage", "gcn"],
                     help="GraphSAGE-mean (the paper's benchmark model) or GCN-sym (App. A.1, SURVEY N3)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -251,7 +253,7 @@ def main():
     t_part = time.time() - t0
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
-                           n_train_global=g.n_train, gemm=args.gemm, model=args.model)
+                           n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
@@ -400,7 +402,11 @@ def main():
     if rank != 0:
         return
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f32" if args.gather == "f32" and args.gemm != "bf16" else
+           ("bf16" if args.gather == "bf16" and args.gemm == "bf16" else
+            "mixed: %s gathers, %s GEMM" % (args.gather, "bf16" if args.gemm == "bf16" else "3xTF32")),
+           "data": "synthetic",
            "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU(s), %s%s, "
                                   "dropout %.1f, Adam%s" % (args.config, g.n, g.nnz, m.widths, parts, world, args.mode,
                                                             ("-" + args.smooth.upper()) if args.smooth else "",
@@ -408,6 +414,7 @@ def main():
                       "global_batch": g.n,
                       "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
                       ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,
+                      "gather": args.gather,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "breakdown": breakdown, "loss": loss_v,

@@ -139,8 +139,8 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       floor(p*2^24 + 0.5), key = ((t(L+1)+l)N + gid)F_{l-1} + col, applied
  *                       to every layer's input after the exchange (App. F; R5).
  *   gemm                0 fp32-grade on the tensor cores: tcgen05 kind::tf32 with the 3xTF32 split
- *                       (hi/lo operands, 1e-4 tier; default); 1 BF16 tensor cores (2e-2 tier, not
- *                       built yet); 2 fp32 SIMT CUDA-core GEMMs (reference kernels).
+ *                       (hi/lo operands, 1e-4 tier; default); 1 BF16 tensor cores (kind::f16, 2e-2
+ *                       tier); 2 fp32 SIMT CUDA-core GEMMs (reference kernels).
  *   loss                0 softmax cross-entropy (labels int32 [n_inner]), 1 sigmoid BCE
  *                       (labels uint8 [n_inner x F_L]); mean over the GLOBAL train set (R6).
  *   n_global            N (dropout keys); n_train_global: |train set| over the whole graph.
@@ -160,6 +160,11 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *   model               0 GraphSAGE-mean (above); 1 GCN-sym (SURVEY N3, App. A.1 PAPER.md:637-647,
  *                       reading R26): Y = P D W + b with P = D~^-1/2 (A + I) D~^-1/2, D~ = d + 1
  *                       (full-graph degrees), W [F_{l-1} x F_l]; tensor-core GEMMs only (gemm 0/1).
+ *   gather              0 fp32 aggregation tables (default); 1 bf16 gather tier (SURVEY N1(iv), 2e-2
+ *                       tier): every table an SpMM gathers (dropout output / T / dZ') is rounded to
+ *                       bf16 first, the SpMMs gather bf16 rows and accumulate in fp32 -- half the
+ *                       gathered bytes.  Everything else (H, J, exchange payloads, GEMM outputs)
+ *                       stays fp32.
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -181,6 +186,7 @@ typedef struct {
   int32_t staleness_stats;
   int32_t model;
   int32_t depth;
+  int32_t gather;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

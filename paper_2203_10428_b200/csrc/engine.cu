@@ -58,6 +58,7 @@ struct PartCtx {
   uint8_t* train = nullptr;
   float* row_loss = nullptr;
   float* G = nullptr;
+  uint16_t* G16 = nullptr;  // bf16 gather tier (cfg.gather): rounded copy of the table an SpMM gathers
 };
 
 struct Arena {
@@ -164,6 +165,7 @@ int validate_cfg(const pgcn_config* c) {
   if (c->model != 0 && c->model != 1) return fail(PGCN_EINVAL, "model must be 0 (GraphSAGE) or 1 (GCN-sym)");
   if (c->model == 1 && c->gemm == 2) return fail(PGCN_EUNSUPPORTED, "GCN-sym needs the tensor-core GEMMs (gemm 0/1)");
   if (c->depth < 0 || c->depth > PGCN_MAX_DEPTH) return fail(PGCN_EINVAL, "depth must be in 0..%d", PGCN_MAX_DEPTH);
+  if (c->gather != 0 && c->gather != 1) return fail(PGCN_EINVAL, "gather must be 0 (fp32) or 1 (bf16)");
   return PGCN_OK;
 }
 
@@ -220,6 +222,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.train = A.take<uint8_t>(p.n_in);
     p.row_loss = A.take<float>(p.n_in);
     p.G = A.take<float>(C->P);
+    if (C->cfg.gather == 1) p.G16 = A.take<uint16_t>(p.n_all * round_up(C->ldmax, 8));
     for (int l = 1; l <= L; ++l) {
       int64_t w = gemm_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
       if (w > dw_need) dw_need = w;
@@ -675,6 +678,10 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     cudaMemsetAsync(C->diag, 0, sizeof(double) * 2 * (PGCN_MAX_LAYERS + 1), C->s);
   const bool tcg = C->cfg.gemm != 2;
   const int bf = C->cfg.gemm == 1;
+  // algorithmic SpMM bytes: gathered rows (fp32, or bf16 in the gather tier) and, in the bf16 tier,
+  // the rounding pass over the table (read fp32, write bf16)
+  auto gat = [&](double F, double e) { return (C->cfg.gather ? 2.0 : 4.0) * F * e; };
+  auto cvt = [&](double F, double rows) { return C->cfg.gather ? 6.0 * F * rows : 0.0; };
   const int kbk = bf ? 64 : 32;
   if (tcg) {
     Scope sc(C, PGCN_K_GEMM_FWD, 0.0);
@@ -748,16 +755,16 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                           ldo, nullptr, nullptr, 0, 0, bf))
             return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
         }
-        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, (p.nnz + p.n_in)) + cvt(Fo, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
                                          4.0 * Fo * p.n_in);
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, p.n_in, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
-                 p.n_all);
+                 p.n_all, p.G16);
         continue;
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (p.nnz + p.n_in)) + cvt(Fi, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
                                          4.0 * Fi * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -774,8 +781,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fo * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fo * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all);
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, p.nnz) + cvt(Fo, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fo * p.n_in);
+        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
+                 p.G16);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -786,8 +794,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       continue;
     }
     {
-      Scope sc(C, PGCN_K_SPMM_FWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all);
+      Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, p.nnz) + cvt(Fi, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -839,6 +847,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
   const float* Wext = params + C->woff[l];
   const int bf = C->cfg.gemm == 1;
+  // algorithmic SpMM bytes: gathered rows (fp32, or bf16 in the gather tier) and, in the bf16 tier,
+  // the rounding pass over the table (read fp32, write bf16)
+  auto gat = [&](double F, double e) { return (C->cfg.gather ? 2.0 : 4.0) * F * e; };
+  auto cvt = [&](double F, double rows) { return C->cfg.gather ? 6.0 * F * rows : 0.0; };
   // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
@@ -849,12 +861,13 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // Q = (A + I)^T (S M) over inner + boundary rows; G = [D'^T Q ; colsum M]; J = mask o s o S (Q W^T)
         const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
         {
-          Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fo * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+          Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, (p.nnz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
                                            8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all);
           scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
           DropSpec none{};
           none.width = (int32_t)C->F[l];
-          spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work);
+          spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+                   p.G16);
         }
         {
           Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
@@ -884,10 +897,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         }
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
-        Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * (p.nnz + p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (p.nnz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
         spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym);
+                 C->work, p.sym, p.G16);
       }
       continue;
     }
@@ -896,12 +909,13 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
       const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
       {
-        Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fo * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
+        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, p.nnz) + cvt(Fo, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
                                          4.0 * Fo * p.n_all);
         scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
         DropSpec none{};
         none.width = (int32_t)C->F[l];
-        spmm_bwd(Lk, p.trp, p.tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work);
+        spmm_bwd(Lk, p.trp, p.tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+                 p.G16);
       }
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
@@ -940,10 +954,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
         }
       }
-      Scope sc(C, PGCN_K_SPMM_BWD, 4.0 * Fi * p.nnz + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
+      Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, p.nnz) + cvt(Fi, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l), C->work);
+               drop_spec(C, t, l), C->work, nullptr, p.G16);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

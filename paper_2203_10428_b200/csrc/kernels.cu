@@ -44,6 +44,19 @@ __device__ __forceinline__ bool keep_at(const DropSpec& d, uint64_t kr, int64_t 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
+// bf16 packing (round to nearest even) and exact widening accumulate of a bf16 pair on FADD2.
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void bf16x2_acc(float& a0, float& a1, uint32_t w) {
+  // mixed-precision adds (fp32 += bf16 half-word): one FHADD.BF16 per element, no unpacking
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "add.rn.f32.bf16 %0, l, %0;\n\tadd.rn.f32.bf16 %1, h, %1;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(w));
+}
 // Neighbour row c's float4 at lane base bq: one IMAD.WIDE.U32 with a 64-bit addend.
 __device__ __forceinline__ const float4* nbr(const char* bq, uint32_t c, uint32_t row_bytes) {
   uint64_t r;
@@ -303,6 +316,209 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
         set_comp(o, j, val);
       }
       J[u0 * ld4 + x] = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- bf16 gather tier
+// The gathered table is first rounded to bf16 (k_to_bf16: rows of ld8 16-byte vectors = 8 columns,
+// padding columns 0); the SpMMs then gather half the bytes and accumulate in fp32 (exact bf16 ->
+// fp32 widening, FADD2 sums).  2e-2 tier (north_star), selected by pgcn_config.gather = 1.
+// src: n_rows rows of stride s4 float4s, of which the first w4 are converted (the rest of the ld8
+// vectors are zero padding).
+__global__ void k_to_bf16(const float4* __restrict__ src, int64_t s4, int64_t w4, int64_t n_rows, int64_t ld8,
+                          uint4* __restrict__ dst) {
+  for (RowCursor rc(ld8); rc.r < n_rows; rc.next((int)ld8)) {
+    const int64_t x0 = 2 * (int64_t)rc.x;
+    const float4 a = x0 < w4 ? src[rc.r * s4 + x0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = x0 + 1 < w4 ? src[rc.r * s4 + x0 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint4 o;
+    o.x = bf16x2_rn(a.x, a.y);
+    o.y = bf16x2_rn(a.z, a.w);
+    o.z = bf16x2_rn(b.x, b.y);
+    o.w = bf16x2_rn(b.z, b.w);
+    dst[rc.r * ld8 + rc.x] = o;
+  }
+}
+
+__device__ __forceinline__ void acc8(float (&a)[8], const uint4& w) {
+  bf16x2_acc(a[0], a[1], w.x);
+  bf16x2_acc(a[2], a[3], w.y);
+  bf16x2_acc(a[4], a[5], w.z);
+  bf16x2_acc(a[6], a[7], w.w);
+}
+__device__ __forceinline__ void set8(float (&a)[8], const uint4& w) {
+  a[0] = __uint_as_float(w.x << 16); a[1] = __uint_as_float(w.x & 0xffff0000u);
+  a[2] = __uint_as_float(w.y << 16); a[3] = __uint_as_float(w.y & 0xffff0000u);
+  a[4] = __uint_as_float(w.z << 16); a[5] = __uint_as_float(w.z & 0xffff0000u);
+  a[6] = __uint_as_float(w.w << 16); a[7] = __uint_as_float(w.w & 0xffff0000u);
+}
+
+// S3 on a bf16 table: same work items / scheduling as k_spmm_fwd, a lane owns 8 columns (one
+// 16-byte bf16 vector) per chunk q; fp32 output (stride ld4 float4s).
+template <int G, int NC, int U, int MINB, bool CHK>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __restrict__ rp,
+                                                               const int32_t* __restrict__ col,
+                                                               const float* __restrict__ inv_deg,
+                                                               const uint4* __restrict__ D, int64_t ld8,
+                                                               int64_t n_rows, int64_t n_valid, int nchunk,
+                                                               float4* __restrict__ Z, int64_t ld4,
+                                                               unsigned long long* work, int self,
+                                                               const float* __restrict__ bias, int64_t n_bias,
+                                                               int relu) {
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const int64_t n_items = n_rows * nchunk;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  const uint32_t row_bytes = (uint32_t)ld8 * 16u;
+  const uint32_t nv = (uint32_t)n_valid;
+  int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+  if (work) first = next_item<G>(work, lane, gm, 0, 0);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+    const int64_t row = it / nchunk;
+    const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
+    const char* bq[NC];
+    float acc[NC][8];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t xq = x0 + q * G < ld8 ? x0 + q * G : ld8 - 1;
+      bq[q] = reinterpret_cast<const char*>(D + xq);
+      if (self) set8(acc[q], __ldg(D + row * ld8 + xq));
+      else
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
+    }
+    const int64_t beg = rp[row], end = rp[row + 1];
+    for (int64_t e0 = beg; e0 < end; e0 += G) {
+      const int cnt = (int)((end - e0) < G ? (end - e0) : G);
+      const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        uint4 v[U][NC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u, G);
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = (!CHK || c < nv) ? __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes)))
+                                       : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
+      }
+      for (; j < cnt; ++j) {
+        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
+        if (!CHK || c < nv) {
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc8(acc[q], __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))));
+        }
+      }
+    }
+    const float s = inv_deg[row];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = x0 + q * G;
+      if (x >= ld8) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t xf = 2 * x + h;
+        if (xf >= ld4) continue;
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float v = acc[q][4 * h + j] * s;
+          if (bias) {
+            v += 4 * xf + j < n_bias ? bias[4 * xf + j] : 0.f;
+            if (relu) v = fmaxf(v, 0.f);
+          }
+          o[j] = v;
+        }
+        Z[row * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
+// S8 on a bf16 copy of dZs (ld8 vectors per row, n_in rows); dDs stays fp32 (stride ldA4).
+template <int G, int NC, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __restrict__ trp,
+                                                               const int32_t* __restrict__ tcol,
+                                                               const uint4* __restrict__ dZs, int64_t ld8,
+                                                               const float4* __restrict__ dDs, int64_t ldA4,
+                                                               int64_t n_in, int64_t n_all, int nchunk,
+                                                               float4* __restrict__ J, int64_t ld4,
+                                                               const int64_t* __restrict__ gid, DropSpec d,
+                                                               unsigned long long* work, const float* __restrict__ rs) {
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const int64_t n_items = n_all * nchunk;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  const uint32_t row_bytes = (uint32_t)ld8 * 16u;
+  int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+  if (work) first = next_item<G>(work, lane, gm, 0, 0);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+    const int64_t u0 = it / nchunk;
+    const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
+    const char* bq[NC];
+    float acc[NC][8];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t xq = x0 + q * G < ld8 ? x0 + q * G : ld8 - 1;
+      bq[q] = reinterpret_cast<const char*>(dZs + xq);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t xf = 2 * xq + h;
+        const float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
+      }
+    }
+    const int64_t beg = trp[u0], end = trp[u0 + 1];
+    for (int64_t e0 = beg; e0 < end; e0 += G) {
+      const int cnt = (int)((end - e0) < G ? (end - e0) : G);
+      const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        uint4 v[U][NC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u, G);
+#pragma unroll
+          for (int q = 0; q < NC; ++q) v[u][q] = __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes)));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
+      }
+      for (; j < cnt; ++j) {
+        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc8(acc[q], __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))));
+      }
+    }
+    const uint64_t kr = row_key(d, gid[u0]);
+    const float sr = rs ? rs[u0] : 1.f;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t x = x0 + q * G;
+      if (x >= ld8) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t xf = 2 * x + h;
+        if (xf >= ld4) continue;
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t c = 4 * xf + j;
+          float val = rs ? acc[q][4 * h + j] * sr : acc[q][4 * h + j];
+          if (c >= d.width) val = 0.f;
+          else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
+          o[j] = val;
+        }
+        J[u0 * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
+      }
     }
   }
 }
@@ -756,8 +972,9 @@ bool spmm_override(int64_t ld4, SpmmShape& s) {
     long long w;
     int g, nc, u, mb, n = 0;
     if (std::sscanf(p, "%lld=%d,%d,%d,%d%n", &w, &g, &nc, &u, &mb, &n) == 5) {
-      if (w == ld4 && spmm_instantiated(g, nc, u, mb)) {
-        s = SpmmShape{g, nc, u, mb, (int)((ld4 + (int64_t)g * nc - 1) / ((int64_t)g * nc))};
+      if (w == ld4 && (ld4 >= 1000000 || spmm_instantiated(g, nc, u, mb))) {
+        const int64_t w4 = ld4 >= 1000000 ? ld4 - 1000000 : ld4;
+        s = SpmmShape{g, nc, u, mb, (int)((w4 + (int64_t)g * nc - 1) / ((int64_t)g * nc))};
         return true;
       }
       p += n;
@@ -792,6 +1009,32 @@ SpmmShape spmm_shape(int64_t ld4) {
   return s;
 }
 
+// bf16 tier: a lane owns one 16-byte vector (8 columns) per chunk; rows of ld8 vectors.
+#define PGCN_SPMM16_CASES(X) \
+  X(32, 1, 16, 2) X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 3) X(32, 3, 2, 3) X(32, 6, 1, 2) \
+  X(8, 1, 16, 2) X(32, 1, 12, 3) X(16, 1, 16, 2)
+
+SpmmShape spmm16_shape(int64_t ld8) {
+  SpmmShape s{32, 1, 8, 4, 1};
+  if (spmm_override(1000000 + ld8, s)) return s;  // PGCN_SPMM_TABLE key 1000000 + ld8 (dev sweeps)
+  if (ld8 <= 16) {
+    int g = 4;
+    while (g < ld8) g *= 2;
+    s.G = g;
+  } else if (ld8 <= 32) {
+    s.U = 16;
+    s.MB = 2;
+  } else if (ld8 <= 64) {
+    s.NC = 2; s.U = 4; s.MB = 3;
+  } else if (ld8 <= 96) {
+    s.NC = 3; s.U = 2; s.MB = 3;
+  } else {
+    s.NC = 6; s.U = 1; s.MB = 2;
+  }
+  s.nchunk = (int)((ld8 + (int64_t)s.G * s.NC - 1) / ((int64_t)s.G * s.NC));
+  return s;
+}
+
 }  // namespace
 
 static void count(const Launch& L, int64_t n = 1) {
@@ -809,9 +1052,44 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
-              int64_t n_bias, int relu, int64_t n_cols) {
+              int64_t n_bias, int relu, int64_t n_cols, void* g16) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
+  if (g16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
+    const int64_t ld8 = (ld + 7) / 8;
+    if (ld8 * 16 >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
+      std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
+      std::abort();
+    }
+    auto G16 = static_cast<uint4*>(g16);
+    k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
+                                                                          ld4, n_valid, ld8, G16);
+    count(L);
+    const bool chk16 = n_cols < 0 || n_valid < n_cols;
+    const SpmmShape sh = spmm16_shape(ld8);
+    if (!dyn_enabled()) work = nullptr;
+    if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
+    const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
+    auto Z4 = reinterpret_cast<float4*>(Z);
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    if (chk16)                                                                                                 \
+      k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
+                                                                       n_valid, sh.nchunk, Z4, ld4, work, self, \
+                                                                       bias, n_bias, relu);                     \
+    else                                                                                                       \
+      k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows, \
+                                                                        n_valid, sh.nchunk, Z4, ld4, work,      \
+                                                                        self, bias, n_bias, relu);              \
+  } else
+    PGCN_SPMM16_CASES(X) {
+      std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
+      std::abort();
+    }
+#undef X
+    count(L);
+    return;
+  }
   if (ld4 * 16 >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
     std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();
@@ -841,9 +1119,39 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
-              const DropSpec& d, unsigned long long* work, const float* rs) {
+              const DropSpec& d, unsigned long long* work, const float* rs, void* g16) {
   if (n_all <= 0) return;
   const int64_t ld4 = ld / 4;
+  if (g16) {  // bf16 gather tier: dZs (n_in rows of stride ld_dA) -> bf16 rows of ld8 vectors
+    const int64_t ld8 = (ld + 7) / 8;
+    if (ld8 * 16 >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
+      std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
+      std::abort();
+    }
+    auto G16 = static_cast<uint4*>(g16);
+    k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
+                                                                       ld_dA / 4, ld4, n_in, ld8, G16);
+    count(L);
+    const SpmmShape sh = spmm16_shape(ld8);
+    if (!dyn_enabled()) work = nullptr;
+    if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
+    const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
+    auto b = reinterpret_cast<const float4*>(dDs);
+    auto J4 = reinterpret_cast<float4*>(J);
+    const int64_t lda4 = ld_dA / 4;
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all, \
+                                                               sh.nchunk, J4, ld4, gid, d, work, rs);          \
+  } else
+    PGCN_SPMM16_CASES(X) {
+      std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
+      std::abort();
+    }
+#undef X
+    count(L);
+    return;
+  }
   if (ld_dA * 4 >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
     std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();

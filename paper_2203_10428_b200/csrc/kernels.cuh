@@ -47,7 +47,8 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 // then checked against n_valid on every edge).
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
-              int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1);
+              int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
+              void* g16 = nullptr);
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
@@ -55,7 +56,11 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
 //     then realises the self loop).
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
-              const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr);
+              const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
+              void* g16 = nullptr);
+// g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1) -- scratch of at least
+// (rows of the gathered table) x round_up(ld, 8) bf16; the table is rounded to bf16 there first and
+// the kernel gathers the bf16 rows (fp32 accumulation, fp32 output).  nullptr = fp32 gathers.
 
 // N4 diagnostics: out[0] += sum_{r < n_rows, c < F} (used(r, c) - fresh(r, c))^2 with fresh rows from a
 // segment table (row_map fmap) and used rows from a segment table (umap), a plain array, or 0.

@@ -50,7 +50,7 @@ class Config(C.Structure):
                 ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
-                ("model", C.c_int32), ("depth", C.c_int32)]
+                ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -182,7 +182,8 @@ def partition(n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0) -> Partit
 def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=False, gamma=0.95,
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
-                transform_first=True, staleness_stats=False, model="sage", depth=1) -> Config:
+                transform_first=True, staleness_stats=False, model="sage", depth=1,
+                gather="f32") -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -201,6 +202,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.staleness_stats = int(bool(staleness_stats))
     c.model = {"sage": 0, "gcn": 1}[model]
     c.depth = int(depth)
+    c.gather = {"f32": 0, "bf16": 1}[gather]
     return c
 
 
