@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "pgcn_dev.h"
@@ -757,8 +758,14 @@ size_t tc_smem_bytes(int BN, int S, int bf, int mode) {
 }
 
 int tc_bn(int64_t N) {
+  static int cap = -1;  // dev knob PGCN_TC_BNMAX: cap the FWD/DA n-tile (A/B experiments)
+  if (cap < 0) {
+    const char* e = std::getenv("PGCN_TC_BNMAX");
+    cap = e ? std::atoi(e) : 256;
+    if (cap < 16 || cap > 256) cap = 256;
+  }
   int64_t bn = (N + 15) / 16 * 16;
-  if (bn > 256) bn = 256;
+  if (bn > cap) bn = cap;
   if (bn < 16) bn = 16;
   return (int)bn;
 }

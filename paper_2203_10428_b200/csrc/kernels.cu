@@ -1022,8 +1022,7 @@ SpmmShape spmm16_shape(int64_t ld8) {
     while (g < ld8) g *= 2;
     s.G = g;
   } else if (ld8 <= 32) {
-    s.U = 16;
-    s.MB = 2;
+    // (32, 1, 8, 4): measured best for 256-wide rows (tools/spmm16_sweep.sh)
   } else if (ld8 <= 64) {
     s.NC = 2; s.U = 4; s.MB = 3;
   } else if (ld8 <= 96) {
