@@ -40,6 +40,8 @@ def parse():
                     help="bf16: the bf16 gather tier (SpMM tables rounded to bf16, 2e-2 tier; SURVEY N1(iv))")
     ap.add_argument("--model", default="sage", choices=["sage", "gcn"],
                     help="GraphSAGE-mean (the paper's benchmark model) or GCN-sym (App. A.1, SURVEY N3)")
+    ap.add_argument("--no-train-sparse", action="store_true",
+                    help="compute the last layer on every row (default: only on train rows, SURVEY N1(ii); exact)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -253,7 +255,8 @@ def main():
     t_part = time.time() - t0
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
-                           n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather)
+                           n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
+                           train_sparse=not args.no_train_sparse)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
@@ -414,7 +417,7 @@ def main():
                       "global_batch": g.n,
                       "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
                       ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,
-                      "gather": args.gather,
+                      "gather": args.gather, "train_sparse_last_layer": not args.no_train_sparse,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "breakdown": breakdown, "loss": loss_v,

@@ -165,6 +165,11 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       bf16 first, the SpMMs gather bf16 rows and accumulate in fp32 -- half the
  *                       gathered bytes.  Everything else (H, J, exchange payloads, GEMM outputs)
  *                       stays fp32.
+ *   train_sparse        1: N1(ii) train-row-sparse last layer (same loss, gradients and weights): the
+ *                       last layer's aggregation runs only on train rows (Y^(L) of other rows is not
+ *                       computed: logits there are stale) and its transposed aggregation only over
+ *                       train sources.  pgcn_set_inputs then builds the train row list and the
+ *                       restricted P_i^T and synchronises the stream (their sizes size the launches).
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -187,6 +192,7 @@ typedef struct {
   int32_t model;
   int32_t depth;
   int32_t gather;
+  int32_t train_sparse;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

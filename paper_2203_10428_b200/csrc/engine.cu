@@ -59,6 +59,14 @@ struct PartCtx {
   float* row_loss = nullptr;
   float* G = nullptr;
   uint16_t* G16 = nullptr;  // bf16 gather tier (cfg.gather): rounded copy of the table an SpMM gathers
+  // N1(ii) train-row-sparse last layer (cfg.train_sparse): train row list, P_i^T restricted to train
+  // sources, and their sizes (read back by pgcn_set_inputs)
+  int32_t* tr_list = nullptr;
+  int64_t* tr_count = nullptr;
+  int64_t* tr_counts = nullptr;
+  int64_t* trp_tr = nullptr;
+  int32_t* tcol_tr = nullptr;
+  int64_t n_tr = 0, nnz_tr = 0;
 };
 
 struct Arena {
@@ -108,6 +116,8 @@ struct pgcn_ctx {
   int64_t depth = 1;    // pipeline depth s (R27): an exchange posted at t is consumed at t + s
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
+  char* sp_tmp = nullptr;               // CUB scratch of the train-row builders (cfg.train_sparse)
+  int64_t sp_tmp_bytes = 0;
   double* diag = nullptr;              // N4: [2][L+1] squared staleness errors of the current iteration
   int64_t exp_t = 1;
   int exp_kind = pgcn::K_FWD, exp_layer = 1;
@@ -166,6 +176,7 @@ int validate_cfg(const pgcn_config* c) {
   if (c->model == 1 && c->gemm == 2) return fail(PGCN_EUNSUPPORTED, "GCN-sym needs the tensor-core GEMMs (gemm 0/1)");
   if (c->depth < 0 || c->depth > PGCN_MAX_DEPTH) return fail(PGCN_EINVAL, "depth must be in 0..%d", PGCN_MAX_DEPTH);
   if (c->gather != 0 && c->gather != 1) return fail(PGCN_EINVAL, "gather must be 0 (fp32) or 1 (bf16)");
+  if (c->train_sparse != 0 && c->train_sparse != 1) return fail(PGCN_EINVAL, "train_sparse must be 0 or 1");
   return PGCN_OK;
 }
 
@@ -223,6 +234,15 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.row_loss = A.take<float>(p.n_in);
     p.G = A.take<float>(C->P);
     if (C->cfg.gather == 1) p.G16 = A.take<uint16_t>(p.n_all * round_up(C->ldmax, 8));
+    if (C->cfg.train_sparse) {
+      p.tr_list = A.take<int32_t>(p.n_in);
+      p.tr_count = A.take<int64_t>(1);
+      p.tr_counts = A.take<int64_t>(p.n_all + 1);
+      p.trp_tr = A.take<int64_t>(p.n_all + 1);
+      p.tcol_tr = A.take<int32_t>(p.nnz);
+      const size_t tb = train_rows_tmp_bytes(p.n_in, p.n_all);
+      if ((int64_t)tb > C->sp_tmp_bytes) C->sp_tmp_bytes = (int64_t)tb;
+    }
     for (int l = 1; l <= L; ++l) {
       int64_t w = gemm_dw_ws_floats(p.n_in, C->F[l - 1], C->F[l]);
       if (w > dw_need) dw_need = w;
@@ -232,6 +252,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   }
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
+  if (C->sp_tmp_bytes > 0) C->sp_tmp = A.take<char>(C->sp_tmp_bytes);
   if (C->nccl && n_local == 1) {
     const PartCtx& p = C->parts[0];
     for (int l = 1; l <= L; ++l)
@@ -661,6 +682,17 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
     cudaMemcpyAsync(p.labels, labels, lb, cudaMemcpyDefault, C->s);
     cudaMemcpyAsync(p.train, train_mask, (size_t)p.n_in, cudaMemcpyDefault, C->s);
   }
+  if (C->cfg.train_sparse) {  // N1(ii): train row list and P_i^T restricted to train sources
+    const Launch Lk{C->s, &C->launches};
+    build_train_rows(Lk, p.train, p.n_in, p.trp, p.tcol, p.n_all, p.tr_list, p.tr_count, p.tr_counts, p.trp_tr,
+                     p.tcol_tr, C->sp_tmp, (size_t)C->sp_tmp_bytes);
+    int64_t h[2] = {0, 0};
+    cudaMemcpyAsync(&h[0], p.tr_count, sizeof(int64_t), cudaMemcpyDeviceToHost, C->s);
+    cudaMemcpyAsync(&h[1], p.trp_tr + p.n_all, sizeof(int64_t), cudaMemcpyDeviceToHost, C->s);
+    cudaStreamSynchronize(C->s);  // sizes of the last layer's launches (documented: synchronous here)
+    p.n_tr = h[0];
+    p.nnz_tr = h[1];
+  }
   return check_cuda(C, "pgcn_set_inputs");
 }
 
@@ -695,6 +727,11 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   }
   for (auto& p : C->parts) {
     float* Hin = layer_in(p, l, b);
+    // N1(ii): the last layer's aggregation only on train rows (the loss reads Y^(L) only there)
+    const bool sp = C->cfg.train_sparse && l == C->L;
+    const int32_t* rl = sp ? p.tr_list : nullptr;
+    const int64_t nr = sp ? p.n_tr : p.n_in;
+    const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
     // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13)
     int64_t n_valid = p.n_all;
     if (C->nccl) {
@@ -755,16 +792,16 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                           ldo, nullptr, nullptr, 0, 0, bf))
             return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
         }
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, (p.nnz + p.n_in)) + cvt(Fo, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
-                                         4.0 * Fo * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, p.n_in, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
-                 p.n_all, p.G16);
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, (nz + nr)) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+                                         4.0 * Fo * nr);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
+                 p.n_all, p.G16, rl);
         continue;
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (p.nnz + p.n_in)) + cvt(Fi, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in +
-                                         4.0 * Fi * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16);
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (nz + nr)) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+                                         4.0 * Fi * nr);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -781,9 +818,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, p.nnz) + cvt(Fo, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fo * p.n_in);
-        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
-                 p.G16);
+        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, nz) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
+        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
+                 p.G16, rl);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -794,8 +831,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       continue;
     }
     {
-      Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, p.nnz) + cvt(Fi, n_valid) + 4.0 * p.nnz + 8.0 * (p.n_in + 1) + 4.0 * p.n_in + 4.0 * Fi * p.n_in);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, p.n_in, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16);
+      Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, nz) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -854,6 +891,12 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
+    // N1(ii): M^(L) is 0 outside the train rows, so the last layer's transposed aggregation only
+    // needs P_i^T restricted to train sources
+    const bool sp = C->cfg.train_sparse && l == C->L;
+    const int64_t* trp = sp ? p.trp_tr : p.trp;
+    const int32_t* tcol = sp ? p.tcol_tr : p.tcol;
+    const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
     const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
     if (C->gcn) {
       // GCN-sym backward (App. A.1 PAPER.md:651-657 with P = S (A + I) S, S = diag(d~^-1/2), R26)
@@ -861,12 +904,12 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // Q = (A + I)^T (S M) over inner + boundary rows; G = [D'^T Q ; colsum M]; J = mask o s o S (Q W^T)
         const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
         {
-          Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, (p.nnz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+          Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, (nz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                            8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all);
           scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
           DropSpec none{};
           none.width = (int32_t)C->F[l];
-          spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+          spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
                    p.G16);
         }
         {
@@ -897,9 +940,9 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         }
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
-        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (p.nnz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) +
+        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
-        spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
+        spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
                  C->work, p.sym, p.G16);
       }
       continue;
@@ -909,12 +952,12 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
       const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
       {
-        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, p.nnz) + cvt(Fo, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
+        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, nz) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
                                          4.0 * Fo * p.n_all);
         scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
         DropSpec none{};
         none.width = (int32_t)C->F[l];
-        spmm_bwd(Lk, p.trp, p.tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+        spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
                  p.G16);
       }
       {
@@ -954,9 +997,9 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
         }
       }
-      Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, p.nnz) + cvt(Fi, p.n_in) + 4.0 * p.nnz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
+      Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
-      spmm_bwd(Lk, p.trp, p.tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
+      spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
                drop_spec(C, t, l), C->work, nullptr, p.G16);
     }
   }

@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              const float4* __restrict__ D, int64_t ld4, int64_t n_rows,
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int self,
-                                                             const float* __restrict__ bias, int64_t n_bias, int relu) {
+                                                             const float* __restrict__ bias, int64_t n_bias, int relu,
+                                                             const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -182,8 +183,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
   if (work) first = next_item<G>(work, lane, gm, 0, 0);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
-    const int64_t row = it / nchunk;
-    const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
+    const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
+    const int64_t row = rows ? (int64_t)rows[ri] : ri;
+    const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
     // Lanes past the row end gather a clamped in-row column (same sectors as their neighbours,
     // no extra traffic) and never store, so the loop carries no column predicates.
     int xq[NC];
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                float4* __restrict__ Z, int64_t ld4,
                                                                unsigned long long* work, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
-                                                               int relu) {
+                                                               int relu, const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -375,8 +377,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
   if (work) first = next_item<G>(work, lane, gm, 0, 0);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
-    const int64_t row = it / nchunk;
-    const int64_t x0 = (it - row * nchunk) * (NC * G) + lane;
+    const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
+    const int64_t row = rows ? (int64_t)rows[ri] : ri;
+    const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
     const char* bq[NC];
     float acc[NC][8];
 #pragma unroll
@@ -1051,7 +1054,7 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
-              int64_t n_bias, int relu, int64_t n_cols, void* g16) {
+              int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows) {
   if (n_rows <= 0) return;
   const int64_t ld4 = ld / 4;
   if (g16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
@@ -1075,11 +1078,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk16)                                                                                                 \
       k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
                                                                        n_valid, sh.nchunk, Z4, ld4, work, self, \
-                                                                       bias, n_bias, relu);                     \
+                                                                       bias, n_bias, relu, rows);               \
     else                                                                                                       \
       k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows, \
                                                                         n_valid, sh.nchunk, Z4, ld4, work,      \
-                                                                        self, bias, n_bias, relu);              \
+                                                                        self, bias, n_bias, relu, rows);        \
   } else
     PGCN_SPMM16_CASES(X) {
       std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
@@ -1105,11 +1108,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
                                                                      n_valid, sh.nchunk, Z4, work, self, bias,  \
-                                                                     n_bias, relu);                             \
+                                                                     n_bias, relu, rows);                       \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,    \
                                                                       n_valid, sh.nchunk, Z4, work, self, bias, \
-                                                                      n_bias, relu);                            \
+                                                                      n_bias, relu, rows);                      \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X

@@ -48,7 +48,9 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
               int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
-              void* g16 = nullptr);
+              void* g16 = nullptr, const int32_t* rows = nullptr);
+// rows (optional): aggregate only the n_rows rows listed (local ids; N1(ii) train-row-sparse last
+// layer); the other output rows are left untouched.
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
@@ -61,6 +63,15 @@ void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const floa
 // g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1) -- scratch of at least
 // (rows of the gathered table) x round_up(ld, 8) bf16; the table is rounded to bf16 there first and
 // the kernel gathers the bf16 rows (fp32 accumulation, fp32 output).  nullptr = fp32 gathers.
+
+// N1(ii) train-row-sparse last layer.  From the train mask of the n_in inner rows: tr_list = inner ids
+// with train != 0 (ascending) and *tr_count; and the transposed CSR restricted to train sources:
+// t_row_ptr_tr[u] / t_col_tr keep, in order, the entries v of P_i^T row u with train[v] != 0.  tmp:
+// device scratch of train_rows_tmp_bytes(n_in, n_all) bytes; counts[n_all + 1] int64 scratch.
+size_t train_rows_tmp_bytes(int64_t n_in, int64_t n_all);
+void build_train_rows(Launch, const uint8_t* train, int64_t n_in, const int64_t* t_row_ptr, const int32_t* t_col,
+                      int64_t n_all, int32_t* tr_list, int64_t* tr_count, int64_t* counts, int64_t* t_row_ptr_tr,
+                      int32_t* t_col_tr, void* tmp, size_t tmp_bytes);
 
 // N4 diagnostics: out[0] += sum_{r < n_rows, c < F} (used(r, c) - fresh(r, c))^2 with fresh rows from a
 // segment table (row_map fmap) and used rows from a segment table (umap), a plain array, or 0.

@@ -50,7 +50,8 @@ class Config(C.Structure):
                 ("loss", C.c_int32), ("n_global", C.c_int64), ("n_train_global", C.c_int64), ("opt", C.c_int32),
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
-                ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32)]
+                ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32),
+                ("train_sparse", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -183,7 +184,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
                 transform_first=True, staleness_stats=False, model="sage", depth=1,
-                gather="f32") -> Config:
+                gather="f32", train_sparse=False) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -203,6 +204,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.model = {"sage": 0, "gcn": 1}[model]
     c.depth = int(depth)
     c.gather = {"f32": 0, "bf16": 1}[gather]
+    c.train_sparse = int(bool(train_sparse))
     return c
 
 
