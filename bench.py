@@ -270,11 +270,13 @@ def main():
         lab = torch.from_numpy(np.ascontiguousarray(g.labels[gid])).pin_memory()
         tm = torch.from_numpy(np.ascontiguousarray(g.train_mask[gid])).pin_memory()
         host.append((X, lab, tm))
-    dev_in = [tuple(a.cuda(non_blocking=True) for a in h) for h in host]
-    torch.cuda.synchronize()
     nloc = len(local_parts)
-    for i in range(nloc):
-        ctx.set_inputs(i, *dev_in[i])
+    for i in range(nloc):  # one partition at a time: the device staging copy is freed right after
+        d_in = tuple(a.cuda(non_blocking=True) for a in host[i])
+        ctx.set_inputs(i, *d_in)
+        torch.cuda.synchronize()
+        del d_in
+    torch.cuda.empty_cache()
     theta = torch.tensor(pgcn.flatten_params(params0), device="cuda")
     grads = torch.zeros_like(theta)
     opt = torch.zeros(2 * theta.numel(), device="cuda")
@@ -317,6 +319,10 @@ def main():
     # step ahead so the copy overlaps the previous step's compute), installed with pgcn_set_inputs
     # (device-to-device into the padded layout) and the step's loss is read back to the host.
     e2e = None
+    if args.config.startswith("papers"):
+        # 14 GB of inputs per step over PCIe would dominate and double-buffered device staging does
+        # not fit next to the 2-partition workspace: no end-to-end leg for the papers-shaped graph
+        args.no_e2e = True
     if not args.no_e2e:
         loss_h = torch.zeros(1).pin_memory()
         h2d = sum(sum(a.numel() * a.element_size() for a in h) for h in host)
@@ -369,6 +375,12 @@ def main():
         peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         ach = kd["flops"] / (kd["ms"] / 1e3) / 1e12
         roof = {"kernel": name, "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    elif name.startswith("spmm") and args.config.startswith("papers"):
+        # papers-shaped partitions (13.9M rows x 192 B) are far larger than L2: the per-edge gathers
+        # are DRAM-side, so the SpMM is reported against the measured HBM copy peak (north_star).
+        ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     elif name.startswith("spmm"):
         # Per-edge gathers are L2 hits (Reddit: 83 % L2 hit rate): bound = L2, peak = measured L2
         # streaming read; the contract's HBM view (same algorithmic bytes / measured HBM copy) beside it.
@@ -421,7 +433,8 @@ def main():
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "breakdown": breakdown, "loss": loss_v,
-           "setup_s": {"generate": t_gen, "partition": t_part}}
+           "setup_s": {"generate": t_gen, "partition": t_part},
+           "workspace_GB": ctx.ws.numel() / 1e9}
     print(json.dumps(out))
 
 

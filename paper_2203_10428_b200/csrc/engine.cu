@@ -223,8 +223,16 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       p.Z[l] = A.take<float>(p.n_in * (C->tf[l] ? C->ld[l] : C->ld[l - 1]));   // Z, or S = inv_deg P T
       if (C->tf[l]) p.T[l] = A.take<float>(p.n_all * C->ld[l]);                 // T = D W_neigh, then Q
     }
-    p.M = A.take<float>(p.n_in * C->ldmax);
-    if (L > 1) p.dA = A.take<float>(p.n_in * 2 * C->ldmax);
+    // M: J^(l) o ReLU' at width F_l (l >= 1); dA: scale_rows output of transform-first layers (width
+    // F_l) or dA = M W^T of aggregate-first layers l >= 2 (width 2 F_{l-1}, F_{l-1} for GCN-sym)
+    int64_t ld_m = 0, ld_da = 0;
+    for (int l = 1; l <= L; ++l) {
+      ld_m = std::max(ld_m, C->ld[l]);
+      if (C->tf[l]) ld_da = std::max(ld_da, C->ld[l]);
+      else if (l >= 2) ld_da = std::max(ld_da, (C->cfg.model == 1 ? 1 : 2) * C->ld[l - 1]);
+    }
+    p.M = A.take<float>(p.n_in * ld_m);
+    if (ld_da > 0) p.dA = A.take<float>(p.n_in * ld_da);
     for (int l = 1; l < L; ++l) {
       for (int b = 0; b < C->nb; ++b) p.J[l][b] = A.take<float>(p.n_all * C->ld[l]);
       if (C->cfg.smooth_g) p.emaG[l] = A.take<float>(p.n_send * C->ld[l]);
@@ -795,13 +803,15 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, (nz + nr)) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
-                 p.n_all, p.G16, rl);
+                 p.n_all, p.G16, rl,
+                 (int64_t)nz);
         continue;
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (nz + nr)) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fi * nr);
-        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl);
+        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
+                 (int64_t)nz);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -820,7 +830,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, nz) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
-                 p.G16, rl);
+                 p.G16, rl,
+                 (int64_t)nz);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -832,7 +843,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
     {
       Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, nz) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl);
+      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
+                 (int64_t)nz);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -910,7 +922,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           DropSpec none{};
           none.width = (int32_t)C->F[l];
           spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                   p.G16);
+                   p.G16, (int64_t)nz);
         }
         {
           Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
@@ -943,7 +955,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
         spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym, p.G16);
+                 C->work, p.sym, p.G16, (int64_t)nz);
       }
       continue;
     }
@@ -958,7 +970,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         DropSpec none{};
         none.width = (int32_t)C->F[l];
         spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                 p.G16);
+                 p.G16, (int64_t)nz);
       }
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
@@ -1000,7 +1012,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l), C->work, nullptr, p.G16);
+               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

@@ -152,15 +152,20 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 // group, ~8 loads in flight).  Neighbour ids are loaded G at a time (coalesced)
 // and broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
 // Work distribution: static grid-stride, or (work != nullptr) dynamic -- each group takes the
-// next item from a per-launch atomic counter, so heavy-tailed degrees do not leave a tail of
-// groups still busy with their statically assigned long rows.
+// next K items from a per-launch atomic counter, so heavy-tailed degrees do not leave a tail of
+// groups still busy with their statically assigned long rows.  K (launcher: ~512 edges per grab)
+// keeps the single counter off the critical path on low-degree graphs (papers-shaped: 14.5 edges
+// per row would otherwise mean one same-address atomic per 14.5 edges).
 template <int G>
 __device__ __forceinline__ int64_t next_item(unsigned long long* work, int lane, unsigned gm, int64_t cur,
-                                             int64_t stride) {
+                                             int64_t stride, int K, int64_t& cend) {
   if (!work) return cur + stride;
+  if (cur + 1 < cend) return cur + 1;
   unsigned long long v = 0;
-  if (lane == 0) v = atomicAdd(work, 1ull);
-  return (int64_t)__shfl_sync(gm, v, 0, G);
+  if (lane == 0) v = atomicAdd(work, (unsigned long long)K);
+  const int64_t b = (int64_t)__shfl_sync(gm, v, 0, G);
+  cend = b + K;
+  return b;
 }
 
 template <int G, int NC, int U, int MINB, bool CHK>
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              const float* __restrict__ inv_deg,
                                                              const float4* __restrict__ D, int64_t ld4, int64_t n_rows,
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
-                                                             unsigned long long* work, int self,
+                                                             unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
                                                              const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x % G;
@@ -181,8 +186,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
   const uint32_t row_bytes = (uint32_t)ld4 * 16u;
   const uint32_t nv = (uint32_t)n_valid;
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-  if (work) first = next_item<G>(work, lane, gm, 0, 0);
-  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+  int64_t cend = 0;
+  if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
     const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
     const int64_t row = rows ? (int64_t)rows[ri] : ri;
     const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
-                                                             unsigned long long* work, const float* __restrict__ rs) {
+                                                             unsigned long long* work, int grabk, const float* __restrict__ rs) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -262,8 +268,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
   const uint32_t row_bytes = (uint32_t)ldA4 * 16u;  // 32-bit hot-loop addressing (see k_spmm_fwd)
   const char* base = reinterpret_cast<const char*>(dZs);
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-  if (work) first = next_item<G>(work, lane, gm, 0, 0);
-  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+  int64_t cend = 0;
+  if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
     const int64_t u0 = it / nchunk;
     const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
     int xq[NC];
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                const uint4* __restrict__ D, int64_t ld8,
                                                                int64_t n_rows, int64_t n_valid, int nchunk,
                                                                float4* __restrict__ Z, int64_t ld4,
-                                                               unsigned long long* work, int self,
+                                                               unsigned long long* work, int grabk, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
                                                                int relu, const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x % G;
@@ -375,8 +382,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
   const uint32_t row_bytes = (uint32_t)ld8 * 16u;
   const uint32_t nv = (uint32_t)n_valid;
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-  if (work) first = next_item<G>(work, lane, gm, 0, 0);
-  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+  int64_t cend = 0;
+  if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
     const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
     const int64_t row = rows ? (int64_t)rows[ri] : ri;
     const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
@@ -453,15 +461,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                int64_t n_in, int64_t n_all, int nchunk,
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
-                                                               unsigned long long* work, const float* __restrict__ rs) {
+                                                               unsigned long long* work, int grabk, const float* __restrict__ rs) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   const uint32_t row_bytes = (uint32_t)ld8 * 16u;
   int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-  if (work) first = next_item<G>(work, lane, gm, 0, 0);
-  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride)) {
+  int64_t cend = 0;
+  if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
+  for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
     const int64_t u0 = it / nchunk;
     const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
     const char* bq[NC];
@@ -598,8 +607,8 @@ __global__ void k_loss_ce(const float* __restrict__ Y, int64_t n, int64_t C, int
   for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
     const float* y = Y + v * ld;
     float* m = M + v * ld;
-    if (!train[v]) {
-      for (int64_t c = lane; c < ld; c += 32) m[c] = 0.f;
+    if (!train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
+      for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane == 0) rl[v] = 0.f;
       continue;
     }
@@ -628,6 +637,11 @@ __global__ void k_loss_bce(const float* __restrict__ Y, int64_t n, int64_t C, in
     const float* y = Y + v * ld;
     float* m = M + v * ld;
     const bool tr = train[v] != 0;
+    if (!tr) {
+      for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lane == 0) rl[v] = 0.f;
+      continue;
+    }
     float l = 0.f;
     for (int64_t c = lane; c < ld; c += 32) {
       float g = 0.f;
@@ -644,9 +658,24 @@ __global__ void k_loss_bce(const float* __restrict__ Y, int64_t n, int64_t C, in
 }
 
 __global__ void k_reduce_sum(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+  // one block, fixed assignment (deterministic); 16-byte loads with 4 independent accumulators per
+  // thread when x is 16-byte aligned, so a single SM streams the 13.9M row losses of a
+  // papers-shaped partition at its full load bandwidth
   __shared__ double sh[1024];
   double a = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += (double)x[i];
+  int64_t head = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int64_t n4 = n / 4;
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 v = x4[i];
+      b0 += (double)v.x; b1 += (double)v.y; b2 += (double)v.z; b3 += (double)v.w;
+    }
+    a = (b0 + b1) + (b2 + b3);
+    head = n4 * 4;
+  }
+  for (int64_t i = head + threadIdx.x; i < n; i += blockDim.x) a += (double)x[i];
   sh[threadIdx.x] = a;
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
@@ -1039,6 +1068,13 @@ SpmmShape spmm16_shape(int64_t ld8) {
 
 }  // namespace
 
+// Items per atomic grab of the dynamic SpMM scheduler: ~512 edges per grab, 1..64 rows.
+static int grab_items(int64_t nnz, int64_t rows) {
+  if (nnz < 0 || rows <= 0) return 1;
+  const int64_t k = (512 * rows) / (nnz > 0 ? nnz : 1);
+  return (int)(k < 1 ? 1 : (k > 64 ? 64 : k));
+}
+
 static void count(const Launch& L, int64_t n = 1) {
   if (L.count) *L.count += n;
 }
@@ -1054,8 +1090,9 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
-              int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows) {
+              int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz) {
   if (n_rows <= 0) return;
+  const int K = grab_items(nnz, n_rows);
   const int64_t ld4 = ld / 4;
   if (g16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
     const int64_t ld8 = (ld + 7) / 8;
@@ -1077,11 +1114,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     if (chk16)                                                                                                 \
       k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
-                                                                       n_valid, sh.nchunk, Z4, ld4, work, self, \
+                                                                       n_valid, sh.nchunk, Z4, ld4, work, K, self, \
                                                                        bias, n_bias, relu, rows);               \
     else                                                                                                       \
       k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows, \
-                                                                        n_valid, sh.nchunk, Z4, ld4, work,      \
+                                                                        n_valid, sh.nchunk, Z4, ld4, work, K,   \
                                                                         self, bias, n_bias, relu, rows);        \
   } else
     PGCN_SPMM16_CASES(X) {
@@ -1107,11 +1144,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
-                                                                     n_valid, sh.nchunk, Z4, work, self, bias,  \
+                                                                     n_valid, sh.nchunk, Z4, work, K, self, bias, \
                                                                      n_bias, relu, rows);                       \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,    \
-                                                                      n_valid, sh.nchunk, Z4, work, self, bias, \
+                                                                      n_valid, sh.nchunk, Z4, work, K, self, bias, \
                                                                       n_bias, relu, rows);                      \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
@@ -1121,8 +1158,9 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
-              const DropSpec& d, unsigned long long* work, const float* rs, void* g16) {
+              const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz) {
   if (n_all <= 0) return;
+  const int K = grab_items(nnz, n_all);
   const int64_t ld4 = ld / 4;
   if (g16) {  // bf16 gather tier: dZs (n_in rows of stride ld_dA) -> bf16 rows of ld8 vectors
     const int64_t ld8 = (ld + 7) / 8;
@@ -1144,7 +1182,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all, \
-                                                               sh.nchunk, J4, ld4, gid, d, work, rs);          \
+                                                               sh.nchunk, J4, ld4, gid, d, work, K, rs);       \
   } else
     PGCN_SPMM16_CASES(X) {
       std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
@@ -1169,7 +1207,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
-                                                             sh.nchunk, J4, ld4, gid, d, work, rs);            \
+                                                             sh.nchunk, J4, ld4, gid, d, work, K, rs);         \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X

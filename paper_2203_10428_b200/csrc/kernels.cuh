@@ -48,7 +48,7 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
               int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
-              void* g16 = nullptr, const int32_t* rows = nullptr);
+              void* g16 = nullptr, const int32_t* rows = nullptr, int64_t nnz = -1);
 // rows (optional): aggregate only the n_rows rows listed (local ids; N1(ii) train-row-sparse last
 // layer); the other output rows are left untouched.
 
@@ -59,7 +59,8 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
-              void* g16 = nullptr);
+              void* g16 = nullptr, int64_t nnz = -1);
+// nnz (both SpMMs): edges the launch visits (sizes the dynamic scheduler's grabs); -1 = one row per grab.
 // g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1) -- scratch of at least
 // (rows of the gathered table) x round_up(ld, 8) bf16; the table is rounded to bf16 there first and
 // the kernel gathers the bf16 rows (fp32 accumulation, fp32 output).  nullptr = fp32 gathers.

@@ -80,6 +80,11 @@ CONFIGS = {
                  feat="gauss", hidden=512, layers=4, dropout=0.1, lr=0.001),
     "papers": dict(n=111059956, nnz=1615685872, f0=128, classes=172, comm=512, train=0.011,
                    multilabel=False, feat="gauss", hidden=48, layers=3, dropout=0.0, lr=0.01),
+    # papers100M recipe at a quarter of the nodes and edges (same degree, widths, train fraction and
+    # community size): 2 partitions of it have the per-GPU shape of the 8-GPU papers100M run
+    # (13.9M inner rows, ~200M local edges each) and fit one B200.
+    "papers-q": dict(n=27764989, nnz=403921468, f0=128, classes=172, comm=128, train=0.011,
+                     multilabel=False, feat="gauss", hidden=48, layers=3, dropout=0.0, lr=0.01),
 }
 
 
