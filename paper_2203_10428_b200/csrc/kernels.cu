@@ -153,7 +153,7 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 // and broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
 // Work distribution: static grid-stride, or (work != nullptr) dynamic -- each group takes the
 // next K items from a per-launch atomic counter, so heavy-tailed degrees do not leave a tail of
-// groups still busy with their statically assigned long rows.  K (launcher: ~512 edges per grab)
+// groups still busy with their statically assigned long rows.  K (launcher: ~128 edges per grab)
 // keeps the single counter off the critical path on low-degree graphs (papers-shaped: 14.5 edges
 // per row would otherwise mean one same-address atomic per 14.5 edges).
 template <int G>
@@ -1068,10 +1068,17 @@ SpmmShape spmm16_shape(int64_t ld8) {
 
 }  // namespace
 
-// Items per atomic grab of the dynamic SpMM scheduler: ~512 edges per grab, 1..64 rows.
+// Items per atomic grab of the dynamic SpMM scheduler: ~128 edges per grab, 1..64 rows (sweep
+// tools/grab_sweep.sh: 64-256 best on Reddit / products / papers-q; 512+ loses L2 locality).
 static int grab_items(int64_t nnz, int64_t rows) {
+  static int64_t target = -1;  // dev knob PGCN_SPMM_GRAB: edges per grab (sweeps)
+  if (target < 0) {
+    const char* e = std::getenv("PGCN_SPMM_GRAB");
+    target = e ? std::atoll(e) : 128;
+    if (target < 1) target = 128;
+  }
   if (nnz < 0 || rows <= 0) return 1;
-  const int64_t k = (512 * rows) / (nnz > 0 ? nnz : 1);
+  const int64_t k = (target * rows) / (nnz > 0 ? nnz : 1);
   return (int)(k < 1 ? 1 : (k > 64 ? 64 : k));
 }
 
