@@ -170,6 +170,14 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       computed: logits there are stale) and its transposed aggregation only over
  *                       train sources.  pgcn_set_inputs then builds the train row list and the
  *                       restricted P_i^T and synchronises the stream (their sizes size the launches).
+ *   spmm_tiles          1: dense-tile aggregation (exact reassociation of Eq. 3's sum, DESIGN.md
+ *                       "Tensor-core tiles"): 128-row x 64-column blocks of P_i / P_i^T holding
+ *                       >= tile_min edges are summed on the tensor cores as a 0/1 block times the 64
+ *                       gathered rows (fp32 tier: 2-term tf32 split of the rows, fp32-grade; bf16
+ *                       tier: bf16 rows), the other edges by the gather SpMM.  Used only where the
+ *                       heavy tiles hold >= 25 % of a pattern's edges and every neighbour row is
+ *                       valid (t > s).  0: gather SpMM only.
+ *   tile_min            heavy-tile threshold in edges per 128 x 64 tile (0: default 96).
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -193,6 +201,8 @@ typedef struct {
   int32_t depth;
   int32_t gather;
   int32_t train_sparse;
+  int32_t spmm_tiles;
+  int32_t tile_min;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

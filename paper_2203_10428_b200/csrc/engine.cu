@@ -25,6 +25,7 @@
 #include "common.h"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "tiles.h"
 #include "pgcn.h"
 #ifdef PGCN_WITH_NCCL
 #include <nccl.h>
@@ -67,6 +68,10 @@ struct PartCtx {
   int64_t* trp_tr = nullptr;
   int32_t* tcol_tr = nullptr;
   int64_t n_tr = 0, nnz_tr = 0;
+  // dense-tile decompositions (cfg.spmm_tiles): [0] P_i (forward), [1] P_i^T (transposed)
+  const TileSet* ts[2] = {nullptr, nullptr};
+  TileDev td[2];
+  const TileDev* tiles(int w) const { return ts[w] ? &td[w] : nullptr; }
 };
 
 struct Arena {
@@ -177,6 +182,8 @@ int validate_cfg(const pgcn_config* c) {
   if (c->depth < 0 || c->depth > PGCN_MAX_DEPTH) return fail(PGCN_EINVAL, "depth must be in 0..%d", PGCN_MAX_DEPTH);
   if (c->gather != 0 && c->gather != 1) return fail(PGCN_EINVAL, "gather must be 0 (fp32) or 1 (bf16)");
   if (c->train_sparse != 0 && c->train_sparse != 1) return fail(PGCN_EINVAL, "train_sparse must be 0 or 1");
+  if (c->spmm_tiles != 0 && c->spmm_tiles != 1) return fail(PGCN_EINVAL, "spmm_tiles must be 0 or 1");
+  if (c->tile_min < 0 || c->tile_min > 128 * 64) return fail(PGCN_EINVAL, "tile_min out of range");
   return PGCN_OK;
 }
 
@@ -242,6 +249,27 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.row_loss = A.take<float>(p.n_in);
     p.G = A.take<float>(C->P);
     if (C->cfg.gather == 1) p.G16 = A.take<uint16_t>(p.n_all * round_up(C->ldmax, 8));
+    if (C->cfg.spmm_tiles) {  // heavy tiles must carry >= 25 % of the edges to pay for the extra pass
+      const int32_t tmin = C->cfg.tile_min > 0 ? C->cfg.tile_min : 96;
+      for (int w = 0; w < 2; ++w) {
+        const TileSet* ts = part_tiles(part, local[i], w, tmin);
+        p.ts[w] = nullptr;
+        if (!ts || ts->n_tiles == 0 || 4 * ts->nnz_heavy < p.nnz) continue;
+        p.ts[w] = ts;
+        TileDev& d = p.td[w];
+        d.rb_ptr = A.take<int32_t>(ts->n_rb + 1);
+        d.order = A.take<int32_t>(ts->n_rb);
+        d.tile_col = A.take<int32_t>(ts->n_tiles);
+        d.mask = A.take<uint64_t>(ts->n_tiles * kTileRows);
+        d.lrp = A.take<int64_t>(ts->n_rows + 1);
+        d.lcol = A.take<int32_t>(ts->nnz_light);
+        d.n_rows = ts->n_rows;
+        d.n_cols = ts->n_cols;
+        d.n_rb = ts->n_rb;
+        d.n_tiles = ts->n_tiles;
+        d.nnz_light = ts->nnz_light;
+      }
+    }
     if (C->cfg.train_sparse) {
       p.tr_list = A.take<int32_t>(p.n_in);
       p.tr_count = A.take<int64_t>(1);
@@ -627,6 +655,23 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     cudaMemcpyAsync(p.inv_pos, v.inv_pos, sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.halo_map, hmap.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.msg_map, mmap.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+    for (int w = 0; w < 2; ++w) {
+      const TileSet* ts = p.ts[w];
+      if (!ts) continue;
+      const TileDev& d = p.td[w];
+      cudaMemcpyAsync(const_cast<int32_t*>(d.rb_ptr), ts->rb_ptr.data(), sizeof(int32_t) * (ts->n_rb + 1),
+                      cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(const_cast<int32_t*>(d.order), ts->order.data(), sizeof(int32_t) * ts->n_rb,
+                      cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(const_cast<int32_t*>(d.tile_col), ts->tile_col.data(), sizeof(int32_t) * ts->n_tiles,
+                      cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(const_cast<uint64_t*>(d.mask), ts->mask.data(), sizeof(uint64_t) * ts->mask.size(),
+                      cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(const_cast<int64_t*>(d.lrp), ts->lrp.data(), sizeof(int64_t) * (ts->n_rows + 1),
+                      cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(const_cast<int32_t*>(d.lcol), ts->lcol.data(), sizeof(int32_t) * ts->nnz_light,
+                      cudaMemcpyHostToDevice, s);
+    }
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
       delete C;
@@ -804,14 +849,14 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                                          4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
                  p.n_all, p.G16, rl,
-                 (int64_t)nz);
+                 (int64_t)nz, p.tiles(0));
         continue;
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (nz + nr)) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fi * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz);
+                 (int64_t)nz, p.tiles(0));
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -831,7 +876,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, nz) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
                  p.G16, rl,
-                 (int64_t)nz);
+                 (int64_t)nz, p.tiles(0));
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -844,7 +889,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     {
       Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, nz) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz);
+                 (int64_t)nz, p.tiles(0));
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -922,7 +967,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           DropSpec none{};
           none.width = (int32_t)C->F[l];
           spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                   p.G16, (int64_t)nz);
+                   p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
         }
         {
           Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
@@ -955,7 +1000,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
         spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym, p.G16, (int64_t)nz);
+                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
       }
       continue;
     }
@@ -970,7 +1015,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         DropSpec none{};
         none.width = (int32_t)C->F[l];
         spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                 p.G16, (int64_t)nz);
+                 p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
       }
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
@@ -1012,7 +1057,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz);
+               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

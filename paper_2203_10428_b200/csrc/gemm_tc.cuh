@@ -34,6 +34,8 @@ struct alignas(64) TcParams {
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
                bool mn_major = false);
+bool tc_map_table(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int64_t rows, int64_t ld, int box_cols,
+                  int box_rows);
 int tc_stages(int BN, int bf, int mode);
 size_t tc_smem_bytes(int BN, int S, int bf, int mode);
 void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, void* WT, void* Wp, void* WJ,

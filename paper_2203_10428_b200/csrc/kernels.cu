@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
-                                                             const int32_t* __restrict__ rows) {
+                                                             const int32_t* __restrict__ rows, int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -203,8 +203,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
     }
     float4 acc[NC];
 #pragma unroll
-    for (int q = 0; q < NC; ++q)  // GCN-sym self loop (A + I, R26): the row's own (inner) input
+    for (int q = 0; q < NC; ++q) {  // GCN-sym self loop (A + I, R26): the row's own (inner) input
       acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc), same row, in place
+    }
     const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -260,7 +262,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
-                                                             unsigned long long* work, int grabk, const float* __restrict__ rs) {
+                                                             unsigned long long* work, int grabk, const float* __restrict__ rs,
+                                                             int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -282,8 +285,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     }
     float4 acc[NC];
 #pragma unroll
-    for (int q = 0; q < NC; ++q)
+    for (int q = 0; q < NC; ++q) {
       acc[q] = (dDs && u0 < n_in) ? dDs[u0 * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc), same row, in place
+    }
     const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
@@ -374,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                float4* __restrict__ Z, int64_t ld4,
                                                                unsigned long long* work, int grabk, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
-                                                               int relu, const int32_t* __restrict__ rows) {
+                                                               int relu, const int32_t* __restrict__ rows,
+                                                               int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -398,6 +404,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
       else
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
+      if (addend) {  // heavy-tile sums (spmm_tc), same row, in place
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t xf = 2 * xq + h;
+          if (xf < ld4) {
+            const float4 a = Z[row * ld4 + xf];
+            acc[q][4 * h] += a.x; acc[q][4 * h + 1] += a.y; acc[q][4 * h + 2] += a.z; acc[q][4 * h + 3] += a.w;
+          }
+        }
+      }
     }
     const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
@@ -461,7 +477,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                int64_t n_in, int64_t n_all, int nchunk,
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
-                                                               unsigned long long* work, int grabk, const float* __restrict__ rs) {
+                                                               unsigned long long* work, int grabk, const float* __restrict__ rs,
+                                                               int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -482,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * xq + h;
-        const float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // heavy-tile sums (spmm_tc), in place
         acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
       }
     }
@@ -1097,8 +1115,17 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
-              int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz) {
+              int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz,
+              const TileDev* tiles) {
   if (n_rows <= 0) return;
+  // Dense tiles on the tensor cores, then the light edges by the gather kernel (addend = the tile
+  // sums): only when every neighbour row is valid and the launch covers all rows of the pattern.
+  const int tcu = tiles && tiles->n_tiles > 0 && !rows && n_cols >= 0 && n_valid >= n_cols && tiles->n_rows == n_rows;
+  if (tcu) {
+    row_ptr = tiles->lrp;
+    col = tiles->lcol;
+    nnz = tiles->nnz_light;
+  }
   const int K = grab_items(nnz, n_rows);
   const int64_t ld4 = ld / 4;
   if (g16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
@@ -1111,6 +1138,10 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
                                                                           ld4, n_valid, ld8, G16);
     count(L);
+    if (tcu && spmm_tc(L, *tiles, G16, 1, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
+      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd, bf16) launch failed\n");
+      std::abort();
+    }
     const bool chk16 = n_cols < 0 || n_valid < n_cols;
     const SpmmShape sh = spmm16_shape(ld8);
     if (!dyn_enabled()) work = nullptr;
@@ -1122,11 +1153,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk16)                                                                                                 \
       k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
                                                                        n_valid, sh.nchunk, Z4, ld4, work, K, self, \
-                                                                       bias, n_bias, relu, rows);               \
+                                                                       bias, n_bias, relu, rows, tcu);          \
     else                                                                                                       \
       k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows, \
                                                                         n_valid, sh.nchunk, Z4, ld4, work, K,   \
-                                                                        self, bias, n_bias, relu, rows);        \
+                                                                        self, bias, n_bias, relu, rows, tcu);   \
   } else
     PGCN_SPMM16_CASES(X) {
       std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
@@ -1141,6 +1172,10 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     std::abort();
   }
   const bool chk = n_cols < 0 || n_valid < n_cols;  // some neighbour rows are not valid yet
+  if (tcu && spmm_tc(L, *tiles, D, 0, ld, n_valid, ld, Z, ld, ld)) {
+    std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
+    std::abort();
+  }
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;
   if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
@@ -1152,11 +1187,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
                                                                      n_valid, sh.nchunk, Z4, work, K, self, bias, \
-                                                                     n_bias, relu, rows);                       \
+                                                                     n_bias, relu, rows, tcu);                  \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,    \
                                                                       n_valid, sh.nchunk, Z4, work, K, self, bias, \
-                                                                      n_bias, relu, rows);                      \
+                                                                      n_bias, relu, rows, tcu);                 \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -1165,8 +1200,15 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
-              const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz) {
+              const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz,
+              const TileDev* tiles) {
   if (n_all <= 0) return;
+  const int tcu = tiles && tiles->n_tiles > 0 && tiles->n_rows == n_all;  // see spmm_fwd
+  if (tcu) {
+    t_row_ptr = tiles->lrp;
+    t_col = tiles->lcol;
+    nnz = tiles->nnz_light;
+  }
   const int K = grab_items(nnz, n_all);
   const int64_t ld4 = ld / 4;
   if (g16) {  // bf16 gather tier: dZs (n_in rows of stride ld_dA) -> bf16 rows of ld8 vectors
@@ -1179,6 +1221,10 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
                                                                        ld_dA / 4, ld4, n_in, ld8, G16);
     count(L);
+    if (tcu && spmm_tc(L, *tiles, G16, 1, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
+      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd, bf16) launch failed\n");
+      std::abort();
+    }
     const SpmmShape sh = spmm16_shape(ld8);
     if (!dyn_enabled()) work = nullptr;
     if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
@@ -1189,7 +1235,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all, \
-                                                               sh.nchunk, J4, ld4, gid, d, work, K, rs);       \
+                                                               sh.nchunk, J4, ld4, gid, d, work, K, rs, tcu);  \
   } else
     PGCN_SPMM16_CASES(X) {
       std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
@@ -1203,6 +1249,10 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();
   }
+  if (tcu && spmm_tc(L, *tiles, dZs, 0, ld, n_in, ld_dA, J, ld, ld)) {
+    std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd) launch failed\n");
+    std::abort();
+  }
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;
   if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
@@ -1214,7 +1264,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
-                                                             sh.nchunk, J4, ld4, gid, d, work, K, rs);         \
+                                                             sh.nchunk, J4, ld4, gid, d, work, K, rs, tcu);    \
   } else
   PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X

@@ -15,13 +15,17 @@
 #include <atomic>
 #include <climits>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <tuple>
 #include <new>
 #include <thread>
 #include <vector>
 
 #include "common.h"
 #include "pgcn.h"
+#include "tiles.h"
 
 struct PartArrays {
   std::vector<int64_t> inner_gid, halo_gid, halo_off, send_off, row_ptr, t_row_ptr, inv_ptr;
@@ -35,6 +39,9 @@ struct pgcn_partitioning {
   int32_t n_parts;
   std::vector<int32_t> part_of;
   std::vector<PartArrays> parts;
+  // dense-tile decompositions of P_i / P_i^T (tiles.h), built on first use
+  std::mutex tile_mu;
+  std::map<std::tuple<int32_t, int, int32_t>, std::unique_ptr<pgcn::TileSet>> tiles;
 };
 
 namespace {
@@ -232,3 +239,25 @@ extern "C" int pgcn_partition_view(const pgcn_partitioning* p, int32_t part, pgc
 extern "C" int64_t pgcn_partition_n_nodes(const pgcn_partitioning* p) { return p ? p->n : -1; }
 
 extern "C" void pgcn_partition_free(pgcn_partitioning* p) { delete p; }
+
+namespace pgcn {
+
+const TileSet* part_tiles(const pgcn_partitioning* p, int32_t part, int which, int32_t min_edges) {
+  if (!p || part < 0 || part >= p->n_parts) return nullptr;
+  auto* q = const_cast<pgcn_partitioning*>(p);
+  std::lock_guard<std::mutex> g(q->tile_mu);
+  auto key = std::make_tuple(part, which, min_edges);
+  auto it = q->tiles.find(key);
+  if (it != q->tiles.end()) return it->second.get();
+  const PartArrays& a = p->parts[part];
+  const int64_t n_in = (int64_t)a.inner_gid.size(), n_all = n_in + (int64_t)a.halo_gid.size();
+  auto ts = std::make_unique<TileSet>();
+  const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (which == 0) build_tiles(a.row_ptr.data(), a.col_idx.data(), n_in, n_all, min_edges, nt, *ts);
+  else build_tiles(a.t_row_ptr.data(), a.t_col_idx.data(), n_all, n_in, min_edges, nt, *ts);
+  const TileSet* r = ts.get();
+  q->tiles.emplace(key, std::move(ts));
+  return r;
+}
+
+}  // namespace pgcn

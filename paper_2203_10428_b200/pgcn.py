@@ -51,7 +51,7 @@ class Config(C.Structure):
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
                 ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32),
-                ("train_sparse", C.c_int32)]
+                ("train_sparse", C.c_int32), ("spmm_tiles", C.c_int32), ("tile_min", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -105,6 +105,7 @@ def lib():
         L.pgcn_staleness.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pgcn_dev_spmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
         L.pgcn_dev_l2_read.argtypes = [vp, i64, i32, vp, vp]
+        L.pgcn_dev_tiles.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.pgcn_nccl_unique_id.argtypes = [vp]
         L.pgcn_nccl_id_bytes.restype = i32
         _lib = L
@@ -163,6 +164,22 @@ class Partitioning:
                     inv_ptr=arr(v.inv_ptr, n_in + 1, np.int64), inv_pos=arr(v.inv_pos, ns, np.int32),
                     deg=arr(v.deg, n_in + n_bd, np.int64))
 
+    def tiles(self, i, which, tile_min) -> dict:
+        """pgcn_dev_tiles (include/pgcn_dev.h): the dense-tile decomposition of P_i (which = 0) or
+        P_i^T (which = 1) used by the tensor-core aggregation."""
+        sz = np.zeros(6, np.int64)
+        _check(lib().pgcn_dev_tiles(self.handle, int(i), int(which), int(tile_min), _ptr(sz), None, None, None, None,
+                                    None, None))
+        n_rows, n_rb, n_tiles, nnz_heavy, nnz_light, n_cols = (int(x) for x in sz)
+        out = dict(n_rows=n_rows, n_rb=n_rb, n_tiles=n_tiles, nnz_heavy=nnz_heavy, nnz_light=nnz_light, n_cols=n_cols,
+                   rb_ptr=np.zeros(n_rb + 1, np.int32), order=np.zeros(n_rb, np.int32),
+                   tile_col=np.zeros(n_tiles, np.int32), mask=np.zeros(128 * n_tiles, np.uint64),
+                   lrp=np.zeros(n_rows + 1, np.int64), lcol=np.zeros(nnz_light, np.int32))
+        _check(lib().pgcn_dev_tiles(self.handle, int(i), int(which), int(tile_min), _ptr(sz), _ptr(out["rb_ptr"]),
+                                    _ptr(out["order"]), _ptr(out["tile_col"]), _ptr(out["mask"]), _ptr(out["lrp"]),
+                                    _ptr(out["lcol"])))
+        return out
+
     def close(self):
         if getattr(self, "handle", None):
             lib().pgcn_partition_free(self.handle)
@@ -184,7 +201,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
                 transform_first=True, staleness_stats=False, model="sage", depth=1,
-                gather="f32", train_sparse=False) -> Config:
+                gather="f32", train_sparse=False, spmm_tiles=True, tile_min=0) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -205,6 +222,8 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.depth = int(depth)
     c.gather = {"f32": 0, "bf16": 1}[gather]
     c.train_sparse = int(bool(train_sparse))
+    c.spmm_tiles = int(bool(spmm_tiles))
+    c.tile_min = int(tile_min)
     return c
 
 
