@@ -59,6 +59,7 @@ struct PartCtx {
   uint8_t* train = nullptr;
   float* row_loss = nullptr;
   float* G = nullptr;
+  uint16_t* T16 = nullptr;  // fp32 tier with tiles: bf16 hi/lo split of the table the tile kernel reads
   uint16_t* G16 = nullptr;  // bf16 gather tier (cfg.gather): rounded copy of the table an SpMM gathers
   // N1(ii) train-row-sparse last layer (cfg.train_sparse): train row list, P_i^T restricted to train
   // sources, and their sizes (read back by pgcn_set_inputs)
@@ -269,6 +270,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         d.n_tiles = ts->n_tiles;
         d.nnz_light = ts->nnz_light;
       }
+      if ((p.ts[0] || p.ts[1]) && C->cfg.gather == 0) p.T16 = A.take<uint16_t>(2 * p.n_all * round_up(C->ldmax, 8));
     }
     if (C->cfg.train_sparse) {
       p.tr_list = A.take<int32_t>(p.n_in);
@@ -849,14 +851,14 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                                          4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
                  p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0));
+                 (int64_t)nz, p.tiles(0), p.T16);
         continue;
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (nz + nr)) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fi * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0));
+                 (int64_t)nz, p.tiles(0), p.T16);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -876,7 +878,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, nz) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
                  p.G16, rl,
-                 (int64_t)nz, p.tiles(0));
+                 (int64_t)nz, p.tiles(0), p.T16);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -889,7 +891,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     {
       Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, nz) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0));
+                 (int64_t)nz, p.tiles(0), p.T16);
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -967,7 +969,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           DropSpec none{};
           none.width = (int32_t)C->F[l];
           spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                   p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
+                   p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
         }
         {
           Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
@@ -1000,7 +1002,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
         spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
+                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
       }
       continue;
     }
@@ -1015,7 +1017,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         DropSpec none{};
         none.width = (int32_t)C->F[l];
         spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                 p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
+                 p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
       }
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
@@ -1057,7 +1059,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1));
+               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

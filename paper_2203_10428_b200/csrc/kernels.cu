@@ -355,6 +355,29 @@ __global__ void k_to_bf16(const float4* __restrict__ src, int64_t s4, int64_t w4
   }
 }
 
+// fp32 tier of the tensor-core tile path (spmm_tc.cu): x = hi + lo + O(2^-18 |x|) with hi = rn_bf16(x),
+// lo = rn_bf16(x - hi) (x - hi is exact in fp32); same row layout as k_to_bf16, two tables.
+__device__ __forceinline__ void split2(float a, float b, uint32_t& h, uint32_t& l) {
+  h = bf16x2_rn(a, b);
+  const float ha = __uint_as_float(h << 16), hb = __uint_as_float(h & 0xffff0000u);
+  l = bf16x2_rn(a - ha, b - hb);
+}
+__global__ void k_split_bf16(const float4* __restrict__ src, int64_t s4, int64_t w4, int64_t n_rows, int64_t ld8,
+                             uint4* __restrict__ hi, uint4* __restrict__ lo) {
+  for (RowCursor rc(ld8); rc.r < n_rows; rc.next((int)ld8)) {
+    const int64_t x0 = 2 * (int64_t)rc.x;
+    const float4 a = x0 < w4 ? src[rc.r * s4 + x0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = x0 + 1 < w4 ? src[rc.r * s4 + x0 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint4 h, l;
+    split2(a.x, a.y, h.x, l.x);
+    split2(a.z, a.w, h.y, l.y);
+    split2(b.x, b.y, h.z, l.z);
+    split2(b.z, b.w, h.w, l.w);
+    hi[rc.r * ld8 + rc.x] = h;
+    lo[rc.r * ld8 + rc.x] = l;
+  }
+}
+
 __device__ __forceinline__ void acc8(float (&a)[8], const uint4& w) {
   bf16x2_acc(a[0], a[1], w.x);
   bf16x2_acc(a[2], a[3], w.y);
@@ -1116,7 +1139,7 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
               int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz,
-              const TileDev* tiles) {
+              const TileDev* tiles, void* t16) {
   if (n_rows <= 0) return;
   // Dense tiles on the tensor cores, then the light edges by the gather kernel (addend = the tile
   // sums): only when every neighbour row is valid and the launch covers all rows of the pattern.
@@ -1138,7 +1161,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
                                                                           ld4, n_valid, ld8, G16);
     count(L);
-    if (tcu && spmm_tc(L, *tiles, G16, 1, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
+    if (tcu && spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
       std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd, bf16) launch failed\n");
       std::abort();
     }
@@ -1172,9 +1195,16 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     std::abort();
   }
   const bool chk = n_cols < 0 || n_valid < n_cols;  // some neighbour rows are not valid yet
-  if (tcu && spmm_tc(L, *tiles, D, 0, ld, n_valid, ld, Z, ld, ld)) {
-    std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
-    std::abort();
+  if (tcu) {  // fp32 tier: bf16 hi/lo split of the table, then the tile sums (2 MMAs per k-step)
+    const int64_t ld8 = (ld + 7) / 8;
+    auto H16 = static_cast<uint4*>(t16);
+    k_split_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
+                                                                             ld4, n_valid, ld8, H16, H16 + n_valid * ld8);
+    count(L);
+    if (spmm_tc(L, *tiles, H16, H16 + n_valid * ld8, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
+      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
+      std::abort();
+    }
   }
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;
@@ -1201,7 +1231,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
               const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz,
-              const TileDev* tiles) {
+              const TileDev* tiles, void* t16) {
   if (n_all <= 0) return;
   const int tcu = tiles && tiles->n_tiles > 0 && tiles->n_rows == n_all;  // see spmm_fwd
   if (tcu) {
@@ -1221,7 +1251,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
                                                                        ld_dA / 4, ld4, n_in, ld8, G16);
     count(L);
-    if (tcu && spmm_tc(L, *tiles, G16, 1, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
+    if (tcu && spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
       std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd, bf16) launch failed\n");
       std::abort();
     }
@@ -1249,9 +1279,16 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();
   }
-  if (tcu && spmm_tc(L, *tiles, dZs, 0, ld, n_in, ld_dA, J, ld, ld)) {
-    std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd) launch failed\n");
-    std::abort();
+  if (tcu) {  // fp32 tier: bf16 hi/lo split of dZs, then the tile sums
+    const int64_t ld8 = (ld + 7) / 8;
+    auto H16 = static_cast<uint4*>(t16);
+    k_split_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
+                                                                          ld_dA / 4, ld4, n_in, ld8, H16, H16 + n_in * ld8);
+    count(L);
+    if (spmm_tc(L, *tiles, H16, H16 + n_in * ld8, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
+      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd) launch failed\n");
+      std::abort();
+    }
   }
   const SpmmShape sh = spmm_shape(ld4);
   if (!dyn_enabled()) work = nullptr;

@@ -43,8 +43,9 @@ struct TileDev {
   int64_t n_rows = 0, n_cols = 0, n_rb = 0, n_tiles = 0, nnz_light = 0;
 };
 // Heavy-tile sums on the tensor cores (spmm_tc.cu): out[r, 0:width) = sum over the heavy-tile edges
-// (r, c) of B[c, 0:width); B rows of b_ld elements (fp32, or bf16 when bf).  0 on success.
-int spmm_tc(Launch L, const TileDev& T, const void* B, int bf, int64_t b_cols, int64_t b_rows, int64_t b_ld,
+// (r, c) of B[c, 0:width), B = hi (+ lo when non-null): bf16 tables of b_rows rows, row stride b_ld
+// elements (fp32 tier: the hi/lo split of the fp32 table; bf16 tier: the rounded table).  0 on success.
+int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t b_cols, int64_t b_rows, int64_t b_ld,
             float* out, int64_t ld_out, int64_t width);
 
 // S3 prologue: D = dropout(H) over rows [0, n_rows); rows >= n_valid are written as 0.
@@ -63,7 +64,8 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
               int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
-              void* g16 = nullptr, const int32_t* rows = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr);
+              void* g16 = nullptr, const int32_t* rows = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr,
+              void* t16 = nullptr);
 // rows (optional): aggregate only the n_rows rows listed (local ids; N1(ii) train-row-sparse last
 // layer); the other output rows are left untouched.
 
@@ -74,10 +76,11 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
-              void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr);
+              void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr, void* t16 = nullptr);
 // tiles (both SpMMs, optional): dense-tile decomposition of the pattern (tiles.h); its heavy tiles are
 // summed by spmm_tc into the output rows first and the gather kernel walks only the light CSR, adding
-// the tile sums (fwd: used only when n_valid >= n_cols and rows == nullptr).
+// the tile sums (fwd: used only when n_valid >= n_cols and rows == nullptr).  t16 (fp32 tier with tiles):
+// scratch for the bf16 hi/lo split of the table, 2 x (table rows) x round_up(ld, 8) bf16.
 // nnz (both SpMMs): edges the launch visits (sizes the dynamic scheduler's grabs); -1 = one row per grab.
 // g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1) -- scratch of at least
 // (rows of the gathered table) x round_up(ld, 8) bf16; the table is rounded to bf16 there first and

@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KIND = [("k_spmm_fwd", "spmm_fwd"), ("k_spmm_bwd", "spmm_bwd"), ("k_umma_gemm", "gemm_tc"), ("k_gemm_fwd", "gemm_fwd"),
+KIND = [("k_spmm_tc", "spmm_tc"), ("k_spmm_fwd", "spmm_fwd"), ("k_spmm_bwd", "spmm_bwd"), ("k_umma_gemm", "gemm_tc"), ("k_gemm_fwd", "gemm_fwd"),
         ("k_gemm_dw", "gemm_dw"), ("k_gemm_da", "gemm_da"), ("k_dropout", "dropout"), ("k_gather", "gather"),
         ("k_grad_reduce", "grad_reduce"), ("k_loss", "loss"), ("k_opt", "update"), ("k_sum_grads", "update"),
         ("k_wprep", "wprep"), ("k_colsum", "colsum"), ("k_split_reduce", "split_reduce"), ("k_reduce_sum", "reduce_sum")]
