@@ -44,11 +44,11 @@ int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, float* out, v
  * 128 rows x column tiles of 64 columns; a tile with >= tile_min edges is "heavy" and stored as a
  * bitmask (mask[128 k + r] bit c = edge (128 b + r, 64 tile_col[k] + c), tiles of block b at
  * [rb_ptr[b], rb_ptr[b+1]), column tiles ascending); the other edges (and a repeated (row, col)
- * pair) form the light CSR lrp / lcol in the original edge order.  order = row blocks by
+ * pair) form the light CSR lrp / lcol, columns ascending within a row.  order = row blocks by
  * descending tile count (stable).  sizes[6] receives n_rows, n_rb, n_tiles, nnz_heavy, nnz_light,
  * n_cols; any array pointer may be NULL (sizes only).  Arrays are caller-owned host buffers of
  * those sizes (rb_ptr n_rb + 1, order n_rb, tile_col n_tiles, mask 128 n_tiles, lrp n_rows + 1,
- * lcol nnz_light).                                                                            */
+ * lcol nnz_light).                                                                           */
 typedef struct pgcn_partitioning pgcn_partitioning;
 int pgcn_dev_tiles(const pgcn_partitioning* p, int32_t part, int32_t which, int32_t tile_min, int64_t* sizes,
                    int32_t* rb_ptr, int32_t* order, int32_t* tile_col, uint64_t* mask, int64_t* lrp, int32_t* lcol);

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -137,6 +138,9 @@ struct pgcn_ctx {
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
   cudaStream_t cs = nullptr;              // comm stream (high priority)
+  cudaStream_t ss = nullptr;              // side stream of the concurrent tile / light-gather SpMM split
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  pgcn::Launch launch() { return pgcn::Launch{s, &launches, ss, ev_fork, ev_join}; }
   cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
   cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};
   float* send_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // packed S_{i,j} rows of the layer-l input
@@ -160,6 +164,9 @@ struct pgcn_ctx {
     if (cr) ncclCommDestroy(cr);
 #endif
     if (cs) cudaStreamDestroy(cs);
+    if (ss) cudaStreamDestroy(ss);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 };
 
@@ -199,7 +206,7 @@ int64_t param_count(const pgcn_config* c) {
 int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local, Arena& A) {
   const int L = C->L;
   C->parts.assign(n_local, PartCtx{});
-  int64_t dw_need = 0;
+  int64_t dw_need = 0, tile_rows = 0;
   for (int i = 0; i < n_local; ++i) {
     PartCtx& p = C->parts[i];
     p.part = local[i];
@@ -271,6 +278,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         d.nnz_light = ts->nnz_light;
       }
       if ((p.ts[0] || p.ts[1]) && C->cfg.gather == 0) p.T16 = A.take<uint16_t>(2 * p.n_all * round_up(C->ldmax, 8));
+      if (p.ts[0] || p.ts[1]) tile_rows = std::max(tile_rows, p.n_all);
     }
     if (C->cfg.train_sparse) {
       p.tr_list = A.take<int32_t>(p.n_in);
@@ -290,6 +298,10 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   }
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
+  // tile sums of the concurrent tile / light-gather split (one SpMM at a time on the context stream)
+  float* tile_part = tile_rows > 0 ? A.take<float>(tile_rows * C->ldmax) : nullptr;
+  for (auto& p : C->parts)
+    for (int w = 0; w < 2; ++w) p.td[w].part = tile_part;
   if (C->sp_tmp_bytes > 0) C->sp_tmp = A.take<char>(C->sp_tmp_bytes);
   if (C->nccl && n_local == 1) {
     const PartCtx& p = C->parts[0];
@@ -680,6 +692,17 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
       return fail(PGCN_ECUDA, "pgcn_ctx_create upload: %s", cudaGetErrorString(e));
     }
   }
+  bool tiles_used = false;
+  for (auto& p : C->parts) tiles_used = tiles_used || p.ts[0] || p.ts[1];
+  const char* conc = std::getenv("PGCN_TILE_CONCURRENT");  // dev knob: 0 = tile and light passes in sequence
+  if (tiles_used && !(conc && std::atoi(conc) == 0)) {
+    if (cudaStreamCreateWithFlags(&C->ss, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      delete C;
+      return fail(PGCN_ECUDA, "side stream creation failed");
+    }
+  }
   if (C->nccl) {
 #ifdef PGCN_WITH_NCCL
     int lo = 0, hi = 0;
@@ -738,7 +761,7 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
     cudaMemcpyAsync(p.train, train_mask, (size_t)p.n_in, cudaMemcpyDefault, C->s);
   }
   if (C->cfg.train_sparse) {  // N1(ii): train row list and P_i^T restricted to train sources
-    const Launch Lk{C->s, &C->launches};
+    const Launch Lk = C->launch();
     build_train_rows(Lk, p.train, p.n_in, p.trp, p.tcol, p.n_all, p.tr_list, p.tr_count, p.tr_counts, p.trp_tr,
                      p.tcol_tr, C->sp_tmp, (size_t)C->sp_tmp_bytes);
     int64_t h[2] = {0, 0};
@@ -756,7 +779,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   int rc = expect(C, t, K_FWD, l, "pgcn_layer_fwd");
   if (rc) return rc;
   if (!params) return fail(PGCN_EINVAL, "params is NULL");
-  const Launch Lk{C->s, &C->launches};
+  const Launch Lk = C->launch();
   const int b = C->bi(t), bp = C->bi(t - 1), bs = C->bi(t - C->depth);
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
@@ -916,7 +939,7 @@ extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
   if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
   int rc = expect(C, t, K_LOSS, 0, "pgcn_loss");
   if (rc) return rc;
-  const Launch Lk{C->s, &C->launches};
+  const Launch Lk = C->launch();
   const int L = C->L;
   for (size_t i = 0; i < C->parts.size(); ++i) {
     PartCtx& p = C->parts[i];
@@ -937,7 +960,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   int rc = expect(C, t, K_BWD, l, "pgcn_layer_bwd");
   if (rc) return rc;
   if (!params) return fail(PGCN_EINVAL, "params is NULL");
-  const Launch Lk{C->s, &C->launches};
+  const Launch Lk = C->launch();
   const int b = C->bi(t), bs = C->bi(t - C->depth);
   const bool pipe = C->cfg.mode == 1;
   const int64_t ldi = C->ld[l - 1], ldo = C->ld[l];
@@ -1122,7 +1145,7 @@ extern "C" int pgcn_update(pgcn_ctx* C, int64_t t, float* params, float* grads, 
   if (rc) return rc;
   if (!params || !grads) return fail(PGCN_EINVAL, "params / grads is NULL");
   if (C->cfg.opt == 1 && !opt_state) return fail(PGCN_EINVAL, "Adam needs opt_state");
-  const Launch Lk{C->s, &C->launches};
+  const Launch Lk = C->launch();
   PtrList G{};
   G.n = (int32_t)C->parts.size();
   for (int i = 0; i < G.n; ++i) G.p[i] = C->parts[i].G;

@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
-                                                             const int32_t* __restrict__ rows, int addend) {
+                                                             const int32_t* __restrict__ rows, int addend,
+                                                             const float4* __restrict__ add2, int edges, int raw) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -205,9 +206,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
 #pragma unroll
     for (int q = 0; q < NC; ++q) {  // GCN-sym self loop (A + I, R26): the row's own (inner) input
       acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc), same row, in place
+      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // partial sums of this row, in place
+      if (add2) f4acc(acc[q], add2[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of the split path
     }
-    const int64_t beg = rp[row], end = rp[row + 1];
+    const int64_t beg = edges ? rp[row] : 0, end = edges ? rp[row + 1] : 0;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
@@ -241,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
+      if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
+        Z[row * ld4 + x] = acc[q];
+        continue;
+      }
       float4 o = f4scale(acc[q], s);
       if (bias) {  // fused node-update epilogue (GCN-sym transform-first: H = act(P (D W) + b))
 #pragma unroll
@@ -263,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
                                                              unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                             int addend) {
+                                                             int addend, const float4* __restrict__ add2, int edges,
+                                                             int raw) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -287,9 +294,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
       acc[q] = (dDs && u0 < n_in) ? dDs[u0 * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc), same row, in place
+      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // partial sums of this row, in place
+      if (add2) f4acc(acc[q], add2[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of the split path
     }
-    const int64_t beg = trp[u0], end = trp[u0 + 1];
+    const int64_t beg = edges ? trp[u0] : 0, end = edges ? trp[u0 + 1] : 0;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
@@ -320,6 +328,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
+      if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
+        J[u0 * ld4 + x] = acc[q];
+        continue;
+      }
       float4 o = rs ? f4scale(acc[q], sr) : acc[q];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -403,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                unsigned long long* work, int grabk, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
                                                                int relu, const int32_t* __restrict__ rows,
-                                                               int addend) {
+                                                               int addend, const float4* __restrict__ add2, int edges,
+                                                               int raw) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -427,18 +440,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
       else
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
-      if (addend) {  // heavy-tile sums (spmm_tc), same row, in place
+      if (addend || add2) {  // partial sums of this row (in place) / heavy-tile sums of the split path
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t xf = 2 * xq + h;
           if (xf < ld4) {
-            const float4 a = Z[row * ld4 + xf];
+            float4 a = addend ? Z[row * ld4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (add2) f4acc(a, add2[row * ld4 + xf]);
             acc[q][4 * h] += a.x; acc[q][4 * h + 1] += a.y; acc[q][4 * h + 2] += a.z; acc[q][4 * h + 3] += a.w;
           }
         }
       }
     }
-    const int64_t beg = rp[row], end = rp[row + 1];
+    const int64_t beg = edges ? rp[row] : 0, end = edges ? rp[row + 1] : 0;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
@@ -475,6 +489,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * x + h;
         if (xf >= ld4) continue;
+        if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
+          Z[row * ld4 + xf] = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
+          continue;
+        }
         float o[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -501,7 +519,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
                                                                unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                               int addend) {
+                                                               int addend, const float4* __restrict__ add2, int edges,
+                                                               int raw) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -523,11 +542,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * xq + h;
         float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // heavy-tile sums (spmm_tc), in place
+        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // partial sums of this row, in place
+        if (add2 && xf < ld4) f4acc(a, add2[u0 * ld4 + xf]);  // heavy-tile sums of the split path
         acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
       }
     }
-    const int64_t beg = trp[u0], end = trp[u0 + 1];
+    const int64_t beg = edges ? trp[u0] : 0, end = edges ? trp[u0 + 1] : 0;
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
@@ -561,6 +581,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * x + h;
         if (xf >= ld4) continue;
+        if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
+          J[u0 * ld4 + xf] = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
+          continue;
+        }
         float o[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1136,96 +1160,116 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
   count(L);
 }
 
+// Tile path (tiles != nullptr, every neighbour row valid): the heavy tiles go to the tensor cores
+// (spmm_tc) and the light edges to the gather kernel.  With a side stream (L.side) the two run
+// concurrently -- the tile kernel is L2-latency bound at one CTA per SM, the light gather of
+// cross-community rows DRAM bound, and both fit on an SM together: the light pass writes raw
+// partial sums into the output on the side stream while the split + tile kernel write the tile
+// sums into tiles->part; after the join a pass without edges adds the two (and the self term)
+// and applies the epilogue.  Without a side stream: tile sums into the output, then the light
+// gather on top.
+
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
               int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz,
               const TileDev* tiles, void* t16) {
   if (n_rows <= 0) return;
-  // Dense tiles on the tensor cores, then the light edges by the gather kernel (addend = the tile
-  // sums): only when every neighbour row is valid and the launch covers all rows of the pattern.
   const int tcu = tiles && tiles->n_tiles > 0 && !rows && n_cols >= 0 && n_valid >= n_cols && tiles->n_rows == n_rows;
   if (tcu) {
     row_ptr = tiles->lrp;
     col = tiles->lcol;
     nnz = tiles->nnz_light;
   }
-  const int K = grab_items(nnz, n_rows);
-  const int64_t ld4 = ld / 4;
-  if (g16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
-    const int64_t ld8 = (ld + 7) / 8;
-    if (ld8 * 16 >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
-      std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
-      std::abort();
-    }
-    auto G16 = static_cast<uint4*>(g16);
-    k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
-                                                                          ld4, n_valid, ld8, G16);
-    count(L);
-    if (tcu && spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
-      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd, bf16) launch failed\n");
-      std::abort();
-    }
-    const bool chk16 = n_cols < 0 || n_valid < n_cols;
-    const SpmmShape sh = spmm16_shape(ld8);
-    if (!dyn_enabled()) work = nullptr;
-    if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
-    const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
-    auto Z4 = reinterpret_cast<float4*>(Z);
-#define X(G_, NC_, U_, MB_)                                                                                     \
-  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
-    if (chk16)                                                                                                 \
-      k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
-                                                                       n_valid, sh.nchunk, Z4, ld4, work, K, self, \
-                                                                       bias, n_bias, relu, rows, tcu);          \
-    else                                                                                                       \
-      k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, G16, ld8, n_rows, \
-                                                                        n_valid, sh.nchunk, Z4, ld4, work, K,   \
-                                                                        self, bias, n_bias, relu, rows, tcu);   \
-  } else
-    PGCN_SPMM16_CASES(X) {
-      std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
-      std::abort();
-    }
-#undef X
-    count(L);
-    return;
-  }
-  if (ld4 * 16 >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
+  const int64_t ld4 = ld / 4, ld8 = (ld + 7) / 8;
+  const bool b16 = g16 != nullptr;
+  if ((b16 ? ld8 * 16 : ld4 * 16) >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
     std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();
   }
-  const bool chk = n_cols < 0 || n_valid < n_cols;  // some neighbour rows are not valid yet
-  if (tcu) {  // fp32 tier: bf16 hi/lo split of the table, then the tile sums (2 MMAs per k-step)
-    const int64_t ld8 = (ld + 7) / 8;
-    auto H16 = static_cast<uint4*>(t16);
-    k_split_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(D), ld4,
-                                                                             ld4, n_valid, ld8, H16, H16 + n_valid * ld8);
-    count(L);
-    if (spmm_tc(L, *tiles, H16, H16 + n_valid * ld8, ld8 * 8, n_valid, ld8 * 8, Z, ld, ld)) {
-      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
-      std::abort();
-    }
-  }
-  const SpmmShape sh = spmm_shape(ld4);
+  const int K = grab_items(nnz, n_rows);
   if (!dyn_enabled()) work = nullptr;
-  if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
-  const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
-  auto D4 = reinterpret_cast<const float4*>(D);
+  const bool chk = !tcu && (n_cols < 0 || n_valid < n_cols);  // some neighbour rows are not valid yet
   auto Z4 = reinterpret_cast<float4*>(Z);
+  auto D4 = reinterpret_cast<const float4*>(D);
+  auto G16 = static_cast<uint4*>(g16);
+  if (b16) {  // bf16 gather tier: round the table's valid rows to bf16, then gather those
+    k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(D4, ld4, ld4, n_valid, ld8, G16);
+    count(L);
+  }
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add, const float4* a2, int edges, int raw) {
+    if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
+    if (b16) {
+      const SpmmShape sh = spmm16_shape(ld8);
+      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     if (chk)                                                                                                   \
-      k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
-                                                                     n_valid, sh.nchunk, Z4, work, K, self, bias, \
-                                                                     n_bias, relu, rows, tcu);                  \
+      k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,   \
+                                                                      n_valid, sh.nchunk, Z4, ld4, wk, K, slf,    \
+                                                                      bias, n_bias, relu, rows, add, a2, edges,   \
+                                                                      raw);                                    \
     else                                                                                                       \
-      k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, L.s>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,    \
-                                                                      n_valid, sh.nchunk, Z4, work, K, self, bias, \
-                                                                      n_bias, relu, rows, tcu);                 \
+      k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
+                                                                       n_valid, sh.nchunk, Z4, ld4, wk, K, slf,   \
+                                                                       bias, n_bias, relu, rows, add, a2, edges,  \
+                                                                       raw);                                   \
   } else
-  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
+      PGCN_SPMM16_CASES(X) {
+        std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
+        std::abort();
+      }
 #undef X
-  count(L);
+    } else {
+      const SpmmShape sh = spmm_shape(ld4);
+      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    if (chk)                                                                                                   \
+      k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,      \
+                                                                    n_valid, sh.nchunk, Z4, wk, K, slf, bias,     \
+                                                                    n_bias, relu, rows, add, a2, edges, raw);     \
+    else                                                                                                       \
+      k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
+                                                                     n_valid, sh.nchunk, Z4, wk, K, slf, bias,    \
+                                                                     n_bias, relu, rows, add, a2, edges, raw);    \
+  } else
+      PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
+#undef X
+    }
+    count(L);
+  };
+  if (!tcu) {
+    gather(L.s, work, self, 0, nullptr, 1, 0);
+    return;
+  }
+  auto tile = [&](float* out) {
+    int rc;
+    if (b16) {
+      rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_valid, ld8 * 8, out, ld, ld);
+    } else {  // fp32 tier: bf16 hi/lo split of the table, then the tile sums (2 MMAs per k-step)
+      auto H16 = static_cast<uint4*>(t16);
+      k_split_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(D4, ld4, ld4, n_valid, ld8, H16,
+                                                                               H16 + n_valid * ld8);
+      count(L);
+      rc = spmm_tc(L, *tiles, H16, H16 + n_valid * ld8, ld8 * 8, n_valid, ld8 * 8, out, ld, ld);
+    }
+    if (rc) {
+      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
+      std::abort();
+    }
+  };
+  if (L.side && tiles->part) {
+    cudaEventRecord(L.ev_fork, L.s);
+    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+    gather(L.side, work, 0, 0, nullptr, 1, 1);  // light edges: raw partial sums into Z
+    tile(tiles->part);
+    cudaEventRecord(L.ev_join, L.side);
+    cudaStreamWaitEvent(L.s, L.ev_join, 0);
+    gather(L.s, nullptr, self, 1, reinterpret_cast<const float4*>(tiles->part), 0, 0);  // sum + epilogue
+  } else {
+    tile(Z);
+    gather(L.s, work, self, 1, nullptr, 1, 0);
+  }
 }
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
@@ -1239,73 +1283,86 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     t_col = tiles->lcol;
     nnz = tiles->nnz_light;
   }
-  const int K = grab_items(nnz, n_all);
-  const int64_t ld4 = ld / 4;
-  if (g16) {  // bf16 gather tier: dZs (n_in rows of stride ld_dA) -> bf16 rows of ld8 vectors
-    const int64_t ld8 = (ld + 7) / 8;
-    if (ld8 * 16 >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
-      std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
-      std::abort();
-    }
-    auto G16 = static_cast<uint4*>(g16);
-    k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
-                                                                       ld_dA / 4, ld4, n_in, ld8, G16);
-    count(L);
-    if (tcu && spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
-      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd, bf16) launch failed\n");
-      std::abort();
-    }
-    const SpmmShape sh = spmm16_shape(ld8);
-    if (!dyn_enabled()) work = nullptr;
-    if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
-    const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
-    auto b = reinterpret_cast<const float4*>(dDs);
-    auto J4 = reinterpret_cast<float4*>(J);
-    const int64_t lda4 = ld_dA / 4;
-#define X(G_, NC_, U_, MB_)                                                                                     \
-  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
-    k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all, \
-                                                               sh.nchunk, J4, ld4, gid, d, work, K, rs, tcu);  \
-  } else
-    PGCN_SPMM16_CASES(X) {
-      std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
-      std::abort();
-    }
-#undef X
-    count(L);
-    return;
-  }
-  if (ld_dA * 4 >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
+  const int64_t ld4 = ld / 4, ld8 = (ld + 7) / 8;
+  const bool b16 = g16 != nullptr;
+  if ((b16 ? ld8 * 16 : ld_dA * 4) >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
     std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
     std::abort();
   }
-  if (tcu) {  // fp32 tier: bf16 hi/lo split of dZs, then the tile sums
-    const int64_t ld8 = (ld + 7) / 8;
-    auto H16 = static_cast<uint4*>(t16);
-    k_split_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(dZs),
-                                                                          ld_dA / 4, ld4, n_in, ld8, H16, H16 + n_in * ld8);
+  const int K = grab_items(nnz, n_all);
+  if (!dyn_enabled()) work = nullptr;
+  auto J4 = reinterpret_cast<float4*>(J);
+  const int64_t lda4 = ld_dA / 4;
+  auto a = reinterpret_cast<const float4*>(dZs);
+  auto G16 = static_cast<uint4*>(g16);
+  if (b16) {  // bf16 gather tier: dZs (n_in rows of stride ld_dA) -> bf16 rows of ld8 vectors
+    k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(a, lda4, ld4, n_in, ld8, G16);
     count(L);
-    if (spmm_tc(L, *tiles, H16, H16 + n_in * ld8, ld8 * 8, n_in, ld8 * 8, J, ld, ld)) {
+  }
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add, const float4* a2, int edges,
+                    int raw) {
+    if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
+    auto b = reinterpret_cast<const float4*>(dD);
+    if (b16) {
+      const SpmmShape sh = spmm16_shape(ld8);
+      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all,  \
+                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, a2,    \
+                                                              edges, raw);                                     \
+  } else
+      PGCN_SPMM16_CASES(X) {
+        std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
+        std::abort();
+      }
+#undef X
+    } else {
+      const SpmmShape sh = spmm_shape(ld4);
+      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
+#define X(G_, NC_, U_, MB_)                                                                                     \
+  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
+    k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
+                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, a2,      \
+                                                            edges, raw);                                       \
+  } else
+      PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
+#undef X
+    }
+    count(L);
+  };
+  if (!tcu) {
+    gather(L.s, work, dDs, 0, nullptr, 1, 0);
+    return;
+  }
+  auto tile = [&](float* out) {
+    int rc;
+    if (b16) {
+      rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_in, ld8 * 8, out, ld, ld);
+    } else {  // fp32 tier: bf16 hi/lo split of dZs, then the tile sums
+      auto H16 = static_cast<uint4*>(t16);
+      k_split_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(a, lda4, ld4, n_in, ld8, H16,
+                                                                            H16 + n_in * ld8);
+      count(L);
+      rc = spmm_tc(L, *tiles, H16, H16 + n_in * ld8, ld8 * 8, n_in, ld8 * 8, out, ld, ld);
+    }
+    if (rc) {
       std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd) launch failed\n");
       std::abort();
     }
+  };
+  if (L.side && tiles->part) {
+    cudaEventRecord(L.ev_fork, L.s);
+    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+    gather(L.side, work, nullptr, 0, nullptr, 1, 1);  // light edges: raw partial sums into J
+    tile(tiles->part);
+    cudaEventRecord(L.ev_join, L.side);
+    cudaStreamWaitEvent(L.s, L.ev_join, 0);
+    gather(L.s, nullptr, dDs, 1, reinterpret_cast<const float4*>(tiles->part), 0, 0);  // sum + mask epilogue
+  } else {
+    tile(J);
+    gather(L.s, work, dDs, 1, nullptr, 1, 0);
   }
-  const SpmmShape sh = spmm_shape(ld4);
-  if (!dyn_enabled()) work = nullptr;
-  if (work) cudaMemsetAsync(work, 0, sizeof(unsigned long long), L.s);
-  const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
-  auto a = reinterpret_cast<const float4*>(dZs);
-  auto b = reinterpret_cast<const float4*>(dDs);
-  auto J4 = reinterpret_cast<float4*>(J);
-  const int64_t lda4 = ld_dA / 4;
-#define X(G_, NC_, U_, MB_)                                                                                     \
-  if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
-    k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, L.s>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,         \
-                                                             sh.nchunk, J4, ld4, gid, d, work, K, rs, tcu);    \
-  } else
-  PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
-#undef X
-  count(L);
 }
 
 void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld, float* dst,

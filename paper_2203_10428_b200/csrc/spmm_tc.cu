@@ -57,8 +57,12 @@ struct Params {
 
 // Per-stage geometry (one stage = one 128 x 64 tile): A 128 x 64 bf16 (16 KB) | NT tables x (64 rows
 // x BN bf16) | mask 1 KB.  Every piece is a multiple of 1 KB (SW128 atoms stay 1024-aligned).
+// TS = 1 (A in TMEM, written by tcgen05.st): no A in shared memory.
 __host__ __device__ inline uint32_t table_bytes(int BN) { return (uint32_t)BN * 64 * 2; }
-__host__ __device__ inline uint32_t stage_bytes(int NT, int BN) { return 16384 + NT * table_bytes(BN) + BM * 8; }
+__host__ __device__ inline uint32_t a_bytes(int TS) { return TS ? 0u : 16384u; }
+__host__ __device__ inline uint32_t stage_bytes(int NT, int BN, int TS) {
+  return a_bytes(TS) + NT * table_bytes(BN) + BM * 8;
+}
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
@@ -69,13 +73,40 @@ __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
   return v;
 }
 
-template <int NT>
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+
+// One 32-column tcgen05.st of this warp's TMEM lane quarter (thread i -> lane 32 q + i).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+// TS = 1: the 128 x 64 A tile of stage s lives in TMEM columns [2 BN + 32 s, + 32) (lane = row, two
+// bf16 k per 32-bit column, k even in the low half -- the UMMA "A from TMEM" layout), written by the
+// builders with tcgen05.st; otherwise in shared memory (SS mode).
+template <int NT, int TS>
 __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  const uint32_t tb = table_bytes(p.BN), sb = stage_bytes(NT, p.BN);
-  const uint32_t mask_off = 16384 + NT * tb;
+  const uint32_t tb = table_bytes(p.BN), sb = stage_bytes(NT, p.BN, TS), ab = a_bytes(TS);
+  const uint32_t mask_off = ab + NT * tb;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * sb);
   uint64_t* full = bars;
   uint64_t* conv = bars + S;
@@ -117,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
       uint32_t ph = 0;
       const uint32_t tx = NT * tb + BM * 8;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int rb = p.order[it / p.n_nt];
+        const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
         const int n0 = (it % p.n_nt) * p.BN;
         for (int k = p.rb_ptr[rb]; k < p.rb_ptr[rb + 1]; ++k) {
           const int row0 = p.tile_col[k] * 64;
@@ -127,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           for (int t = 0; t < NT; ++t)
             for (int kh = 0; kh < 2; ++kh)  // two k-halves of 32 rows, natom SW128 atoms of 64 x 32 each
               for (int j = 0; j < natom; ++j)
-                tma_load_2d(st + 16384 + t * tb + (kh * natom + j) * 4096, &p.map_b[t], &full[s], n0 + 64 * j,
+                tma_load_2d(st + ab + t * tb + (kh * natom + j) * 4096, &p.map_b[t], &full[s], n0 + 64 * j,
                             row0 + 32 * kh);
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -150,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
       int acc = 0;
       uint32_t acc_ph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int rb = p.order[it / p.n_nt];
+        const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
         mbar_wait(&tempty[acc], acc_ph ^ 1, 12);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * p.BN);
@@ -160,13 +191,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           mbar_wait(&conv[s], ph, 13);
           tc_fence_after();
           const uint32_t A = sbase + (uint32_t)s * sb;
+          const uint32_t ta = tmem_base + (uint32_t)(2 * p.BN + 32 * s);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // k-steps of 16: A 32 bytes apart; B 16-row steps in k-half kk/2
+          for (int kk = 0; kk < 4; ++kk) {  // k-steps of 16: A 32 bytes (SS) / 8 columns (TS) apart;
+                                            // B 16-row steps in k-half kk/2
             const uint64_t a = make_desc(A + kk * 32, 16, 1024);
-            const uint32_t boff = 16384u + (uint32_t)((kk >> 1) * natom * 4096 + (kk & 1) * 2048);
+            const uint32_t boff = ab + (uint32_t)((kk >> 1) * natom * 4096 + (kk & 1) * 2048);
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-              mma_bf16(d, a, make_desc(A + boff + t * tb, 4096, 1024), idesc, accum);
+              const uint64_t b = make_desc(A + boff + t * tb, 4096, 1024);
+              if (TS) mma_bf16_ts(d, ta + 8 * kk, b, idesc, accum);
+              else mma_bf16(d, a, b, idesc, accum);
               accum = 1u;
             }
           }
@@ -183,11 +218,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
     int s = 0;
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int rb = p.order[it / p.n_nt];
+      const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
       const int nt = p.rb_ptr[rb + 1] - p.rb_ptr[rb];
       for (int k = 0; k < nt; ++k) {
         mbar_wait(&full[s], ph, 14);
         const uint32_t st = sbase + (uint32_t)s * sb;
+        if (TS) {  // this thread's row r = 32 (warp % 4) + lane: 64 bits -> 32 columns of bf16 pairs
+          const int q = warp & 3, r = 32 * q + lane;
+          const uint64_t m = lds64(st + mask_off + r * 8);
+          uint32_t v[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            v[c] = (((m >> (2 * c)) & 1ull) ? 0x3F80u : 0u) | (((m >> (2 * c + 1)) & 1ull) ? 0x3F800000u : 0u);
+          tmem_st32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * p.BN + 32 * s), v);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&conv[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         // row r = 128 bytes (64 bf16 of k); 16-byte chunk j (k = 8j..8j+7) at r*128 + ((j ^ (r&7)) << 4)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -210,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int rb = p.order[it / p.n_nt];
+      const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
       const int n0 = (it % p.n_nt) * p.BN;
       const bool none = p.rb_ptr[rb + 1] == p.rb_ptr[rb];
       mbar_wait(&tfull[acc], acc_ph, 15);
@@ -272,30 +321,58 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.n_nt = (int)((width + bn - 1) / bn);
   p.n_rb = (int)T.n_rb;
   p.rb_ptr = T.rb_ptr;
-  p.order = T.order;
+  static int env_order = -1;  // dev knob PGCN_TC_SPMM_ORDER: 1 = descending tile count (LPT), 0 = natural
+  if (env_order < 0) {
+    const char* e = std::getenv("PGCN_TC_SPMM_ORDER");
+    env_order = e ? std::atoi(e) : 1;
+  }
+  p.order = env_order ? T.order : nullptr;
   p.tile_col = T.tile_col;
   p.mask = T.mask;
   p.out = out;
   p.n_rows = T.n_rows;
   p.ld_out = ld_out;
   p.width = (int)width;
-  p.tmem_cols = tc_tmem_cols(p.BN);
-  const uint32_t stage = stage_bytes(NT, p.BN);
+  static int env_ts = -1;  // dev knob PGCN_TC_SPMM_TS: 0 forces SS mode (A in shared memory)
+  if (env_ts < 0) {
+    const char* e = std::getenv("PGCN_TC_SPMM_TS");
+    env_ts = e ? std::atoi(e) : 1;
+  }
+  int TS = env_ts && 2 * p.BN + 32 * 2 <= 512;
+  uint32_t stage = stage_bytes(NT, p.BN, TS);
   int S = (int)((210 * 1024) / stage);
-  p.stages = S > 8 ? 8 : (S < 2 ? 2 : S);
+  S = S > 8 ? 8 : (S < 2 ? 2 : S);
+  if (TS) {
+    while (S > 2 && 2 * p.BN + 32 * S > 512) --S;
+    if (2 * p.BN + 32 * S > 512) TS = 0;
+  }
+  if (!TS) {
+    stage = stage_bytes(NT, p.BN, 0);
+    S = (int)((210 * 1024) / stage);
+    S = S > 8 ? 8 : (S < 2 ? 2 : S);
+  }
+  p.stages = S;
+  p.tmem_cols = TS ? 512 : tc_tmem_cols(p.BN);
   const size_t smem = 1024 + (size_t)p.stages * stage + (3 * p.stages + 4) * 8 + 16;
   if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_spmm_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_spmm_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_spmm_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_spmm_tc<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_spmm_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_spmm_tc<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int n_items = p.n_rb * p.n_nt;
   const int grid = n_items < 148 ? n_items : 148;
-  if (NT == 2) k_spmm_tc<2><<<grid, kThreads, smem, L.s>>>(p);
-  else k_spmm_tc<1><<<grid, kThreads, smem, L.s>>>(p);
+  if (NT == 2) {
+    if (TS) k_spmm_tc<2, 1><<<grid, kThreads, smem, L.s>>>(p);
+    else k_spmm_tc<2, 0><<<grid, kThreads, smem, L.s>>>(p);
+  } else {
+    if (TS) k_spmm_tc<1, 1><<<grid, kThreads, smem, L.s>>>(p);
+    else k_spmm_tc<1, 0><<<grid, kThreads, smem, L.s>>>(p);
+  }
   if (L.count) *L.count += 1;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

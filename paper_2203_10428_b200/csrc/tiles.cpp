@@ -1,6 +1,6 @@
 // Host builder of the dense-tile decomposition (tiles.h).  One pass per 128-row block: count the
 // edges per 64-column tile, keep the tiles with >= min_edges as bitmasks, route the rest (and any
-// repeated (row, col) pair) to the light CSR in the original edge order.
+// repeated (row, col) pair) to the light CSR, sorted by column within each row.
 #include "tiles.h"
 
 #include "common.h"
@@ -37,7 +37,8 @@ void one_block(const int64_t* rp, const int32_t* col, int64_t r0, int64_t r1, in
     }
   o.mask.assign(o.tcol.size() * kTileRows, 0ull);
   o.lcnt.assign((size_t)(r1 - r0), 0);
-  for (int64_t r = r0; r < r1; ++r)
+  for (int64_t r = r0; r < r1; ++r) {
+    const size_t row_begin = o.lcol.size();
     for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
       const int32_t c = col[e], j = c / kTileCols;
       if (slot[j] >= 0) {
@@ -51,6 +52,8 @@ void one_block(const int64_t* rp, const int32_t* col, int64_t r0, int64_t r1, in
       o.lcol.push_back(c);
       ++o.lcnt[(size_t)(r - r0)];
     }
+    std::sort(o.lcol.begin() + row_begin, o.lcol.end());
+  }
   for (int32_t j : touched) {
     cnt[j] = 0;
     slot[j] = -1;

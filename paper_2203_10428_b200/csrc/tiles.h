@@ -4,8 +4,9 @@
 // of 128 rows and column tiles of 64 columns.  A tile holding at least `min_edges` edges is
 // "heavy": its edges are stored as a 128 x 64 bitmask (one uint64 per row) and aggregated as a
 // dense 0/1 block times the 64 gathered rows on the tensor cores; every other edge (and a repeated
-// (row, col) pair, which a bitmask cannot count twice) stays in the "light" CSR, in the original
-// order, for the gather SpMM.  sum over heavy bits + light edges = the pattern, exactly.
+// (row, col) pair, which a bitmask cannot count twice) stays in the "light" CSR, columns ascending
+// within a row, for the gather SpMM.
+// sum over heavy bits + light edges = the pattern, exactly.
 #pragma once
 #include <cstdint>
 #include <vector>
@@ -24,7 +25,7 @@ struct TileSet {
   std::vector<int32_t> order;     // [n_rb] row blocks by descending heavy-tile count (static LPT work list)
   std::vector<int32_t> tile_col;  // [n_tiles] column tile j (columns 64 j .. 64 j + 63), ascending per block
   std::vector<uint64_t> mask;     // [n_tiles x 128] bit c of word r: edge (128 b + r, 64 j + c)
-  std::vector<int64_t> lrp;       // [n_rows + 1] light CSR
+  std::vector<int64_t> lrp;       // [n_rows + 1] light CSR, columns ascending within a row
   std::vector<int32_t> lcol;      // [nnz_light]
 };
 

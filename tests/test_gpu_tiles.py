@@ -53,6 +53,26 @@ def test_tiles_vs_oracle(P, name, tmin, tf, gather):
     check_against_oracle(gpu, ora, L, n_parts, tol=tol, what=f"tiles {name} t{tmin} tf{tf} {gather}")
 
 
+@pytest.mark.parametrize("gather", ["f32", "bf16"])
+@pytest.mark.parametrize("model", ["sage", "gcn"])
+@pytest.mark.parametrize("concurrent", ["1", "0"])
+def test_tiles_light_mix(P, gather, model, concurrent, monkeypatch):
+    """A quarter of the edges light (tile_min 200): the light gather on the side stream (raw partial
+    sums) concurrent with the tile kernel, then the combining pass (self loop, row scale, dropout mask
+    epilogues), or both sequential (PGCN_TILE_CONCURRENT=0); both tiers, GraphSAGE and GCN-sym."""
+    monkeypatch.setenv("PGCN_TILE_CONCURRENT", concurrent)
+    g, widths, loss, n_parts = case("dense")
+    tol = 1e-4 if gather == "f32" else 2e-2
+    params0 = glorot_params(widths, 3, model=model)
+    for tf in (True, False):
+        kw = dict(mode="pipe", smooth_f=True, dropout=0.3, loss=loss, opt="sgd", lr=0.5, transform_first=tf,
+                  gather=gather, model=model, spmm_tiles=True, tile_min=200)
+        gpu, _ = run_gpu(P, g, widths, n_parts, 3, params0, **kw)
+        cfg = ModelCfg(widths=widths, dropout=0.3, lr=0.5, opt="sgd", loss=loss, model=model)
+        ora = oracle_run(gpu, g, n_parts, params0, cfg, 3, tol=tol, mode="pipe", smooth_f=True)
+        check_against_oracle(gpu, ora, 3, n_parts, tol=tol, what=f"light-mix {gather} {model} tf{tf} c{concurrent}")
+
+
 @pytest.mark.parametrize("tf", [True, False])
 @pytest.mark.parametrize("mode", ["pipe", "vanilla"])
 def test_tiles_gcn(P, tf, mode):
@@ -69,14 +89,15 @@ def test_tiles_gcn(P, tf, mode):
 
 def test_tiles_on_off_agree(P):
     """Same run with and without the tile path: the sums are only reassociated (fp32 tier), so the loss
-    and every layer output agree to fp32 rounding (1e-5 relative) over 4 iterations.  (G is compared
-    with the oracle above: a ReLU' decision at |Y| ~ 1e-7 may legitimately differ between two fp32
-    summation orders and moves G by a whole J entry -- reading R25.)"""
+    and every layer output agree to fp32 rounding (1e-5 relative) at t = 1 (gather only) and t = 2 (tile
+    path, same weights).  Later iterations are compared with the oracle above only: a ReLU' decision
+    at |Y| ~ 1e-7 may legitimately differ between two fp32 summation orders and moves G by a whole J
+    entry (reading R25), so the weights of t >= 3 differ slightly.)"""
     g, widths, loss, n_parts = case("dense")
     params0 = glorot_params(widths, 3)
     kw = dict(mode="pipe", smooth_g=True, dropout=0.3, loss=loss, opt="sgd", lr=0.5)
-    a, _ = run_gpu(P, g, widths, n_parts, 4, params0, spmm_tiles=True, tile_min=16, **kw)
-    b, _ = run_gpu(P, g, widths, n_parts, 4, params0, spmm_tiles=False, **kw)
+    a, _ = run_gpu(P, g, widths, n_parts, 2, params0, spmm_tiles=True, tile_min=16, **kw)
+    b, _ = run_gpu(P, g, widths, n_parts, 2, params0, spmm_tiles=False, **kw)
     for t, (x, y) in enumerate(zip(a, b), start=1):
         assert abs(x["loss"] - y["loss"]) <= 1e-5 * abs(y["loss"]), t
         for l in x["H"]:
