@@ -138,9 +138,7 @@ struct pgcn_ctx {
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
   cudaStream_t cs = nullptr;              // comm stream (high priority)
-  cudaStream_t ss = nullptr;              // side stream of the concurrent tile / light-gather SpMM split
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  pgcn::Launch launch() { return pgcn::Launch{s, &launches, ss, ev_fork, ev_join}; }
+  pgcn::Launch launch() { return pgcn::Launch{s, &launches}; }
   cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
   cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};
   float* send_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // packed S_{i,j} rows of the layer-l input
@@ -164,9 +162,6 @@ struct pgcn_ctx {
     if (cr) ncclCommDestroy(cr);
 #endif
     if (cs) cudaStreamDestroy(cs);
-    if (ss) cudaStreamDestroy(ss);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
   }
 };
 
@@ -206,7 +201,7 @@ int64_t param_count(const pgcn_config* c) {
 int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local, Arena& A) {
   const int L = C->L;
   C->parts.assign(n_local, PartCtx{});
-  int64_t dw_need = 0, tile_rows = 0;
+  int64_t dw_need = 0;
   for (int i = 0; i < n_local; ++i) {
     PartCtx& p = C->parts[i];
     p.part = local[i];
@@ -278,7 +273,6 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
         d.nnz_light = ts->nnz_light;
       }
       if ((p.ts[0] || p.ts[1]) && C->cfg.gather == 0) p.T16 = A.take<uint16_t>(2 * p.n_all * round_up(C->ldmax, 8));
-      if (p.ts[0] || p.ts[1]) tile_rows = std::max(tile_rows, p.n_all);
     }
     if (C->cfg.train_sparse) {
       p.tr_list = A.take<int32_t>(p.n_in);
@@ -298,10 +292,6 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   }
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
-  // tile sums of the concurrent tile / light-gather split (one SpMM at a time on the context stream)
-  float* tile_part = tile_rows > 0 ? A.take<float>(tile_rows * C->ldmax) : nullptr;
-  for (auto& p : C->parts)
-    for (int w = 0; w < 2; ++w) p.td[w].part = tile_part;
   if (C->sp_tmp_bytes > 0) C->sp_tmp = A.take<char>(C->sp_tmp_bytes);
   if (C->nccl && n_local == 1) {
     const PartCtx& p = C->parts[0];
@@ -690,17 +680,6 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     if (e != cudaSuccess) {
       delete C;
       return fail(PGCN_ECUDA, "pgcn_ctx_create upload: %s", cudaGetErrorString(e));
-    }
-  }
-  bool tiles_used = false;
-  for (auto& p : C->parts) tiles_used = tiles_used || p.ts[0] || p.ts[1];
-  const char* conc = std::getenv("PGCN_TILE_CONCURRENT");  // dev knob: 0 = tile and light passes in sequence
-  if (tiles_used && !(conc && std::atoi(conc) == 0)) {
-    if (cudaStreamCreateWithFlags(&C->ss, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming) != cudaSuccess) {
-      delete C;
-      return fail(PGCN_ECUDA, "side stream creation failed");
     }
   }
   if (C->nccl) {

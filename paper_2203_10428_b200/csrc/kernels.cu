@@ -176,8 +176,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
-                                                             const int32_t* __restrict__ rows, int addend,
-                                                             const float4* __restrict__ add2, int edges, int raw) {
+                                                             const int32_t* __restrict__ rows, int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -206,10 +205,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
 #pragma unroll
     for (int q = 0; q < NC; ++q) {  // GCN-sym self loop (A + I, R26): the row's own (inner) input
       acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // partial sums of this row, in place
-      if (add2) f4acc(acc[q], add2[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of the split path
+      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of this row, in place
     }
-    const int64_t beg = edges ? rp[row] : 0, end = edges ? rp[row + 1] : 0;
+    const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
@@ -243,10 +241,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
-      if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
-        Z[row * ld4 + x] = acc[q];
-        continue;
-      }
       float4 o = f4scale(acc[q], s);
       if (bias) {  // fused node-update epilogue (GCN-sym transform-first: H = act(P (D W) + b))
 #pragma unroll
@@ -269,8 +263,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
                                                              unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                             int addend, const float4* __restrict__ add2, int edges,
-                                                             int raw) {
+                                                             int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -294,10 +287,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
       acc[q] = (dDs && u0 < n_in) ? dDs[u0 * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // partial sums of this row, in place
-      if (add2) f4acc(acc[q], add2[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of the split path
+      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of this row, in place
     }
-    const int64_t beg = edges ? trp[u0] : 0, end = edges ? trp[u0 + 1] : 0;
+    const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
@@ -328,10 +320,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
-      if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
-        J[u0 * ld4 + x] = acc[q];
-        continue;
-      }
       float4 o = rs ? f4scale(acc[q], sr) : acc[q];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -415,8 +403,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                unsigned long long* work, int grabk, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
                                                                int relu, const int32_t* __restrict__ rows,
-                                                               int addend, const float4* __restrict__ add2, int edges,
-                                                               int raw) {
+                                                               int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -440,19 +427,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
       else
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
-      if (addend || add2) {  // partial sums of this row (in place) / heavy-tile sums of the split path
+      if (addend) {  // heavy-tile sums (spmm_tc) of this row, in place
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t xf = 2 * xq + h;
           if (xf < ld4) {
-            float4 a = addend ? Z[row * ld4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (add2) f4acc(a, add2[row * ld4 + xf]);
+            const float4 a = Z[row * ld4 + xf];
             acc[q][4 * h] += a.x; acc[q][4 * h + 1] += a.y; acc[q][4 * h + 2] += a.z; acc[q][4 * h + 3] += a.w;
           }
         }
       }
     }
-    const int64_t beg = edges ? rp[row] : 0, end = edges ? rp[row + 1] : 0;
+    const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
@@ -489,10 +475,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * x + h;
         if (xf >= ld4) continue;
-        if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
-          Z[row * ld4 + xf] = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
-          continue;
-        }
         float o[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -519,8 +501,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
                                                                unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                               int addend, const float4* __restrict__ add2, int edges,
-                                                               int raw) {
+                                                               int addend) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -542,12 +523,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * xq + h;
         float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // partial sums of this row, in place
-        if (add2 && xf < ld4) f4acc(a, add2[u0 * ld4 + xf]);  // heavy-tile sums of the split path
+        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // heavy-tile sums (spmm_tc) of this row, in place
         acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
       }
     }
-    const int64_t beg = edges ? trp[u0] : 0, end = edges ? trp[u0 + 1] : 0;
+    const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
       const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
@@ -581,10 +561,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * x + h;
         if (xf >= ld4) continue;
-        if (raw) {  // partial sum only (the light pass of the split tile path), no epilogue
-          J[u0 * ld4 + xf] = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
-          continue;
-        }
         float o[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1161,13 +1137,10 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 }
 
 // Tile path (tiles != nullptr, every neighbour row valid): the heavy tiles go to the tensor cores
-// (spmm_tc) and the light edges to the gather kernel.  With a side stream (L.side) the two run
-// concurrently -- the tile kernel is L2-latency bound at one CTA per SM, the light gather of
-// cross-community rows DRAM bound, and both fit on an SM together: the light pass writes raw
-// partial sums into the output on the side stream while the split + tile kernel write the tile
-// sums into tiles->part; after the join a pass without edges adds the two (and the self term)
-// and applies the epilogue.  Without a side stream: tile sums into the output, then the light
-// gather on top.
+// (spmm_tc, writing the tile sums into the output rows) and the gather kernel then walks the light
+// edges on top of them (addend) and applies the epilogue.  (Running the light gather concurrently
+// on a side stream, one block per SM next to the tile kernel's CTA, measured 15-25 % slower: both
+// passes contend for the same L2 / DRAM path.)
 
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
@@ -1196,7 +1169,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(D4, ld4, ld4, n_valid, ld8, G16);
     count(L);
   }
-  auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add, const float4* a2, int edges, int raw) {
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add) {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     if (b16) {
       const SpmmShape sh = spmm16_shape(ld8);
@@ -1206,13 +1179,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,   \
                                                                       n_valid, sh.nchunk, Z4, ld4, wk, K, slf,    \
-                                                                      bias, n_bias, relu, rows, add, a2, edges,   \
-                                                                      raw);                                    \
+                                                                      bias, n_bias, relu, rows, add);                                    \
     else                                                                                                       \
       k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
                                                                        n_valid, sh.nchunk, Z4, ld4, wk, K, slf,   \
-                                                                       bias, n_bias, relu, rows, add, a2, edges,  \
-                                                                       raw);                                   \
+                                                                       bias, n_bias, relu, rows, add);                                   \
   } else
       PGCN_SPMM16_CASES(X) {
         std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
@@ -1227,11 +1198,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,      \
                                                                     n_valid, sh.nchunk, Z4, wk, K, slf, bias,     \
-                                                                    n_bias, relu, rows, add, a2, edges, raw);     \
+                                                                    n_bias, relu, rows, add);     \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
                                                                      n_valid, sh.nchunk, Z4, wk, K, slf, bias,    \
-                                                                     n_bias, relu, rows, add, a2, edges, raw);    \
+                                                                     n_bias, relu, rows, add);    \
   } else
       PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -1239,7 +1210,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     count(L);
   };
   if (!tcu) {
-    gather(L.s, work, self, 0, nullptr, 1, 0);
+    gather(L.s, work, self, 0);
     return;
   }
   auto tile = [&](float* out) {
@@ -1258,18 +1229,8 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
       std::abort();
     }
   };
-  if (L.side && tiles->part) {
-    cudaEventRecord(L.ev_fork, L.s);
-    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
-    gather(L.side, work, 0, 0, nullptr, 1, 1);  // light edges: raw partial sums into Z
-    tile(tiles->part);
-    cudaEventRecord(L.ev_join, L.side);
-    cudaStreamWaitEvent(L.s, L.ev_join, 0);
-    gather(L.s, nullptr, self, 1, reinterpret_cast<const float4*>(tiles->part), 0, 0);  // sum + epilogue
-  } else {
-    tile(Z);
-    gather(L.s, work, self, 1, nullptr, 1, 0);
-  }
+  tile(Z);
+  gather(L.s, work, self, 1);
 }
 
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
@@ -1299,8 +1260,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(a, lda4, ld4, n_in, ld8, G16);
     count(L);
   }
-  auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add, const float4* a2, int edges,
-                    int raw) {
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add) {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     auto b = reinterpret_cast<const float4*>(dD);
     if (b16) {
@@ -1309,8 +1269,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all,  \
-                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, a2,    \
-                                                              edges, raw);                                     \
+                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add);                                     \
   } else
       PGCN_SPMM16_CASES(X) {
         std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
@@ -1323,8 +1282,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
-                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, a2,      \
-                                                            edges, raw);                                       \
+                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add);                                       \
   } else
       PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -1332,7 +1290,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     count(L);
   };
   if (!tcu) {
-    gather(L.s, work, dDs, 0, nullptr, 1, 0);
+    gather(L.s, work, dDs, 0);
     return;
   }
   auto tile = [&](float* out) {
@@ -1351,18 +1309,8 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
       std::abort();
     }
   };
-  if (L.side && tiles->part) {
-    cudaEventRecord(L.ev_fork, L.s);
-    cudaStreamWaitEvent(L.side, L.ev_fork, 0);
-    gather(L.side, work, nullptr, 0, nullptr, 1, 1);  // light edges: raw partial sums into J
-    tile(tiles->part);
-    cudaEventRecord(L.ev_join, L.side);
-    cudaStreamWaitEvent(L.s, L.ev_join, 0);
-    gather(L.s, nullptr, dDs, 1, reinterpret_cast<const float4*>(tiles->part), 0, 0);  // sum + mask epilogue
-  } else {
-    tile(J);
-    gather(L.s, work, dDs, 1, nullptr, 1, 0);
-  }
+  tile(J);
+  gather(L.s, work, dDs, 1);
 }
 
 void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld, float* dst,

@@ -26,13 +26,10 @@ struct DropSpec {
   int32_t on;
 };
 
-// Launch counter (per context) incremented by every launcher.  side / ev_fork / ev_join (optional): a
-// second stream and two events for launchers that fork concurrent work (the tile SpMM path).
+// Launch counter (per context) incremented by every launcher.
 struct Launch {
   cudaStream_t s;
   int64_t* count;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // Device copy of a dense-tile decomposition (tiles.h) of an SpMM pattern.
@@ -43,7 +40,6 @@ struct TileDev {
   const uint64_t* mask = nullptr;
   const int64_t* lrp = nullptr;   // light CSR (columns ascending within a row)
   const int32_t* lcol = nullptr;
-  float* part = nullptr;          // n_rows x ld scratch for the tile sums of the concurrent split path
   int64_t n_rows = 0, n_cols = 0, n_rb = 0, n_tiles = 0, nnz_light = 0;
 };
 // Heavy-tile sums on the tensor cores (spmm_tc.cu): out[r, 0:width) = sum over the heavy-tile edges

@@ -55,12 +55,10 @@ def test_tiles_vs_oracle(P, name, tmin, tf, gather):
 
 @pytest.mark.parametrize("gather", ["f32", "bf16"])
 @pytest.mark.parametrize("model", ["sage", "gcn"])
-@pytest.mark.parametrize("concurrent", ["1", "0"])
-def test_tiles_light_mix(P, gather, model, concurrent, monkeypatch):
-    """A quarter of the edges light (tile_min 200): the light gather on the side stream (raw partial
-    sums) concurrent with the tile kernel, then the combining pass (self loop, row scale, dropout mask
-    epilogues), or both sequential (PGCN_TILE_CONCURRENT=0); both tiers, GraphSAGE and GCN-sym."""
-    monkeypatch.setenv("PGCN_TILE_CONCURRENT", concurrent)
+def test_tiles_light_mix(P, gather, model):
+    """A quarter of the edges light (tile_min 200): the gather pass adds the light edges to the tile
+    sums and applies the epilogues (self loop and row scale of GCN-sym, dropout mask of the
+    transposed pass); both tiers, GraphSAGE and GCN-sym, both aggregation orders."""
     g, widths, loss, n_parts = case("dense")
     tol = 1e-4 if gather == "f32" else 2e-2
     params0 = glorot_params(widths, 3, model=model)
@@ -70,7 +68,7 @@ def test_tiles_light_mix(P, gather, model, concurrent, monkeypatch):
         gpu, _ = run_gpu(P, g, widths, n_parts, 3, params0, **kw)
         cfg = ModelCfg(widths=widths, dropout=0.3, lr=0.5, opt="sgd", loss=loss, model=model)
         ora = oracle_run(gpu, g, n_parts, params0, cfg, 3, tol=tol, mode="pipe", smooth_f=True)
-        check_against_oracle(gpu, ora, 3, n_parts, tol=tol, what=f"light-mix {gather} {model} tf{tf} c{concurrent}")
+        check_against_oracle(gpu, ora, 3, n_parts, tol=tol, what=f"light-mix {gather} {model} tf{tf}")
 
 
 @pytest.mark.parametrize("tf", [True, False])
