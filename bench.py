@@ -40,6 +40,9 @@ def parse():
                     help="bf16: the bf16 gather tier (SpMM tables rounded to bf16, 2e-2 tier; SURVEY N1(iv))")
     ap.add_argument("--model", default="sage", choices=["sage", "gcn"],
                     help="GraphSAGE-mean (the paper's benchmark model) or GCN-sym (App. A.1, SURVEY N3)")
+    ap.add_argument("--no-tiles", action="store_true",
+                    help="gather-only aggregation (default: dense 128x64 tiles of P_i / P_i^T on the tensor cores "
+                         "where they hold >= 25 %% of the edges; DESIGN.md 'Tensor-core tiles')")
     ap.add_argument("--no-train-sparse", action="store_true",
                     help="compute the last layer on every row (default: only on train rows, SURVEY N1(ii); exact)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -256,7 +259,7 @@ def main():
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
                            n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
-                           train_sparse=not args.no_train_sparse)
+                           train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
@@ -382,15 +385,18 @@ def main():
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     elif name.startswith("spmm"):
-        # Per-edge gathers are L2 hits (Reddit: 83 % L2 hit rate): bound = L2, peak = measured L2
-        # streaming read; the contract's HBM view (same algorithmic bytes / measured HBM copy) beside it.
+        # L2-served aggregation: bound = L2, peak = measured L2 streaming read.  Algorithmic bytes per
+        # launch (engine Scope): per-edge gather model s*F*nnz on the gather path; on the
+        # tensor-core tile path what that algorithm moves instead -- heavy-tile table rows (hi/lo) and
+        # bitmasks per tile, light-edge gathers, the hi/lo split, tile-sum write + re-read (DESIGN.md
+        # "Tensor-core tiles").  The contract's HBM view (same bytes / measured HBM copy) beside it.
         ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
         l2 = l2_ceilings(pgcn, torch, views[0]["row_ptr"], int(views[0]["n_inner"]), stream)
         roof = {"kernel": name, "bound": "l2", "achieved": ach, "peak": l2["l2_read_GBps"], "unit": "GB/s",
                 "frac": ach / l2["l2_read_GBps"], "peak_source": "measured live: L2 streaming read, 64 MB",
                 "gather_ceiling_GBps": {"604": l2["gather_604_GBps"], "256": l2["gather_256_GBps"]},
                 "hbm_view": {"peak": pk["hbm_gbs"], "frac": ach / pk["hbm_gbs"],
-                             "note": "algorithmic gather bytes over measured HBM copy peak; > 1 because gathers hit L2"}}
+                             "note": "same algorithmic bytes over the measured HBM copy peak; > 1 means L2-served"}}
     else:
         ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -430,6 +436,7 @@ def main():
                       "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
                       ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,
                       "gather": args.gather, "train_sparse_last_layer": not args.no_train_sparse,
+                      "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "breakdown": breakdown, "loss": loss_v,

@@ -197,6 +197,22 @@ int64_t param_count(const pgcn_config* c) {
   return P;
 }
 
+// Algorithmic bytes of an aggregation launch on the tile path (tiles.h / spmm_tc.cu), replacing the
+// per-edge gather term s F nnz of the gather model by what this algorithm moves: the
+// table's split into bf16 hi/lo (fp32 tier: read 4F, write 4F per table row; the bf16 tier's rounding
+// pass is counted by the caller), per heavy tile and n-tile the 64 table rows (hi + lo: 4F per row;
+// bf16: 2F) and the 1 KB bitmask, the tile-sum write and its re-read by the light pass, and the light
+// gathers themselves (s F bytes per light edge).  Bound: L2 (the table slices are L2-resident).
+double tile_path_bytes(const pgcn_ctx* C, const TileDev& T, double F, double n_table) {
+  const double Fp = (double)round_up((int64_t)F, 8);
+  const double row = C->cfg.gather ? 2.0 * Fp : 4.0 * Fp;
+  const double bn = C->cfg.gather ? 256.0 : 128.0;
+  const double n_nt = std::ceil(F / bn);
+  const double split = C->cfg.gather ? 0.0 : 8.0 * Fp * n_table;
+  return split + (double)T.n_tiles * (64.0 * row + 1024.0 * n_nt) + 8.0 * F * (double)T.n_rows +
+         (double)T.nnz_light * row;  // (the caller counts 4 bytes of column index per edge)
+}
+
 // Lays out every buffer (dry run when A.base == nullptr).
 int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local, Arena& A) {
   const int L = C->L;
@@ -789,6 +805,12 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const int32_t* rl = sp ? p.tr_list : nullptr;
     const int64_t nr = sp ? p.n_tr : p.n_in;
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
+    // gathered bytes of e edges at width F: per-edge model, or the tile path's traffic when it runs
+    auto sgat = [&](double F, double e, int64_t nv) {
+      const TileDev* T = p.tiles(0);
+      if (T && !rl && nv >= p.n_all) return tile_path_bytes(C, *T, F, (double)nv) + gat(F, e - nz);
+      return gat(F, e);
+    };
     // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13)
     int64_t n_valid = p.n_all;
     if (C->nccl) {
@@ -849,7 +871,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                           ldo, nullptr, nullptr, 0, 0, bf))
             return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
         }
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, (nz + nr)) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fo, (nz + nr), n_valid) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
                  p.n_all, p.G16, rl,
@@ -857,7 +879,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         continue;
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, (nz + nr)) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fi, (nz + nr), n_valid) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fi * nr);
         spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
@@ -877,7 +899,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, gat(Fo, nz) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
+        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fo, nz, n_valid) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
         spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
                  p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
@@ -891,7 +913,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       continue;
     }
     {
-      Scope sc(C, PGCN_K_SPMM_FWD, gat(Fi, nz) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
+      Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fi, nz, n_valid) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
     }
@@ -958,6 +980,11 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const int64_t* trp = sp ? p.trp_tr : p.trp;
     const int32_t* tcol = sp ? p.tcol_tr : p.tcol;
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
+    auto sgat = [&](double F, double e) {  // see the forward: per-edge model or the tile path's traffic
+      const TileDev* T = p.tiles(1);
+      if (T && !sp) return tile_path_bytes(C, *T, F, (double)p.n_in) + gat(F, e - nz);
+      return gat(F, e);
+    };
     const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
     if (C->gcn) {
       // GCN-sym backward (App. A.1 PAPER.md:651-657 with P = S (A + I) S, S = diag(d~^-1/2), R26)
@@ -965,7 +992,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // Q = (A + I)^T (S M) over inner + boundary rows; G = [D'^T Q ; colsum M]; J = mask o s o S (Q W^T)
         const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
         {
-          Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, (nz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
+          Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fo, (nz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                            8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all);
           scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
           DropSpec none{};
@@ -1001,7 +1028,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         }
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
-        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
+        Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all);
         spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
                  C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
@@ -1013,7 +1040,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
       const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
       {
-        Scope sc(C, PGCN_K_SPMM_BWD, gat(Fo, nz) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
+        Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fo, nz) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
                                          4.0 * Fo * p.n_all);
         scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
         DropSpec none{};
@@ -1058,7 +1085,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
         }
       }
-      Scope sc(C, PGCN_K_SPMM_BWD, gat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
+      Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
                drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);

@@ -15,7 +15,8 @@
 // none); the gather SpMM then adds the light edges on top (its `addend`), applies inv_deg, the
 // self term, bias / ReLU or the dropout mask -- so the result is the same sum, reassociated.
 //
-// Roles (320 threads): warp 0 TMA producer (B boxes + the tile's 1 KB bitmask by bulk copy), warp 1
+// Roles (320 threads): warp 0 TMA producer (the tile's 1 KB bitmask by bulk copy on its own barrier,
+// so A can be built while B is in flight; then the B boxes), warp 1
 // TMEM owner + single-thread MMA issuer, warps 2-5 builders (bitmask -> A tile in the UMMA K-major
 // SW128 layout, shared-space stores), warps 6-9 epilogue (tcgen05.ld -> float4 stores).  Work list:
 // (row block, n-tile) items in the host's descending-tile-count order, strided over a persistent
@@ -53,6 +54,7 @@ struct Params {
   float* out;
   int64_t n_rows, ld_out;
   int n_rb, n_nt, BN, stages, tmem_cols, width;
+  int dbg;  // dev knob PGCN_TC_SPMM_DBG (bottleneck probes, wrong results): 1 skip B loads, 2 skip MMAs
 };
 
 // Per-stage geometry (one stage = one 128 x 64 tile): A 128 x 64 bf16 (16 KB) | NT tables x (64 rows
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
   uint64_t* empty = bars + 2 * S;
   uint64_t* tfull = bars + 3 * S;
   uint64_t* tempty = bars + 3 * S + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* mfull = bars + 3 * S + 4;  // the tile's bitmask only: the builders need not wait for B
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * S + 4);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n_items = p.n_rb * p.n_nt;
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], kBuildThreads);
       mbar_init(&empty[s], 1);
+      mbar_init(&mfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = NT * tb + BM * 8;
+      const uint32_t tx = (p.dbg & 1) ? 0u : NT * tb;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
         const int n0 = (it % p.n_nt) * p.BN;
@@ -154,18 +158,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           const int row0 = p.tile_col[k] * 64;
           mbar_wait(&empty[s], ph ^ 1, 11);
           uint8_t* st = smem + (size_t)s * sb;
-          mbar_expect_tx(&full[s], tx);
-          for (int t = 0; t < NT; ++t)
-            for (int kh = 0; kh < 2; ++kh)  // two k-halves of 32 rows, natom SW128 atoms of 64 x 32 each
-              for (int j = 0; j < natom; ++j)
-                tma_load_2d(st + ab + t * tb + (kh * natom + j) * 4096, &p.map_b[t], &full[s], n0 + 64 * j,
-                            row0 + 32 * kh);
+          if (!TS) {  // SS mode: the builders read the bitmask from shared memory
+          mbar_expect_tx(&mfull[s], BM * 8);
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                   smem_u32(st + mask_off)),
               "l"(reinterpret_cast<uint64_t>(p.mask + (size_t)k * BM)), "r"((uint32_t)(BM * 8)),
-              "r"(smem_u32(&full[s]))
+              "r"(smem_u32(&mfull[s]))
               : "memory");
+          }
+          mbar_expect_tx(&full[s], tx);
+          if (tx)
+            for (int t = 0; t < NT; ++t)
+              for (int kh = 0; kh < 2; ++kh)  // two k-halves of 32 rows, natom SW128 atoms of 64 x 32 each
+                for (int j = 0; j < natom; ++j)
+                  tma_load_2d(st + ab + t * tb + (kh * natom + j) * 4096, &p.map_b[t], &full[s], n0 + 64 * j,
+                              row0 + 32 * kh);
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -189,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
         const int nst = p.rb_ptr[rb + 1] - p.rb_ptr[rb];
         for (int i = 0; i < nst; ++i) {
           mbar_wait(&conv[s], ph, 13);
+          mbar_wait(&full[s], ph, 16);
           tc_fence_after();
           const uint32_t A = sbase + (uint32_t)s * sb;
           const uint32_t ta = tmem_base + (uint32_t)(2 * p.BN + 32 * s);
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
               const uint64_t b = make_desc(A + boff + t * tb, 4096, 1024);
+              if (p.dbg & 2) continue;
               if (TS) mma_bf16_ts(d, ta + 8 * kk, b, idesc, accum);
               else mma_bf16(d, a, b, idesc, accum);
               accum = 1u;
@@ -217,26 +227,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
     const int ct = threadIdx.x - 64;
     int s = 0;
     uint32_t ph = 0;
+    if (TS) {
+      // A in TMEM: each thread owns row r = 32 (warp % 4) + lane and reads that row's 64-bit mask word
+      // straight from global memory, two tiles ahead, so the build of stage s waits only for the MMAs
+      // that last read A[s] (empty[s]) -- not for any copy.  64 bits -> 32 columns of bf16 pairs.
+      const int q = warp & 3, r = 32 * q + lane;
+      int nit = blockIdx.x, kk = 0, ke = 0;
+      auto next_tile = [&]() -> int {  // this CTA's (item, tile) sequence, as the producer / MMA walk it
+        while (kk >= ke) {
+          if (nit >= n_items) return -1;
+          const int rb = p.order ? p.order[nit / p.n_nt] : nit / p.n_nt;
+          kk = p.rb_ptr[rb];
+          ke = p.rb_ptr[rb + 1];
+          nit += gridDim.x;
+        }
+        return kk++;
+      };
+      auto load_mask = [&](int t) -> uint64_t { return t >= 0 ? __ldg(p.mask + (size_t)t * BM + r) : 0ull; };
+      int t0 = next_tile(), t1 = next_tile();
+      uint64_t m0 = load_mask(t0), m1 = load_mask(t1);
+      const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * p.BN);
+      while (t0 >= 0) {
+        const int t2 = next_tile();
+        const uint64_t m2 = load_mask(t2);
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          v[c] = (((m0 >> (2 * c)) & 1ull) ? 0x3F80u : 0u) | (((m0 >> (2 * c + 1)) & 1ull) ? 0x3F800000u : 0u);
+        mbar_wait(&empty[s], ph ^ 1, 14);
+        tc_fence_after();
+        tmem_st32(trow + (uint32_t)(32 * s), v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&conv[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+        t0 = t1;
+        m0 = m1;
+        t1 = t2;
+        m1 = m2;
+      }
+    } else
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int rb = p.order ? p.order[it / p.n_nt] : it / p.n_nt;
       const int nt = p.rb_ptr[rb + 1] - p.rb_ptr[rb];
       for (int k = 0; k < nt; ++k) {
-        mbar_wait(&full[s], ph, 14);
+        mbar_wait(&mfull[s], ph, 14);
         const uint32_t st = sbase + (uint32_t)s * sb;
-        if (TS) {  // this thread's row r = 32 (warp % 4) + lane: 64 bits -> 32 columns of bf16 pairs
-          const int q = warp & 3, r = 32 * q + lane;
-          const uint64_t m = lds64(st + mask_off + r * 8);
-          uint32_t v[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            v[c] = (((m >> (2 * c)) & 1ull) ? 0x3F80u : 0u) | (((m >> (2 * c + 1)) & 1ull) ? 0x3F800000u : 0u);
-          tmem_st32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * p.BN + 32 * s), v);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-          mbar_arrive(&conv[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
-          continue;
-        }
         // row r = 128 bytes (64 bf16 of k); 16-byte chunk j (k = 8j..8j+7) at r*128 + ((j ^ (r&7)) << 4)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -327,6 +363,12 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
     env_order = e ? std::atoi(e) : 1;
   }
   p.order = env_order ? T.order : nullptr;
+  static int env_dbg = -1;
+  if (env_dbg < 0) {
+    const char* e = std::getenv("PGCN_TC_SPMM_DBG");
+    env_dbg = e ? std::atoi(e) : 0;
+  }
+  p.dbg = env_dbg;
   p.tile_col = T.tile_col;
   p.mask = T.mask;
   p.out = out;
@@ -353,7 +395,7 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   }
   p.stages = S;
   p.tmem_cols = TS ? 512 : tc_tmem_cols(p.BN);
-  const size_t smem = 1024 + (size_t)p.stages * stage + (3 * p.stages + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
   if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   static bool attr = false;
