@@ -54,7 +54,8 @@ struct Params {
   float* out;
   int64_t n_rows, ld_out;
   int n_rb, n_nt, BN, stages, tmem_cols, width;
-  int dbg;  // dev knob PGCN_TC_SPMM_DBG (bottleneck probes, wrong results): 1 skip B loads, 2 skip MMAs
+  int nacc;  // TMEM accumulator buffers: 2 (epilogue overlaps the next item) or 1 (two CTAs per SM)
+  int dbg;   // dev knob PGCN_TC_SPMM_DBG (bottleneck probes, wrong results): 1 skip B loads, 2 skip MMAs
 };
 
 // Per-stage geometry (one stage = one 128 x 64 tile): A 128 x 64 bf16 (16 KB) | NT tables x (64 rows
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           mbar_wait(&full[s], ph, 16);
           tc_fence_after();
           const uint32_t A = sbase + (uint32_t)s * sb;
-          const uint32_t ta = tmem_base + (uint32_t)(2 * p.BN + 32 * s);
+          const uint32_t ta = tmem_base + (uint32_t)(p.nacc * p.BN + 32 * s);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // k-steps of 16: A 32 bytes (SS) / 8 columns (TS) apart;
                                             // B 16-row steps in k-half kk/2
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           if (++s == S) { s = 0; ph ^= 1; }
         }
         tc_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+        if (++acc == p.nacc) { acc = 0; acc_ph ^= 1; }
       }
     }
   } else if (warp < 2 + kBuildWarps) {
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
       auto load_mask = [&](int t) -> uint64_t { return t >= 0 ? __ldg(p.mask + (size_t)t * BM + r) : 0ull; };
       int t0 = next_tile(), t1 = next_tile();
       uint64_t m0 = load_mask(t0), m1 = load_mask(t1);
-      const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * p.BN);
+      const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(p.nacc * p.BN);
       while (t0 >= 0) {
         const int t2 = next_tile();
         const uint64_t m2 = load_mask(t2);
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      if (++acc == p.nacc) { acc = 0; acc_ph ^= 1; }
     }
   }
   tc_fence_before();
@@ -375,26 +376,34 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.n_rows = T.n_rows;
   p.ld_out = ld_out;
   p.width = (int)width;
-  static int env_ts = -1;  // dev knob PGCN_TC_SPMM_TS: 0 forces SS mode (A in shared memory)
-  if (env_ts < 0) {
+  static int env_ts = -1, env_ctas = -1;  // dev knobs PGCN_TC_SPMM_TS (0: A in shared memory),
+  if (env_ts < 0) {                        // PGCN_TC_SPMM_CTAS (2: two CTAs per SM)
     const char* e = std::getenv("PGCN_TC_SPMM_TS");
     env_ts = e ? std::atoi(e) : 1;
+    e = std::getenv("PGCN_TC_SPMM_CTAS");
+    env_ctas = e ? std::atoi(e) : 1;
   }
-  int TS = env_ts && 2 * p.BN + 32 * 2 <= 512;
+  // Two CTAs per SM: one accumulator each, <= 110 KB of stages, <= 256 TMEM columns (TS mode only).
+  const int ctas = (env_ctas == 2 && env_ts) ? 2 : 1;
+  p.nacc = ctas == 2 ? 1 : 2;
+  const int smem_budget = ctas == 2 ? 104 * 1024 : 210 * 1024;
+  const int tmem_budget = ctas == 2 ? 256 : 512;
+  int TS = env_ts && p.nacc * p.BN + 32 * 2 <= tmem_budget;
   uint32_t stage = stage_bytes(NT, p.BN, TS);
-  int S = (int)((210 * 1024) / stage);
+  int S = (int)(smem_budget / stage);
   S = S > 8 ? 8 : (S < 2 ? 2 : S);
   if (TS) {
-    while (S > 2 && 2 * p.BN + 32 * S > 512) --S;
-    if (2 * p.BN + 32 * S > 512) TS = 0;
+    while (S > 2 && p.nacc * p.BN + 32 * S > tmem_budget) --S;
+    if (p.nacc * p.BN + 32 * S > tmem_budget) TS = 0;
   }
   if (!TS) {
+    p.nacc = 2;
     stage = stage_bytes(NT, p.BN, 0);
     S = (int)((210 * 1024) / stage);
     S = S > 8 ? 8 : (S < 2 ? 2 : S);
   }
   p.stages = S;
-  p.tmem_cols = TS ? 512 : tc_tmem_cols(p.BN);
+  p.tmem_cols = TS ? (ctas == 2 ? 256 : 512) : tc_tmem_cols(p.BN);
   const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
   if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
@@ -407,7 +416,8 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
     attr = true;
   }
   const int n_items = p.n_rb * p.n_nt;
-  const int grid = n_items < 148 ? n_items : 148;
+  const int grid_cap = (TS && ctas == 2) ? 2 * 148 : 148;
+  const int grid = n_items < grid_cap ? n_items : grid_cap;
   if (NT == 2) {
     if (TS) k_spmm_tc<2, 1><<<grid, kThreads, smem, L.s>>>(p);
     else k_spmm_tc<2, 0><<<grid, kThreads, smem, L.s>>>(p);

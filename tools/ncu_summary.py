@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KIND = [("k_spmm_tc", "spmm_tc"), ("k_spmm_fwd", "spmm_fwd"), ("k_spmm_bwd", "spmm_bwd"), ("k_umma_gemm", "gemm_tc"), ("k_gemm_fwd", "gemm_fwd"),
+KIND = [("k_spmm_tc", "spmm_tc"), ("k_split_bf16", "split_bf16"), ("k_to_bf16", "to_bf16"), ("k_spmm_fwd", "spmm_fwd"), ("k_spmm_bwd", "spmm_bwd"), ("k_umma_gemm", "gemm_tc"), ("k_gemm_fwd", "gemm_fwd"),
         ("k_gemm_dw", "gemm_dw"), ("k_gemm_da", "gemm_da"), ("k_dropout", "dropout"), ("k_gather", "gather"),
         ("k_grad_reduce", "grad_reduce"), ("k_loss", "loss"), ("k_opt", "update"), ("k_sum_grads", "update"),
         ("k_wprep", "wprep"), ("k_colsum", "colsum"), ("k_split_reduce", "split_reduce"), ("k_reduce_sum", "reduce_sum")]
@@ -60,6 +60,37 @@ def launches(path):
         if d["Metric Name"] == "gpu__time_duration.sum":
             cnt[k] += 1
     return agg, cnt
+
+
+def scope_traffic(path):
+    """DRAM bytes per aggregation *scope* (what bench.py times as spmm_fwd / spmm_bwd): the table
+    rounding / split and tensor-core tile launches that precede a gather launch belong to it."""
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        if d["Metric Name"] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            continue
+        e = per.setdefault(d["ID"], [kind_of(d["Kernel Name"]), 0.0])
+        try:
+            e[1] += float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
+        except ValueError:
+            pass
+    pending, tot, n = 0.0, collections.defaultdict(float), collections.Counter()
+    for kind, b in per.values():
+        if kind in ("spmm_tc", "split_bf16", "to_bf16"):
+            pending += b
+        elif kind in ("spmm_fwd", "spmm_bwd"):
+            tot[kind] += b + pending
+            n[kind] += 1
+            pending = 0.0
+    return {k: tot[k] / n[k] for k in tot}
 
 
 def raw(rep):
@@ -114,6 +145,7 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     cur = json.load(open(tpath)) if os.path.exists(tpath) else {}
     cur.update({k: v for k, v in traffic.items()})
+    cur.update(scope_traffic(lcsv))  # spmm_fwd / spmm_bwd: whole aggregation scope (tile path incl.)
     cur["_source"] = "%s: ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (mean over launches)" % tag
     json.dump(cur, open(tpath, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
