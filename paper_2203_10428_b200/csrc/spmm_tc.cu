@@ -377,33 +377,33 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.ld_out = ld_out;
   p.width = (int)width;
   static int env_ts = -1, env_ctas = -1;  // dev knobs PGCN_TC_SPMM_TS (0: A in shared memory),
-  if (env_ts < 0) {                        // PGCN_TC_SPMM_CTAS (2: two CTAs per SM)
+  if (env_ts < 0) {                        // PGCN_TC_SPMM_CTAS (CTAs per SM, 1 or 2; default 2)
     const char* e = std::getenv("PGCN_TC_SPMM_TS");
     env_ts = e ? std::atoi(e) : 1;
     e = std::getenv("PGCN_TC_SPMM_CTAS");
-    env_ctas = e ? std::atoi(e) : 1;
+    env_ctas = e ? std::atoi(e) : 2;
   }
-  // Two CTAs per SM: one accumulator each, <= 110 KB of stages, <= 256 TMEM columns (TS mode only).
-  const int ctas = (env_ctas == 2 && env_ts) ? 2 : 1;
-  p.nacc = ctas == 2 ? 1 : 2;
-  const int smem_budget = ctas == 2 ? 104 * 1024 : 210 * 1024;
-  const int tmem_budget = ctas == 2 ? 256 : 512;
-  int TS = env_ts && p.nacc * p.BN + 32 * 2 <= tmem_budget;
-  uint32_t stage = stage_bytes(NT, p.BN, TS);
-  int S = (int)(smem_budget / stage);
-  S = S > 8 ? 8 : (S < 2 ? 2 : S);
-  if (TS) {
-    while (S > 2 && p.nacc * p.BN + 32 * S > tmem_budget) --S;
-    if (p.nacc * p.BN + 32 * S > tmem_budget) TS = 0;
+  // The kernel is latency-bound (one chain TMA -> build -> MMA per stage), so two CTAs per SM (two
+  // independent pipelines sharing the tensor core) beat one CTA with twice the stages: 2 CTAs x
+  // (<= 104 KB of stages, one TMEM accumulator, <= 256 TMEM columns).  A in TMEM (TS) when the
+  // accumulator leaves room for >= 2 A buffers of 32 columns, else A in shared memory (SS).
+  int ctas = env_ctas == 1 ? 1 : 2, TS = 0, S = 0, smem_budget = 0, tmem_budget = 0;
+  uint32_t stage = 0;
+  for (;; ctas = 1) {  // two stages must fit next to a second CTA, else one CTA per SM
+    smem_budget = ctas == 2 ? 104 * 1024 : 210 * 1024;
+    tmem_budget = ctas == 2 ? 256 : 512;
+    p.nacc = ctas == 2 ? 1 : 2;
+    TS = env_ts && p.nacc * p.BN + 32 * 2 <= tmem_budget;
+    stage = stage_bytes(NT, p.BN, TS);
+    S = (int)(smem_budget / stage);
+    S = S > 8 ? 8 : S;
+    if (TS)
+      while (S > 2 && p.nacc * p.BN + 32 * S > tmem_budget) --S;
+    if (S >= 2 || ctas == 1) break;
   }
-  if (!TS) {
-    p.nacc = 2;
-    stage = stage_bytes(NT, p.BN, 0);
-    S = (int)((210 * 1024) / stage);
-    S = S > 8 ? 8 : (S < 2 ? 2 : S);
-  }
+  if (S < 2) S = 2;
   p.stages = S;
-  p.tmem_cols = TS ? (ctas == 2 ? 256 : 512) : tc_tmem_cols(p.BN);
+  p.tmem_cols = tmem_budget == 256 ? 256 : (TS ? 512 : tc_tmem_cols(p.BN));
   const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
   if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
   if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
@@ -416,7 +416,7 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
     attr = true;
   }
   const int n_items = p.n_rb * p.n_nt;
-  const int grid_cap = (TS && ctas == 2) ? 2 * 148 : 148;
+  const int grid_cap = ctas * 148;
   const int grid = n_items < grid_cap ? n_items : grid_cap;
   if (NT == 2) {
     if (TS) k_spmm_tc<2, 1><<<grid, kThreads, smem, L.s>>>(p);
