@@ -54,7 +54,9 @@ struct Params {
   float* out;
   int64_t n_rows, ld_out;
   int n_rb, n_nt, BN, stages, tmem_cols, width;
-  int nacc;  // TMEM accumulator buffers: 2 (epilogue overlaps the next item) or 1 (two CTAs per SM)
+  int nacc;   // TMEM accumulator buffers: 2 (epilogue overlaps the next item) or 1 (two CTAs per SM)
+  int box64;  // B boxes of 64 rows (one SW128 atom column of 8 KB per 64 table columns) instead of two
+              // k-halves of 32-row boxes
   int dbg;   // dev knob PGCN_TC_SPMM_DBG (bottleneck probes, wrong results): 1 skip B loads, 2 skip MMAs
 };
 
@@ -169,7 +171,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
               : "memory");
           }
           mbar_expect_tx(&full[s], tx);
-          if (tx)
+          if (tx && p.box64)
+            for (int t = 0; t < NT; ++t)
+              for (int j = 0; j < natom; ++j)  // natom SW128 atoms of 64 columns x 64 rows (8 KB)
+                tma_load_2d(st + ab + t * tb + j * 8192, &p.map_b[t], &full[s], n0 + 64 * j, row0);
+          else if (tx)
             for (int t = 0; t < NT; ++t)
               for (int kh = 0; kh < 2; ++kh)  // two k-halves of 32 rows, natom SW128 atoms of 64 x 32 each
                 for (int j = 0; j < natom; ++j)
@@ -206,10 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
           for (int kk = 0; kk < 4; ++kk) {  // k-steps of 16: A 32 bytes (SS) / 8 columns (TS) apart;
                                             // B 16-row steps in k-half kk/2
             const uint64_t a = make_desc(A + kk * 32, 16, 1024);
-            const uint32_t boff = ab + (uint32_t)((kk >> 1) * natom * 4096 + (kk & 1) * 2048);
+            const uint32_t boff =
+                ab + (p.box64 ? (uint32_t)(kk * 2048) : (uint32_t)((kk >> 1) * natom * 4096 + (kk & 1) * 2048));
+            const uint32_t lbo = p.box64 ? 8192u : 4096u;  // MN-direction atom stride
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-              const uint64_t b = make_desc(A + boff + t * tb, 4096, 1024);
+              const uint64_t b = make_desc(A + boff + t * tb, lbo, 1024);
               if (p.dbg & 2) continue;
               if (TS) mma_bf16_ts(d, ta + 8 * kk, b, idesc, accum);
               else mma_bf16(d, a, b, idesc, accum);
@@ -405,8 +413,15 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.stages = S;
   p.tmem_cols = tmem_budget == 256 ? 256 : (TS ? 512 : tc_tmem_cols(p.BN));
   const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
-  if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
-  if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, 32)) return -1;
+  static int env_box = -1;  // dev knob PGCN_TC_SPMM_BOX64 (0: 32-row boxes)
+  if (env_box < 0) {
+    const char* e = std::getenv("PGCN_TC_SPMM_BOX64");
+    env_box = e ? std::atoi(e) : 0;
+  }
+  p.box64 = env_box ? 1 : 0;
+  const int box_rows = p.box64 ? 64 : 32;
+  if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, box_rows)) return -1;
+  if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, box_rows)) return -1;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_spmm_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
