@@ -413,10 +413,10 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.stages = S;
   p.tmem_cols = tmem_budget == 256 ? 256 : (TS ? 512 : tc_tmem_cols(p.BN));
   const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
-  static int env_box = -1;  // dev knob PGCN_TC_SPMM_BOX64 (0: 32-row boxes)
+  static int env_box = -1;  // dev knob PGCN_TC_SPMM_BOX64 (0: two 32-row boxes per atom column)
   if (env_box < 0) {
     const char* e = std::getenv("PGCN_TC_SPMM_BOX64");
-    env_box = e ? std::atoi(e) : 0;
+    env_box = e ? std::atoi(e) : 1;
   }
   p.box64 = env_box ? 1 : 0;
   const int box_rows = p.box64 ? 64 : 32;
