@@ -399,6 +399,8 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   for (int l = 1; l <= C->L; ++l) {
     const int64_t fi = C->ld[l - 1], fo = C->ld[l];
     C->tf[l] = (cfg->transform_first == 1 && cfg->gemm != 2) ? (l == 1 ? 2 * fo < fi : fo < fi) : 0;
+    if (const char* m = std::getenv("PGCN_TF_OFF"))  // dev knob: bitmask of layers forced aggregate-first
+      if ((std::atoi(m) >> l) & 1) C->tf[l] = 0;
   }
   C->P = C->woff[C->L + 1];
   return PGCN_OK;
