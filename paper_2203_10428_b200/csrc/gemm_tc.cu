@@ -580,20 +580,10 @@ __global__ void k_colsum(const float* __restrict__ Mg, int64_t M, int64_t ld, in
   __shared__ float sh[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = r0 + rps < M ? r0 + rps : M;
-  // four independent partial sums (rows r, r + 8, r + 16, r + 24 of each 32-row step) keep four
-  // loads in flight per thread; combined in a fixed order (deterministic)
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  if (n < N) {
-    int64_t r = r0 + threadIdx.y;
-    for (; r + 24 < r1; r += 32) {
-      a0 += Mg[r * ld + n];
-      a1 += Mg[(r + 8) * ld + n];
-      a2 += Mg[(r + 16) * ld + n];
-      a3 += Mg[(r + 24) * ld + n];
-    }
-    for (; r < r1; r += 8) a0 += Mg[r * ld + n];
-  }
-  sh[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
+  float a = 0.f;
+  if (n < N)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) a += Mg[r * ld + n];
+  sh[threadIdx.y][threadIdx.x] = a;
   __syncthreads();
   if (threadIdx.y == 0 && n < N) {
     float s = 0.f;
