@@ -70,6 +70,12 @@ struct PartCtx {
   int64_t* trp_tr = nullptr;
   int32_t* tcol_tr = nullptr;
   int64_t n_tr = 0, nnz_tr = 0;
+  // compact train rows of an aggregate-first GraphSAGE last layer (pgcn_ctx::cl): row k = tr_list[k]
+  int32_t* tr_pos = nullptr;   // [n_in] position of inner row v in tr_list, or -1
+  float* Dtr = nullptr;        // [n_tr x ld_{L-1}] layer-L input rows of the train rows (aliases dA)
+  float* Ytr = nullptr;        // [n_tr x ld_L] logits of the train rows (aliases M)
+  void* lab_tr = nullptr;      // labels of the train rows
+  float* invdeg_tr = nullptr;  // [n_tr]
   // dense-tile decompositions (cfg.spmm_tiles): [0] P_i (forward), [1] P_i^T (transposed)
   const TileSet* ts[2] = {nullptr, nullptr};
   TileDev td[2];
@@ -120,6 +126,10 @@ struct pgcn_ctx {
   // N1 transform-before-aggregate per layer: Y = P(D W_neigh) + D W_self + b instead of (PD) W_neigh
   int tf[PGCN_MAX_LAYERS + 1] = {};
   int gcn = 0, ns = 2;  // cfg.model == 1 (GCN-sym, R26); weight row segments
+  // N1(ii) with an aggregate-first GraphSAGE last layer on the tensor cores: the whole last layer (SpMM
+  // output, [Z | D] W, loss, dW, dA) runs on compact train rows; only the transposed aggregation
+  // scatters back to every local row.  (papers-shaped: 1.1 % train rows.)
+  int cl = 0;
   int64_t depth = 1;    // pipeline depth s (R27): an exchange posted at t is consumed at t + s
   float* part_loss = nullptr;
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
@@ -296,6 +306,13 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       p.tr_counts = A.take<int64_t>(p.n_all + 1);
       p.trp_tr = A.take<int64_t>(p.n_all + 1);
       p.tcol_tr = A.take<int32_t>(p.nnz);
+      if (C->cl) {  // Y_tr lives in M (free until the loss, which turns it into M_tr in place); D_tr in dA
+        p.tr_pos = A.take<int32_t>(p.n_in);
+        p.Ytr = p.M;
+        p.Dtr = (p.dA && ld_da >= C->ld[L - 1]) ? p.dA : A.take<float>(p.n_in * C->ld[L - 1]);
+        p.lab_tr = C->cfg.loss == 0 ? (void*)A.take<int32_t>(p.n_in) : (void*)A.take<uint8_t>(p.n_in * C->F[L]);
+        p.invdeg_tr = A.take<float>(p.n_in);
+      }
       const size_t tb = train_rows_tmp_bytes(p.n_in, p.n_all);
       if ((int64_t)tb > C->sp_tmp_bytes) C->sp_tmp_bytes = (int64_t)tb;
     }
@@ -402,6 +419,7 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
     if (const char* m = std::getenv("PGCN_TF_OFF"))  // dev knob: bitmask of layers forced aggregate-first
       if ((std::atoi(m) >> l) & 1) C->tf[l] = 0;
   }
+  C->cl = cfg->train_sparse && !C->tf[C->L] && cfg->model == 0 && cfg->gemm != 2;
   C->P = C->woff[C->L + 1];
   return PGCN_OK;
 }
@@ -767,6 +785,12 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
     cudaStreamSynchronize(C->s);  // sizes of the last layer's launches (documented: synchronous here)
     p.n_tr = h[0];
     p.nnz_tr = h[1];
+    if (C->cl) {  // compact train rows: positions, P_i^T restricted columns -> positions, labels, inv_deg
+      compact_train_setup(Lk, p.tr_list, p.n_tr, p.n_in, p.tr_pos, p.tcol_tr, p.nnz_tr);
+      const int64_t lw = C->cfg.loss == 0 ? (int64_t)sizeof(int32_t) : C->F[C->L];
+      gather_bytes(Lk, p.labels, p.tr_list, p.n_tr, lw, p.lab_tr);
+      gather_bytes(Lk, p.inv_deg, p.tr_list, p.n_tr, (int64_t)sizeof(float), p.invdeg_tr);
+    }
   }
   return check_cuda(C, "pgcn_set_inputs");
 }
@@ -914,10 +938,26 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       continue;
     }
+    const bool cl = C->cl && l == C->L;  // compact train rows (pgcn_ctx::cl)
     {
       Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fi, nz, n_valid) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0), p.T16);
+                 (int64_t)nz, p.tiles(0), p.T16, cl);
+    }
+    if (cl) {  // Z rows are compact; gather the train rows of D, Y_tr = [Z | D_tr] W + b, logits scattered
+      SegTable tab{};
+      tab.base[0] = D;
+      tab.off[0] = 0;
+      tab.off[1] = p.n_tr;
+      tab.n_seg = 1;
+      Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_tr * (3 * Fi + 2 * Fo) + 4.0 * (2 * Fi + 1) * Fo,
+               2.0 * p.n_tr * (2 * Fi + 1) * Fo);
+      gather_rows(Lk, tab, p.tr_list, p.n_tr, ldi, p.Dtr, nullptr, 0.f, 0, 0);
+      if (p.n_tr > 0 && gemm_fwd_tc(Lk, p.Z[l], p.Dtr, ldi, p.n_tr, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], bias,
+                                    C->F[l], p.Ytr, ldo, 0, bf))
+        return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
+      scatter_rows(Lk, p.Ytr, p.tr_list, p.n_tr, ldo, p.logits);
+      continue;
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
     {
@@ -946,6 +986,13 @@ extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
   const int L = C->L;
   for (size_t i = 0; i < C->parts.size(); ++i) {
     PartCtx& p = C->parts[i];
+    if (C->cl) {  // compact train rows: every row of Y_tr is a train row; M rows compact too
+      Scope sc(C, PGCN_K_LOSS, 8.0 * p.n_tr * C->F[L] + 8.0 * p.n_tr);
+      loss_rows(Lk, C->cfg.loss, p.Ytr, p.n_tr, C->F[L], C->ld[L], p.lab_tr, nullptr, (double)C->cfg.n_train_global,
+                p.M, p.row_loss);  // in place: Y_tr (in M) -> M_tr, row by row
+      reduce_sum(Lk, p.row_loss, p.n_tr, C->part_loss + i);
+      continue;
+    }
     Scope sc(C, PGCN_K_LOSS, 8.0 * p.n_in * C->F[L] + 5.0 * p.n_in);
     loss_rows(Lk, C->cfg.loss, p.logits, p.n_in, C->F[L], C->ld[L], p.labels, p.train,
               (double)C->cfg.n_train_global, p.M, p.row_loss);
@@ -1065,10 +1112,13 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       continue;
     }
+    const bool cl = C->cl && l == C->L;  // compact train rows: Z, D_tr, M and dA rows are positions
+    const int64_t mr = cl ? p.n_tr : p.n_in;
+    if (cl) D = p.Dtr;
     {
-      Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (2 * Fi + Fo), 2.0 * p.n_in * (2 * Fi + 1) * Fo);
+      Scope sc(C, PGCN_K_GEMM_DW, 4.0 * mr * (2 * Fi + Fo), 2.0 * mr * (2 * Fi + 1) * Fo);
       if (C->cfg.gemm != 2) {
-        if (gemm_dw_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
+        if (gemm_dw_tc(Lk, p.Z[l], D, ldi, mr, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
                        C->dw_ws_floats, bf))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       } else {
@@ -1078,10 +1128,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
     if (l >= 2) {
       {
-        Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * 2 * Fi);
+        Scope sc(C, PGCN_K_GEMM_DA, 4.0 * mr * (2 * Fi + Fo) + 4.0 * mr, 2.0 * mr * Fo * 2 * Fi);
         if (C->cfg.gemm != 2) {
-          if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.inv_deg,
-                         p.dA, ldi, bf, 2))
+          if (mr > 0 && gemm_da_tc(Lk, p.M, ldo, mr, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1],
+                                   cl ? p.invdeg_tr : p.inv_deg, p.dA, ldi, bf, 2))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         } else {
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
@@ -1090,7 +1140,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all);
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
-               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
+               drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16,
+               cl ? p.tr_pos : nullptr);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
-                                                             const int32_t* __restrict__ rows, int addend) {
+                                                             const int32_t* __restrict__ rows, int addend, int compact) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
           set_comp(o, j, relu ? fmaxf(v, 0.f) : v);
         }
       }
-      Z[row * ld4 + x] = o;
+      Z[(compact ? ri : row) * ld4 + x] = o;  // compact: output row = position in the row list
     }
   }
 }
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
                                                              unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                             int addend) {
+                                                             int addend, const int32_t* __restrict__ dmap) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -286,7 +286,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     float4 acc[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
-      acc[q] = (dDs && u0 < n_in) ? dDs[u0 * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
+      // dmap (compact train-row dA): dD_self of u lives in row dmap[u] (-1: none)
+      const int64_t du = dmap ? (u0 < n_in ? (int64_t)dmap[u0] : -1) : (u0 < n_in ? u0 : -1);
+      acc[q] = (dDs && du >= 0) ? dDs[du * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
       if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of this row, in place
     }
     const int64_t beg = trp[u0], end = trp[u0 + 1];
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
                                                                unsigned long long* work, int grabk, int self,
                                                                const float* __restrict__ bias, int64_t n_bias,
                                                                int relu, const int32_t* __restrict__ rows,
-                                                               int addend) {
+                                                               int addend, int compact) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
           }
           o[j] = v;
         }
-        Z[row * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
+        Z[(compact ? ri : row) * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
   }
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
                                                                unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                               int addend) {
+                                                               int addend, const int32_t* __restrict__ dmap) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -522,7 +524,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * xq + h;
-        float4 a = (dDs && u0 < n_in && xf < ld4) ? dDs[u0 * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t du = dmap ? (u0 < n_in ? (int64_t)dmap[u0] : -1) : (u0 < n_in ? u0 : -1);
+        float4 a = (dDs && du >= 0 && xf < ld4) ? dDs[du * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
         if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // heavy-tile sums (spmm_tc) of this row, in place
         acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
       }
@@ -573,6 +576,31 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
         J[u0 * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------- compact train rows (N1(ii))
+// dst[map[r]] = src[r] over n rows of ld4 float4s
+__global__ void k_scatter_rows(const float4* __restrict__ src, const int32_t* __restrict__ map, int64_t n, int64_t ld4,
+                               float4* __restrict__ dst) {
+  for (RowCursor rc(ld4); rc.r < n; rc.next((int)ld4)) dst[(int64_t)map[rc.r] * ld4 + rc.x] = src[rc.r * ld4 + rc.x];
+}
+// pos[v] = k where list[k] = v, else -1 (pos pre-filled with -1)
+__global__ void k_positions(const int32_t* __restrict__ list, int64_t n, int32_t* __restrict__ pos) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    pos[list[k]] = (int32_t)k;
+}
+// a[e] = pos[a[e]] (in place)
+__global__ void k_remap(int32_t* __restrict__ a, int64_t n, const int32_t* __restrict__ pos) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    a[e] = pos[a[e]];
+}
+// dst[k * w + j] = src[list[k] * w + j] (bytes)
+__global__ void k_gather_bytes(const uint8_t* __restrict__ src, const int32_t* __restrict__ list, int64_t n, int64_t w,
+                               uint8_t* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * w; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / w, j = i - k * w;
+    dst[i] = src[(int64_t)list[k] * w + j];
   }
 }
 
@@ -641,14 +669,15 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-__global__ void k_loss_ce(const float* __restrict__ Y, int64_t n, int64_t C, int64_t ld, const int32_t* __restrict__ lab,
-                          const uint8_t* __restrict__ train, float inv_nt, float* __restrict__ M, float* __restrict__ rl) {
+// Y and M may alias (compact train rows: the logits become J^(L) in place, each row read before written)
+__global__ void k_loss_ce(const float* Y, int64_t n, int64_t C, int64_t ld, const int32_t* __restrict__ lab,
+                          const uint8_t* __restrict__ train, float inv_nt, float* M, float* __restrict__ rl) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
     const float* y = Y + v * ld;
     float* m = M + v * ld;
-    if (!train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
+    if (train && !train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
       for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane == 0) rl[v] = 0.f;
       continue;
@@ -661,23 +690,25 @@ __global__ void k_loss_ce(const float* __restrict__ Y, int64_t n, int64_t C, int
     s = warp_sum(s);
     const int32_t t = lab[v];
     const float ls = logf(s);
+    const float yt = y[t];
+    __syncwarp();
     for (int64_t c = lane; c < ld; c += 32) {
       float g = 0.f;
       if (c < C) g = (expf(y[c] - mx) / s - (c == t ? 1.f : 0.f)) * inv_nt;
       m[c] = g;
     }
-    if (lane == 0) rl[v] = (ls + mx - y[t]) * inv_nt;
+    if (lane == 0) rl[v] = (ls + mx - yt) * inv_nt;
   }
 }
 
-__global__ void k_loss_bce(const float* __restrict__ Y, int64_t n, int64_t C, int64_t ld, const uint8_t* __restrict__ lab,
-                           const uint8_t* __restrict__ train, float inv_ntc, float* __restrict__ M, float* __restrict__ rl) {
+__global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, const uint8_t* __restrict__ lab,
+                           const uint8_t* __restrict__ train, float inv_ntc, float* M, float* __restrict__ rl) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
     const float* y = Y + v * ld;
     float* m = M + v * ld;
-    const bool tr = train[v] != 0;
+    const bool tr = !train || train[v] != 0;
     if (!tr) {
       for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane == 0) rl[v] = 0.f;
@@ -1145,7 +1176,7 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
               int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz,
-              const TileDev* tiles, void* t16) {
+              const TileDev* tiles, void* t16, int compact) {
   if (n_rows <= 0) return;
   const int tcu = tiles && tiles->n_tiles > 0 && !rows && n_cols >= 0 && n_valid >= n_cols && tiles->n_rows == n_rows;
   if (tcu) {
@@ -1179,11 +1210,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd16<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,   \
                                                                       n_valid, sh.nchunk, Z4, ld4, wk, K, slf,    \
-                                                                      bias, n_bias, relu, rows, add);                                    \
+                                                                      bias, n_bias, relu, rows, add, compact);    \
     else                                                                                                       \
       k_spmm_fwd16<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, G16, ld8, n_rows,  \
                                                                        n_valid, sh.nchunk, Z4, ld4, wk, K, slf,   \
-                                                                       bias, n_bias, relu, rows, add);                                   \
+                                                                       bias, n_bias, relu, rows, add, compact);   \
   } else
       PGCN_SPMM16_CASES(X) {
         std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
@@ -1198,11 +1229,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,      \
                                                                     n_valid, sh.nchunk, Z4, wk, K, slf, bias,     \
-                                                                    n_bias, relu, rows, add);     \
+                                                                    n_bias, relu, rows, add, compact);            \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
                                                                      n_valid, sh.nchunk, Z4, wk, K, slf, bias,    \
-                                                                     n_bias, relu, rows, add);    \
+                                                                     n_bias, relu, rows, add, compact);           \
   } else
       PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -1236,7 +1267,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
 void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
               const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz,
-              const TileDev* tiles, void* t16) {
+              const TileDev* tiles, void* t16, const int32_t* dmap) {
   if (n_all <= 0) return;
   const int tcu = tiles && tiles->n_tiles > 0 && tiles->n_rows == n_all;  // see spmm_fwd
   if (tcu) {
@@ -1269,7 +1300,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all,  \
-                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add);                                     \
+                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                     \
   } else
       PGCN_SPMM16_CASES(X) {
         std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
@@ -1282,7 +1313,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
-                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add);                                       \
+                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                       \
   } else
       PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
 #undef X
@@ -1333,6 +1364,34 @@ void grad_reduce(Launch L, const int64_t* inv_ptr, const int32_t* inv_pos, const
       inv_ptr, inv_pos, msg, row_map, reinterpret_cast<float4*>(ema), gamma, use_ema, first,
       reinterpret_cast<float4*>(J), write_j, reinterpret_cast<const float4*>(Hprev), reinterpret_cast<float4*>(M), n_in,
       ld4);
+  count(L);
+}
+
+void scatter_rows(Launch L, const float* src, const int32_t* map, int64_t n, int64_t ld, float* dst) {
+  if (n <= 0) return;
+  const int64_t ld4 = ld / 4;
+  k_scatter_rows<<<grid_for(n * ld4, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(src), map, n, ld4,
+                                                                    reinterpret_cast<float4*>(dst));
+  count(L);
+}
+
+void compact_train_setup(Launch L, const int32_t* list, int64_t n_tr, int64_t n_in, int32_t* pos, int32_t* cols,
+                         int64_t n_cols) {
+  cudaMemsetAsync(pos, 0xff, sizeof(int32_t) * (size_t)n_in, L.s);
+  if (n_tr > 0) {
+    k_positions<<<grid_for(n_tr, kThreads), kThreads, 0, L.s>>>(list, n_tr, pos);
+    count(L);
+  }
+  if (n_cols > 0) {
+    k_remap<<<grid_for(n_cols, kThreads), kThreads, 0, L.s>>>(cols, n_cols, pos);
+    count(L);
+  }
+}
+
+void gather_bytes(Launch L, const void* src, const int32_t* list, int64_t n, int64_t w, void* dst) {
+  if (n <= 0 || w <= 0) return;
+  k_gather_bytes<<<grid_for(n * w, kThreads), kThreads, 0, L.s>>>(static_cast<const uint8_t*>(src), list, n, w,
+                                                                   static_cast<uint8_t*>(dst));
   count(L);
 }
 

@@ -65,9 +65,10 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
               int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
               void* g16 = nullptr, const int32_t* rows = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr,
-              void* t16 = nullptr);
+              void* t16 = nullptr, int compact = 0);
 // rows (optional): aggregate only the n_rows rows listed (local ids; N1(ii) train-row-sparse last
-// layer); the other output rows are left untouched.
+// layer); the other output rows are left untouched.  compact: output row k of the list goes to Z[k].
+// dmap (spmm_bwd, optional): dDs of inner row u is row dmap[u] of dDs (-1: none) -- compact train rows.
 
 // S8: J[u] = mask_u * s * ( [u < n_in] dDs[u] + sum_{v in T(u)} dZs[v] ),  u in [0, n_all)
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
@@ -76,7 +77,8 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
 void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
-              void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr, void* t16 = nullptr);
+              void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr, void* t16 = nullptr,
+              const int32_t* dmap = nullptr);
 // tiles (both SpMMs, optional): dense-tile decomposition of the pattern (tiles.h); its heavy tiles are
 // summed by spmm_tc into the output rows first and the gather kernel walks only the light CSR, adding
 // the tile sums (fwd: used only when n_valid >= n_cols and rows == nullptr).  t16 (fp32 tier with tiles):
@@ -94,6 +96,13 @@ size_t train_rows_tmp_bytes(int64_t n_in, int64_t n_all);
 void build_train_rows(Launch, const uint8_t* train, int64_t n_in, const int64_t* t_row_ptr, const int32_t* t_col,
                       int64_t n_all, int32_t* tr_list, int64_t* tr_count, int64_t* counts, int64_t* t_row_ptr_tr,
                       int32_t* t_col_tr, void* tmp, size_t tmp_bytes);
+
+// Compact train rows of the last layer (N1(ii)): dst[map[r]] = src[r]; pos[v] = index of v in list (or
+// -1) and cols[e] = pos[cols[e]] in place; dst[k] = src[list[k]] for rows of w bytes.
+void scatter_rows(Launch, const float* src, const int32_t* map, int64_t n, int64_t ld, float* dst);
+void compact_train_setup(Launch, const int32_t* list, int64_t n_tr, int64_t n_in, int32_t* pos, int32_t* cols,
+                         int64_t n_cols);
+void gather_bytes(Launch, const void* src, const int32_t* list, int64_t n, int64_t w, void* dst);
 
 // N4 diagnostics: out[0] += sum_{r < n_rows, c < F} (used(r, c) - fresh(r, c))^2 with fresh rows from a
 // segment table (row_map fmap) and used rows from a segment table (umap), a plain array, or 0.
@@ -113,7 +122,8 @@ void grad_reduce(Launch, const int64_t* inv_ptr, const int32_t* inv_pos, const S
                  const int32_t* row_map, float* ema, float gamma, int use_ema, int first, float* J,
                  int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld);
 
-// S5: CE (labels int32) or BCE (labels uint8 [n x C]) on rows with train[v] != 0.
+// S5: CE (labels int32) or BCE (labels uint8 [n x C]) on rows with train[v] != 0 (train == nullptr:
+// every row is a train row).
 // M = J^(L) (zero outside the train set), row_loss[v] = loss term of v (already / n_train).
 void loss_rows(Launch, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
                const uint8_t* train, double n_train, float* M, float* row_loss);
