@@ -672,15 +672,39 @@ int tc_tmem_cols(int BN) {
   return c;
 }
 
-cudaError_t tc_launch(const TcParams& p, cudaStream_t s, int sms) {
+// Narrow forward / dA GEMMs (TMEM accumulators <= 256 columns, >= 2 stages in 104 KB) run two CTAs per
+// SM: their pipelines are TMA-latency bound (memory-bound shapes: papers-shaped 48-wide layers), and
+// two independent pipelines per SM hide more of it (papers-q forward GEMMs 18.9 -> 15.7 ms per step;
+// the dW GEMM measured slower, its split-K plan fills 148-CTA waves).  Dev knob PGCN_TC_GEMM_CTAS=1.
+static int gemm_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PGCN_TC_GEMM_CTAS");
+    v = e ? std::atoi(e) : 2;
+  }
+  return v;
+}
+
+cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   static bool attr_set = false;
-  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode);
   if (!attr_set) {
     cudaFuncSetAttribute(tc::k_umma_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(tc::k_umma_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  int grid = p.n_tiles < sms ? p.n_tiles : sms;
+  TcParams p = p0;
+  int ctas = 1;
+  if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW) {  // dW: split-K plan is sized for 148 CTAs
+    const size_t stage = tc::geometry(p.bf, p.mode, p.BN).stage();
+    int S = (int)((104 * 1024 - 1024 - 64) / stage);
+    if (S >= 2) {
+      p.stages = S < p.stages ? S : p.stages;
+      ctas = 2;
+    }
+  }
+  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode);
+  const int cap = ctas * sms;
+  int grid = p.n_tiles < cap ? p.n_tiles : cap;
   if (grid < 1) return cudaSuccess;
   if (p.bf) tc::k_umma_gemm<1><<<grid, tc::kThreads, smem, s>>>(p);
   else tc::k_umma_gemm<0><<<grid, tc::kThreads, smem, s>>>(p);
