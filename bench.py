@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-tiles", action="store_true",
                     help="gather-only aggregation (default: dense 128x64 tiles of P_i / P_i^T on the tensor cores "
                          "where they hold >= 25 %% of the edges; DESIGN.md 'Tensor-core tiles')")
+    ap.add_argument("--tile-min", type=int, default=0, help="heavy-tile threshold in edges per 128x64 tile (0: library default)")
     ap.add_argument("--no-train-sparse", action="store_true",
                     help="compute the last layer on every row (default: only on train rows, SURVEY N1(ii); exact)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -259,7 +260,8 @@ def main():
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
                            n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
-                           train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles)
+                           train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles,
+                           tile_min=args.tile_min)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
