@@ -592,6 +592,37 @@ __global__ void k_colsum(const float* __restrict__ Mg, int64_t M, int64_t ld, in
   }
 }
 
+// Same partial with `sub` row chunks per split (more blocks for narrow N / few splits): chunk s of
+// split z sums rows [z rps + s rpsub, ...) into scratch[(z sub + s) N + n]; k_colsum_fin then adds the
+// sub partials of each split in ascending s (fixed order, deterministic).
+__global__ void k_colsum_sub(const float* __restrict__ Mg, int64_t M, int64_t ld, int N, int64_t rps, int sub,
+                             int64_t rpsub, float* __restrict__ scratch) {
+  __shared__ float sh[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int z = blockIdx.y / sub, sc = blockIdx.y % sub;
+  const int64_t zend = (int64_t)(z + 1) * rps < M ? (int64_t)(z + 1) * rps : M;
+  const int64_t r0 = (int64_t)z * rps + (int64_t)sc * rpsub, r1 = r0 + rpsub < zend ? r0 + rpsub : zend;
+  float a = 0.f;
+  if (n < N)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) a += Mg[r * ld + n];
+  sh[threadIdx.y][threadIdx.x] = a;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float s = 0.f;
+    for (int y = 0; y < 8; ++y) s += sh[y][threadIdx.x];
+    scratch[(int64_t)blockIdx.y * N + n] = s;
+  }
+}
+__global__ void k_colsum_fin(const float* __restrict__ scratch, int sub, int N, int Zs, float* __restrict__ part,
+                             int64_t zstride, int64_t row_off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)Zs * N) return;
+  const int z = (int)(i / N), n = (int)(i - (int64_t)z * N);
+  float s = 0.f;
+  for (int k = 0; k < sub; ++k) s += scratch[((int64_t)z * sub + k) * N + n];
+  part[(int64_t)z * zstride + row_off + n] = s;
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------------------------------------------ host side
@@ -750,6 +781,7 @@ static int dw_bn(int64_t N, int bf) {
 // by "W x largest tile + per-tile overhead").  Balancing per segment matters for transform-first layers,
 // whose two segments have n_all and n_in rows.
 constexpr int kDwMaxWaves = 3;
+constexpr int kColsumSub = 16;  // max row chunks per split of the bias-row column sums
 static int dw_base(int64_t F, int64_t N) { return (int)(((F + 127) / 128) * ((N + dw_bn(N, 0) - 1) / dw_bn(N, 0))); }
 static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
   const int64_t ovh = 6;  // per-tile fill / drain, in k-block units
@@ -780,7 +812,7 @@ int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
   const int64_t kb = (M + 31) / 32;
   if (Z > kb) Z = kb;
   if (Z < 1) Z = 1;
-  return Z * (2 * F + 1) * ((N + 3) / 4 * 4);
+  return Z * (2 * F + 1) * ((N + 3) / 4 * 4) + Z * kColsumSub * N;  // + the bias-row sub partials
 }
 
 // FWD-mode launch with 1 or 2 K-major A segments sharing one pre-converted B operand copy
@@ -955,7 +987,22 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int64_t kbb = (rowsMb + 31) / 32;
   const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
   dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
-  if (rowsMb > 0) {
+  // narrow N / few splits leave most SMs idle: split each split's rows into `sub` chunks (>= 2 blocks per
+  // SM in total) with a fixed-order second pass, when the workspace has room for the sub partials
+  int sub = (int)((2 * 148 + (int64_t)grid.x * Zs - 1) / ((int64_t)grid.x * Zs));
+  sub = sub > kColsumSub ? kColsumSub : sub;
+  const int64_t room = ws_floats - (int64_t)Zs * K * NP;
+  while (sub > 1 && (int64_t)Zs * sub * N > room) --sub;
+  const int64_t rpsub = ((rps + sub - 1) / sub + 7) / 8 * 8;  // sub chunks cover the split
+  if (rowsMb > 0 && sub > 1) {
+    float* scratch = ws + (int64_t)Zs * K * NP;
+    tc::k_colsum_sub<<<dim3(grid.x, (unsigned)(Zs * sub)), block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N,
+                                                                           rps > 0 ? rps : 32, sub, rpsub, scratch);
+    const int64_t tot = (int64_t)Zs * N;
+    tc::k_colsum_fin<<<(unsigned)((tot + 255) / 256), 256, 0, L.s>>>(scratch, sub, (int)N, Zs, ws, K * NP,
+                                                                      nseg * F * NP);
+    if (L.count) *L.count += 1;
+  } else if (rowsMb > 0) {
     tc::k_colsum<<<grid, block, 0, L.s>>>(Mb, rowsMb, ldB, (int)N, rps > 0 ? rps : 32, ws, K * NP, nseg * F * NP);
   } else {
     for (int z = 0; z < Zs; ++z) cudaMemsetAsync(ws + z * K * NP + nseg * F * NP, 0, sizeof(float) * N, L.s);
