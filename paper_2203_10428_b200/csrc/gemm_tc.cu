@@ -987,9 +987,9 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const int64_t kbb = (rowsMb + 31) / 32;
   const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
   dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
-  // narrow N / few splits leave most SMs idle: split each split's rows into `sub` chunks (>= 2 blocks per
+  // narrow N / few splits leave most SMs idle: split each split's rows into `sub` chunks (>= 4 blocks per
   // SM in total) with a fixed-order second pass, when the workspace has room for the sub partials
-  int sub = (int)((2 * 148 + (int64_t)grid.x * Zs - 1) / ((int64_t)grid.x * Zs));
+  int sub = (int)((4 * 148 + (int64_t)grid.x * Zs - 1) / ((int64_t)grid.x * Zs));
   sub = sub > kColsumSub ? kColsumSub : sub;
   const int64_t room = ws_floats - (int64_t)Zs * K * NP;
   while (sub > 1 && (int64_t)Zs * sub * N > room) --sub;

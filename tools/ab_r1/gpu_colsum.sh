@@ -5,6 +5,7 @@ run() {
 import json; d=json.load(open('gpurun_out/bc.json')); print('$1', round(d['value'],3), round(d['ms_per_step'],2), {k: round(v['ms_per_step'],2) for k,v in d['breakdown'].items() if v['ms_per_step'] > 0.5})" || tail -3 gpurun_out/bc.json
 }
 run reddit
+run reddit
 run products
 run yelp
 run papers-q
