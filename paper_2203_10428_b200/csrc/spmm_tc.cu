@@ -15,14 +15,17 @@
 // none); the gather SpMM then adds the light edges on top (its `addend`), applies inv_deg, the
 // self term, bias / ReLU or the dropout mask -- so the result is the same sum, reassociated.
 //
-// Roles (320 threads): warp 0 TMA producer (the tile's 1 KB bitmask by bulk copy on its own barrier,
-// so A can be built while B is in flight; then the B boxes), warp 1
-// TMEM owner + single-thread MMA issuer, warps 2-5 builders (bitmask -> A tile in the UMMA K-major
-// SW128 layout, shared-space stores), warps 6-9 epilogue (tcgen05.ld -> float4 stores).  Work list:
-// (row block, n-tile) items in the host's descending-tile-count order, strided over a persistent
-// grid of one CTA per SM.  Operand layouts are the proven ones of gemm_tc.cu's bf16 variant: A as
-// its FWD K-major A (128-byte rows of 64 bf16), B as its DW MN-major B (SW128 atoms of 64 bf16 x
-// 32 rows, 4 KB; a 64-row stage = two k-halves of BN/64 atoms).
+// Roles (320 threads): warp 0 TMA producer (B boxes; in SS mode also the tile's 1 KB bitmask by bulk
+// copy on its own barrier), warp 1 TMEM owner + single-thread MMA issuer, warps 2-5 build the A tile:
+// TS mode (default) -- each thread reads its row's 64-bit mask word from global two tiles ahead and
+// writes 32 columns of bf16 0/1 pairs to TMEM with tcgen05.st (A from TMEM); SS mode (bf16 tier,
+// BN = 256) -- expand the bitmask into the UMMA K-major SW128 layout in shared memory.  Warps 6-9:
+// epilogue (tcgen05.ld -> float4 stores).  Work list: (row block, n-tile) items in the host's
+// descending-tile-count order, strided over a persistent grid of two CTAs per SM (one TMEM
+// accumulator each; the kernel is latency-bound and two independent pipelines per SM beat one
+// deeper one).  Operand layouts are the proven ones of gemm_tc.cu's bf16 variant: A as its FWD
+// K-major A (128-byte rows of 64 bf16), B MN-major SW128 (atoms of 64 bf16 columns; 64-row boxes of
+// 8 KB, LBO = atom stride -- or two k-halves of 32-row boxes, PGCN_TC_SPMM_BOX64=0).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
