@@ -387,6 +387,11 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.n_rows = T.n_rows;
   p.ld_out = ld_out;
   p.width = (int)width;
+  static int env_nacc1 = -1;  // dev knob PGCN_TC_SPMM_NACC1=1: one TMEM accumulator even with one CTA per SM
+  if (env_nacc1 < 0) {
+    const char* e = std::getenv("PGCN_TC_SPMM_NACC1");
+    env_nacc1 = e ? std::atoi(e) : 0;
+  }
   static int env_ts = -1, env_ctas = -1;  // dev knobs PGCN_TC_SPMM_TS (0: A in shared memory),
   if (env_ts < 0) {                        // PGCN_TC_SPMM_CTAS (CTAs per SM, 1 or 2; default 2)
     const char* e = std::getenv("PGCN_TC_SPMM_TS");
@@ -403,7 +408,7 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   for (;; ctas = 1) {  // two stages must fit next to a second CTA, else one CTA per SM
     smem_budget = ctas == 2 ? 104 * 1024 : 210 * 1024;
     tmem_budget = ctas == 2 ? 256 : 512;
-    p.nacc = ctas == 2 ? 1 : 2;
+    p.nacc = (ctas == 2 || env_nacc1) ? 1 : 2;
     TS = env_ts && p.nacc * p.BN + 32 * 2 <= tmem_budget;
     stage = stage_bytes(NT, p.BN, TS);
     S = (int)(smem_budget / stage);
