@@ -126,3 +126,26 @@ def test_tiles_empty(P):
         for which in (0, 1):
             t = part.tiles(i, which, 1)
             assert t["n_tiles"] == 0 and t["nnz_light"] == 0
+
+
+def test_config_fields_reach_the_library(P):
+    """pgcn_config.spmm_tiles / tile_min / train_sparse cross the C ABI (ctypes layout = include/pgcn.h):
+    the workspace grows by the tile sets exactly when the tile path is enabled on a dense graph, shrinks
+    when a huge tile_min leaves no heavy tiles, and invalid values are rejected."""
+    import ctypes
+    import numpy as np
+    g = gen_graph("reddit", seed=3, n=1500, nnz=60000, f0=16, classes=4)
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 2)
+    local = np.arange(2, dtype=np.int32)
+
+    def ws(**kw):
+        cfg = P.make_config([16, 32, 4], n_global=g.n, n_train_global=g.n_train, **kw)
+        nb = ctypes.c_size_t()
+        rc = P.lib().pgcn_workspace_bytes(part.handle, local.ctypes.data, 2, ctypes.byref(cfg), ctypes.byref(nb))
+        return rc, nb.value
+    rc0, off = ws(spmm_tiles=False)
+    rc1, on = ws(spmm_tiles=True, tile_min=1)
+    rc2, none = ws(spmm_tiles=True, tile_min=128 * 64)
+    assert rc0 == rc1 == rc2 == 0
+    assert on > off and none == off
+    assert ws(spmm_tiles=True, tile_min=-1)[0] == P.EINVAL
