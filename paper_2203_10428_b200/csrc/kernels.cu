@@ -145,6 +145,8 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 }
 
 // ---------------------------------------------------------------- SpMM forward (S3)
+// Output rows, their in-place partial sums and dD_self are touched once per launch: streamed with
+// evict-first hints (__ldcs / __stcs) so they do not displace the gathered table from L2.
 // Work item = (row, chunk): a group of G lanes owns NC*G float4 columns of one output row (for
 // every width used here one chunk covers the whole row) and keeps NC float4 accumulators; U
 // neighbour rows are in flight per step, so each lane has NC*U 16-byte loads outstanding.  The
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
 #pragma unroll
     for (int q = 0; q < NC; ++q) {  // GCN-sym self loop (A + I, R26): the row's own (inner) input
       acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], Z[row * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of this row, in place
+      if (addend) f4acc(acc[q], __ldcs(Z + row * ld4 + xq[q]));  // heavy-tile sums (spmm_tc) of this row, in place
     }
     const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
           set_comp(o, j, relu ? fmaxf(v, 0.f) : v);
         }
       }
-      Z[(compact ? ri : row) * ld4 + x] = o;  // compact: output row = position in the row list
+      __stcs(Z + (compact ? ri : row) * ld4 + x, o);  // compact: output row = position in the row list
     }
   }
 }
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       // dmap (compact train-row dA): dD_self of u lives in row dmap[u] (-1: none)
       const int64_t du = dmap ? (u0 < n_in ? (int64_t)dmap[u0] : -1) : (u0 < n_in ? u0 : -1);
-      acc[q] = (dDs && du >= 0) ? dDs[du * ldA4 + xq[q]] : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend) f4acc(acc[q], J[u0 * ld4 + xq[q]]);  // heavy-tile sums (spmm_tc) of this row, in place
+      acc[q] = (dDs && du >= 0) ? __ldcs(dDs + du * ldA4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (addend) f4acc(acc[q], __ldcs(J + u0 * ld4 + xq[q]));  // heavy-tile sums (spmm_tc) of this row, in place
     }
     const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
         else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
         set_comp(o, j, val);
       }
-      J[u0 * ld4 + x] = o;
+      __stcs(J + u0 * ld4 + x, o);
     }
   }
 }
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
         for (int h = 0; h < 2; ++h) {
           const int64_t xf = 2 * xq + h;
           if (xf < ld4) {
-            const float4 a = Z[row * ld4 + xf];
+            const float4 a = __ldcs(Z + row * ld4 + xf);
             acc[q][4 * h] += a.x; acc[q][4 * h + 1] += a.y; acc[q][4 * h + 2] += a.z; acc[q][4 * h + 3] += a.w;
           }
         }
@@ -487,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
           }
           o[j] = v;
         }
-        Z[(compact ? ri : row) * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
+        __stcs(Z + (compact ? ri : row) * ld4 + xf, make_float4(o[0], o[1], o[2], o[3]));
       }
     }
   }
@@ -525,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * xq + h;
         const int64_t du = dmap ? (u0 < n_in ? (int64_t)dmap[u0] : -1) : (u0 < n_in ? u0 : -1);
-        float4 a = (dDs && du >= 0 && xf < ld4) ? dDs[du * ldA4 + xf] : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (addend && xf < ld4) f4acc(a, J[u0 * ld4 + xf]);  // heavy-tile sums (spmm_tc) of this row, in place
+        float4 a = (dDs && du >= 0 && xf < ld4) ? __ldcs(dDs + du * ldA4 + xf) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (addend && xf < ld4) f4acc(a, __ldcs(J + u0 * ld4 + xf));  // heavy-tile sums (spmm_tc) of this row, in place
         acc[q][4 * h] = a.x; acc[q][4 * h + 1] = a.y; acc[q][4 * h + 2] = a.z; acc[q][4 * h + 3] = a.w;
       }
     }
@@ -573,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
           else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
           o[j] = val;
         }
-        J[u0 * ld4 + xf] = make_float4(o[0], o[1], o[2], o[3]);
+        __stcs(J + u0 * ld4 + xf, make_float4(o[0], o[1], o[2], o[3]));
       }
     }
   }

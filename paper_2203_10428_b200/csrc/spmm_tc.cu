@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spmm_tc(const __grid_constant__
             const float4 o = none ? make_float4(0.f, 0.f, 0.f, 0.f)
                                   : make_float4(__uint_as_float(r[4 * g4]), __uint_as_float(r[4 * g4 + 1]),
                                                 __uint_as_float(r[4 * g4 + 2]), __uint_as_float(r[4 * g4 + 3]));
-            *reinterpret_cast<float4*>(out + n) = o;
+            __stcs(reinterpret_cast<float4*>(out + n), o);  // streamed: keep L2 for the B tiles
           }
         }
       }
