@@ -310,9 +310,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
               const uint8_t* raw = part == 0 ? base : base + geo.a_raw + geo.a_cvt;
               uint8_t* cvt = part == 0 ? base + geo.a_raw : base + geo.a_raw + geo.a_cvt + geo.b_raw;
               const int nf = part == 0 ? BM : p.BN;
-              const int items = (nf / 8) * 32;
+              const int nch = nf / 8, items = nch * 32;
               for (int i = ct; i < items; i += kConvThreads) {
-                const int r = i & 31, hc = i >> 5;  // hc: 8-feature chunk index
+                // chunk index fastest across a warp: its LDS.128s walk along 128-byte rows of the raw box
+                // (a row-fastest order put 8 threads of a phase on one bank group, 8-way conflicts)
+                const int hc = i % nch, r = i / nch;  // hc: 8-feature chunk index
                 const float4* src = reinterpret_cast<const float4*>(raw + (hc >> 2) * 4096 + r * 128 + (hc & 3) * 32);
                 const float4 x = src[0], y = src[1];
                 uint4 o;
