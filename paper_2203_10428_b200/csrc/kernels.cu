@@ -40,6 +40,17 @@ __device__ __forceinline__ uint64_t row_key(const DropSpec& d, int64_t gid) {
 __device__ __forceinline__ bool keep_at(const DropSpec& d, uint64_t kr, int64_t c) {
   return smix_top24((kr + (uint64_t)c) ^ d.seed) >= d.thr;
 }
+// Same decision as keep_at on the high word only: (z >> 40) >= thr  <=>  hi32(z) >= thr << 8 (thr < 2^24),
+// and the last multiply only needs hi32 of the product.  k_dropout is ALU-bound on this hash (the
+// branchy per-element form ran ~50 instructions per element, ~4.3 TB/s), so it is written out.
+__device__ __forceinline__ bool keep_fast(uint64_t key, uint64_t seed, uint32_t thr8) {
+  uint64_t z = (key ^ seed) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  const uint32_t top = __umulhi(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu;
+  return top >= thr8;
+}
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
@@ -123,23 +134,35 @@ struct RowCursor {
 };
 
 // ---------------------------------------------------------------- dropout (S3 prologue, R5)
+__device__ __forceinline__ float4 drop4(const float4 h, int64_t x, uint64_t kr, float sr, const DropSpec& d) {
+  float4 out;
+  if (d.on && d.thr < (1u << 24) && 4 * x + 4 <= d.width) {  // whole float4 in the row: branch-free mask
+    const uint64_t k0 = kr + (uint64_t)(4 * x);
+    const uint32_t thr8 = d.thr << 8;
+    out.x = keep_fast(k0, d.seed, thr8) ? h.x * d.scale * sr : 0.f;
+    out.y = keep_fast(k0 + 1, d.seed, thr8) ? h.y * d.scale * sr : 0.f;
+    out.z = keep_fast(k0 + 2, d.seed, thr8) ? h.z * d.scale * sr : 0.f;
+    out.w = keep_fast(k0 + 3, d.seed, thr8) ? h.w * d.scale * sr : 0.f;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = 4 * x + j;
+      float v = 0.f;
+      if (c < d.width && (!d.on || keep_at(d, kr, c))) v = comp(h, j) * d.scale * sr;
+      set_comp(out, j, v);
+    }
+  }
+  return out;
+}
+
+// One float4 per thread per grid-stride step (two loads in flight per thread, hashed after both
+// landed, measured no faster: r1n).
 __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, int64_t ld4, int64_t n_rows,
                           int64_t n_valid, const int64_t* __restrict__ gid, DropSpec d, const float* __restrict__ rs) {
   for (RowCursor rc(ld4); rc.r < n_rows; rc.next((int)ld4)) {
     const int64_t r = rc.r, x = rc.x, i = r * ld4 + x;
     float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < n_valid) {
-      const float4 h = H[i];
-      const uint64_t kr = row_key(d, gid[r]);
-      const float sr = rs ? rs[r] : 1.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t c = 4 * x + j;
-        float v = 0.f;
-        if (c < d.width && (!d.on || keep_at(d, kr, c))) v = comp(h, j) * d.scale * sr;
-        set_comp(out, j, v);
-      }
-    }
+    if (r < n_valid) out = drop4(H[i], x, row_key(d, gid[r]), rs ? rs[r] : 1.f, d);
     D[i] = out;
   }
 }
