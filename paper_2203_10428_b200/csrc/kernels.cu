@@ -134,6 +134,7 @@ struct RowCursor {
 };
 
 // ---------------------------------------------------------------- dropout (S3 prologue, R5)
+// d.scale is applied only when d.on (the transposed SpMMs pass a zero-initialised "no dropout" spec).
 __device__ __forceinline__ float4 drop4(const float4 h, int64_t x, uint64_t kr, float sr, const DropSpec& d) {
   float4 out;
   if (d.on && d.thr < (1u << 24) && 4 * x + 4 <= d.width) {  // whole float4 in the row: branch-free mask
@@ -148,7 +149,7 @@ __device__ __forceinline__ float4 drop4(const float4 h, int64_t x, uint64_t kr, 
     for (int j = 0; j < 4; ++j) {
       const int64_t c = 4 * x + j;
       float v = 0.f;
-      if (c < d.width && (!d.on || keep_at(d, kr, c))) v = comp(h, j) * d.scale * sr;
+      if (c < d.width && (!d.on || keep_at(d, kr, c))) v = (d.on ? comp(h, j) * d.scale : comp(h, j)) * sr;
       set_comp(out, j, v);
     }
   }
@@ -347,15 +348,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
     for (int q = 0; q < NC; ++q) {
       const int64_t x = x0 + q * G;
       if (x >= ld4) continue;
-      float4 o = rs ? f4scale(acc[q], sr) : acc[q];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t c = 4 * x + j;
-        float val = comp(o, j);
-        if (c >= d.width) val = 0.f;
-        else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
-        set_comp(o, j, val);
-      }
+      const float4 o = drop4(rs ? f4scale(acc[q], sr) : acc[q], x, kr, 1.f, d);  // mask of R5, J's own row
       __stcs(J + u0 * ld4 + x, o);
     }
   }
@@ -589,16 +582,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
       for (int h = 0; h < 2; ++h) {
         const int64_t xf = 2 * x + h;
         if (xf >= ld4) continue;
-        float o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t c = 4 * xf + j;
-          float val = rs ? acc[q][4 * h + j] * sr : acc[q][4 * h + j];
-          if (c >= d.width) val = 0.f;
-          else if (d.on) val = keep_at(d, kr, c) ? val * d.scale : 0.f;
-          o[j] = val;
-        }
-        __stcs(J + u0 * ld4 + xf, make_float4(o[0], o[1], o[2], o[3]));
+        float4 o = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
+        if (rs) o = f4scale(o, sr);
+        __stcs(J + u0 * ld4 + xf, drop4(o, xf, kr, 1.f, d));
       }
     }
   }
