@@ -7,9 +7,14 @@ every partition with the boundary exchange, loss, backward with stale-gradient a
 gradient all-reduce and the Adam update (Table 3) -- every row of SURVEY.md section 8(a).
 Workload at N=1: BASELINE configs[1], the synthetic Reddit-shaped graph (232,965 nodes,
 ~114.6M CSR non-zeros, 602 features, 41 classes), 4-layer GraphSAGE hidden 256, 2 partitions
-hosted on the one GPU (local transport), PIPE mode, dropout 0.5, fp32.
-Timing: W untimed warm-up iterations, then K iterations bracketed by CUDA events on the
-context stream (synchronize on both sides); inputs are far larger than L2 (X alone 563 MB).
+hosted on the one GPU exchanging through the LOOPBACK transport (the NCCL path's posted exchange:
+pack -> comm stream -> one device copy per peer segment -> events), PIPE mode, dropout 0.5, Adam,
+fp32 tier.  N > 1: one partition per GPU over NCCL; run outside torchrun, `--gpus N` launches the N
+ranks itself and refuses (exit 3) when fewer than N GPUs are visible.
+Timing: W untimed warm-up iterations, then K iterations bracketed by CUDA events on the context
+stream (barrier + synchronize on both sides, max over ranks), no per-kernel instrumentation; a
+second, instrumented pass gives the per-kernel breakdown and the roofline; inputs are far larger
+than L2 (X alone 563 MB).
 """
 import argparse
 import json
@@ -22,6 +27,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "full-graph epochs/s (max over ranks)"
+EXIT_NOT_ENOUGH_GPUS = 3
 UNIT = "epochs/s"
 
 
@@ -46,6 +52,13 @@ def parse():
     ap.add_argument("--tile-min", type=int, default=0, help="heavy-tile threshold in edges per 128x64 tile (0: library default)")
     ap.add_argument("--no-train-sparse", action="store_true",
                     help="compute the last layer on every row (default: only on train rows, SURVEY N1(ii); exact)")
+    ap.add_argument("--transport", default="loopback", choices=["loopback", "local"],
+                    help="single-GPU runs: 'loopback' = the posted exchange of the NCCL path (pack -> comm stream "
+                         "-> one device copy per peer segment -> events; App. F) or 'local' = direct gathers")
+    ap.add_argument("--halo-payload", default="f32", choices=["f32", "bf16"],
+                    help="bf16: exchange payloads rounded to bf16 (SURVEY N1(iv), 2e-2 tier)")
+    ap.add_argument("--depth", type=int, default=1, help="pipeline depth s (R27)")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the no-communication timing ablation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -110,48 +123,6 @@ def peaks():
                 "_fallback": True}
 
 
-def l2_ceilings(pgcn, torch, g_rp, n_rows, stream):
-    """Roofline denominators for the L2-served aggregation, measured live:
-    l2_read   -- hardware L2 streaming-read bandwidth (64 MB buffer, resident in the 126 MB L2);
-    gather_*  -- the product SpMM kernel (pgcn_dev_spmm) on this partition's row pointers with
-                 random columns into an L2-resident 30k-row table (604- and 256-wide rows)."""
-    import numpy as np
-    L = pgcn.lib()
-    s = stream.cuda_stream
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nbytes = 64 << 20
-    buf = torch.ones(nbytes // 4, device="cuda")
-    out = torch.empty(148 * 8, device="cuda")
-    reps = 50
-    best = 0.0
-    for variant in (0, 1, 2):
-        with torch.cuda.stream(stream):
-            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | 2, out.data_ptr(), s)
-            e0.record(stream)
-            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | reps, out.data_ptr(), s)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
-    res = {"l2_read_GBps": best}
-    rp = torch.tensor(g_rp, device="cuda")
-    nnz = int(g_rp[-1])
-    col = torch.randint(0, 30000, (nnz,), device="cuda", dtype=torch.int32)
-    inv = torch.ones(n_rows, device="cuda")
-    for ld in (604, 256):
-        D = torch.randn(30000, ld, device="cuda")
-        Z = torch.empty(n_rows, ld, device="cuda")
-        args = (rp.data_ptr(), col.data_ptr(), inv.data_ptr(), D.data_ptr(), ld, n_rows, 30000, Z.data_ptr(), s)
-        with torch.cuda.stream(stream):
-            L.pgcn_dev_spmm(*args)
-            e0.record(stream)
-            for _ in range(3):
-                L.pgcn_dev_spmm(*args)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        res["gather_%d_GBps" % ld] = 3 * 4.0 * ld * nnz / (e0.elapsed_time(e1) / 1e3) / 1e9
-    return res
-
-
 def max_over_ranks(x, dist):
     """Device-timed milliseconds -> the max over ranks (the slowest rank sets the epoch time)."""
     if dist is None:
@@ -195,7 +166,9 @@ def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2, model="sage"
     scale = c["n"] / sample_n
     epoch_s = dt * scale
     cores = len(os.sched_getaffinity(0))
-    return {"value": 1.0 / epoch_s, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": 1.0 / epoch_s, "unit": UNIT, "cores": cores, "kind": "oracle", "extrapolated": True,
+            "extrapolation": "measured s/iteration on the N=%d sample x N_full/N_sample = %.1f (every epoch term is "
+                             "linear in N at fixed degree and widths)" % (sample_n, c["n"] / sample_n),
             "sample": "oracle PipeGCN (%s, %s) %d iterations on a %s-recipe graph with N=%d (nnz=%d, same degree, "
                       "widths, dropout, %d partitions); %.2f s/iteration x N_full/N_sample=%.1f" % (
                           mode, model, iters, name, sample_n, g.nnz, parts, dt, scale)}
@@ -228,11 +201,97 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def spawn_ranks(args):
+    """`--gpus N` (N > 1) outside torchrun: launch N ranks (one partition per GPU, NCCL) with
+    torch.distributed.run on 127.0.0.1.  Refuses (exit 3, one JSON line) when fewer than N GPUs are
+    visible -- a multi-GPU number is never produced by a single GPU."""
+    import socket
+
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": "--gpus %d needs %d visible GPUs, found %d" % (args.gpus, args.gpus, n),
+                          "n_gpus": args.gpus, "n_gpus_visible": n}))
+        sys.exit(EXIT_NOT_ENOUGH_GPUS)
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % args.gpus,
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def roofline(name, kd, pk, args, l2_peak):
+    """Roofline object of the dominant kernel.  Per launch: achieved = algorithmic
+    bytes (or flops) / mean launch duration, both measured live with CUDA events on the context
+    stream during the instrumented pass.
+      spmm_*  bound hbm: B_min (gathered table read once -- the compulsory traffic) over the measured
+              HBM copy peak; beside it the per-edge B_gather model over the live L2 read peak.
+      gemm_*  bound tensor: tensor-pipe flops executed (3xTF32 = 3 tf32 MMAs per fp32 product; bf16:
+              1) over the dense peak of that dtype (MEASURED bf16 x nominal tf32/bf16 ratio 1/2).
+      other   bound hbm: algorithmic bytes over the HBM copy peak."""
+    n = max(kd["launches"], 1)
+    sec = kd["ms"] / 1e3 / n
+    roof = {"kernel": name, "launches_timed": kd["launches"], "ms_per_launch": kd["ms"] / n}
+    tr = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get(name)
+    except Exception:
+        pass
+    if name.startswith("gemm"):
+        mult = 1.0 if args.gemm == "bf16" else 3.0
+        peak = pk["bf16_tflops"] * (1.0 if args.gemm == "bf16" else 0.5)
+        ach = mult * kd["flops"] / n / sec / 1e12
+        roof.update(bound="tensor", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
+                    peak_source="MEASURED_PEAKS.json bf16_tflops%s" % ("" if args.gemm == "bf16" else " x 1/2 (tf32)"),
+                    traffic=tr, flops_per_launch=kd["flops"] / n, tensor_flop_multiplier=mult)
+        return roof
+    ach = kd["bytes"] / n / sec / 1e9
+    roof.update(bound="hbm", achieved=ach, peak=pk["hbm_gbs"], unit="GB/s", frac=ach / pk["hbm_gbs"],
+                peak_source="MEASURED_PEAKS.json hbm_gbs", traffic=tr, bytes_per_launch=kd["bytes"] / n)
+    if name.startswith("spmm"):
+        g = kd["gather_bytes"] / n / sec / 1e9
+        roof["B_min_per_launch"] = kd["bytes"] / n
+        roof["B_gather_per_launch"] = kd["gather_bytes"] / n
+        roof["gather_view"] = {"achieved": g, "unit": "GB/s", "hbm_frac": g / pk["hbm_gbs"],
+                               "l2_peak": l2_peak, "l2_frac": (g / l2_peak) if l2_peak else None,
+                               "note": "per-edge model B_gather (a table row per edge); > HBM means L2/L1-served "
+                                       "or on-chip reuse (tensor-core tiles)"}
+        if tr:
+            roof["dram_view"] = {"achieved": tr / sec / 1e9, "frac": tr / sec / 1e9 / pk["hbm_gbs"],
+                                 "note": "ncu DRAM bytes per launch (profiles/) over this run's launch time"}
+    return roof
+
+
+def l2_read_peak(pgcn, torch, stream):
+    """Live L2 streaming-read bandwidth (64 MB buffer, resident in the 126 MB L2): the ceiling of
+    L2-served gathers, reported beside the HBM roofline."""
+    L = pgcn.lib()
+    s = stream.cuda_stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nbytes = 64 << 20
+    buf = torch.ones(nbytes // 4, device="cuda")
+    out = torch.empty(148 * 8, device="cuda")
+    reps, best = 50, 0.0
+    for variant in (0, 1, 2):
+        with torch.cuda.stream(stream):
+            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | 2, out.data_ptr(), s)
+            e0.record(stream)
+            L.pgcn_dev_l2_read(buf.data_ptr(), nbytes, (variant << 24) | reps, out.data_ptr(), s)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     import numpy as np
     import torch
 
@@ -241,6 +300,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -248,7 +309,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = local_rank
     torch.cuda.set_device(dev)
-    # N = 1: the configuration's partitions hosted on one GPU (local transport); N > 1: one
+    # N = 1: the configuration's partitions hosted on one GPU (loopback or local transport); N > 1: one
     # partition per GPU (NCCL transport), n_parts = N.
     parts = args.parts or (max(2, args.gpus) if world == 1 else world)
     if world > 1 and parts != world:
@@ -257,11 +318,14 @@ def main():
     t0 = time.time()
     part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
     t_part = time.time() - t0
+    transport = args.transport if world == 1 else "nccl"
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
                            n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
                            train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles,
-                           tile_min=args.tile_min)
+                           tile_min=args.tile_min, depth=args.depth,
+                           transport="loopback" if transport == "loopback" else "local",
+                           halo_payload=args.halo_payload)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
@@ -293,73 +357,68 @@ def main():
             t += 1
             ctx.step(t, theta, grads, opt, loss)
     torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(k_steps, per_step=None):
+        """k_steps iterations bracketed by CUDA events on the context stream (barrier + synchronize on
+        both sides); returns the max over ranks of the elapsed milliseconds."""
+        nonlocal t
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(k_steps):
+            t += 1
+            ctx.step(t, theta, grads, opt, loss)
+            if per_step is not None:
+                per_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1), dist)
+
+    # (1) headline: K iterations, no instrumentation
     clocks = Clocks(dev)
     clocks.start()
     launches0 = ctx.launch_count()
-    ctx.timing_enable(True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-        torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(K):
-        t += 1
-        ctx.step(t, theta, grads, opt, loss)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1), dist)
+    xb0 = ctx.exchange_bytes()
+    ms_total = timed(K)
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
-    kern = {name: ctx.timing_read(k) for k, name in enumerate(pgcn.KERNELS)}
-    ctx.timing_enable(False)
+    xb1 = ctx.exchange_bytes()
     ms = ms_total / K
     value = 1000.0 / ms
     loss_v = float(loss.item())
+    # (2) instrumented pass: per-kernel CUDA events on the context stream (roofline, breakdown)
+    ctx.timing_enable(True)
+    ms_instr = timed(K) / K
+    kern = {name: ctx.timing_read(k) for k, name in enumerate(pgcn.KERNELS)}
+    ctx.timing_enable(False)
 
-    # End to end through the public API: every step's inputs are copied from pinned host memory
-    # (H2D over PCIe on a copy stream into a double-buffered device staging area, prefetched one
-    # step ahead so the copy overlaps the previous step's compute), installed with pgcn_set_inputs
-    # (device-to-device into the padded layout) and the step's loss is read back to the host.
+    # (3) end to end through the C ABI with HOST buffers: every iteration's X, labels and train mask
+    # are copied from pinned host memory by pgcn_stage_inputs (library copy stream, overlapped with the
+    # iteration in flight), and each iteration's loss is read back to the host.
     e2e = None
     if args.config.startswith("papers"):
-        # 14 GB of inputs per step over PCIe would dominate and double-buffered device staging does
-        # not fit next to the 2-partition workspace: no end-to-end leg for the papers-shaped graph
-        args.no_e2e = True
+        args.no_e2e = True  # 14 GB of inputs per step over PCIe: no end-to-end leg for the papers shape
     if not args.no_e2e:
         loss_h = torch.zeros(1).pin_memory()
         h2d = sum(sum(a.numel() * a.element_size() for a in h) for h in host)
-        copy_s = torch.cuda.Stream()
-        stage = [[tuple(torch.empty_like(a, device="cuda") for a in h) for h in host] for _ in range(2)]
-        ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_used = [torch.cuda.Event(), torch.cuda.Event()]
-
-        def issue_copy(k):
-            buf = stage[k % 2]
-            with torch.cuda.stream(copy_s):
-                copy_s.wait_event(ev_used[k % 2])
-                for i in range(nloc):
-                    for dst, src in zip(buf[i], host[i]):
-                        dst.copy_(src, non_blocking=True)
-                ev_copied[k % 2].record(copy_s)
-
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         e0 = time.perf_counter()
         ev0.record(stream)
-        issue_copy(0)
+        for i in range(nloc):
+            ctx.stage_inputs(i, *host[i])
         for k in range(K):
             t += 1
-            stream.wait_event(ev_copied[k % 2])
-            for i in range(nloc):
-                ctx.set_inputs(i, *stage[k % 2][i])
-            ev_used[k % 2].record(stream)
-            if k + 1 < K:
-                issue_copy(k + 1)
             ctx.step(t, theta, grads, opt, loss)
+            if k + 1 < K:
+                for i in range(nloc):
+                    ctx.stage_inputs(i, *host[i])
             with torch.cuda.stream(stream):
                 loss_h.copy_(loss, non_blocking=True)
             stream.synchronize()
@@ -369,50 +428,27 @@ def main():
         e_ms = max_over_ranks(ev0.elapsed_time(ev1), dist) / K
         e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
                "ms_per_step": e_ms, "host_wall_ms_per_step": 1000.0 * (time.perf_counter() - e0) / K,
-               "note": "pinned host -> device copy of every step's X, labels, train mask (prefetched one step "
-                       "ahead on a copy stream), pgcn_set_inputs, pgcn_step, loss read back each step"}
+               "note": "pgcn_stage_inputs(host pinned X, labels, train mask) every iteration (library copy "
+                       "stream, overlapped with the iteration in flight) + pgcn_step + loss read back each step"}
+
+    # (4) exposed communication: the same iterations with the transfers skipped (PGCN_XH_NOCOMM;
+    # timing only -- the halo state is stale afterwards).  exposed = T - T_nocomm.
+    comm_info = None
+    if transport != "local":
+        comm_info = {"transport": transport, "payload": args.halo_payload,
+                     "bytes_per_step": {"fwd": (xb1[0] - xb0[0]) / K, "bwd": (xb1[1] - xb0[1]) / K}}
+        if not args.no_ablation:
+            ctx.exchange_hook(0, pgcn.XH_NOCOMM)
+            ms_nc = timed(K) / K
+            ctx.exchange_hook(0, 0)
+            comm_info.update(ms_per_step_nocomm=ms_nc, exposed_ms_per_step=ms - ms_nc)
 
     pk = peaks()
-    top = max(kern.items(), key=lambda kv: kv[1]["ms"])
-    name, kd = top
-    if name.startswith("gemm") and args.gemm == "simt":
-        # SIMT fp32: bound by FFMA issue, 148 SMs x 128 lanes x 2 flop x max SM clock
-        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        ach = kd["flops"] / (kd["ms"] / 1e3) / 1e12
-        roof = {"kernel": name, "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
-    elif name.startswith("spmm") and args.config.startswith("papers"):
-        # papers-shaped partitions (13.9M rows x 192 B) are far larger than L2: the per-edge gathers
-        # are DRAM-side, so the SpMM is reported against the measured HBM copy peak (north_star).
-        ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    elif name.startswith("spmm"):
-        # L2-served aggregation: bound = L2, peak = measured L2 streaming read.  Algorithmic bytes per
-        # launch (engine Scope): per-edge gather model s*F*nnz on the gather path; on the
-        # tensor-core tile path what that algorithm moves instead -- heavy-tile table rows (hi/lo) and
-        # bitmasks per tile, light-edge gathers, the hi/lo split, tile-sum write + re-read (DESIGN.md
-        # "Tensor-core tiles").  The contract's HBM view (same bytes / measured HBM copy) beside it.
-        ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
-        l2 = l2_ceilings(pgcn, torch, views[0]["row_ptr"], int(views[0]["n_inner"]), stream)
-        roof = {"kernel": name, "bound": "l2", "achieved": ach, "peak": l2["l2_read_GBps"], "unit": "GB/s",
-                "frac": ach / l2["l2_read_GBps"], "peak_source": "measured live: L2 streaming read, 64 MB",
-                "gather_ceiling_GBps": {"604": l2["gather_604_GBps"], "256": l2["gather_256_GBps"]},
-                "hbm_view": {"peak": pk["hbm_gbs"], "frac": ach / pk["hbm_gbs"],
-                             "note": "same algorithmic bytes over the measured HBM copy peak; > 1 means L2-served"}}
-    else:
-        ach = kd["bytes"] / (kd["ms"] / 1e3) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / pk["hbm_gbs"]}
-    roof["launches_timed"] = kd["launches"]
-    roof["ms_per_launch"] = kd["ms"] / max(kd["launches"], 1)
-    roof["share_of_step"] = kd["ms"] / ms_total
-    roof["traffic"] = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        roof["traffic"] = tr.get(name)
-    except Exception:
-        pass
-    breakdown = {k: {"ms_per_step": v["ms"] / K, "share": v["ms"] / ms_total,
+    name, kd = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    l2p = l2_read_peak(pgcn, torch, stream) if name.startswith("spmm") else None
+    roof = roofline(name, kd, pk, args, l2p)
+    roof["share_of_step"] = kd["ms"] / (ms_instr * K)
+    breakdown = {k: {"ms_per_step": v["ms"] / K, "share": v["ms"] / (ms_instr * K),
                      "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
                      "TFLOPs": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None}
                  for k, v in kern.items() if v["launches"]}
@@ -424,24 +460,30 @@ def main():
             cpu = {"error": str(e)}
     if rank != 0:
         return
+    tier = {("f32", "tc"): "fp32 tier: 3xTF32 tensor-core GEMMs, fp32 gathers, 2xbf16-split tile aggregation"
+                           if not args.no_tiles else "fp32 tier: 3xTF32 tensor-core GEMMs, IEEE fp32 gathers",
+            ("f32", "simt"): "IEEE fp32 (SIMT GEMMs, fp32 gathers)%s" % ("" if args.no_tiles else ", 2xbf16 tiles"),
+            ("f32", "bf16"): "bf16 tensor-core GEMMs, fp32 gathers (2e-2 tier)",
+            ("bf16", "tc"): "3xTF32 GEMMs, bf16 gathers (2e-2 tier)",
+            ("bf16", "bf16"): "bf16 tensor-core GEMMs and gathers (2e-2 tier)",
+            ("bf16", "simt"): "SIMT GEMMs, bf16 gathers (2e-2 tier)"}[(args.gather, args.gemm)]
+    dtype = "f32" if (args.gather, args.gemm, args.halo_payload) == ("f32", "tc", "f32") or args.gemm == "simt" else "bf16"
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "f32" if args.gather == "f32" and args.gemm != "bf16" else
-           ("bf16" if args.gather == "bf16" and args.gemm == "bf16" else
-            "mixed: %s gathers, %s GEMM" % (args.gather, "bf16" if args.gemm == "bf16" else "3xTF32")),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+           "precision": tier + ("" if args.halo_payload == "f32" else "; bf16 exchange payloads"),
            "data": "synthetic",
            "config": {"workload": "%s-synthetic N=%d nnz=%d F=%s, %d partitions on %d GPU(s), %s%s, "
                                   "dropout %.1f, Adam%s" % (args.config, g.n, g.nnz, m.widths, parts, world, args.mode,
                                                             ("-" + args.smooth.upper()) if args.smooth else "",
                                                             m.dropout, "" if args.model == "sage" else ", GCN-sym"),
                       "global_batch": g.n,
-                      "parallelism": ("partition x%d (local transport)" % parts) if world == 1 else
-                      ("partition x%d, NCCL p2p halo exchange + all-reduce" % world), "gemm": args.gemm,
-                      "gather": args.gather, "train_sparse_last_layer": not args.no_train_sparse,
-                      "spmm_tiles": not args.no_tiles,
+                      "parallelism": ("partition x%d on one GPU (%s transport)" % (parts, transport)) if world == 1 else
+                      ("partition x%d, one per GPU: NCCL p2p halo exchange on a comm stream + all-reduce" % world),
+                      "gemm": args.gemm, "gather": args.gather, "depth": args.depth,
+                      "train_sparse_last_layer": not args.no_train_sparse, "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-           "breakdown": breakdown, "loss": loss_v,
+           "comm": comm_info, "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
            "setup_s": {"generate": t_gen, "partition": t_part},
            "workspace_GB": ctx.ws.numel() / 1e9}
     print(json.dumps(out))

@@ -178,6 +178,22 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       heavy tiles hold >= 25 % of a pattern's edges and every neighbour row is
  *                       valid (t > s).  0: gather SpMM only.
  *   tile_min            heavy-tile threshold in edges per 128 x 64 tile (0: default 96).
+ *   transport           single-process contexts only (multi-process runs always use NCCL):
+ *                       0 LOCAL    -- the install reads the owners' rows straight out of their buffers
+ *                                     and the accumulate reads the peers' boundary-row gradients (one
+ *                                     gather kernel each, no message buffers);
+ *                       1 LOOPBACK -- the posted exchange of the NCCL transport (Alg. 1 l.12-13, l.27;
+ *                                     App. F: a second stream carries all communication):
+ *                                     pack S_{i,j} rows on the compute stream, event, then on the comm
+ *                                     stream one cudaMemcpyAsync per (sender, receiver) segment into the
+ *                                     receiver's boundary rows / gradient message buffer, event; the
+ *                                     consumer waits for the event of the iteration it consumes.  Same
+ *                                     buffers, rotation, events and waits as NCCL; the transfer is a
+ *                                     device copy instead of ncclSend/ncclRecv.
+ *   halo_payload        posted transports (LOOPBACK, NCCL): 0 fp32 exchange payloads; 1 bf16 payloads
+ *                       (SURVEY N1(iv), 2e-2 tier): the packed boundary features and the boundary-row
+ *                       gradients are rounded to bf16 (round to nearest even) for the transfer and
+ *                       widened on receipt (EMA and sums in fp32) -- half the exchanged bytes.
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -203,6 +219,8 @@ typedef struct {
   int32_t train_sparse;
   int32_t spmm_tiles;
   int32_t tile_min;
+  int32_t transport;
+  int32_t halo_payload;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this
@@ -239,6 +257,19 @@ int pgcn_ctx_destroy(pgcn_ctx* ctx);
  * or device pointers; copied asynchronously on the context stream into the workspace.     */
 int pgcn_set_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* labels,
                     const uint8_t* train_mask);
+
+/* Streaming re-upload of a hosted partition's inputs between iterations (the end-to-end path: inputs
+ * live in host memory and are copied every iteration).  Same layouts as pgcn_set_inputs; X, labels and
+ * train_mask are HOST pointers (pinned memory makes the copy asynchronous).  The copies run on the
+ * library's copy stream and overlap the iteration in flight: X is overwritten only after that
+ * iteration's last read of X (layer 1's dropout, or layer 1's weight gradient when dropout = 0),
+ * labels / mask only after its loss; the next pgcn_layer_fwd(layer 1) waits for the copies.  The train
+ * set must be the one given to pgcn_set_inputs (the train row lists are not rebuilt), and X must hold
+ * the same values (X's boundary rows are exchanged once, reading R10).  Caller keeps the host buffers
+ * alive until the next iteration's layer 1 has been enqueued and the stream has passed it.
+ * Errors: PGCN_EINVAL (null / range), PGCN_ESTATE (poisoned, or pgcn_set_inputs never called).     */
+int pgcn_stage_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* labels,
+                      const uint8_t* train_mask);
 
 /* Flat parameter vector theta = vec[W^(1), b^(1), ..., W^(L), b^(L)], fp32,
  * unpadded: W^(l) is [2F_{l-1} x F_l] row-major (rows 0..F_{l-1}-1 multiply z, the rest h;
@@ -305,6 +336,10 @@ enum {
 int pgcn_timing_enable(pgcn_ctx* ctx, int32_t on); /* also resets the accumulators */
 int pgcn_timing_read(pgcn_ctx* ctx, int32_t kind, double* ms, int64_t* launches, double* alg_bytes,
                      double* alg_flops);
+/* For the aggregation kinds (PGCN_K_SPMM_*), alg_bytes above is SURVEY 8(d)'s compulsory B_min (the
+ * gathered table read once); this returns the per-edge B_gather of the same launches (the table row
+ * read once per edge).  Other kinds: equal to alg_bytes.                                            */
+int pgcn_timing_read_gather(pgcn_ctx* ctx, int32_t kind, double* gather_bytes);
 
 #ifdef __cplusplus
 }

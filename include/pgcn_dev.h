@@ -53,6 +53,23 @@ typedef struct pgcn_partitioning pgcn_partitioning;
 int pgcn_dev_tiles(const pgcn_partitioning* p, int32_t part, int32_t which, int32_t tile_min, int64_t* sizes,
                    int32_t* rb_ptr, int32_t* order, int32_t* tile_col, uint64_t* mask, int64_t* lrp, int32_t* lcol);
 
+/* Exchange hook of the posted transports (pgcn_config.transport = LOOPBACK, or NCCL), used by the
+ * stream/event-contract tests (SURVEY 4.6 delay injection) and the exposed-communication ablation:
+ *   spin_ns   > 0: before every transfer (forward and backward, every layer) a one-thread kernel
+ *             spins this many nanoseconds on the comm stream, delaying the messages.  With the
+ *             contract intact results are bit-identical to spin_ns = 0.
+ *   flags     PGCN_XH_SKIP_F_WAIT / PGCN_XH_SKIP_B_WAIT: fault injection -- drop the compute stream's
+ *             wait for the forward / backward exchange events (results must then change under delay);
+ *             PGCN_XH_NOCOMM: skip the transfers themselves (everything else runs; boundary rows keep
+ *             whatever they held -- a timing ablation, T_PIPE - T_nocomm = exposed communication).
+ * Applies to every later call on ctx.  PGCN_EUNSUPPORTED on a LOCAL-transport context.             */
+typedef struct pgcn_ctx pgcn_ctx;
+enum { PGCN_XH_SKIP_F_WAIT = 1, PGCN_XH_SKIP_B_WAIT = 2, PGCN_XH_NOCOMM = 4 };
+int pgcn_dev_exchange_hook(pgcn_ctx* ctx, int64_t spin_ns, int32_t flags);
+/* Payload bytes this context has posted to peers so far (forward features, backward gradients; counted
+ * at enqueue; 0 on a LOCAL-transport context, whose install reads the owners' rows in place).        */
+int pgcn_dev_exchange_bytes(const pgcn_ctx* ctx, int64_t* fwd_bytes, int64_t* bwd_bytes);
+
 #ifdef __cplusplus
 }
 #endif

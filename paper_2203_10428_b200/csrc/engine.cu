@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "tiles.h"
 #include "pgcn.h"
+#include "pgcn_dev.h"
 #ifdef PGCN_WITH_NCCL
 #include <nccl.h>
 #endif
@@ -80,7 +81,15 @@ struct PartCtx {
   const TileSet* ts[2] = {nullptr, nullptr};
   TileDev td[2];
   const TileDev* tiles(int w) const { return ts[w] ? &td[w] : nullptr; }
+  // posted-exchange message buffers (LOOPBACK / NCCL transports; fp32, or bf16 with halo_payload = 1),
+  // rotating over the pipeline depth (slot = t mod (s + 1); layer 1 has one slot: X is exchanged once)
+  void* send_f[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // packed S_{i,j} rows of the layer-l input   [n_send x ld]
+  void* recv_f[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // staged boundary rows (EMA-F or bf16)     [n_bd x ld]
+  void* send_b[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // bf16 boundary-row gradients (bf16 only)  [n_bd x ld]
+  void* recv_b[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // received gradient rows, send order       [n_send x ld]
 };
+
+enum { XP_LOCAL = 0, XP_LOOPBACK = 1, XP_NCCL = 2 };
 
 struct Arena {
   char* base = nullptr;
@@ -100,7 +109,14 @@ struct KTimer {
   std::vector<cudaEvent_t> ev;  // (start, stop) pairs
   size_t used = 0;
   int64_t n = 0;
-  double bytes = 0.0, flops = 0.0;
+  double bytes = 0.0, flops = 0.0, gbytes = 0.0;
+};
+
+// Algorithmic bytes of an aggregation launch: B_min reads the gathered table once
+// (compulsory), B_gather once per edge (the per-edge model); both add the index stream, the output
+// and the epilogue operands (`rest`).
+struct SpmmBytes {
+  double min, gather;
 };
 
 }  // namespace pgcn
@@ -142,8 +158,19 @@ struct pgcn_ctx {
   int64_t launches = 0;
   int timing = 0;
   pgcn::KTimer kt[PGCN_K_COUNT];
-  // ---- NCCL transport (one partition per rank)
+  // ---- exchange transport: LOCAL gathers, or the posted exchange on the comm
+  // stream -- LOOPBACK (device copies between the hosted partitions) or NCCL (one partition per rank)
   int nccl = 0, rank = 0, nranks = 1;
+  int xp = pgcn::XP_LOCAL;
+  int posted = 0;           // xp != XP_LOCAL
+  int p16 = 0;              // bf16 payloads (cfg.halo_payload)
+  int64_t hook_spin_ns = 0; // pgcn_dev_exchange_hook: delay injected on the comm stream before each transfer
+  int32_t hook_flags = 0;   // PGCN_XH_* (pgcn_dev.h)
+  int64_t xbytes[2] = {0, 0};  // payload bytes posted by this context's transfers (fwd, bwd)
+  // ---- streaming inputs (pgcn_stage_inputs): copy stream and its events
+  cudaStream_t cps = nullptr;
+  cudaEvent_t ev_x_free = nullptr, ev_lab_free = nullptr, ev_in_ready = nullptr;
+  int in_pending = 0, inputs_set = 0;
 #ifdef PGCN_WITH_NCCL
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
@@ -151,9 +178,6 @@ struct pgcn_ctx {
   pgcn::Launch launch() { return pgcn::Launch{s, &launches}; }
   cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
   cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};
-  float* send_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // packed S_{i,j} rows of the layer-l input
-  float* recv_f[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // received boundary rows (EMA-F only)
-  float* recv_b[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};  // received gradient rows, send order
   int nb = 2;                                              // buffers in rotation = depth + 1
   int bi(int64_t t) const { return (int)(((t % nb) + nb) % nb); }
   ~pgcn_ctx() {
@@ -172,6 +196,10 @@ struct pgcn_ctx {
     if (cr) ncclCommDestroy(cr);
 #endif
     if (cs) cudaStreamDestroy(cs);
+    if (ev_x_free) cudaEventDestroy(ev_x_free);
+    if (ev_lab_free) cudaEventDestroy(ev_lab_free);
+    if (ev_in_ready) cudaEventDestroy(ev_in_ready);
+    if (cps) cudaStreamDestroy(cps);
   }
 };
 
@@ -197,6 +225,8 @@ int validate_cfg(const pgcn_config* c) {
   if (c->train_sparse != 0 && c->train_sparse != 1) return fail(PGCN_EINVAL, "train_sparse must be 0 or 1");
   if (c->spmm_tiles != 0 && c->spmm_tiles != 1) return fail(PGCN_EINVAL, "spmm_tiles must be 0 or 1");
   if (c->tile_min < 0 || c->tile_min > 128 * 64) return fail(PGCN_EINVAL, "tile_min out of range");
+  if (c->transport != 0 && c->transport != 1) return fail(PGCN_EINVAL, "transport must be 0 (LOCAL) or 1 (LOOPBACK)");
+  if (c->halo_payload != 0 && c->halo_payload != 1) return fail(PGCN_EINVAL, "halo_payload must be 0 (fp32) or 1 (bf16)");
   return PGCN_OK;
 }
 
@@ -207,20 +237,11 @@ int64_t param_count(const pgcn_config* c) {
   return P;
 }
 
-// Algorithmic bytes of an aggregation launch on the tile path (tiles.h / spmm_tc.cu), replacing the
-// per-edge gather term s F nnz of the gather model by what this algorithm moves: the
-// table's split into bf16 hi/lo (fp32 tier: read 4F, write 4F per table row; the bf16 tier's rounding
-// pass is counted by the caller), per heavy tile and n-tile the 64 table rows (hi + lo: 4F per row;
-// bf16: 2F) and the 1 KB bitmask, the tile-sum write and its re-read by the light pass, and the light
-// gathers themselves (s F bytes per light edge).  Bound: L2 (the table slices are L2-resident).
-double tile_path_bytes(const pgcn_ctx* C, const TileDev& T, double F, double n_table) {
-  const double Fp = (double)round_up((int64_t)F, 8);
-  const double row = C->cfg.gather ? 2.0 * Fp : 4.0 * Fp;
-  const double bn = C->cfg.gather ? 256.0 : 128.0;
-  const double n_nt = std::ceil(F / bn);
-  const double split = C->cfg.gather ? 0.0 : 8.0 * Fp * n_table;
-  return split + (double)T.n_tiles * (64.0 * row + 1024.0 * n_nt) + 8.0 * F * (double)T.n_rows +
-         (double)T.nnz_light * row;  // (the caller counts 4 bytes of column index per edge)
+// Posted exchange: boundary features are received into a staging buffer (and installed from it at
+// consume time) under EMA-F (the smoothing needs the previous value) or bf16 payloads;
+// otherwise they land straight in the boundary rows of the layer input that consumes them.
+bool staged_recv(const pgcn_ctx* C, int l) {
+  return C->p16 || (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2);
 }
 
 // Lays out every buffer (dry run when A.base == nullptr).
@@ -326,14 +347,19 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
   C->dw_ws_floats = dw_need;
   C->dw_ws = A.take<float>(dw_need);
   if (C->sp_tmp_bytes > 0) C->sp_tmp = A.take<char>(C->sp_tmp_bytes);
-  if (C->nccl && n_local == 1) {
-    const PartCtx& p = C->parts[0];
-    for (int l = 1; l <= L; ++l)
-      for (int b = 0; b < (l == 1 ? 1 : C->nb); ++b) {
-        C->send_f[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
-        if (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2) C->recv_f[l][b] = A.take<float>(p.n_bd * C->ld[l - 1]);
-        if (l >= 2) C->recv_b[l][b] = A.take<float>(p.n_send * C->ld[l - 1]);
-      }
+  if (C->posted) {  // message buffers of the posted exchange (per hosted partition, per rotation slot)
+    const int64_t eb = C->p16 ? 2 : 4;  // payload bytes per element
+    for (auto& p : C->parts)
+      for (int l = 1; l <= L; ++l)
+        for (int b = 0; b < (l == 1 ? 1 : C->nb); ++b) {
+          const int64_t ld = C->ld[l - 1];
+          p.send_f[l][b] = A.take<char>(eb * p.n_send * ld);
+          if (staged_recv(C, l)) p.recv_f[l][b] = A.take<char>(eb * p.n_bd * ld);
+          if (l >= 2) {
+            if (C->p16) p.send_b[l][b] = A.take<char>(eb * p.n_bd * ld);
+            p.recv_b[l][b] = A.take<char>(eb * p.n_send * ld);
+          }
+        }
   }
   const int64_t ns = C->ns;  // weight row segments: 2 GraphSAGE [W_neigh; W_self], 1 GCN-sym
   if (C->cfg.gemm == 0) {     // 3xTF32 operand copies: fp32 hi/lo, k-blocks of 32
@@ -388,13 +414,19 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
     C->nccl = 1;
     C->rank = comm->rank;
     C->nranks = comm->nranks;
+    C->xp = XP_NCCL;
 #endif
   } else {
     if (n_local != v0.n_parts)
       return fail(PGCN_EUNSUPPORTED, "a single-process context hosts all %d partitions (got %d)", v0.n_parts, n_local);
     for (int i = 0; i < n_local; ++i)
       if (local[i] != i) return fail(PGCN_EINVAL, "local_parts must be 0..n_parts-1 in order");
+    C->xp = cfg->transport == 1 ? XP_LOOPBACK : XP_LOCAL;
   }
+  C->posted = C->xp != XP_LOCAL;
+  C->p16 = cfg->halo_payload == 1;
+  if (C->p16 && !C->posted)
+    return fail(PGCN_EUNSUPPORTED, "bf16 exchange payloads need a posted transport (LOOPBACK or NCCL)");
   if (cfg->n_global != pgcn_partition_n_nodes(part)) return fail(PGCN_EINVAL, "cfg.n_global != partition N");
   C->cfg = *cfg;
   C->L = cfg->n_layers;
@@ -483,7 +515,8 @@ inline float* layer_in(PartCtx& p, int l, int b) { return l == 1 ? p.X : p.H[l -
 struct Scope {
   pgcn_ctx* C;
   int k;
-  Scope(pgcn_ctx* c, int kind, double bytes, double flops = 0.0) : C(c), k(kind) {
+  Scope(pgcn_ctx* c, int kind, SpmmBytes sb) : Scope(c, kind, sb.min, 0.0, sb.gather) {}
+  Scope(pgcn_ctx* c, int kind, double bytes, double flops = 0.0, double gbytes = -1.0) : C(c), k(kind) {
     if (!C->timing) return;
     KTimer& t = C->kt[k];
     if (t.used + 2 > t.ev.size()) {
@@ -497,6 +530,7 @@ struct Scope {
     t.n += 1;
     t.bytes += bytes;
     t.flops += flops;
+    t.gbytes += gbytes >= 0.0 ? gbytes : bytes;
   }
   ~Scope() {
     if (!C->timing) return;
@@ -511,101 +545,202 @@ int nccl_fail(pgcn_ctx* C, ncclResult_t r, const char* where) {
   C->poisoned = 1;
   return fail(PGCN_ENCCL, "%s: %s", where, ncclGetErrorString(r));
 }
+#endif
 
-// Alg. 1 l.9-13 over NCCL (one partition per rank).  PIPE: wait for the exchange posted at t-1
-// (and smooth it, Sec. 3.4), then post this iteration's exchange, consumed at t+1; the receive
-// lands directly in the boundary rows of the next parity buffer.  VANILLA: post and wait.
-// Depth s (R27): the exchange posted at t is consumed at t + s; buffers rotate over s + 1 slots.
-int nccl_fwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, float* Hin, const Launch& Lk, int64_t* n_valid) {
+// ---------------------------------------------------------------------------------------------------
+// Posted exchange (LOOPBACK / NCCL transports).  One code path for both; only the transfer of a
+// segment differs (ncclSend/ncclRecv across ranks vs one cudaMemcpyAsync from the sender's buffer into
+// the receiver's, both on the comm stream).  Stream/event contract, per layer l:
+//   forward  (Alg. 1 l.9-13)  consume: the compute stream waits ev_f_done[l][t-s] (PIPE) before the
+//                             install / the layer reads its boundary rows;
+//                             post:    pack S_{i,j} rows (compute stream) -> ev_f_pack -> comm stream
+//                             transfers into the receivers' rows read at t+s (PIPE) or t (VANILLA, which
+//                             then waits at once) -> ev_f_done[l][t].
+//   backward (Alg. 1 l.22-27) post:    ev_b_ready (J^(l-1) complete) -> comm stream transfers of the
+//                             boundary-row gradients into the owners' recv_b[l][t] -> ev_b_done[l][t];
+//                             consume: wait ev_b_done[l][t-s] (PIPE) or [t] (VANILLA), then accumulate.
+// Rotation over s + 1 slots makes every buffer's next writer wait (through these events) for its
+// last reader: send_f[t] is repacked at t+s+1 after the wait at t+s for ev_f_done[t]; recv_b[t] is
+// rewritten at t+s+1 after ev_b_ready, recorded behind the accumulate of t+s that consumed it; the J
+// boundary rows sent at t are rewritten at t+s+1, after the wait for ev_b_done[t] at t+s.
+namespace {
+
+// destination of the boundary-row features received at (t, l) by hosted partition q, and whether the
+// receive goes to the staging buffer (installed at consume time) instead of the consuming rows
+void* fwd_dst(pgcn_ctx* C, PartCtx& q, int64_t t, int l) {
+  const int64_t ldi = C->ld[l - 1];
+  const bool pipe = C->cfg.mode == 1;
+  if (staged_recv(C, l)) return q.recv_f[l][l == 1 ? 0 : C->bi(t)];
+  if (l == 1) return q.X + q.n_in * ldi;
+  if (!pipe) return q.H[l - 1][C->bi(t)] + q.n_in * ldi;
+  return q.H[l - 1][C->bi(t + C->depth)] + q.n_in * ldi;  // lands in the buffer read at t + s
+}
+
+// Alg. 1 l.12-13 / l.27 transfers of hosted partition i (sender) for one direction.  fwd: i's packed
+// S_{i,j} rows -> j's boundary segment for owner i; bwd: i's boundary rows owned by j -> j's message
+// rows for i (send order).  NCCL: one grouped send/recv per peer; LOOPBACK: one copy per segment.
+int transfer(pgcn_ctx* C, int64_t t, int l, bool fwd) {
+  const int64_t ldi = C->ld[l - 1];
+  const int64_t eb = C->p16 ? 2 : 4;
+  const int b = C->bi(t);
+  if (C->hook_spin_ns > 0) spin_ns(C->cs, C->hook_spin_ns);
+  if (C->hook_flags & PGCN_XH_NOCOMM) return PGCN_OK;
+  if (C->xp == XP_LOOPBACK) {
+    for (auto& pi : C->parts) {
+      const int i = pi.part;
+      for (auto& pj : C->parts) {
+        const int j = pj.part;
+        if (j == i) continue;
+        if (fwd) {
+          const int64_t n = pi.v.send_off[j + 1] - pi.v.send_off[j];
+          if (!n) continue;
+          const char* src = static_cast<const char*>(pi.send_f[l][l == 1 ? 0 : b]) + eb * pi.v.send_off[j] * ldi;
+          char* dst = static_cast<char*>(fwd_dst(C, pj, t, l));
+          const int64_t row_b = staged_recv(C, l) ? eb * ldi : 4 * ldi;  // unstaged receives are fp32 rows
+          cudaMemcpyAsync(dst + row_b * pj.v.halo_off[i], src, (size_t)(eb * n * ldi), cudaMemcpyDeviceToDevice, C->cs);
+          C->xbytes[0] += eb * n * ldi;
+        } else {
+          const int64_t n = pi.v.halo_off[j + 1] - pi.v.halo_off[j];
+          if (!n) continue;
+          const char* src = C->p16 ? static_cast<const char*>(pi.send_b[l][b]) + eb * pi.v.halo_off[j] * ldi
+                                   : reinterpret_cast<const char*>(pi.J[l - 1][b] + (pi.n_in + pi.v.halo_off[j]) * ldi);
+          char* dst = static_cast<char*>(pj.recv_b[l][b]) + eb * pj.v.send_off[i] * ldi;
+          cudaMemcpyAsync(dst, src, (size_t)(eb * n * ldi), cudaMemcpyDeviceToDevice, C->cs);
+          C->xbytes[1] += eb * n * ldi;
+        }
+      }
+    }
+    return PGCN_OK;
+  }
+#ifdef PGCN_WITH_NCCL
+  PartCtx& p = C->parts[0];
+  const ncclDataType_t ty = C->p16 ? ncclBfloat16 : ncclFloat;
+  ncclResult_t r = ncclGroupStart();
+  for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
+    if (j == C->rank) continue;
+    const int64_t ns = p.v.send_off[j + 1] - p.v.send_off[j], nh = p.v.halo_off[j + 1] - p.v.halo_off[j];
+    if (fwd) {
+      const char* sendb = static_cast<const char*>(p.send_f[l][l == 1 ? 0 : b]);
+      char* dst = static_cast<char*>(fwd_dst(C, p, t, l));
+      const int64_t row_b = staged_recv(C, l) ? eb * ldi : 4 * ldi;
+      if (ns) r = ncclSend(sendb + eb * p.v.send_off[j] * ldi, (size_t)(ns * ldi), ty, j, C->ch, C->cs);
+      C->xbytes[0] += eb * ns * ldi;
+      if (nh && r == ncclSuccess) r = ncclRecv(dst + row_b * p.v.halo_off[j], (size_t)(nh * ldi), ty, j, C->ch, C->cs);
+    } else {
+      const char* src = C->p16 ? static_cast<const char*>(p.send_b[l][b]) + eb * p.v.halo_off[j] * ldi
+                               : reinterpret_cast<const char*>(p.J[l - 1][b] + (p.n_in + p.v.halo_off[j]) * ldi);
+      if (nh) r = ncclSend(src, (size_t)(nh * ldi), ty, j, C->ch, C->cs);
+      C->xbytes[1] += eb * nh * ldi;
+      if (ns && r == ncclSuccess)
+        r = ncclRecv(static_cast<char*>(p.recv_b[l][b]) + eb * p.v.send_off[j] * ldi, (size_t)(ns * ldi), ty, j, C->ch,
+                     C->cs);
+    }
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return nccl_fail(C, r != ncclSuccess ? r : r2, fwd ? "halo exchange (fwd)" : "halo exchange (bwd)");
+  return PGCN_OK;
+#else
+  return fail(PGCN_EUNSUPPORTED, "library built without NCCL");
+#endif
+}
+
+}  // namespace
+
+// Alg. 1 l.9-13 for every hosted partition: consume the exchange of t - s (PIPE) and post this
+// iteration's, consumed at t + s (PIPE) or right away (VANILLA).  X is exchanged once (R10).
+// n_valid[i]: rows of partition i's layer input that hold data this iteration.
+int post_fwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, int64_t* n_valid) {
   const bool pipe = C->cfg.mode == 1;
   const int64_t s = C->depth;
   const int b = C->bi(t), bp = C->bi(t - 1), bs = C->bi(t - s);
   const int64_t ldi = C->ld[l - 1];
-  *n_valid = p.n_all;
+  const bool staged = staged_recv(C, l);
+  const bool skip_wait = (C->hook_flags & PGCN_XH_SKIP_F_WAIT) != 0;
+  // consume (PIPE): the exchange posted at t - s (layer 1: the one X exchange of t = 1)
   if (pipe && t > s) {
-    if (l == 1) {
-      cudaStreamWaitEvent(C->s, C->ev_f_done[1][C->bi(1)], 0);  // X boundary rows, received at t = 1 (R10)
-    } else {
-      cudaStreamWaitEvent(C->s, C->ev_f_done[l][bs], 0);
-      if (C->cfg.smooth_f && p.n_bd > 0) {
-        SegTable src{};
-        src.n_seg = 1;
-        src.off[1] = p.n_bd;
-        src.base[0] = C->recv_f[l][bs];
-        const bool first = C->cfg.ema_init == 0 && t == s + 1;
-        Scope sc(C, PGCN_K_GATHER, 12.0 * C->F[l - 1] * p.n_bd);
-        gather_rows(Lk, src, nullptr, p.n_bd, ldi, Hin + p.n_in * ldi, p.H[l - 1][bp] + p.n_in * ldi,
-                    (float)C->cfg.gamma, 1, first);
+    if (!skip_wait) cudaStreamWaitEvent(C->s, C->ev_f_done[l][l == 1 ? C->bi(1) : bs], 0);
+    if (staged && (l >= 2 || t == s + 1)) {
+      const bool ema = C->cfg.smooth_f && l >= 2;
+      const bool first = ema && C->cfg.ema_init == 0 && t == s + 1;
+      for (auto& p : C->parts) {
+        if (p.n_bd == 0) continue;
+        float* dst = layer_in(p, l, b) + p.n_in * ldi;
+        const void* src = p.recv_f[l][l == 1 ? 0 : bs];
+        const float* prev = p.H[l - 1][bp] + p.n_in * ldi;  // (l >= 2) previous smoothed value
+        Scope sc(C, PGCN_K_GATHER, ((C->p16 ? 6.0 : 8.0) + (ema && !first ? 4.0 : 0.0)) * C->F[l - 1] * p.n_bd);
+        if (C->p16) {
+          install_bf16(Lk, src, p.n_bd, ldi, dst, prev, (float)C->cfg.gamma, ema && !first);
+        } else {
+          SegTable tab{};
+          tab.n_seg = 1;
+          tab.off[1] = p.n_bd;
+          tab.base[0] = static_cast<const float*>(src);
+          gather_rows(Lk, tab, nullptr, p.n_bd, ldi, dst, prev, (float)C->cfg.gamma, ema, first);
+        }
       }
     }
   }
-  if (l == 1 ? t == 1 : true) {
-    if (p.n_send > 0) {
-      SegTable src{};
-      src.n_seg = 1;
-      src.off[1] = p.n_send;
-      src.base[0] = Hin;
-      Scope sc(C, PGCN_K_GATHER, 8.0 * C->F[l - 1] * p.n_send + 4.0 * p.n_send);
-      gather_rows(Lk, src, p.send_idx, p.n_send, ldi, C->send_f[l][l == 1 ? 0 : b], nullptr, 0.f, 0, 0);
+  // post
+  if (l >= 2 || t == 1) {
+    for (auto& p : C->parts) {
+      if (p.n_send == 0) continue;
+      const float* Hin = layer_in(p, l, b);
+      void* dst = p.send_f[l][l == 1 ? 0 : b];
+      Scope sc(C, PGCN_K_GATHER, ((C->p16 ? 6.0 : 8.0) * C->F[l - 1] + 4.0) * p.n_send);
+      if (C->p16) {
+        pack_rows_bf16(Lk, Hin, p.send_idx, p.n_send, ldi, dst);
+      } else {
+        SegTable src{};
+        src.n_seg = 1;
+        src.off[1] = p.n_send;
+        src.base[0] = Hin;
+        gather_rows(Lk, src, p.send_idx, p.n_send, ldi, static_cast<float*>(dst), nullptr, 0.f, 0, 0);
+      }
     }
     cudaEventRecord(C->ev_f_pack[l], C->s);
     cudaStreamWaitEvent(C->cs, C->ev_f_pack[l], 0);
-    float* dst;
-    if (l == 1) dst = p.X + p.n_in * ldi;
-    else if (!pipe) dst = p.H[l - 1][b] + p.n_in * ldi;
-    else if (C->cfg.smooth_f) dst = C->recv_f[l][b];
-    else dst = p.H[l - 1][C->bi(t + s)] + p.n_in * ldi;  // lands in the buffer read at t + s
-    const float* sendb = C->send_f[l][l == 1 ? 0 : b];
-    ncclResult_t r = ncclGroupStart();
-    for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
-      if (j == C->rank) continue;
-      const int64_t ns = p.v.send_off[j + 1] - p.v.send_off[j], nr = p.v.halo_off[j + 1] - p.v.halo_off[j];
-      if (ns) r = ncclSend(sendb + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
-      if (nr && r == ncclSuccess)
-        r = ncclRecv(dst + p.v.halo_off[j] * ldi, (size_t)(nr * ldi), ncclFloat, j, C->ch, C->cs);
-    }
-    ncclResult_t r2 = ncclGroupEnd();
-    if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(C, r != ncclSuccess ? r : r2, "halo exchange (fwd)");
+    int rc = transfer(C, t, l, true);
+    if (rc) return rc;
     cudaEventRecord(C->ev_f_done[l][b], C->cs);
-    if (!pipe) cudaStreamWaitEvent(C->s, C->ev_f_done[l][b], 0);
+    if (!pipe) {
+      if (!skip_wait) cudaStreamWaitEvent(C->s, C->ev_f_done[l][b], 0);
+      if (staged && (l >= 2 || t == 1))
+        for (auto& p : C->parts) {  // VANILLA bf16: widen the fresh rows into the layer input
+          if (p.n_bd == 0) continue;
+          Scope sc(C, PGCN_K_GATHER, 6.0 * C->F[l - 1] * p.n_bd);
+          install_bf16(Lk, p.recv_f[l][l == 1 ? 0 : b], p.n_bd, ldi, layer_in(p, l, b) + p.n_in * ldi, nullptr, 0.f, 0);
+        }
+    }
   }
-  if (pipe && l == 1 && t <= s) *n_valid = p.n_in;  // X boundary rows not installed yet: zero (l.6)
+  for (size_t i = 0; i < C->parts.size(); ++i)
+    n_valid[i] = (pipe && l == 1 && t <= s) ? C->parts[i].n_in : C->parts[i].n_all;  // X rows not in yet (l.6)
   return PGCN_OK;
 }
 
-// Alg. 1 l.22-27 over NCCL: post the boundary-row gradients of J^(l-1) (parity t) to their owners
-// and return the message table to accumulate now (PIPE: the one received at t-1).
-int nccl_bwd_exchange(pgcn_ctx* C, PartCtx& p, int64_t t, int l, SegTable& msg, bool& have) {
+// Alg. 1 l.22-27 for every hosted partition (l >= 2): post the boundary-row gradients of J^(l-1)
+// (slot t) to their owners and make the compute stream wait for the messages to accumulate now
+// (PIPE: those posted at t - s).  have: whether there is anything to accumulate this iteration.
+int post_bwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, bool* have) {
   const bool pipe = C->cfg.mode == 1;
   const int64_t s = C->depth;
-  const int b = C->bi(t), bs = C->bi(t - s);
+  const int b = C->bi(t);
   const int64_t ldi = C->ld[l - 1];
-  const float* J = p.J[l - 1][b];
+  if (C->p16)
+    for (auto& p : C->parts) {
+      if (p.n_bd == 0) continue;
+      Scope sc(C, PGCN_K_GATHER, 6.0 * C->F[l - 1] * p.n_bd);
+      pack_rows_bf16(Lk, p.J[l - 1][b] + p.n_in * ldi, nullptr, p.n_bd, ldi, p.send_b[l][b]);
+    }
   cudaEventRecord(C->ev_b_ready[l], C->s);
   cudaStreamWaitEvent(C->cs, C->ev_b_ready[l], 0);
-  ncclResult_t r = ncclGroupStart();
-  for (int j = 0; j < C->nranks && r == ncclSuccess; ++j) {
-    if (j == C->rank) continue;
-    const int64_t nh = p.v.halo_off[j + 1] - p.v.halo_off[j], ns = p.v.send_off[j + 1] - p.v.send_off[j];
-    if (nh) r = ncclSend(J + (p.n_in + p.v.halo_off[j]) * ldi, (size_t)(nh * ldi), ncclFloat, j, C->ch, C->cs);
-    if (ns && r == ncclSuccess)
-      r = ncclRecv(C->recv_b[l][b] + p.v.send_off[j] * ldi, (size_t)(ns * ldi), ncclFloat, j, C->ch, C->cs);
-  }
-  ncclResult_t r2 = ncclGroupEnd();
-  if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(C, r != ncclSuccess ? r : r2, "halo exchange (bwd)");
+  int rc = transfer(C, t, l, false);
+  if (rc) return rc;
   cudaEventRecord(C->ev_b_done[l][b], C->cs);
-  msg = SegTable{};
-  have = p.n_send > 0 && (!pipe || t > s);
-  if (have) {
-    const int sb = pipe ? bs : b;
-    cudaStreamWaitEvent(C->s, C->ev_b_done[l][sb], 0);
-    msg.n_seg = 1;
-    msg.off[1] = p.n_send;
-    msg.base[0] = C->recv_b[l][sb];
-  }
+  *have = !pipe || t > s;
+  if (*have && !(C->hook_flags & PGCN_XH_SKIP_B_WAIT)) cudaStreamWaitEvent(C->s, C->ev_b_done[l][pipe ? C->bi(t - s) : b], 0);
   return PGCN_OK;
 }
-#endif
 
 }  // namespace
 }  // namespace pgcn
@@ -718,8 +853,14 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
       return fail(PGCN_ECUDA, "pgcn_ctx_create upload: %s", cudaGetErrorString(e));
     }
   }
-  if (C->nccl) {
-#ifdef PGCN_WITH_NCCL
+  if (cudaStreamCreateWithFlags(&C->cps, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_x_free, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_lab_free, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&C->ev_in_ready, cudaEventDisableTiming) != cudaSuccess) {
+    delete C;
+    return fail(PGCN_ECUDA, "copy stream / event creation failed");
+  }
+  if (C->posted) {  // comm stream (high priority, App. F) and the exchange events
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&C->cs, cudaStreamNonBlocking, hi) != cudaSuccess) {
@@ -734,6 +875,9 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
         cudaEventCreateWithFlags(&C->ev_b_done[l][b], cudaEventDisableTiming);
       }
     }
+  }
+  if (C->nccl) {
+#ifdef PGCN_WITH_NCCL
     ncclUniqueId ih, ir;
     std::memcpy(&ih, comm->nccl_id_halo, sizeof(ih));
     std::memcpy(&ir, comm->nccl_id_reduce, sizeof(ir));
@@ -757,6 +901,8 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
 extern "C" int pgcn_ctx_destroy(pgcn_ctx* C) {
   if (!C) return PGCN_OK;
   if (C->s) cudaStreamSynchronize(C->s);
+  if (C->cs) cudaStreamSynchronize(C->cs);
+  if (C->cps) cudaStreamSynchronize(C->cps);
   delete C;
   return PGCN_OK;
 }
@@ -792,7 +938,30 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
       gather_bytes(Lk, p.inv_deg, p.tr_list, p.n_tr, (int64_t)sizeof(float), p.invdeg_tr);
     }
   }
+  C->inputs_set = 1;
   return check_cuda(C, "pgcn_set_inputs");
+}
+
+extern "C" int pgcn_stage_inputs(pgcn_ctx* C, int32_t local, const float* X, const void* labels,
+                                 const uint8_t* train_mask) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  if (C->poisoned) return fail(PGCN_ESTATE, "context poisoned");
+  if (!C->inputs_set) return fail(PGCN_ESTATE, "pgcn_stage_inputs before pgcn_set_inputs");
+  if (local < 0 || local >= (int)C->parts.size()) return fail(PGCN_EINVAL, "local index out of range");
+  PartCtx& p = C->parts[local];
+  if (p.n_in == 0) return PGCN_OK;
+  if (!X || !labels || !train_mask) return fail(PGCN_EINVAL, "null input");
+  // X after the in-flight iteration's last read of X; labels / mask after its loss
+  cudaStreamWaitEvent(C->cps, C->ev_x_free, 0);
+  cudaMemcpy2DAsync(p.X, sizeof(float) * C->ld[0], X, sizeof(float) * C->F[0], sizeof(float) * C->F[0], p.n_in,
+                    cudaMemcpyHostToDevice, C->cps);
+  cudaStreamWaitEvent(C->cps, C->ev_lab_free, 0);
+  const size_t lb = C->cfg.loss == 0 ? sizeof(int32_t) * p.n_in : (size_t)p.n_in * C->F[C->L];
+  cudaMemcpyAsync(p.labels, labels, lb, cudaMemcpyHostToDevice, C->cps);
+  cudaMemcpyAsync(p.train, train_mask, (size_t)p.n_in, cudaMemcpyHostToDevice, C->cps);
+  cudaEventRecord(C->ev_in_ready, C->cps);
+  C->in_pending = 1;
+  return check_cuda(C, "pgcn_stage_inputs");
 }
 
 extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* params) {
@@ -824,6 +993,12 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                C->WT_lo[l], C->Wp_hi[l], C->Wp_lo[l], C->WJ_hi[l], C->WJ_lo[l], C->s);
     ++C->launches;
   }
+  if (l == 1 && C->in_pending) {  // streamed inputs of this iteration (pgcn_stage_inputs)
+    cudaStreamWaitEvent(C->s, C->ev_in_ready, 0);
+    C->in_pending = 0;
+  }
+  int64_t nv_posted[PGCN_MAX_PARTS];
+  if (C->posted && (rc = post_fwd(C, t, l, Lk, nv_posted))) return rc;
   for (auto& p : C->parts) {
     float* Hin = layer_in(p, l, b);
     // N1(ii): the last layer's aggregation only on train rows (the loss reads Y^(L) only there)
@@ -832,17 +1007,12 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const int64_t nr = sp ? p.n_tr : p.n_in;
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
     // gathered bytes of e edges at width F: per-edge model, or the tile path's traffic when it runs
-    auto sgat = [&](double F, double e, int64_t nv) {
-      const TileDev* T = p.tiles(0);
-      if (T && !rl && nv >= p.n_all) return tile_path_bytes(C, *T, F, (double)nv) + gat(F, e - nz);
-      return gat(F, e);
-    };
+    // table of nv rows at width F, e edges, `rest` = index / output / epilogue bytes
+    auto sb = [&](double F, double nv, double e, double rest) { return SpmmBytes{gat(F, nv) + rest, gat(F, e) + rest}; };
     // S1 / S2: boundary rows of the layer input (Alg. 1 l.9-13)
     int64_t n_valid = p.n_all;
-    if (C->nccl) {
-#ifdef PGCN_WITH_NCCL
-      if ((rc = nccl_fwd_exchange(C, p, t, l, Hin, Lk, &n_valid))) return rc;
-#endif
+    if (C->posted) {
+      n_valid = nv_posted[&p - C->parts.data()];
     } else if (C->n_parts > 1 && p.n_bd > 0) {  // local transport: device gather from the owners
       bool do_install = false, ema = false, first = false;
       const float* prev = nullptr;
@@ -870,7 +1040,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
     }
     // N4: ||boundary rows used - owners' fresh rows||^2 (local transport only)
-    if (C->cfg.staleness_stats && !C->nccl && C->n_parts > 1 && p.n_bd > 0) {
+    if (C->cfg.staleness_stats && C->xp != XP_NCCL && C->n_parts > 1 && p.n_bd > 0) {
       SegTable fresh{};
       fresh.n_seg = C->n_parts;
       for (int j = 0; j <= C->n_parts; ++j) fresh.off[j] = p.v.halo_off[j];
@@ -897,16 +1067,16 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                           ldo, nullptr, nullptr, 0, 0, bf))
             return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
         }
-        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fo, (nz + nr), n_valid) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
-                                         4.0 * Fo * nr);
+        Scope sc(C, PGCN_K_SPMM_FWD, sb(Fo, n_valid, nz + nr, cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+                                         4.0 * Fo * nr));
         spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
                  p.n_all, p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
         continue;
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fi, (nz + nr), n_valid) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
-                                         4.0 * Fi * nr);
+        Scope sc(C, PGCN_K_SPMM_FWD, sb(Fi, n_valid, nz + nr, cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
+                                         4.0 * Fi * nr));
         spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
       }
@@ -925,7 +1095,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (T) failed (layer %d)", l);
       }
       {
-        Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fo, nz, n_valid) + cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr);
+        Scope sc(C, PGCN_K_SPMM_FWD, sb(Fo, n_valid, nz, cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr));
         spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
                  p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16);
@@ -940,7 +1110,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
     const bool cl = C->cl && l == C->L;  // compact train rows (pgcn_ctx::cl)
     {
-      Scope sc(C, PGCN_K_SPMM_FWD, sgat(Fi, nz, n_valid) + cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr);
+      Scope sc(C, PGCN_K_SPMM_FWD, sb(Fi, n_valid, nz, cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr));
       spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
                  (int64_t)nz, p.tiles(0), p.T16, cl);
     }
@@ -972,6 +1142,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
     }
   }
+  // X's last reader this iteration: layer 1's dropout (with p = 0 GraphSAGE reads X itself later, in
+  // layer 1's weight gradient -- recorded in pgcn_layer_bwd)
+  if (l == 1 && (C->cfg.dropout > 0.0 || C->gcn)) cudaEventRecord(C->ev_x_free, C->s);
   rc = check_cuda(C, "pgcn_layer_fwd");
   if (rc) return rc;
   advance(C);
@@ -999,6 +1172,7 @@ extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
     reduce_sum(Lk, p.row_loss, p.n_in, C->part_loss + i);
   }
   if (loss_dev) reduce_sum(Lk, C->part_loss, (int64_t)C->parts.size(), loss_dev);
+  cudaEventRecord(C->ev_lab_free, C->s);
   rc = check_cuda(C, "pgcn_loss");
   if (rc) return rc;
   advance(C);
@@ -1029,11 +1203,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const int64_t* trp = sp ? p.trp_tr : p.trp;
     const int32_t* tcol = sp ? p.tcol_tr : p.tcol;
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
-    auto sgat = [&](double F, double e) {  // see the forward: per-edge model or the tile path's traffic
-      const TileDev* T = p.tiles(1);
-      if (T && !sp) return tile_path_bytes(C, *T, F, (double)p.n_in) + gat(F, e - nz);
-      return gat(F, e);
-    };
+    auto sb = [&](double F, double nv, double e, double rest) { return SpmmBytes{gat(F, nv) + rest, gat(F, e) + rest}; };
     const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
     if (C->gcn) {
       // GCN-sym backward (App. A.1 PAPER.md:651-657 with P = S (A + I) S, S = diag(d~^-1/2), R26)
@@ -1041,8 +1211,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // Q = (A + I)^T (S M) over inner + boundary rows; G = [D'^T Q ; colsum M]; J = mask o s o S (Q W^T)
         const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
         {
-          Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fo, (nz + p.n_in)) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
-                                           8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all);
+          Scope sc(C, PGCN_K_SPMM_BWD, sb(Fo, p.n_in, nz + p.n_in, cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
+                                           8.0 * Fo * p.n_in + 4.0 * Fo * p.n_all));
           scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
           DropSpec none{};
           none.width = (int32_t)C->F[l];
@@ -1077,8 +1247,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         }
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
-        Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fi, (nz + p.n_in)) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
-                                         4.0 * Fi * p.n_all + 12.0 * p.n_all);
+        Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz + p.n_in, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
+                                         4.0 * Fi * p.n_all + 12.0 * p.n_all));
         spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
                  C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
       }
@@ -1089,8 +1259,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       // G = [D^T Q ; D_in^T M ; colsum M];  J^(l-1) = mask o s o ([Q | M] [W_neigh | W_self]^T)
       const int64_t nv = p.n_valid[l] ? p.n_valid[l] : p.n_all;
       {
-        Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fo, nz) + cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
-                                         4.0 * Fo * p.n_all);
+        Scope sc(C, PGCN_K_SPMM_BWD, sb(Fo, p.n_in, nz, cvt(Fo, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 8.0 * Fo * p.n_in +
+                                         4.0 * Fo * p.n_all));
         scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
         DropSpec none{};
         none.width = (int32_t)C->F[l];
@@ -1137,8 +1307,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
         }
       }
-      Scope sc(C, PGCN_K_SPMM_BWD, sgat(Fi, nz) + cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
-                                       4.0 * Fi * p.n_all + 8.0 * p.n_all);
+      Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
+                                       4.0 * Fi * p.n_all + 8.0 * p.n_all));
       spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
                drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16,
                cl ? p.tr_pos : nullptr);
@@ -1146,37 +1316,37 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)
   if (l >= 2) {
+    bool posted_have = false;
+    if (C->posted && (rc = post_bwd(C, t, l, Lk, &posted_have))) return rc;
     for (auto& p : C->parts) {
       SegTable msg{};
       msg.n_seg = 0;
       bool use_ema = false, first = false;
-      bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t > C->depth);
-      const int32_t* row_map = p.msg_map;
-      if (C->nccl) {
-#ifdef PGCN_WITH_NCCL
-        if ((rc = nccl_bwd_exchange(C, p, t, l, msg, have))) return rc;
-        row_map = nullptr;
-        if (have && pipe && C->cfg.smooth_g) {
-          use_ema = true;
-          first = C->cfg.ema_init == 0 && t == C->depth + 1;
+      const bool have = C->n_parts > 1 && p.n_send > 0 && (!pipe || t > C->depth);
+      const int sb = pipe ? bs : b;  // messages of t - s (PIPE) or t (VANILLA)
+      const int32_t* row_map = C->posted ? nullptr : p.msg_map;
+      if (have) {
+        if (C->posted) {  // one segment: the received rows in send order
+          msg.n_seg = 1;
+          msg.off[1] = p.n_send;
+          msg.base[0] = static_cast<const float*>(p.recv_b[l][sb]);
+        } else {          // local: the peers' boundary rows of J^(l-1), read in place
+          msg.n_seg = C->n_parts;
+          for (int j = 0; j <= C->n_parts; ++j) msg.off[j] = p.v.send_off[j];
+          for (int j = 0; j < C->n_parts; ++j) msg.base[j] = C->parts[j].J[l - 1][sb];
         }
-#endif
-      } else if (have) {
-        msg.n_seg = C->n_parts;
-        const int sb = pipe ? bs : b;  // peers' boundary-row gradients of t - s (PIPE) or t (VANILLA)
-        for (int j = 0; j <= C->n_parts; ++j) msg.off[j] = p.v.send_off[j];
-        for (int j = 0; j < C->n_parts; ++j) msg.base[j] = C->parts[j].J[l - 1][sb];
         if (pipe && C->cfg.smooth_g) {
           use_ema = true;
           first = C->cfg.ema_init == 0 && t == C->depth + 1;
         }
       }
+      const int m16 = C->posted && C->p16;
       const double Fi = (double)C->F[l - 1];
       Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j) + 8.0 * p.n_in +
-                                          (msg.n_seg ? (4.0 * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
+                                          (msg.n_seg ? ((m16 ? 2.0 : 4.0) * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
       grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, row_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
-                  p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi);
-      if (C->cfg.staleness_stats && !C->nccl && C->n_parts > 1 && p.n_send > 0) {
+                  p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi, m16);
+      if (C->cfg.staleness_stats && C->xp != XP_NCCL && C->n_parts > 1 && p.n_send > 0) {
         // N4: ||gradient messages used - fresh ones||^2 (fresh = peers' boundary rows of this iteration;
         // used = the smoothed state, the stale messages, or 0 when nothing was received)
         SegTable fresh{};
@@ -1191,7 +1361,9 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                     C->diag + PGCN_MAX_LAYERS + 1 + l);
       }
     }
+    (void)posted_have;
   }
+  if (l == 1 && !(C->cfg.dropout > 0.0 || C->gcn)) cudaEventRecord(C->ev_x_free, C->s);
   rc = check_cuda(C, "pgcn_layer_bwd");
   if (rc) return rc;
   advance(C);
@@ -1277,10 +1449,27 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
 
 extern "C" int64_t pgcn_launch_count(const pgcn_ctx* C) { return C ? C->launches : -1; }
 
+extern "C" int pgcn_dev_exchange_bytes(const pgcn_ctx* C, int64_t* fwd_bytes, int64_t* bwd_bytes) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  if (fwd_bytes) *fwd_bytes = C->xbytes[0];
+  if (bwd_bytes) *bwd_bytes = C->xbytes[1];
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_dev_exchange_hook(pgcn_ctx* C, int64_t spin_ns, int32_t flags) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  if (!C->posted) return fail(PGCN_EUNSUPPORTED, "exchange hook: posted transports (LOOPBACK / NCCL) only");
+  if (spin_ns < 0 || (flags & ~(PGCN_XH_SKIP_F_WAIT | PGCN_XH_SKIP_B_WAIT | PGCN_XH_NOCOMM)))
+    return fail(PGCN_EINVAL, "exchange hook: bad argument");
+  C->hook_spin_ns = spin_ns;
+  C->hook_flags = flags;
+  return PGCN_OK;
+}
+
 extern "C" int pgcn_staleness(pgcn_ctx* C, int32_t layer, double* feat_err, double* grad_err) {
   if (!C || layer < 1 || layer > C->L) return fail(PGCN_EINVAL, "pgcn_staleness: bad argument");
   if (!C->cfg.staleness_stats) return fail(PGCN_ESTATE, "pgcn_staleness: context created without staleness_stats");
-  if (C->nccl) return fail(PGCN_EUNSUPPORTED, "pgcn_staleness: local transport only");
+  if (C->nccl) return fail(PGCN_EUNSUPPORTED, "pgcn_staleness: single-process contexts only");
   double h[2];
   cudaStreamSynchronize(C->s);
   cudaMemcpy(&h[0], C->diag + layer, sizeof(double), cudaMemcpyDeviceToHost);
@@ -1297,7 +1486,7 @@ extern "C" int pgcn_timing_enable(pgcn_ctx* C, int32_t on) {
   for (auto& k : C->kt) {
     k.used = 0;
     k.n = 0;
-    k.bytes = k.flops = 0.0;
+    k.bytes = k.flops = k.gbytes = 0.0;
   }
   return PGCN_OK;
 }
@@ -1318,6 +1507,12 @@ extern "C" int pgcn_timing_read(pgcn_ctx* C, int32_t kind, double* ms, int64_t* 
   if (launches) *launches = k.n;
   if (bytes) *bytes = k.bytes;
   if (flops) *flops = k.flops;
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_timing_read_gather(pgcn_ctx* C, int32_t kind, double* gather_bytes) {
+  if (!C || kind < 0 || kind >= PGCN_K_COUNT || !gather_bytes) return fail(PGCN_EINVAL, "bad argument");
+  *gather_bytes = C->kt[kind].gbytes;
   return PGCN_OK;
 }
 

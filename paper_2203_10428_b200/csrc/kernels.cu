@@ -633,12 +633,53 @@ __global__ void k_gather(const __grid_constant__ SegTable t, const int32_t* __re
   }
 }
 
+// bf16 exchange payloads (pgcn_config.halo_payload = 1): a float4 of a row travels as
+// one uint2 (4 bf16, round to nearest even) and is widened exactly on receipt.
+__device__ __forceinline__ uint2 f4_to_bf16x4(const float4 v) {
+  return make_uint2(bf16x2_rn(v.x, v.y), bf16x2_rn(v.z, v.w));
+}
+__device__ __forceinline__ float4 bf16x4_to_f4(const uint2 w) {
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                     __uint_as_float(w.y & 0xffff0000u));
+}
+// S2 pack in bf16: dst[r] = bf16(src(r)), src row = row_map[r] (or r) of one fp32 table
+__global__ void k_pack_bf16(const float4* __restrict__ src, const int32_t* __restrict__ row_map, int64_t n_rows,
+                            int64_t ld4, uint2* __restrict__ dst) {
+  for (RowCursor rc(ld4); rc.r < n_rows; rc.next((int)ld4)) {
+    const int64_t srow = row_map ? (int64_t)row_map[rc.r] : rc.r;
+    dst[rc.r * ld4 + rc.x] = f4_to_bf16x4(__ldg(src + srow * ld4 + rc.x));
+  }
+}
+// S1 install of bf16 payloads: dst[r] = widen(src[r]) or EMA: gamma * prev[r] + (1 - gamma) * widen(src[r])
+__global__ void k_install_bf16(const uint2* __restrict__ src, int64_t n_rows, int64_t ld4, float4* __restrict__ dst,
+                               const float4* __restrict__ prev, float gamma, int ema) {
+  for (RowCursor rc(ld4); rc.r < n_rows; rc.next((int)ld4)) {
+    const int64_t i = rc.r * ld4 + rc.x;
+    float4 v = bf16x4_to_f4(__ldg(src + i));
+    if (ema) {
+      const float4 p = prev[i];
+      const float a = gamma, b = 1.0f - gamma;
+      v = make_float4(a * p.x + b * v.x, a * p.y + b * v.y, a * p.z + b * v.z, a * p.w + b * v.w);
+    }
+    dst[i] = v;
+  }
+}
+// Delay injection on the comm stream (tests of the stream/event contract): one thread spins on the
+// global nanosecond timer.
+__global__ void k_spin(int64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((int64_t)(t - t0) < ns);
+}
+
 // ---------------------------------------------------------------- stale gradient accumulate + M (S9)
 __global__ void k_grad_reduce(const int64_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv_pos,
                               const __grid_constant__ SegTable msg, const int32_t* __restrict__ row_map,
                               float4* __restrict__ ema, float gamma, int use_ema, int first, float4* __restrict__ J,
                               int write_j, const float4* __restrict__ Hprev, float4* __restrict__ M, int64_t n_in,
-                              int64_t ld4) {
+                              int64_t ld4, int msg16) {
   const int64_t total = n_in * ld4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i / ld4, x = i - v * ld4;
@@ -649,7 +690,8 @@ __global__ void k_grad_reduce(const int64_t* __restrict__ inv_ptr, const int32_t
         const int64_t k = inv_pos[q];
         const int s = find_seg(msg, k);
         const int64_t srow = row_map ? (int64_t)row_map[k] : k - msg.off[s];
-        float4 c = __ldg(reinterpret_cast<const float4*>(msg.base[s]) + srow * ld4 + x);
+        float4 c = msg16 ? bf16x4_to_f4(__ldg(reinterpret_cast<const uint2*>(msg.base[s]) + srow * ld4 + x))
+                         : __ldg(reinterpret_cast<const float4*>(msg.base[s]) + srow * ld4 + x);
         if (use_ema) {
           if (!first) {
             const float4 e = ema[k * ld4 + x];
@@ -1368,14 +1410,36 @@ void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t 
 
 void grad_reduce(Launch L, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg, const int32_t* row_map,
                  float* ema, float gamma, int use_ema, int first, float* J, int write_j, const float* Hprev, float* M,
-                 int64_t n_in, int64_t ld) {
+                 int64_t n_in, int64_t ld, int msg16) {
   if (n_in <= 0) return;
   const int64_t ld4 = ld / 4;
   k_grad_reduce<<<grid_for(n_in * ld4, kThreads), kThreads, 0, L.s>>>(
       inv_ptr, inv_pos, msg, row_map, reinterpret_cast<float4*>(ema), gamma, use_ema, first,
       reinterpret_cast<float4*>(J), write_j, reinterpret_cast<const float4*>(Hprev), reinterpret_cast<float4*>(M), n_in,
-      ld4);
+      ld4, msg16);
   count(L);
+}
+
+void pack_rows_bf16(Launch L, const float* src, const int32_t* row_map, int64_t n_rows, int64_t ld, void* dst) {
+  if (n_rows <= 0) return;
+  const int64_t ld4 = ld / 4;
+  k_pack_bf16<<<grid_for(n_rows * ld4, kThreads), kThreads, 0, L.s>>>(reinterpret_cast<const float4*>(src), row_map,
+                                                                      n_rows, ld4, static_cast<uint2*>(dst));
+  count(L);
+}
+
+void install_bf16(Launch L, const void* src, int64_t n_rows, int64_t ld, float* dst, const float* prev, float gamma,
+                  int ema) {
+  if (n_rows <= 0) return;
+  const int64_t ld4 = ld / 4;
+  k_install_bf16<<<grid_for(n_rows * ld4, kThreads), kThreads, 0, L.s>>>(
+      static_cast<const uint2*>(src), n_rows, ld4, reinterpret_cast<float4*>(dst),
+      reinterpret_cast<const float4*>(prev), gamma, ema);
+  count(L);
+}
+
+void spin_ns(cudaStream_t s, int64_t ns) {
+  if (ns > 0) k_spin<<<1, 1, 0, s>>>(ns);
 }
 
 void scatter_rows(Launch L, const float* src, const int32_t* map, int64_t n, int64_t ld, float* dst) {

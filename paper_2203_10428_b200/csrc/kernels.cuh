@@ -118,9 +118,19 @@ void gather_rows(Launch, const SegTable& src, const int32_t* row_map, int64_t n_
 
 // S9 + M: J[v] += sum_{k in inv(v)} C_hat[k] (ascending k; C_hat = message or its EMA, state in
 // ema[k]); M[v] = J[v] o 1[Hprev[v] > 0].  msg may have n_seg == 0 (nothing received).
+// msg16: the message rows are bf16 (halo_payload = 1; 4 bf16 per float4 of the row, row stride ld).
 void grad_reduce(Launch, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg,
                  const int32_t* row_map, float* ema, float gamma, int use_ema, int first, float* J,
-                 int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld);
+                 int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld, int msg16 = 0);
+
+// bf16 exchange payloads (pgcn_config.halo_payload = 1).  Rows of ld bf16 (ld % 4 == 0).
+// pack:    dst[r] = bf16_rn(src[row_map ? row_map[r] : r])                     (S2 / S10 pack)
+// install: dst[r] = widen(src[r]), or EMA gamma * prev[r] + (1 - gamma) * widen(src[r])   (S1)
+void pack_rows_bf16(Launch, const float* src, const int32_t* row_map, int64_t n_rows, int64_t ld, void* dst);
+void install_bf16(Launch, const void* src, int64_t n_rows, int64_t ld, float* dst, const float* prev, float gamma,
+                  int ema);
+// Delay injection: one thread spinning `ns` nanoseconds on stream s (not counted as a launch).
+void spin_ns(cudaStream_t s, int64_t ns);
 
 // S5: CE (labels int32) or BCE (labels uint8 [n x C]) on rows with train[v] != 0 (train == nullptr:
 // every row is a train row).

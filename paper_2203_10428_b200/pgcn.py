@@ -21,6 +21,7 @@ MAX_PARTS = 64
 
 OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 T_H, T_HIN, T_Z, T_J, T_G = 0, 1, 2, 3, 4
+XH_SKIP_F_WAIT, XH_SKIP_B_WAIT, XH_NOCOMM = 1, 2, 4  # pgcn_dev_exchange_hook flags (include/pgcn_dev.h)
 KERNELS = ["spmm_fwd", "spmm_bwd", "gemm_fwd", "gemm_dw", "gemm_da", "dropout", "gather", "grad_reduce", "loss",
            "update"]
 
@@ -51,7 +52,8 @@ class Config(C.Structure):
                 ("dump_j", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
                 ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32),
-                ("train_sparse", C.c_int32), ("spmm_tiles", C.c_int32), ("tile_min", C.c_int32)]
+                ("train_sparse", C.c_int32), ("spmm_tiles", C.c_int32), ("tile_min", C.c_int32),
+                ("transport", C.c_int32), ("halo_payload", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -85,6 +87,7 @@ def lib():
                                       C.POINTER(vp)]
         L.pgcn_ctx_destroy.argtypes = [vp]
         L.pgcn_set_inputs.argtypes = [vp, i32, vp, vp, vp]
+        L.pgcn_stage_inputs.argtypes = [vp, i32, vp, vp, vp]
         L.pgcn_param_count.argtypes = [C.POINTER(Config)]
         L.pgcn_param_count.restype = i64
         L.pgcn_layer_fwd.argtypes = [vp, i64, i32, vp]
@@ -96,6 +99,7 @@ def lib():
         L.pgcn_launch_count.argtypes = [vp]
         L.pgcn_launch_count.restype = i64
         L.pgcn_timing_enable.argtypes = [vp, i32]
+        L.pgcn_timing_read_gather.argtypes = [vp, i32, C.POINTER(C.c_double)]
         L.pgcn_timing_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pgcn_dev_gemm_scratch_bytes.argtypes = [i64, i64, i64]
@@ -107,6 +111,8 @@ def lib():
         L.pgcn_dev_l2_read.argtypes = [vp, i64, i32, vp, vp]
         L.pgcn_dev_tiles.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.pgcn_nccl_unique_id.argtypes = [vp]
+        L.pgcn_dev_exchange_hook.argtypes = [vp, i64, i32]
+        L.pgcn_dev_exchange_bytes.argtypes = [vp, vp, vp]
         L.pgcn_nccl_id_bytes.restype = i32
         _lib = L
     return _lib
@@ -201,7 +207,8 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
                 ema_init="first", dropout=0.0, seed=4, gemm="tc", loss="ce", n_global=0, n_train_global=1,
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
                 transform_first=True, staleness_stats=False, model="sage", depth=1,
-                gather="f32", train_sparse=False, spmm_tiles=True, tile_min=0) -> Config:
+                gather="f32", train_sparse=False, spmm_tiles=True, tile_min=0, transport="local",
+                halo_payload="f32") -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -224,6 +231,8 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.train_sparse = int(bool(train_sparse))
     c.spmm_tiles = int(bool(spmm_tiles))
     c.tile_min = int(tile_min)
+    c.transport = {"local": 0, "loopback": 1}[transport]
+    c.halo_payload = {"f32": 0, "bf16": 1}[halo_payload]
     return c
 
 
@@ -300,12 +309,29 @@ class Context:
                                      C.byref(comm) if comm is not None else None, self.ws.data_ptr(),
                                      self.ws.numel(), self.stream.cuda_stream, C.byref(h)))
         self.handle = h
+        self._keep = {}
         self.P = param_count(cfg)
         self.widths = [cfg.width[i] for i in range(cfg.n_layers + 1)]
 
     def set_inputs(self, local, X, labels, train_mask):
-        self._keep = (X, labels, train_mask)
+        """pgcn_set_inputs: the copies are asynchronous on the context stream, so the sources are kept
+        alive per hosted partition until the next call for that partition (device tensors are also
+        marked as used on the context stream for torch's caching allocator)."""
+        srcs = (X, labels, train_mask)
+        for a in srcs:
+            if hasattr(a, "record_stream") and getattr(a, "is_cuda", False):
+                a.record_stream(self.stream)
+        self._keep[int(local)] = srcs
         _check(lib().pgcn_set_inputs(self.handle, int(local), _ptr(X), _ptr(labels), _ptr(train_mask)))
+
+    def stage_inputs(self, local, X, labels, train_mask):
+        """pgcn_stage_inputs: per-iteration re-upload of partition `local`'s inputs from HOST memory
+        (numpy arrays or pinned CPU tensors), overlapped with the iteration in flight."""
+        for a in (X, labels, train_mask):
+            if getattr(a, "is_cuda", False):
+                raise ValueError("stage_inputs takes host buffers")
+        self._keep[("stage", int(local))] = (X, labels, train_mask)
+        _check(lib().pgcn_stage_inputs(self.handle, int(local), _ptr(X), _ptr(labels), _ptr(train_mask)))
 
     def layer_fwd(self, t, layer, params):
         _check(lib().pgcn_layer_fwd(self.handle, int(t), int(layer), _ptr(params)))
@@ -340,13 +366,25 @@ class Context:
     def timing_read(self, kind):
         ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         _check(lib().pgcn_timing_read(self.handle, int(kind), C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
-        return dict(ms=ms.value, launches=n.value, bytes=by.value, flops=fl.value)
+        gb = C.c_double()
+        _check(lib().pgcn_timing_read_gather(self.handle, int(kind), C.byref(gb)))
+        return dict(ms=ms.value, launches=n.value, bytes=by.value, flops=fl.value, gather_bytes=gb.value)
 
     def staleness(self, layer):
         """(feature error, gradient error) of the last iteration for `layer` (Fig. 5/7)."""
         f, g = C.c_double(), C.c_double()
         _check(lib().pgcn_staleness(self.handle, int(layer), C.byref(f), C.byref(g)))
         return f.value, g.value
+
+    def exchange_hook(self, spin_ns=0, flags=0):
+        """pgcn_dev_exchange_hook (include/pgcn_dev.h): delay / fault injection on the posted exchange."""
+        _check(lib().pgcn_dev_exchange_hook(self.handle, int(spin_ns), int(flags)))
+
+    def exchange_bytes(self):
+        """pgcn_dev_exchange_bytes: (forward, backward) payload bytes posted so far."""
+        f, b = C.c_int64(), C.c_int64()
+        _check(lib().pgcn_dev_exchange_bytes(self.handle, C.byref(f), C.byref(b)))
+        return f.value, b.value
 
     def launch_count(self) -> int:
         return int(lib().pgcn_launch_count(self.handle))
