@@ -359,24 +359,32 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def timed(k_steps, per_step=None):
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+
+    def timed(k_steps, per_step_ms=None):
         """k_steps iterations bracketed by CUDA events on the context stream (barrier + synchronize on
-        both sides); returns the max over ranks of the elapsed milliseconds."""
+        both sides); returns the max over ranks of the elapsed milliseconds.  per_step_ms (optional
+        list) receives this rank's per-iteration durations (an event after every step)."""
         nonlocal t
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
             torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(k_steps):
+        for k in range(k_steps):
             t += 1
             ctx.step(t, theta, grads, opt, loss)
-            if per_step is not None:
-                per_step()
+            if per_step_ms is not None:
+                step_ev[k].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
+        if per_step_ms is not None:
+            prev = ev0
+            for k in range(k_steps):
+                per_step_ms.append(prev.elapsed_time(step_ev[k]))
+                prev = step_ev[k]
         return max_over_ranks(ev0.elapsed_time(ev1), dist)
 
     # (1) headline: K iterations, no instrumentation
@@ -384,7 +392,8 @@ def main():
     clocks.start()
     launches0 = ctx.launch_count()
     xb0 = ctx.exchange_bytes()
-    ms_total = timed(K)
+    step_ms = []
+    ms_total = timed(K, step_ms)
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
     xb1 = ctx.exchange_bytes()
@@ -483,7 +492,7 @@ def main():
                       "train_sparse_last_layer": not args.no_train_sparse, "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-           "comm": comm_info, "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
+           "comm": comm_info, "step_ms": [round(x, 3) for x in step_ms], "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
            "setup_s": {"generate": t_gen, "partition": t_part},
            "workspace_GB": ctx.ws.numel() / 1e9}
     print(json.dumps(out))

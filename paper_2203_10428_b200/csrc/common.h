@@ -12,6 +12,22 @@ namespace pgcn {
 int fail(int code, const char* fmt, ...);
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Streaming multiprocessors of the current device (queried once per device; B200: 148).  Persistent
+// grids and grid caps are sized from it.
+int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func`, once per (device, kernel).  0 / -1.
+int smem_attr_once(const void* func, int bytes);
+
+// Developer A/B knobs (PGCN_* environment variables used by the tools/ sweeps), read once per process
+// (thread-safe); the defaults are the measured choices.
+struct DevKnobs {
+  int tc_spmm_bn = 0, tc_spmm_order = 1, tc_spmm_dbg = 0, tc_spmm_nacc1 = 0, tc_spmm_ts = 1, tc_spmm_ctas = 2,
+      tc_spmm_box64 = 1, tc_bnmax = 256, tc_gemm_ctas = 2, spmm_dyn = 1, tf_off = 0;
+  long long spmm_grab = 128;
+  const char* spmm_table = nullptr;
+};
+const DevKnobs& knobs();
 inline int64_t ld_of(int64_t f) { return round_up(f, 4); }
 
 }  // namespace pgcn

@@ -448,8 +448,7 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   for (int l = 1; l <= C->L; ++l) {
     const int64_t fi = C->ld[l - 1], fo = C->ld[l];
     C->tf[l] = (cfg->transform_first == 1 && cfg->gemm != 2) ? (l == 1 ? 2 * fo < fi : fo < fi) : 0;
-    if (const char* m = std::getenv("PGCN_TF_OFF"))  // dev knob: bitmask of layers forced aggregate-first
-      if ((std::atoi(m) >> l) & 1) C->tf[l] = 0;
+    if ((knobs().tf_off >> l) & 1) C->tf[l] = 0;  // dev knob PGCN_TF_OFF: layers forced aggregate-first
   }
   C->cl = cfg->train_sparse && !C->tf[C->L] && cfg->model == 0 && cfg->gemm != 2;
   C->P = C->woff[C->L + 1];
@@ -466,6 +465,12 @@ DropSpec drop_spec(const pgcn_ctx* C, int64_t t, int l) {
   d.scale = d.on ? (float)(1.0 / (1.0 - p)) : 1.0f;
   d.width = (int32_t)C->F[l - 1];
   return d;
+}
+
+// A failed launch leaves the context's buffers in an unknown state: every later call returns PGCN_ESTATE.
+int poison(pgcn_ctx* C, int rc) {
+  C->poisoned = 1;
+  return rc;
 }
 
 int check_cuda(pgcn_ctx* C, const char* where) {
@@ -1020,8 +1025,10 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       src.n_seg = C->n_parts;
       for (int j = 0; j <= C->n_parts; ++j) src.off[j] = p.v.halo_off[j];
       if (l == 1) {
-        // X is constant: one exchange at t = 1, consumed at t = 1 (VANILLA) or t = 1 + s (PIPE) (R10)
+        // X is constant: one exchange at t = 1, consumed at t = 1 (VANILLA) or t = 1 + s (PIPE) (R10);
+        // until then X's boundary rows are not valid (0, l.6) -- the same n_valid as the posted transports
         do_install = pipe ? t == 1 + C->depth : t == 1;
+        if (pipe && t <= C->depth) n_valid = p.n_in;
         for (int j = 0; j < C->n_parts; ++j) src.base[j] = C->parts[j].X;
       } else {
         const int sb = pipe ? bs : b;  // owners' layer output of t - s (PIPE) or t (VANILLA)
@@ -1069,16 +1076,16 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         }
         Scope sc(C, PGCN_K_SPMM_FWD, sb(Fo, n_valid, nz + nr, cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fo * nr));
-        spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
+        if ((rc = spmm_fwd(Lk, p.rp, p.col, p.sym, p.T[l], ldo, nr, n_valid, out, C->work, 1, bias, C->F[l], l < C->L,
                  p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0), p.T16);
+                 (int64_t)nz, p.tiles(0), p.T16))) return poison(C, rc);
         continue;
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, sb(Fi, n_valid, nz + nr, cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr +
                                          4.0 * Fi * nr));
-        spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0), p.T16);
+        if ((rc = spmm_fwd(Lk, p.rp, p.col, p.sym, D, ldi, nr, n_valid, p.Z[l], C->work, 1, nullptr, 0, 0, p.n_all, p.G16, rl,
+                 (int64_t)nz, p.tiles(0), p.T16))) return poison(C, rc);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
@@ -1096,9 +1103,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       {
         Scope sc(C, PGCN_K_SPMM_FWD, sb(Fo, n_valid, nz, cvt(Fo, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fo * nr));
-        spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
+        if ((rc = spmm_fwd(Lk, p.rp, p.col, p.inv_deg, p.T[l], ldo, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all,
                  p.G16, rl,
-                 (int64_t)nz, p.tiles(0), p.T16);
+                 (int64_t)nz, p.tiles(0), p.T16))) return poison(C, rc);
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
@@ -1111,8 +1118,8 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const bool cl = C->cl && l == C->L;  // compact train rows (pgcn_ctx::cl)
     {
       Scope sc(C, PGCN_K_SPMM_FWD, sb(Fi, n_valid, nz, cvt(Fi, n_valid) + 4.0 * nz + 8.0 * (nr + 1) + 4.0 * nr + 4.0 * Fi * nr));
-      spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
-                 (int64_t)nz, p.tiles(0), p.T16, cl);
+      if ((rc = spmm_fwd(Lk, p.rp, p.col, p.inv_deg, D, ldi, nr, n_valid, p.Z[l], C->work, 0, nullptr, 0, 0, p.n_all, p.G16, rl,
+                 (int64_t)nz, p.tiles(0), p.T16, cl))) return poison(C, rc);
     }
     if (cl) {  // Z rows are compact; gather the train rows of D, Y_tr = [Z | D_tr] W + b, logits scattered
       SegTable tab{};
@@ -1216,8 +1223,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
           scale_rows(Lk, p.M, p.sym, p.n_in, ldo, p.dA);
           DropSpec none{};
           none.width = (int32_t)C->F[l];
-          spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                   p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
+          if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+                   p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16))) return poison(C, rc);
         }
         {
           Scope sc(C, PGCN_K_GEMM_DW, 4.0 * nv * (Fi + Fo) + 4.0 * p.n_in * Fo, 2.0 * nv * Fi * Fo);
@@ -1249,8 +1256,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
         Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz + p.n_in, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all));
-        spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
+        if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
+                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16))) return poison(C, rc);
       }
       continue;
     }
@@ -1264,8 +1271,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         scale_rows(Lk, p.M, p.inv_deg, p.n_in, ldo, p.dA);
         DropSpec none{};
         none.width = (int32_t)C->F[l];
-        spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
-                 p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16);
+        if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, nullptr, ldo, p.n_in, p.n_all, p.T[l], ldo, p.gid, none, C->work, nullptr,
+                 p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16))) return poison(C, rc);
       }
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
@@ -1309,9 +1316,9 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all));
-      spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
+      if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
                drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16,
-               cl ? p.tr_pos : nullptr);
+               cl ? p.tr_pos : nullptr))) return poison(C, rc);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)

@@ -687,12 +687,7 @@ size_t tc_smem_bytes(int BN, int S, int bf, int mode) {
 }
 
 int tc_bn(int64_t N) {
-  static int cap = -1;  // dev knob PGCN_TC_BNMAX: cap the FWD/DA n-tile (A/B experiments)
-  if (cap < 0) {
-    const char* e = std::getenv("PGCN_TC_BNMAX");
-    cap = e ? std::atoi(e) : 256;
-    if (cap < 16 || cap > 256) cap = 256;
-  }
+  const int cap = knobs().tc_bnmax;  // dev knob PGCN_TC_BNMAX: cap the FWD/DA n-tile (A/B experiments)
   int64_t bn = (N + 15) / 16 * 16;
   if (bn > cap) bn = cap;
   if (bn < 16) bn = 16;
@@ -709,22 +704,11 @@ int tc_tmem_cols(int BN) {
 // SM: their pipelines are TMA-latency bound (memory-bound shapes: papers-shaped 48-wide layers), and
 // two independent pipelines per SM hide more of it (papers-q forward GEMMs 18.9 -> 15.7 ms per step;
 // the dW GEMM measured slower, its split-K plan fills 148-CTA waves).  Dev knob PGCN_TC_GEMM_CTAS=1.
-static int gemm_ctas() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PGCN_TC_GEMM_CTAS");
-    v = e ? std::atoi(e) : 2;
-  }
-  return v;
-}
+static int gemm_ctas() { return knobs().tc_gemm_ctas; }
 
 cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tc::k_umma_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tc::k_umma_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  if (smem_attr_once((const void*)tc::k_umma_gemm<0>, 227 * 1024) || smem_attr_once((const void*)tc::k_umma_gemm<1>, 227 * 1024))
+    return cudaErrorInvalidValue;
   TcParams p = p0;
   int ctas = 1;
   if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW) {  // dW: split-K plan is sized for 148 CTAs
@@ -748,7 +732,7 @@ void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns,
                    cudaStream_t s) {
   const int64_t total = (int64_t)N * ns * Fp + (int64_t)ns * F * Kp + (WJ ? (int64_t)F * ns * Kq : 0);
   int grid = (int)((total + 255) / 256);
-  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid > sm_count() * 8) grid = sm_count() * 8;
   tc::k_wprep_bf16<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, ns, static_cast<__nv_bfloat16*>(WT),
                                         static_cast<__nv_bfloat16*>(Wp), static_cast<__nv_bfloat16*>(WJ));
 }
@@ -757,7 +741,7 @@ void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, floa
               float* Wp_lo, float* WJ_hi, float* WJ_lo, cudaStream_t s) {
   const int64_t total = (int64_t)N * ns * Fp + (int64_t)ns * F * Kp + (WJ_hi ? (int64_t)F * ns * Kq : 0);
   int grid = (int)((total + 255) / 256);
-  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid > sm_count() * 8) grid = sm_count() * 8;
   tc::k_wprep<<<grid, 256, 0, s>>>(W, F, N, Fp, Kp, Kq, ns, WT_hi, WT_lo, Wp_hi, Wp_lo, WJ_hi, WJ_lo);
 }
 
@@ -791,14 +775,14 @@ static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
   Z[0] = 1;
   Z[1] = nseg > 1 ? 1 : 0;
   for (int W = 1; W <= kDwMaxWaves; ++W) {
-    const int slots = W * 148 / base;
+    const int slots = W * sm_count() / base;
     if (slots < nseg) continue;
     const int lo = 1, hi = nseg > 1 ? slots - 1 : slots;
     for (int z0 = lo; z0 <= hi; ++z0) {
       int64_t a = z0 < kb0 ? z0 : (kb0 > 0 ? kb0 : 1);
       int64_t b = nseg > 1 ? (slots - z0 < kb1 ? slots - z0 : (kb1 > 0 ? kb1 : 1)) : 0;
       const int64_t kpt = std::max((kb0 + a - 1) / a, nseg > 1 ? (kb1 + b - 1) / b : (int64_t)0);
-      const int64_t waves = ((a + b) * base + 147) / 148;
+      const int64_t waves = ((a + b) * base + sm_count() - 1) / sm_count();
       const int64_t cost = waves * (kpt + ovh);
       if (cost < best) {
         best = cost;
@@ -810,7 +794,7 @@ static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
 }
 
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
-  int64_t Z = kDwMaxWaves * 148 / dw_base(F, N);
+  int64_t Z = kDwMaxWaves * sm_count() / dw_base(F, N);
   const int64_t kb = (M + 31) / 32;
   if (Z > kb) Z = kb;
   if (Z < 1) Z = 1;
@@ -843,7 +827,7 @@ static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* 
   p.M = (int)M;
   p.N = (int)N;
   if (L.count) *L.count += 1;
-  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+  return tc_launch(p, L.s, sm_count()) == cudaSuccess ? 0 : -2;
 }
 
 int64_t tc_kpad(int64_t K, int bf) { return bf ? (K + 63) / 64 * 64 : (K + 31) / 32 * 32; }
@@ -934,7 +918,7 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   p.out = dA;
   p.inv_deg = inv_deg;
   if (L.count) *L.count += 1;
-  return tc_launch(p, L.s, 148) == cudaSuccess ? 0 : -2;
+  return tc_launch(p, L.s, sm_count()) == cudaSuccess ? 0 : -2;
 }
 
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
@@ -984,14 +968,14 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.K_out = (int)K;
   p.ld_out = NP;
   p.out = ws;
-  if (tc_launch(p, L.s, 148) != cudaSuccess) return -2;
+  if (tc_launch(p, L.s, sm_count()) != cudaSuccess) return -2;
   // bias row: colsum of Mb in the same Z splits (rows per split = a multiple of 32)
   const int64_t kbb = (rowsMb + 31) / 32;
   const int64_t rps = ((kbb + Zs - 1) / Zs) * 32;
   dim3 block(32, 8), grid((unsigned)((N + 31) / 32), (unsigned)Zs);
   // narrow N / few splits leave most SMs idle: split each split's rows into `sub` chunks (>= 4 blocks per
   // SM in total) with a fixed-order second pass, when the workspace has room for the sub partials
-  int sub = (int)((4 * 148 + (int64_t)grid.x * Zs - 1) / ((int64_t)grid.x * Zs));
+  int sub = (int)((4 * sm_count() + (int64_t)grid.x * Zs - 1) / ((int64_t)grid.x * Zs));
   sub = sub > kColsumSub ? kColsumSub : sub;
   const int64_t room = ws_floats - (int64_t)Zs * K * NP;
   while (sub > 1 && (int64_t)Zs * sub * N > room) --sub;

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "common.h"
 #include "kernels.cuh"
 #include "pgcn_dev.h"
 
@@ -15,9 +16,8 @@ namespace pgcn {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSMs = 148;
-
-inline int grid_for(int64_t work, int per_block, int max_blocks = kSMs * 16) {
+inline int grid_for(int64_t work, int per_block, int max_blocks = 0) {
+  if (max_blocks <= 0) max_blocks = sm_count() * 16;
   int64_t b = (work + per_block - 1) / per_block;
   if (b < 1) b = 1;
   if (b > max_blocks) b = max_blocks;
@@ -1101,14 +1101,7 @@ struct SpmmShape {
   X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
   X(32, 4, 2, 3) X(32, 2, 8, 2)
 
-static bool dyn_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PGCN_SPMM_DYN");
-    v = e ? std::atoi(e) : 1;
-  }
-  return v != 0;
-}
+static bool dyn_enabled() { return knobs().spmm_dyn != 0; }
 
 bool spmm_instantiated(int G, int NC, int U, int MB) {
 #define X(G_, NC_, U_, MB_) \
@@ -1122,7 +1115,7 @@ bool spmm_instantiated(int G, int NC, int U, int MB) {
 // listed widths (used by the in-situ sweep in tools/); combinations that are not instantiated are
 // ignored (the default shape is used), so a kernel is never skipped.
 bool spmm_override(int64_t ld4, SpmmShape& s) {
-  const char* e = std::getenv("PGCN_SPMM_TABLE");
+  const char* e = knobs().spmm_table;
   if (!e) return false;
   const char* p = e;
   while (*p) {
@@ -1196,12 +1189,7 @@ SpmmShape spmm16_shape(int64_t ld8) {
 // Items per atomic grab of the dynamic SpMM scheduler: ~128 edges per grab, 1..64 rows (sweep
 // tools/grab_sweep.sh: 64-256 best on Reddit / products / papers-q; 512+ loses L2 locality).
 static int grab_items(int64_t nnz, int64_t rows) {
-  static int64_t target = -1;  // dev knob PGCN_SPMM_GRAB: edges per grab (sweeps)
-  if (target < 0) {
-    const char* e = std::getenv("PGCN_SPMM_GRAB");
-    target = e ? std::atoll(e) : 128;
-    if (target < 1) target = 128;
-  }
+  const int64_t target = knobs().spmm_grab;  // dev knob PGCN_SPMM_GRAB: edges per grab (sweeps)
   if (nnz < 0 || rows <= 0) return 1;
   const int64_t k = (target * rows) / (nnz > 0 ? nnz : 1);
   return (int)(k < 1 ? 1 : (k > 64 ? 64 : k));
@@ -1226,11 +1214,11 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
 // on a side stream, one block per SM next to the tile kernel's CTA, measured 15-25 % slower: both
 // passes contend for the same L2 / DRAM path.)
 
-void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
+int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
               int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work, int self, const float* bias,
               int64_t n_bias, int relu, int64_t n_cols, void* g16, const int32_t* rows, int64_t nnz,
               const TileDev* tiles, void* t16, int compact) {
-  if (n_rows <= 0) return;
+  if (n_rows <= 0) return 0;
   const int tcu = tiles && tiles->n_tiles > 0 && !rows && n_cols >= 0 && n_valid >= n_cols && tiles->n_rows == n_rows;
   if (tcu) {
     row_ptr = tiles->lrp;
@@ -1240,8 +1228,7 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
   const int64_t ld4 = ld / 4, ld8 = (ld + 7) / 8;
   const bool b16 = g16 != nullptr;
   if ((b16 ? ld8 * 16 : ld4 * 16) >= (int64_t(1) << 32) || n_valid >= (int64_t(1) << 31)) {
-    std::fprintf(stderr, "pgcn: spmm_fwd row stride / id range exceeds 32-bit addressing\n");
-    std::abort();
+    return fail(PGCN_EUNSUPPORTED, "spmm_fwd: row stride / id range exceeds 32-bit addressing");
   }
   const int K = grab_items(nnz, n_rows);
   if (!dyn_enabled()) work = nullptr;
@@ -1253,11 +1240,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
     k_to_bf16<<<grid_for(n_valid * ld8, kThreads), kThreads, 0, L.s>>>(D4, ld4, ld4, n_valid, ld8, G16);
     count(L);
   }
-  auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add) {
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add) -> int {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     if (b16) {
       const SpmmShape sh = spmm16_shape(ld8);
-      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
+      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     if (chk)                                                                                                   \
@@ -1269,14 +1256,11 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
                                                                        n_valid, sh.nchunk, Z4, ld4, wk, K, slf,   \
                                                                        bias, n_bias, relu, rows, add, compact);   \
   } else
-      PGCN_SPMM16_CASES(X) {
-        std::fprintf(stderr, "pgcn: no bf16 spmm_fwd shape for ld8=%lld\n", (long long)ld8);
-        std::abort();
-      }
+      PGCN_SPMM16_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no bf16 spmm_fwd shape for ld8=%lld", (long long)ld8); }
 #undef X
     } else {
       const SpmmShape sh = spmm_shape(ld4);
-      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, kSMs * 64);
+      const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     if (chk)                                                                                                   \
@@ -1288,16 +1272,14 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
                                                                      n_valid, sh.nchunk, Z4, wk, K, slf, bias,    \
                                                                      n_bias, relu, rows, add, compact);           \
   } else
-      PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_fwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
+      PGCN_SPMM_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no spmm_fwd shape for ld4=%lld", (long long)ld4); }
 #undef X
     }
     count(L);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
   };
-  if (!tcu) {
-    gather(L.s, work, self, 0);
-    return;
-  }
-  auto tile = [&](float* out) {
+  if (!tcu) return gather(L.s, work, self, 0);
+  auto tile = [&](float* out) -> int {
     int rc;
     if (b16) {
       rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_valid, ld8 * 8, out, ld, ld);
@@ -1308,20 +1290,17 @@ void spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float*
       count(L);
       rc = spmm_tc(L, *tiles, H16, H16 + n_valid * ld8, ld8 * 8, n_valid, ld8 * 8, out, ld, ld);
     }
-    if (rc) {
-      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (fwd) launch failed\n");
-      std::abort();
-    }
+    return rc ? fail(PGCN_ECUDA, "tensor-core tile SpMM (fwd) launch failed") : 0;
   };
-  tile(Z);
-  gather(L.s, work, self, 1);
+  if (int rc = tile(Z)) return rc;
+  return gather(L.s, work, self, 1);
 }
 
-void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
+int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
               const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz,
               const TileDev* tiles, void* t16, const int32_t* dmap) {
-  if (n_all <= 0) return;
+  if (n_all <= 0) return 0;
   const int tcu = tiles && tiles->n_tiles > 0 && tiles->n_rows == n_all;  // see spmm_fwd
   if (tcu) {
     t_row_ptr = tiles->lrp;
@@ -1331,8 +1310,7 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
   const int64_t ld4 = ld / 4, ld8 = (ld + 7) / 8;
   const bool b16 = g16 != nullptr;
   if ((b16 ? ld8 * 16 : ld_dA * 4) >= (int64_t(1) << 32) || n_in >= (int64_t(1) << 31)) {
-    std::fprintf(stderr, "pgcn: spmm_bwd row stride / id range exceeds 32-bit addressing\n");
-    std::abort();
+    return fail(PGCN_EUNSUPPORTED, "spmm_bwd: row stride / id range exceeds 32-bit addressing");
   }
   const int K = grab_items(nnz, n_all);
   if (!dyn_enabled()) work = nullptr;
@@ -1344,40 +1322,35 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
     k_to_bf16<<<grid_for(n_in * ld8, kThreads), kThreads, 0, L.s>>>(a, lda4, ld4, n_in, ld8, G16);
     count(L);
   }
-  auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add) {
+  auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add) -> int {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     auto b = reinterpret_cast<const float4*>(dD);
     if (b16) {
       const SpmmShape sh = spmm16_shape(ld8);
-      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
+      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all,  \
                                                               sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                     \
   } else
-      PGCN_SPMM16_CASES(X) {
-        std::fprintf(stderr, "pgcn: no bf16 spmm_bwd shape for ld8=%lld\n", (long long)ld8);
-        std::abort();
-      }
+      PGCN_SPMM16_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no bf16 spmm_bwd shape for ld8=%lld", (long long)ld8); }
 #undef X
     } else {
       const SpmmShape sh = spmm_shape(ld4);
-      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, kSMs * 64);
+      const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
                                                             sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                       \
   } else
-      PGCN_SPMM_CASES(X) { std::fprintf(stderr, "pgcn: no spmm_bwd shape for ld4=%lld\n", (long long)ld4); std::abort(); }
+      PGCN_SPMM_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no spmm_bwd shape for ld4=%lld", (long long)ld4); }
 #undef X
     }
     count(L);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
   };
-  if (!tcu) {
-    gather(L.s, work, dDs, 0);
-    return;
-  }
-  auto tile = [&](float* out) {
+  if (!tcu) return gather(L.s, work, dDs, 0);
+  auto tile = [&](float* out) -> int {
     int rc;
     if (b16) {
       rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_in, ld8 * 8, out, ld, ld);
@@ -1388,13 +1361,10 @@ void spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const fl
       count(L);
       rc = spmm_tc(L, *tiles, H16, H16 + n_in * ld8, ld8 * 8, n_in, ld8 * 8, out, ld, ld);
     }
-    if (rc) {
-      std::fprintf(stderr, "pgcn: tensor-core tile SpMM (bwd) launch failed\n");
-      std::abort();
-    }
+    return rc ? fail(PGCN_ECUDA, "tensor-core tile SpMM (bwd) launch failed") : 0;
   };
-  tile(J);
-  gather(L.s, work, dDs, 1);
+  if (int rc = tile(J)) return rc;
+  return gather(L.s, work, dDs, 1);
 }
 
 void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t n_rows, int64_t ld, float* dst,
@@ -1473,7 +1443,7 @@ void gather_bytes(Launch L, const void* src, const int32_t* list, int64_t n, int
 void loss_rows(Launch L, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
                const uint8_t* train, double n_train, float* M, float* row_loss) {
   if (n <= 0) return;
-  const int grid = grid_for(n, kThreads / 32, kSMs * 32);
+  const int grid = grid_for(n, kThreads / 32, sm_count() * 32);
   if (kind == 0)
     k_loss_ce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const int32_t*>(labels), train,
                                           (float)(1.0 / n_train), M, row_loss);
@@ -1500,7 +1470,7 @@ void gemm_fwd_f32(Launch L, const float* Z, const float* D, int64_t ldA, int64_t
 int64_t gemm_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
   const int64_t K = 2 * F + 1;
   const int64_t tiles = ((K + BM - 1) / BM) * ((N + BN - 1) / BN);
-  int64_t splits = (2 * kSMs + tiles - 1) / tiles;
+  int64_t splits = (2 * sm_count() + tiles - 1) / tiles;
   const int64_t max_splits = (M + 255) / 256;
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
@@ -1555,7 +1525,7 @@ void stale_err(Launch L, const SegTable& fresh, const int32_t* fmap, const SegTa
                const float* used, int64_t n_rows, int64_t ld, int64_t F, double* out) {
   if (n_rows <= 0) return;
   SegTable none{};
-  k_stale_err<<<grid_for(n_rows * F, 256, kSMs * 4), 256, 0, L.s>>>(fresh, fmap, used_tab ? *used_tab : none, umap, used,
+  k_stale_err<<<grid_for(n_rows * F, 256, sm_count() * 4), 256, 0, L.s>>>(fresh, fmap, used_tab ? *used_tab : none, umap, used,
                                                                     used_tab ? 1 : 0, n_rows, ld, F, out);
   count(L);
 }

@@ -61,7 +61,7 @@ void dropout_fwd(Launch, const float* H, float* D, int64_t ld, int64_t n_rows, i
 // bias (optional, n_bias entries): Z = act(Z + b) epilogue (relu = ReLU), fusing the node update of
 // a transform-first GCN layer.  n_cols: rows of D (neighbour ids < n_cols); -1 = unknown (ids are
 // then checked against n_valid on every edge).
-void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
+int spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* inv_deg,
               const float* D, int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, unsigned long long* work,
               int self = 0, const float* bias = nullptr, int64_t n_bias = 0, int relu = 0, int64_t n_cols = -1,
               void* g16 = nullptr, const int32_t* rows = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr,
@@ -74,11 +74,12 @@ void spmm_fwd(Launch, const int64_t* row_ptr, const int32_t* col, const float* i
 //     dZs = inv_deg-scaled dZ (first half of dA), dDs = second half; both stride ld_dA.
 //     rs (optional, GCN-sym R26): the sum is scaled by rs[u] = d~_u^-1/2 before the mask (dDs = dZs
 //     then realises the self loop).
-void spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
+int spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs,
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
               void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr, void* t16 = nullptr,
               const int32_t* dmap = nullptr);
+// Both SpMMs return 0, or a PGCN_E* code (message set) when a launch cannot be made.
 // tiles (both SpMMs, optional): dense-tile decomposition of the pattern (tiles.h); its heavy tiles are
 // summed by spmm_tc into the output rows first and the gather kernel walks only the light CSR, adding
 // the tile sums (fwd: used only when n_valid >= n_cols and rows == nullptr).  t16 (fp32 tier with tiles):

@@ -9,12 +9,15 @@
 // boundary sets are known, so they run on separate threads); every output order is the
 // canonical one of include/pgcn.h (reading R20), so the result does not depend on the
 // thread count.  Global -> local lookups use one shared int32 array of size N
-// (`pos_in_part`, a node's rank inside its owner) plus a per-thread halo map that is
-// reset after use.
+// (`pos_in_part`, a node's rank inside its owner); V_i comes from one counting pass over the
+// nodes, and each partition's boundary scan marks seen nodes in an N-bit set (N/8 bytes per
+// thread).  A worker that throws (std::bad_alloc) hands the exception to the calling thread,
+// which returns PGCN_ENOMEM.
 #include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -46,6 +49,8 @@ struct pgcn_partitioning {
 
 namespace {
 
+// Runs f(0..n_items) on up to n_threads threads; the first exception thrown by any item is
+// rethrown on the calling thread after every worker has joined.
 template <class F>
 void run_threads(int n_items, int n_threads, F f) {
   n_threads = std::max(1, std::min(n_threads, n_items));
@@ -55,11 +60,20 @@ void run_threads(int n_items, int n_threads, F f) {
   }
   std::vector<std::thread> th;
   std::atomic<int> next{0};
+  std::mutex mu;
+  std::exception_ptr err;
   for (int k = 0; k < n_threads; ++k)
     th.emplace_back([&] {
-      for (int i = next++; i < n_items; i = next++) f(i);
+      try {
+        for (int i = next++; i < n_items; i = next++) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+        next = n_items;  // stop handing out items
+      }
     });
   for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
 }
 
 }  // namespace
@@ -113,19 +127,22 @@ extern "C" int pgcn_partition(int64_t n, const int64_t* row_ptr, const int32_t* 
     std::vector<int64_t> count(n_parts, 0);
     for (int64_t v = 0; v < n; ++v) pos_in_part[v] = (int32_t)count[part_of[v]]++;
     P->parts.resize(n_parts);
+    for (int32_t i = 0; i < n_parts; ++i) P->parts[i].inner_gid.resize(count[i]);
+    for (int64_t v = 0; v < n; ++v) P->parts[part_of[v]].inner_gid[pos_in_part[v]] = v;  // V_i ascending
 
-    // l.1: V_i and B_i (boundary sorted by (owner, gid))
+    // l.1: B_i (boundary sorted by (owner, gid))
     run_threads(n_parts, n_threads, [&](int i) {
       PartArrays& A = P->parts[i];
-      A.inner_gid.reserve(count[i]);
-      for (int64_t v = 0; v < n; ++v)
-        if (part_of[v] == i) A.inner_gid.push_back(v);
-      std::vector<uint8_t> seen(n, 0);
+      std::vector<uint64_t> seen((size_t)(n + 63) / 64, 0);
       std::vector<int64_t> halo;
       for (int64_t v : A.inner_gid)
         for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
-          int32_t u = col_idx[e];
-          if (part_of[u] != i && !seen[u]) { seen[u] = 1; halo.push_back(u); }
+          const int32_t u = col_idx[e];
+          const uint64_t bit = uint64_t(1) << (u & 63);
+          if (part_of[u] != i && !(seen[u >> 6] & bit)) {
+            seen[u >> 6] |= bit;
+            halo.push_back(u);
+          }
         }
       std::sort(halo.begin(), halo.end(), [&](int64_t a, int64_t b) {
         return part_of[a] != part_of[b] ? part_of[a] < part_of[b] : a < b;
@@ -204,6 +221,8 @@ extern "C" int pgcn_partition(int64_t n, const int64_t* row_ptr, const int32_t* 
     });
   } catch (const std::bad_alloc&) {
     return fail(PGCN_ENOMEM, "pgcn_partition: host allocation failed");
+  } catch (...) {
+    return fail(PGCN_ENOMEM, "pgcn_partition: worker failed");
   }
   *out = P.release();
   return PGCN_OK;

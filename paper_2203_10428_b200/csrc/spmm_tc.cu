@@ -355,12 +355,8 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   using namespace tcs;
   if (T.n_rb <= 0) return 0;
   const int NT = lo ? 2 : 1;
-  static int env_cap = -1;  // dev knob PGCN_TC_SPMM_BN: n-tile cap (64 / 128 / 192 / 256) for A/B sweeps
-  if (env_cap < 0) {
-    const char* e = std::getenv("PGCN_TC_SPMM_BN");
-    env_cap = e ? std::atoi(e) : 0;
-    if (env_cap != 64 && env_cap != 128 && env_cap != 192 && env_cap != 256) env_cap = 0;
-  }
+  const DevKnobs& kn = knobs();
+  const int env_cap = kn.tc_spmm_bn;
   const int bn_cap = env_cap ? env_cap : (NT == 2 ? 128 : 256);
   Params p{};
   int64_t bn = (width + 63) / 64 * 64;
@@ -369,17 +365,9 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.n_nt = (int)((width + bn - 1) / bn);
   p.n_rb = (int)T.n_rb;
   p.rb_ptr = T.rb_ptr;
-  static int env_order = -1;  // dev knob PGCN_TC_SPMM_ORDER: 1 = descending tile count (LPT), 0 = natural
-  if (env_order < 0) {
-    const char* e = std::getenv("PGCN_TC_SPMM_ORDER");
-    env_order = e ? std::atoi(e) : 1;
-  }
+  const int env_order = kn.tc_spmm_order;
   p.order = env_order ? T.order : nullptr;
-  static int env_dbg = -1;
-  if (env_dbg < 0) {
-    const char* e = std::getenv("PGCN_TC_SPMM_DBG");
-    env_dbg = e ? std::atoi(e) : 0;
-  }
+  const int env_dbg = kn.tc_spmm_dbg;
   p.dbg = env_dbg;
   p.tile_col = T.tile_col;
   p.mask = T.mask;
@@ -387,18 +375,7 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.n_rows = T.n_rows;
   p.ld_out = ld_out;
   p.width = (int)width;
-  static int env_nacc1 = -1;  // dev knob PGCN_TC_SPMM_NACC1=1: one TMEM accumulator even with one CTA per SM
-  if (env_nacc1 < 0) {
-    const char* e = std::getenv("PGCN_TC_SPMM_NACC1");
-    env_nacc1 = e ? std::atoi(e) : 0;
-  }
-  static int env_ts = -1, env_ctas = -1;  // dev knobs PGCN_TC_SPMM_TS (0: A in shared memory),
-  if (env_ts < 0) {                        // PGCN_TC_SPMM_CTAS (CTAs per SM, 1 or 2; default 2)
-    const char* e = std::getenv("PGCN_TC_SPMM_TS");
-    env_ts = e ? std::atoi(e) : 1;
-    e = std::getenv("PGCN_TC_SPMM_CTAS");
-    env_ctas = e ? std::atoi(e) : 2;
-  }
+  const int env_nacc1 = kn.tc_spmm_nacc1, env_ts = kn.tc_spmm_ts, env_ctas = kn.tc_spmm_ctas;
   // The kernel is latency-bound (one chain TMA -> build -> MMA per stage), so two CTAs per SM (two
   // independent pipelines sharing the tensor core) beat one CTA with twice the stages: 2 CTAs x
   // (<= 104 KB of stages, one TMEM accumulator, <= 256 TMEM columns).  A in TMEM (TS) when the
@@ -421,25 +398,16 @@ int spmm_tc(Launch L, const TileDev& T, const void* hi, const void* lo, int64_t 
   p.stages = S;
   p.tmem_cols = tmem_budget == 256 ? 256 : (TS ? 512 : tc_tmem_cols(p.BN));
   const size_t smem = 1024 + (size_t)p.stages * stage + (4 * p.stages + 4) * 8 + 16;
-  static int env_box = -1;  // dev knob PGCN_TC_SPMM_BOX64 (0: two 32-row boxes per atom column)
-  if (env_box < 0) {
-    const char* e = std::getenv("PGCN_TC_SPMM_BOX64");
-    env_box = e ? std::atoi(e) : 1;
-  }
+  const int env_box = kn.tc_spmm_box64;
   p.box64 = env_box ? 1 : 0;
   const int box_rows = p.box64 ? 64 : 32;
   if (!tc_map_table(&p.map_b[0], hi, true, b_cols, b_rows, b_ld, 64, box_rows)) return -1;
   if (NT == 2 && !tc_map_table(&p.map_b[1], lo, true, b_cols, b_rows, b_ld, 64, box_rows)) return -1;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_spmm_tc<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_spmm_tc<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_spmm_tc<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_spmm_tc<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  if (smem_attr_once((const void*)k_spmm_tc<1, 0>, 227 * 1024) || smem_attr_once((const void*)k_spmm_tc<2, 0>, 227 * 1024) ||
+      smem_attr_once((const void*)k_spmm_tc<1, 1>, 227 * 1024) || smem_attr_once((const void*)k_spmm_tc<2, 1>, 227 * 1024))
+    return -2;
   const int n_items = p.n_rb * p.n_nt;
-  const int grid_cap = ctas * 148;
+  const int grid_cap = ctas * sm_count();
   const int grid = n_items < grid_cap ? n_items : grid_cap;
   if (NT == 2) {
     if (TS) k_spmm_tc<2, 1><<<grid, kThreads, smem, L.s>>>(p);

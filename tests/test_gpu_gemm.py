@@ -88,3 +88,38 @@ def test_input_gradient(P, variant, M, F, N):
     assert rel(got[:, :F], dA[:, :F] * inv[:, None]) <= TOLS[variant]
     assert rel(got[:, L:L + F], dA[:, F:]) <= TOLS[variant]
     assert (got[:, F:L] == 0).all() and (got[:, L + F:] == 0).all()
+
+
+# The dW GEMM at the row counts the bench reduces over: a Reddit-shaped partition (116,483 rows; the
+# split-K plan with many splits) and a papers100M-shaped 8-way partition (13.9M rows; the colsum bias
+# row's chunked second pass).  Inputs are drawn on the device (seeded); the reference is the same
+# contraction in float64 (cuBLAS DGEMM through torch: a library primitive, the plain definition A^T M).
+BIG = [(116483, 256, 256), (116483, 602, 256), (13_900_000, 48, 48), (13_900_000, 128, 48)]
+
+
+@pytest.mark.parametrize("variant", ["tc", "bf16"])
+@pytest.mark.parametrize("M,F,N", BIG)
+def test_weight_gradient_full_size(P, variant, M, F, N):
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(M + F + N)
+    A0 = torch.zeros((M, ld(F)), device="cuda")
+    A1 = torch.zeros((M, ld(F)), device="cuda")
+    A0[:, :F] = torch.randn((M, F), device="cuda", generator=gen)
+    A1[:, :F] = torch.randn((M, F), device="cuda", generator=gen)
+    Mg = torch.zeros((M, ld(N)), device="cuda")
+    Mg[:, :N] = torch.randn((M, N), device="cuda", generator=gen) * 1e-3
+    W = torch.zeros((2 * F + 1, N), device="cuda")
+    out = torch.zeros((2 * F + 1, N), device="cuda")
+    P.dev_gemm(1, variant, A0, A1, M, F, W, N, out, N, Mg=Mg)
+    torch.cuda.synchronize()
+    ref = torch.zeros((2 * F + 1, N), dtype=torch.float64, device="cuda")
+    step = 1 << 21
+    for r0 in range(0, M, step):  # fp64 A^T M in row chunks (bounded scratch)
+        r1 = min(M, r0 + step)
+        m = Mg[r0:r1, :N].double()
+        ref[:F] += A0[r0:r1, :F].double().T @ m
+        ref[F:2 * F] += A1[r0:r1, :F].double().T @ m
+        ref[2 * F] += m.sum(0)
+    got, ref = out.double(), ref
+    err = float((got - ref).abs().max() / ref.abs().max())
+    assert err <= TOLS[variant], (M, F, N, variant, err)

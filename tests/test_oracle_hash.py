@@ -1,7 +1,7 @@
 """Pins for oracle/hashmask.py (dropout mask, reading R5)."""
 import numpy as np
 
-from oracle.hashmask import keep_mask, keep_threshold, splitmix64
+from oracle.hashmask import dropout, keep_mask, keep_threshold, splitmix64
 
 GAMMA = 0x9E3779B97F4A7C15
 
@@ -47,10 +47,32 @@ def test_mask_keyed_by_gid_not_position():
     assert (a != c).any() and (a != d).any()
 
 
-def test_mask_key_formula_by_hand():
-    # key = ((t*(L+1)+l)*N + gid)*F + col ; keep iff (SplitMix64(key ^ seed) >> 40) >= thr
-    t, l, L, N, F, seed, p = 3, 2, 4, 1000, 7, 123, 0.5
-    gid, col = 42, 5
-    key = ((t * (L + 1) + l) * N + gid) * F + col
-    h = int(splitmix64(key ^ seed))
-    assert bool(keep_mask(t, l, L, N, [gid], F, seed, p)[0, col]) == ((h >> 40) >= (1 << 23))
+def test_masks_of_different_iterations_and_layers_are_independent():
+    # R5 keys every (t, l, gid, col) to its own counter; masks of two different (t, l) on the same rows
+    # must agree as often as two independent Bernoulli(1-p) draws: p^2 + (1-p)^2, within 4 sigma (a key
+    # collision between layers or iterations -- e.g. a dropped (L+1) or N factor -- shows up as ~100%)
+    p, n, F = 0.3, 20000, 50
+    base = keep_mask(5, 2, 3, 40000, np.arange(n), F, seed=9, p=p)
+    q = p * p + (1 - p) * (1 - p)
+    sigma = np.sqrt(q * (1 - q) / base.size)
+    for t, l in ((6, 2), (5, 3), (5, 1), (4, 2)):
+        other = keep_mask(t, l, 3, 40000, np.arange(n), F, seed=9, p=p)
+        assert abs((base == other).mean() - q) < 4 * sigma, (t, l)
+    # neighbouring rows and columns of one mask are independent too (no shared key between (g, F-1)
+    # and (g+1, 0) beyond the formula's contiguity): agreement of column c with column c+1
+    agree = (base[:, :-1] == base[:, 1:]).mean()
+    sigma2 = np.sqrt(q * (1 - q) / base[:, 1:].size)
+    assert abs(agree - q) < 4 * sigma2
+
+
+def test_dropout_preserves_the_mean():
+    # PAPER.md:983 applies standard (inverted) dropout: E[D] = H, i.e. the kept entries are scaled by
+    # 1/(1-p).  With H = 1 the sample mean of D must be 1 within 4 sigma (sigma^2 = p/((1-p) n)); a
+    # missing scale (mean 1-p) or a 1/p scale (mean (1-p)/p) fails.
+    for p in (0.1, 0.3, 0.5):
+        n, F = 20000, 40
+        H = np.ones((n, F))
+        D, keep = dropout(H, 3, 2, 3, 50000, np.arange(n), seed=4, p=p)
+        sigma = np.sqrt(p / ((1 - p) * H.size))
+        assert abs(D.mean() - 1.0) < 4 * sigma, p
+        assert np.all(D[keep] == 1.0 / (1.0 - p)) and np.all(D[~keep] == 0.0)
