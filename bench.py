@@ -342,6 +342,7 @@ def main():
     nloc = len(local_parts)
     for i in range(nloc):  # one partition at a time: the device staging copy is freed right after
         d_in = tuple(a.cuda(non_blocking=True) for a in host[i])
+        torch.cuda.synchronize()  # the H2D copies (current stream) land before the context stream reads them
         ctx.set_inputs(i, *d_in)
         torch.cuda.synchronize()
         del d_in
@@ -400,6 +401,8 @@ def main():
     ms = ms_total / K
     value = 1000.0 / ms
     loss_v = float(loss.item())
+    if not (loss_v > 0.0 and loss_v == loss_v):  # every partition has train rows: the loss is positive
+        raise SystemExit("bench: loss %r after the timed steps -- inputs not installed?" % loss_v)
     # (2) instrumented pass: per-kernel CUDA events on the context stream (roofline, breakdown)
     ctx.timing_enable(True)
     ms_instr = timed(K) / K
@@ -414,6 +417,8 @@ def main():
         args.no_e2e = True  # 14 GB of inputs per step over PCIe: no end-to-end leg for the papers shape
     if not args.no_e2e:
         loss_h = torch.zeros(1).pin_memory()
+        ld0 = (m.widths[0] + 3) // 4 * 4  # host X kept in the library's padded row layout: one copy per step
+        host = [(torch.nn.functional.pad(X, (0, ld0 - X.shape[1])).pin_memory(), lab, tm) for X, lab, tm in host]
         h2d = sum(sum(a.numel() * a.element_size() for a in h) for h in host)
         torch.cuda.synchronize()
         if dist is not None:

@@ -259,8 +259,10 @@ int pgcn_set_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* la
                     const uint8_t* train_mask);
 
 /* Streaming re-upload of a hosted partition's inputs between iterations (the end-to-end path: inputs
- * live in host memory and are copied every iteration).  Same layouts as pgcn_set_inputs; X, labels and
- * train_mask are HOST pointers (pinned memory makes the copy asynchronous).  The copies run on the
+ * live in host memory and are copied every iteration).  Same layouts as pgcn_set_inputs, except that X
+ * has row stride ld_x = F_0 or round_up(F_0, 4) (the context's own padded layout: one contiguous copy
+ * instead of n_inner row copies); X, labels and train_mask are HOST pointers (pinned memory makes the
+ * copy asynchronous).  The copies run on the
  * library's copy stream and overlap the iteration in flight: X is overwritten only after that
  * iteration's last read of X (layer 1's dropout, or layer 1's weight gradient when dropout = 0),
  * labels / mask only after its loss; the next pgcn_layer_fwd(layer 1) waits for the copies.  The train
@@ -268,7 +270,7 @@ int pgcn_set_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* la
  * the same values (X's boundary rows are exchanged once, reading R10).  Caller keeps the host buffers
  * alive until the next iteration's layer 1 has been enqueued and the stream has passed it.
  * Errors: PGCN_EINVAL (null / range), PGCN_ESTATE (poisoned, or pgcn_set_inputs never called).     */
-int pgcn_stage_inputs(pgcn_ctx* ctx, int32_t local, const float* X, const void* labels,
+int pgcn_stage_inputs(pgcn_ctx* ctx, int32_t local, const float* X, int64_t ld_x, const void* labels,
                       const uint8_t* train_mask);
 
 /* Flat parameter vector theta = vec[W^(1), b^(1), ..., W^(L), b^(L)], fp32,
@@ -293,6 +295,32 @@ int pgcn_layer_bwd(pgcn_ctx* ctx, int64_t t, int32_t layer, const float* params)
  * params updated in place.  opt_state: [2 * param_count] fp32 device (Adam m, v; zero at t=1),
  * may be NULL for SGD.                                                                     */
 int pgcn_update(pgcn_ctx* ctx, int64_t t, float* params, float* grads, float* opt_state);
+
+/* (3') / (5') Caller-buffer forms of the per-layer calls (SURVEY 8(b) signatures): the same Alg. 1 steps
+ * as pgcn_layer_fwd / pgcn_layer_bwd (and the same call-order rules -- they count as those calls), with
+ * the layer's weights and the activations in caller-owned device buffers.  Pointer arrays are indexed
+ * by hosted partition k = 0..n_local-1 (n_inner_k rows each); a NULL array or entry means "not given".
+ *   W [ns F_{l-1} x F_l] row-major (ns = 2 GraphSAGE [W_neigh; W_self], 1 GCN-sym), b [F_l]: the layer's
+ *       weights W_{t-1}; the context stages them in theta layout (the backward call must pass the same
+ *       weights as the forward call of iteration t).
+ *   fwd h_in[k]  [n_inner_k x F_{l-1}], row stride ld_in: replaces the inner rows of the layer input
+ *       H^(l-1) (layer 1: X, constant by reading R10) before the layer runs -- this is what is sent to
+ *       the peers (Alg. 1 l.12-13); NULL keeps the output of the previous layer call.
+ *   fwd h_out[k] [n_inner_k x F_l], row stride ld_out: receives H^(l) (ReLU for l < L; logits for l = L,
+ *       valid on train rows only under train_sparse).
+ *   bwd j_out[k] [n_inner_k x F_l], row stride ld_jo: replaces the accumulated J^(l) of the layer's output
+ *       (l = L: dLoss/dH^(L); EUNSUPPORTED for l = L with train_sparse on a GraphSAGE aggregate-first last
+ *       layer, whose rows are compact); NULL keeps the context's own (from pgcn_loss / the layer above).
+ *   bwd dW_local [ns F_{l-1} x F_l], db_local [F_l]: sum over the hosted partitions (ascending i) of G_i^(l)
+ *       (Alg. 1 l.18) -- this context's contribution before the all-reduce of pgcn_update.
+ *   bwd j_in[k] [n_inner_k x F_{l-1}] (l >= 2), row stride ld_ji: receives J^(l-1) after the stale-
+ *       gradient accumulation (l.22-25).
+ * Asynchronous on the context stream; buffers must stay valid until the stream has passed the call.   */
+int pgcn_layer_fwd_io(pgcn_ctx* ctx, int64_t t, int32_t layer, const float* W, const float* b,
+                      const float* const* h_in, int64_t ld_in, float* const* h_out, int64_t ld_out);
+int pgcn_layer_bwd_io(pgcn_ctx* ctx, int64_t t, int32_t layer, const float* W, const float* b,
+                      const float* const* j_out, int64_t ld_jo, float* dW_local, float* db_local,
+                      float* const* j_in, int64_t ld_ji);
 
 /* (7) One iteration t of Alg. 1 (l.8-32).                                                   */
 int pgcn_step(pgcn_ctx* ctx, int64_t t, float* params, float* grads, float* opt_state,

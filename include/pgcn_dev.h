@@ -32,6 +32,13 @@ int pgcn_dev_gemm(int32_t op, int32_t variant, const float* A0, const float* A1,
 int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D, int64_t ld,
                   int64_t n_rows, int64_t n_valid, float* Z, void* stream);
 
+/* Random-row gather microbenchmark (roofline denominator for DRAM-served aggregation): reads rows
+ * idx[0 .. n_idx) (row_floats floats each, multiple of 4, <= 128) of tab in full, U rows in flight per
+ * lane group (variant 0: U = 8, 1: U = 16), and writes checksums to out[] (sm_count x 8 x 256 floats).
+ * Bytes moved = n_idx x 4 x row_floats; the caller times it.                                       */
+int pgcn_dev_gather_read(const float* tab, int64_t row_floats, const int32_t* idx, int64_t n_idx, float* out,
+                         int32_t variant, void* stream);
+
 /* L2 streaming-read microbenchmark (roofline denominator for L2-served kernels): warps stream
  * contiguous chunks of buf[0 .. bytes) with __ldcg, `reps` passes (low 24 bits of reps), and write
  * one checksum per block to out[] (up to 148 x 8 blocks of 256 threads).  reps bits 24..31 pick the

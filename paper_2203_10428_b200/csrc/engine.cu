@@ -148,6 +148,7 @@ struct pgcn_ctx {
   int cl = 0;
   int64_t depth = 1;    // pipeline depth s (R27): an exchange posted at t is consumed at t + s
   float* part_loss = nullptr;
+  float* theta_io = nullptr;  // [P] weights staged by the caller-buffer layer calls (theta layout)
   unsigned long long* work = nullptr;  // SpMM dynamic-scheduling counter
   char* sp_tmp = nullptr;               // CUB scratch of the train-row builders (cfg.train_sparse)
   int64_t sp_tmp_bytes = 0;
@@ -171,6 +172,7 @@ struct pgcn_ctx {
   cudaStream_t cps = nullptr;
   cudaEvent_t ev_x_free = nullptr, ev_lab_free = nullptr, ev_in_ready = nullptr;
   int in_pending = 0, inputs_set = 0;
+  int force_write_j = 0;  // pgcn_layer_bwd_io with j_in: the stale-gradient accumulate writes J^(l-1) inner rows
 #ifdef PGCN_WITH_NCCL
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
@@ -389,6 +391,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     }
   }
   C->part_loss = A.take<float>(n_local);
+  C->theta_io = A.take<float>(C->P);
   C->work = A.take<unsigned long long>(4);
   C->diag = A.take<double>(2 * (PGCN_MAX_LAYERS + 1));
   return PGCN_OK;
@@ -947,7 +950,7 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
   return check_cuda(C, "pgcn_set_inputs");
 }
 
-extern "C" int pgcn_stage_inputs(pgcn_ctx* C, int32_t local, const float* X, const void* labels,
+extern "C" int pgcn_stage_inputs(pgcn_ctx* C, int32_t local, const float* X, int64_t ld_x, const void* labels,
                                  const uint8_t* train_mask) {
   if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
   if (C->poisoned) return fail(PGCN_ESTATE, "context poisoned");
@@ -956,10 +959,14 @@ extern "C" int pgcn_stage_inputs(pgcn_ctx* C, int32_t local, const float* X, con
   PartCtx& p = C->parts[local];
   if (p.n_in == 0) return PGCN_OK;
   if (!X || !labels || !train_mask) return fail(PGCN_EINVAL, "null input");
+  if (ld_x != C->F[0] && ld_x != C->ld[0]) return fail(PGCN_EINVAL, "ld_x must be F_0 or round_up(F_0, 4)");
   // X after the in-flight iteration's last read of X; labels / mask after its loss
   cudaStreamWaitEvent(C->cps, C->ev_x_free, 0);
-  cudaMemcpy2DAsync(p.X, sizeof(float) * C->ld[0], X, sizeof(float) * C->F[0], sizeof(float) * C->F[0], p.n_in,
-                    cudaMemcpyHostToDevice, C->cps);
+  if (ld_x == C->ld[0])  // the context's padded layout: one contiguous copy (full PCIe rate)
+    cudaMemcpyAsync(p.X, X, sizeof(float) * C->ld[0] * p.n_in, cudaMemcpyHostToDevice, C->cps);
+  else
+    cudaMemcpy2DAsync(p.X, sizeof(float) * C->ld[0], X, sizeof(float) * C->F[0], sizeof(float) * C->F[0], p.n_in,
+                      cudaMemcpyHostToDevice, C->cps);
   cudaStreamWaitEvent(C->cps, C->ev_lab_free, 0);
   const size_t lb = C->cfg.loss == 0 ? sizeof(int32_t) * p.n_in : (size_t)p.n_in * C->F[C->L];
   cudaMemcpyAsync(p.labels, labels, lb, cudaMemcpyHostToDevice, C->cps);
@@ -1352,7 +1359,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j) + 8.0 * p.n_in +
                                           (msg.n_seg ? ((m16 ? 2.0 : 4.0) * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
       grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, row_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
-                  p.J[l - 1][b], C->cfg.dump_j, p.H[l - 1][b], p.M, p.n_in, ldi, m16);
+                  p.J[l - 1][b], C->cfg.dump_j || C->force_write_j, p.H[l - 1][b], p.M, p.n_in, ldi, m16);
       if (C->cfg.staleness_stats && C->xp != XP_NCCL && C->n_parts > 1 && p.n_send > 0) {
         // N4: ||gradient messages used - fresh ones||^2 (fresh = peers' boundary rows of this iteration;
         // used = the smoothed state, the stale messages, or 0 when nothing was received)
@@ -1409,6 +1416,93 @@ extern "C" int pgcn_update(pgcn_ctx* C, int64_t t, float* params, float* grads, 
   if (rc) return rc;
   advance(C);
   return PGCN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Caller-buffer forms of the per-layer calls: stage W, b into theta layout, optionally
+// replace the layer's input / output-gradient rows, run the layer, copy results out.
+namespace {
+int stage_weights(pgcn_ctx* C, int l, const float* W, const float* b) {
+  if (!W || !b) return fail(PGCN_EINVAL, "W / b is NULL");
+  const int64_t nW = C->ns * C->F[l - 1] * C->F[l];
+  cudaMemcpyAsync(C->theta_io + C->woff[l], W, sizeof(float) * nW, cudaMemcpyDeviceToDevice, C->s);
+  cudaMemcpyAsync(C->theta_io + C->woff[l] + nW, b, sizeof(float) * C->F[l], cudaMemcpyDeviceToDevice, C->s);
+  return PGCN_OK;
+}
+void copy_rows(pgcn_ctx* C, float* dst, int64_t ldd, const float* src, int64_t lds, int64_t F, int64_t rows) {
+  if (rows > 0)
+    cudaMemcpy2DAsync(dst, sizeof(float) * ldd, src, sizeof(float) * lds, sizeof(float) * F, rows,
+                      cudaMemcpyDeviceToDevice, C->s);
+}
+}  // namespace
+
+extern "C" int pgcn_layer_fwd_io(pgcn_ctx* C, int64_t t, int32_t l, const float* W, const float* b,
+                                 const float* const* h_in, int64_t ld_in, float* const* h_out, int64_t ld_out) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_FWD, l, "pgcn_layer_fwd_io");
+  if (rc) return rc;
+  if ((h_in && ld_in < C->F[l - 1]) || (h_out && ld_out < C->F[l])) return fail(PGCN_EINVAL, "row stride too small");
+  if ((rc = stage_weights(C, l, W, b))) return rc;
+  const int bb = C->bi(t);
+  if (h_in)
+    for (size_t k = 0; k < C->parts.size(); ++k) {
+      PartCtx& p = C->parts[k];
+      if (h_in[k]) copy_rows(C, layer_in(p, l, bb), C->ld[l - 1], h_in[k], ld_in, C->F[l - 1], p.n_in);
+    }
+  if ((rc = pgcn_layer_fwd(C, t, l, C->theta_io))) return rc;
+  if (h_out)
+    for (size_t k = 0; k < C->parts.size(); ++k) {
+      PartCtx& p = C->parts[k];
+      if (h_out[k]) copy_rows(C, h_out[k], ld_out, l < C->L ? p.H[l][bb] : p.logits, C->ld[l], C->F[l], p.n_in);
+    }
+  return check_cuda(C, "pgcn_layer_fwd_io");
+}
+
+extern "C" int pgcn_layer_bwd_io(pgcn_ctx* C, int64_t t, int32_t l, const float* W, const float* b,
+                                 const float* const* j_out, int64_t ld_jo, float* dW_local, float* db_local,
+                                 float* const* j_in, int64_t ld_ji) {
+  if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
+  int rc = expect(C, t, K_BWD, l, "pgcn_layer_bwd_io");
+  if (rc) return rc;
+  if ((j_out && ld_jo < C->F[l]) || (j_in && l >= 2 && ld_ji < C->F[l - 1])) return fail(PGCN_EINVAL, "row stride too small");
+  if (j_out && l == C->L && C->cl) return fail(PGCN_EUNSUPPORTED, "j_out of the last layer with compact train rows");
+  if ((rc = stage_weights(C, l, W, b))) return rc;
+  const int bb = C->bi(t);
+  const Launch Lk = C->launch();
+  if (j_out)
+    for (size_t k = 0; k < C->parts.size(); ++k) {
+      PartCtx& p = C->parts[k];
+      if (!j_out[k]) continue;
+      if (l == C->L) {  // M^(L) = J^(L)
+        copy_rows(C, p.M, C->ld[l], j_out[k], ld_jo, C->F[l], p.n_in);
+      } else {          // M^(l) = J^(l) o 1[H^(l) > 0]: the accumulate kernel with no messages
+        copy_rows(C, p.J[l][bb], C->ld[l], j_out[k], ld_jo, C->F[l], p.n_in);
+        SegTable none{};
+        grad_reduce(Lk, p.inv_ptr, p.inv_pos, none, nullptr, nullptr, 0.f, 0, 0, p.J[l][bb], 0, p.H[l][bb], p.M,
+                    p.n_in, C->ld[l]);
+      }
+    }
+  C->force_write_j = j_in != nullptr && l >= 2;
+  rc = pgcn_layer_bwd(C, t, l, C->theta_io);
+  C->force_write_j = 0;
+  if (rc) return rc;
+  if (j_in && l >= 2)
+    for (size_t k = 0; k < C->parts.size(); ++k) {
+      PartCtx& p = C->parts[k];
+      if (j_in[k]) copy_rows(C, j_in[k], ld_ji, p.J[l - 1][bb], C->ld[l - 1], C->F[l - 1], p.n_in);
+    }
+  const int64_t nW = C->ns * C->F[l - 1] * C->F[l];
+  PtrList G{};
+  G.n = (int32_t)C->parts.size();
+  if (dW_local) {
+    for (int i = 0; i < G.n; ++i) G.p[i] = C->parts[i].G + C->woff[l];
+    sum_grads(Lk, G, nW, dW_local);
+  }
+  if (db_local) {
+    for (int i = 0; i < G.n; ++i) G.p[i] = C->parts[i].G + C->woff[l] + nW;
+    sum_grads(Lk, G, C->F[l], db_local);
+  }
+  return check_cuda(C, "pgcn_layer_bwd_io");
 }
 
 extern "C" int pgcn_step(pgcn_ctx* C, int64_t t, float* params, float* grads, float* opt_state, float* loss_dev) {

@@ -769,11 +769,23 @@ static int dw_bn(int64_t N, int bf) {
 constexpr int kDwMaxWaves = 3;
 constexpr int kColsumSub = 16;  // max row chunks per split of the bias-row column sums
 static int dw_base(int64_t F, int64_t N) { return (int)(((F + 127) / 128) * ((N + dw_bn(N, 0) - 1) / dw_bn(N, 0))); }
+// Longest accumulation chain of one dW tile, in k-blocks of 32 rows (dev knob PGCN_DW_KMAX; 0 = none).
+// The tensor core's fp32 accumulation does not round to nearest, so its error grows with the chain
+// length instead of averaging out: a 13.9M-row dW in ~1000-k-block chains measured 1.3e-3 relative
+// error against fp64; splitting longer reductions into more tiles (summed in fp32 round-to-nearest by
+// the fixed-order second pass) keeps every chain short.
+static int64_t dw_kmax() { return knobs().dw_kmax; }
+static int64_t zmin_for(int64_t kb) {
+  const int64_t km = dw_kmax();
+  return km > 0 ? std::max<int64_t>(1, (kb + km - 1) / km) : 1;
+}
 static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
   const int64_t ovh = 6;  // per-tile fill / drain, in k-block units
   int64_t best = INT64_MAX;
-  Z[0] = 1;
-  Z[1] = nseg > 1 ? 1 : 0;
+  const int64_t zm0 = zmin_for(kb0), zm1 = nseg > 1 ? zmin_for(kb1) : 0;
+  Z[0] = (int)zm0;
+  Z[1] = (int)zm1;
+  if ((zm0 + zm1) * base > (int64_t)kDwMaxWaves * sm_count()) return;  // chains cap the split count
   for (int W = 1; W <= kDwMaxWaves; ++W) {
     const int slots = W * sm_count() / base;
     if (slots < nseg) continue;
@@ -781,6 +793,7 @@ static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
     for (int z0 = lo; z0 <= hi; ++z0) {
       int64_t a = z0 < kb0 ? z0 : (kb0 > 0 ? kb0 : 1);
       int64_t b = nseg > 1 ? (slots - z0 < kb1 ? slots - z0 : (kb1 > 0 ? kb1 : 1)) : 0;
+      if (a < zm0 || (nseg > 1 && b < zm1)) continue;
       const int64_t kpt = std::max((kb0 + a - 1) / a, nseg > 1 ? (kb1 + b - 1) / b : (int64_t)0);
       const int64_t waves = ((a + b) * base + sm_count() - 1) / sm_count();
       const int64_t cost = waves * (kpt + ovh);
@@ -797,6 +810,7 @@ int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
   int64_t Z = kDwMaxWaves * sm_count() / dw_base(F, N);
   const int64_t kb = (M + 31) / 32;
   if (Z > kb) Z = kb;
+  Z = std::max(Z, zmin_for(kb));
   if (Z < 1) Z = 1;
   return Z * (2 * F + 1) * ((N + 3) / 4 * 4) + Z * kColsumSub * N;  // + the bias-row sub partials
 }

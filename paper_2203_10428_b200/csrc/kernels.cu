@@ -1548,6 +1548,30 @@ void opt_update(Launch L, const float* grads, int64_t P, float* params, float* m
 }
 
 namespace {
+// Random-row gather ceiling (roofline denominator for the DRAM-served aggregation): groups of G lanes
+// read whole rows idx[k] (row4 float4 each, row4 <= G) with U rows in flight per group, and fold them
+// into one checksum per thread.  No arithmetic beyond the adds: the hardware's random-row read rate.
+template <int G, int U>
+__global__ void __launch_bounds__(256) k_gather_read(const float4* __restrict__ tab, int64_t row4,
+                                                     const int32_t* __restrict__ idx, int64_t n_idx,
+                                                     float* __restrict__ out) {
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t n_grp = (int64_t)gridDim.x * blockDim.x / G;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t k0 = grp * U; k0 < n_idx; k0 += n_grp * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + u;
+      v[u] = (k < n_idx && lane < row4) ? __ldg(tab + (int64_t)__ldg(idx + k) * row4 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
+  }
+  out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc.x + acc.y + acc.z + acc.w;
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) k_l2_read(const float4* __restrict__ buf, int64_t n4, int reps,
                                                  float* __restrict__ out) {
@@ -1588,8 +1612,32 @@ __global__ void __launch_bounds__(256) k_l2_read(const float4* __restrict__ buf,
 extern "C" int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_deg, const float* D,
                              int64_t ld, int64_t n_rows, int64_t n_valid, float* Z, void* stream) {
   if (!row_ptr || !col || !inv_deg || !D || !Z || ld % 4 || n_rows < 0) return -1;
-  pgcn::spmm_fwd(pgcn::Launch{static_cast<cudaStream_t>(stream), nullptr}, row_ptr, col, inv_deg, D, ld, n_rows,
-                 n_valid, Z, nullptr, 0, nullptr, 0, 0, n_valid);
+  const int rc = pgcn::spmm_fwd(pgcn::Launch{static_cast<cudaStream_t>(stream), nullptr}, row_ptr, col, inv_deg, D,
+                                ld, n_rows, n_valid, Z, nullptr, 0, nullptr, 0, 0, n_valid);
+  return rc ? rc : (cudaGetLastError() == cudaSuccess ? 0 : -3);
+}
+
+extern "C" int pgcn_dev_gather_read(const float* tab, int64_t row_floats, const int32_t* idx, int64_t n_idx,
+                                    float* out, int32_t variant, void* stream) {
+  if (!tab || !idx || !out || row_floats % 4 || row_floats <= 0 || row_floats > 4 * 32 || n_idx < 0) return -1;
+  const int64_t row4 = row_floats / 4;
+  const int blocks = pgcn::sm_count() * 8;  // out holds blocks * 256 floats
+  auto s = static_cast<cudaStream_t>(stream);
+  auto t4 = reinterpret_cast<const float4*>(tab);
+  const int U = variant == 1 ? 16 : 8;
+  if (row4 <= 4) {
+    if (U == 8) pgcn::k_gather_read<4, 8><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+    else pgcn::k_gather_read<4, 16><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+  } else if (row4 <= 8) {
+    if (U == 8) pgcn::k_gather_read<8, 8><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+    else pgcn::k_gather_read<8, 16><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+  } else if (row4 <= 16) {
+    if (U == 8) pgcn::k_gather_read<16, 8><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+    else pgcn::k_gather_read<16, 16><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+  } else {
+    if (U == 8) pgcn::k_gather_read<32, 8><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+    else pgcn::k_gather_read<32, 16><<<blocks, 256, 0, s>>>(t4, row4, idx, n_idx, out);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -1601,8 +1649,9 @@ extern "C" int pgcn_dev_l2_read(const void* buf, int64_t bytes, int32_t reps, fl
   reps &= 0xffffff;
   auto s = static_cast<cudaStream_t>(stream);
   auto b4 = static_cast<const float4*>(buf);
-  if (variant == 0) pgcn::k_l2_read<4><<<148 * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
-  else if (variant == 1) pgcn::k_l2_read<8><<<148 * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
-  else pgcn::k_l2_read<8><<<148 * 4, 256, 0, s>>>(b4, bytes / 16, reps, out);
+  const int sms = pgcn::sm_count();  // out holds up to sms x 8 floats
+  if (variant == 0) pgcn::k_l2_read<4><<<sms * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
+  else if (variant == 1) pgcn::k_l2_read<8><<<sms * 8, 256, 0, s>>>(b4, bytes / 16, reps, out);
+  else pgcn::k_l2_read<8><<<sms * 4, 256, 0, s>>>(b4, bytes / 16, reps, out);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

@@ -87,7 +87,7 @@ def lib():
                                       C.POINTER(vp)]
         L.pgcn_ctx_destroy.argtypes = [vp]
         L.pgcn_set_inputs.argtypes = [vp, i32, vp, vp, vp]
-        L.pgcn_stage_inputs.argtypes = [vp, i32, vp, vp, vp]
+        L.pgcn_stage_inputs.argtypes = [vp, i32, vp, i64, vp, vp]
         L.pgcn_param_count.argtypes = [C.POINTER(Config)]
         L.pgcn_param_count.restype = i64
         L.pgcn_layer_fwd.argtypes = [vp, i64, i32, vp]
@@ -95,6 +95,8 @@ def lib():
         L.pgcn_layer_bwd.argtypes = [vp, i64, i32, vp]
         L.pgcn_update.argtypes = [vp, i64, vp, vp, vp]
         L.pgcn_step.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.pgcn_layer_fwd_io.argtypes = [vp, i64, i32, vp, vp, vp, i64, vp, i64]
+        L.pgcn_layer_bwd_io.argtypes = [vp, i64, i32, vp, vp, vp, i64, vp, vp, vp, i64]
         L.pgcn_tensor.argtypes = [vp, i32, i32, i32, i64, C.POINTER(TensorDesc)]
         L.pgcn_launch_count.argtypes = [vp]
         L.pgcn_launch_count.restype = i64
@@ -109,6 +111,7 @@ def lib():
         L.pgcn_staleness.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.pgcn_dev_spmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp, vp]
         L.pgcn_dev_l2_read.argtypes = [vp, i64, i32, vp, vp]
+        L.pgcn_dev_gather_read.argtypes = [vp, i64, vp, i64, vp, i32, vp]
         L.pgcn_dev_tiles.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.pgcn_nccl_unique_id.argtypes = [vp]
         L.pgcn_dev_exchange_hook.argtypes = [vp, i64, i32]
@@ -318,6 +321,10 @@ class Context:
         alive per hosted partition until the next call for that partition (device tensors are also
         marked as used on the context stream for torch's caching allocator)."""
         srcs = (X, labels, train_mask)
+        if any(getattr(a, "is_cuda", False) for a in srcs):
+            # device inputs produced on the caller's current stream (e.g. a non_blocking H2D copy) must be
+            # complete before the context stream reads them
+            self.stream.wait_stream(self.torch.cuda.current_stream(self.device))
         for a in srcs:
             if hasattr(a, "record_stream") and getattr(a, "is_cuda", False):
                 a.record_stream(self.stream)
@@ -326,15 +333,42 @@ class Context:
 
     def stage_inputs(self, local, X, labels, train_mask):
         """pgcn_stage_inputs: per-iteration re-upload of partition `local`'s inputs from HOST memory
-        (numpy arrays or pinned CPU tensors), overlapped with the iteration in flight."""
+        (numpy arrays or pinned CPU tensors), overlapped with the iteration in flight.  X may be
+        [n_inner x F_0] or already padded to [n_inner x round_up(F_0, 4)] (one contiguous copy)."""
         for a in (X, labels, train_mask):
             if getattr(a, "is_cuda", False):
                 raise ValueError("stage_inputs takes host buffers")
         self._keep[("stage", int(local))] = (X, labels, train_mask)
-        _check(lib().pgcn_stage_inputs(self.handle, int(local), _ptr(X), _ptr(labels), _ptr(train_mask)))
+        ld_x = int(X.stride(0)) if hasattr(X, "stride") and callable(X.stride) else int(X.strides[0] // 4)
+        _check(lib().pgcn_stage_inputs(self.handle, int(local), _ptr(X), ld_x, _ptr(labels), _ptr(train_mask)))
 
     def layer_fwd(self, t, layer, params):
         _check(lib().pgcn_layer_fwd(self.handle, int(t), int(layer), _ptr(params)))
+
+    @staticmethod
+    def _ptr_array(tensors):
+        """(ctypes void* array, row stride) of a per-hosted-partition list of 2-D tensors (None entries
+        allowed), or (None, 0)."""
+        if tensors is None:
+            return None, 0
+        arr = (C.c_void_p * len(tensors))(*[_ptr(x) for x in tensors])
+        lds = {int(x.stride(0)) for x in tensors if x is not None}
+        if len(lds) > 1:
+            raise ValueError("all row strides must be equal")
+        return arr, (lds.pop() if lds else 0)
+
+    def layer_fwd_io(self, t, layer, W, b, h_in=None, h_out=None):
+        """pgcn_layer_fwd_io: Alg. 1 l.9-14 with caller-owned W, b and per-partition H^(l-1) / H^(l)."""
+        a_in, ld_in = self._ptr_array(h_in)
+        a_out, ld_out = self._ptr_array(h_out)
+        _check(lib().pgcn_layer_fwd_io(self.handle, int(t), int(layer), _ptr(W), _ptr(b), a_in, ld_in, a_out, ld_out))
+
+    def layer_bwd_io(self, t, layer, W, b, j_out=None, dW_local=None, db_local=None, j_in=None):
+        """pgcn_layer_bwd_io: Alg. 1 l.18-27 with caller-owned W, b, J^(l), G^(l) and J^(l-1)."""
+        a_jo, ld_jo = self._ptr_array(j_out)
+        a_ji, ld_ji = self._ptr_array(j_in)
+        _check(lib().pgcn_layer_bwd_io(self.handle, int(t), int(layer), _ptr(W), _ptr(b), a_jo, ld_jo, _ptr(dW_local),
+                                       _ptr(db_local), a_ji, ld_ji))
 
     def loss(self, t, loss_dev=None):
         _check(lib().pgcn_loss(self.handle, int(t), _ptr(loss_dev)))

@@ -229,10 +229,12 @@ def test_stage_inputs_overlapped_reupload(P, p):
     host = []
     for i in range(3):
         gid = part.view(i)["inner_gid"]
-        h = (torch.tensor(g.X[gid]).pin_memory(), torch.tensor(g.labels[gid]).pin_memory(),
-             torch.tensor(g.train_mask[gid]).pin_memory())
+        X = torch.tensor(g.X[gid])
+        if p == 0.0:  # the library's padded row layout (one contiguous copy) instead of F_0-wide rows
+            X = torch.nn.functional.pad(X, (0, (X.shape[1] + 3) // 4 * 4 - X.shape[1]))
+        h = (X.pin_memory(), torch.tensor(g.labels[gid]).pin_memory(), torch.tensor(g.train_mask[gid]).pin_memory())
         host.append(h)
-        ctx.set_inputs(i, *(a.cuda() for a in h))
+        ctx.set_inputs(i, torch.tensor(g.X[gid]).cuda(), h[1].cuda(), h[2].cuda())
     theta = torch.tensor(P.flatten_params(params0)).cuda()
     grads = torch.zeros_like(theta)
     loss = torch.zeros(1, device="cuda")
@@ -248,3 +250,66 @@ def test_stage_inputs_overlapped_reupload(P, p):
     torch.cuda.synchronize()
     assert [float(x.item()) for x in losses] == [r["loss"] for r in ref]
     assert np.array_equal(theta.cpu().numpy(), ref[-1]["params"])
+
+
+@pytest.mark.parametrize("model", ["sage", "gcn"])
+def test_caller_buffer_layer_calls(P, model):
+    """pgcn_layer_fwd_io / pgcn_layer_bwd_io (SURVEY 8(b) signatures): an iteration composed from the
+    caller-buffer layer calls -- weights as separate W, b buffers, every H^(l) copied out and fed back
+    in as the next layer's h_in, J^(l) fed back as j_out, dW/db and J^(l-1) copied out -- is bit-identical
+    to pgcn_step, and its outputs equal the context's own tensors."""
+    import torch
+    g = gen_graph("yelp", seed=2, n=3001, nnz=40000, f0=103, classes=13)
+    widths = [103, 70, 45, 13]
+    L = 3
+    params0 = glorot_params(widths, 5, model=model)
+    kw = dict(mode="pipe", smooth_g=True, dropout=0.3, loss="bce", opt="sgd", lr=2.0, transport="loopback", model=model)
+    T = 3
+    ref, _ = run_ctx(P, g, widths, 3, T, params0, **kw)
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 3)
+    cfg = P.make_config(widths, n_global=g.n, n_train_global=g.n_train, dump_j=True, **kw)
+    ctx = P.Context(part, cfg)
+    n_in = []
+    for i in range(3):
+        gid = part.view(i)["inner_gid"]
+        n_in.append(len(gid))
+        ctx.set_inputs(i, torch.tensor(g.X[gid]).cuda(), torch.tensor(g.labels[gid]).cuda(),
+                       torch.tensor(g.train_mask[gid]).cuda())
+    theta = torch.tensor(P.flatten_params(params0)).cuda()
+    grads = torch.zeros_like(theta)
+    loss = torch.zeros(1, device="cuda")
+    ns = 2 if model == "sage" else 1
+    for t in range(1, T + 1):
+        lay = P.unflatten_params(theta, widths, model)
+        Ws = [W.contiguous().clone() for W, _ in lay]
+        bs = [b.contiguous().clone() for _, b in lay]
+        H = {}
+        for l in range(1, L + 1):
+            h_in = None if l == 1 else H[l - 1]
+            H[l] = [torch.full((n, widths[l]), float("nan"), device="cuda") for n in n_in]
+            ctx.layer_fwd_io(t, l, Ws[l - 1], bs[l - 1], h_in=h_in, h_out=H[l])
+        ctx.loss(t, loss)
+        Jnext = None
+        dWs = {}
+        for l in range(L, 0, -1):
+            dW = torch.empty((ns * widths[l - 1], widths[l]), device="cuda")
+            db = torch.empty(widths[l], device="cuda")
+            j_in = [torch.empty((n, widths[l - 1]), device="cuda") for n in n_in] if l >= 2 else None
+            ctx.layer_bwd_io(t, l, Ws[l - 1], bs[l - 1], j_out=Jnext, dW_local=dW, db_local=db, j_in=j_in)
+            dWs[l] = (dW, db)
+            if l >= 2:
+                torch.cuda.synchronize()
+                for i in range(3):  # the context's own accumulated J^(l-1) (dump_j) equals j_in
+                    assert torch.equal(j_in[i], ctx.tensor(i, P.T_J, l - 1, t)[:, :widths[l - 1]])
+            Jnext = j_in
+        ctx.update(t, theta, grads)
+        torch.cuda.synchronize()
+        r = ref[t - 1]
+        assert float(loss.item()) == r["loss"]
+        assert np.array_equal(theta.cpu().numpy(), r["params"]), t
+        assert np.array_equal(grads.cpu().numpy(), r["G"]), t
+        for l in range(1, L):
+            for i in range(3):
+                assert np.array_equal(H[l][i].cpu().numpy(), r["H"][l][i]), (t, l, i)
+        flatG = torch.cat([torch.cat([dWs[l][0].ravel(), dWs[l][1]]) for l in range(1, L + 1)])
+        assert np.array_equal(flatG.cpu().numpy(), r["G"]), t  # one context: dW_local sums = G

@@ -73,7 +73,7 @@ def kernel_relu_decision(gpu, tol=TOL):  # noqa: D401
     the fp32 arithmetic, so the oracle takes the kernel's decision (H > 0) there and keeps its own
     everywhere else.  The band is measured per (t, layer, partition): 4 x max|H_gpu - Y| over the
     elements both sides find positive (where H_gpu = Y_gpu), capped at the tier tolerance tol*max|Y|.
-    The overridden fraction is asserted by oracle_run (<= 1e-3 at the 1e-4 tier)."""
+    The overridden fraction is asserted by oracle_run (<= 1e-3 at the 1e-4 tier, <= 8e-2 at 2e-2)."""
     stats = {"overridden": 0, "differ": 0, "total": 0, "max_band_rel": 0.0}
 
     def decide(t, l, i, Y):
@@ -109,7 +109,9 @@ def oracle_run(gpu, g, n_parts, params0, cfg, T, tol=TOL, **kw):
     print("R25 hook: %d of %d sigma' decisions in the measured band (%.2e), %d taken from the kernel against "
           "the oracle's own, band <= %.1e max|Y|" % (st["overridden"], st["total"], frac, st["differ"],
                                                     st["max_band_rel"]))
-    assert frac <= (1e-3 if tol <= 1e-4 else 3e-2), st
+    # fp32 tier: the band is a few ulps of the pre-activations -> a tiny fraction; 2e-2 tier: the band can
+    # reach the 2 % cap, and for roughly Gaussian Y (max ~ 4 sigma) P(|Y| < 0.02 max) ~ 6 %
+    assert frac <= (1e-3 if tol <= 1e-4 else 8e-2), st
     return ora
 
 
