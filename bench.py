@@ -52,9 +52,10 @@ def parse():
     ap.add_argument("--tile-min", type=int, default=0, help="heavy-tile threshold in edges per 128x64 tile (0: library default)")
     ap.add_argument("--no-train-sparse", action="store_true",
                     help="compute the last layer on every row (default: only on train rows, SURVEY N1(ii); exact)")
-    ap.add_argument("--transport", default="loopback", choices=["loopback", "local"],
+    ap.add_argument("--transport", default="loopback", choices=["loopback", "local", "push"],
                     help="single-GPU runs: 'loopback' = the posted exchange of the NCCL path (pack -> comm stream "
-                         "-> one device copy per peer segment -> events; App. F) or 'local' = direct gathers")
+                         "-> one device copy per peer segment -> events; App. F), 'local' = direct gathers, "
+                         "'push' = producers store the exchanged rows into the receivers from their epilogues (N2)")
     ap.add_argument("--halo-payload", default="f32", choices=["f32", "bf16"],
                     help="bf16: exchange payloads rounded to bf16 (SURVEY N1(iv), 2e-2 tier)")
     ap.add_argument("--depth", type=int, default=1, help="pipeline depth s (R27)")
@@ -324,7 +325,7 @@ def main():
                            n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
                            train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles,
                            tile_min=args.tile_min, depth=args.depth,
-                           transport="loopback" if transport == "loopback" else "local",
+                           transport=transport if transport in ("loopback", "push") else "local",
                            halo_payload=args.halo_payload)
     stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]

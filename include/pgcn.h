@@ -190,6 +190,16 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                                     consumer waits for the event of the iteration it consumes.  Same
  *                                     buffers, rotation, events and waits as NCCL; the transfer is a
  *                                     device copy instead of ncclSend/ncclRecv.
+ *                       2 PUSH     -- SURVEY N2, fusion with the exchange: the kernel that produces rows a
+ *                                     peer consumes stores them straight into the peer's receive rows
+ *                                     from its epilogue (forward: the node-update GEMM's epilogue stores
+ *                                     each S_{i,j} row into j's boundary rows of the slot read at t + s;
+ *                                     backward: the transposed SpMM / input-gradient GEMM epilogue stores
+ *                                     each boundary row of J^(l-1) into its owner's message rows).  No
+ *                                     pack kernel, no copy; same slots and rotation as LOOPBACK, ordered
+ *                                     by the compute stream.  Layers whose output comes from the SpMM
+ *                                     (GCN-sym transform-first) or a SIMT GEMM keep LOOPBACK's pack +
+ *                                     copy; layer 1's X exchange (once, R10) too.  fp32 payloads only.
  *   halo_payload        posted transports (LOOPBACK, NCCL): 0 fp32 exchange payloads; 1 bf16 payloads
  *                       (SURVEY N1(iv), 2e-2 tier): the packed boundary features and the boundary-row
  *                       gradients are rounded to bf16 (round to nearest even) for the transfer and

@@ -87,9 +87,12 @@ struct PartCtx {
   void* recv_f[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // staged boundary rows (EMA-F or bf16)     [n_bd x ld]
   void* send_b[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // bf16 boundary-row gradients (bf16 only)  [n_bd x ld]
   void* recv_b[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};  // received gradient rows, send order       [n_send x ld]
+  // N2 fused push (PUSH transport): destination (peer, receive row) of every send position k and of
+  // every boundary row r
+  int32_t *fpush_part = nullptr, *fpush_row = nullptr, *bpush_part = nullptr, *bpush_row = nullptr;
 };
 
-enum { XP_LOCAL = 0, XP_LOOPBACK = 1, XP_NCCL = 2 };
+enum { XP_LOCAL = 0, XP_LOOPBACK = 1, XP_NCCL = 2, XP_PUSH = 3 };
 
 struct Arena {
   char* base = nullptr;
@@ -168,6 +171,8 @@ struct pgcn_ctx {
   int64_t hook_spin_ns = 0; // pgcn_dev_exchange_hook: delay injected on the comm stream before each transfer
   int32_t hook_flags = 0;   // PGCN_XH_* (pgcn_dev.h)
   int64_t xbytes[2] = {0, 0};  // payload bytes posted by this context's transfers (fwd, bwd)
+  // PUSH: iteration in which layer l's input boundary rows / J^(l-1) messages were pushed by their producer
+  int64_t fpushed[PGCN_MAX_LAYERS + 2] = {}, bpushed[PGCN_MAX_LAYERS + 2] = {};
   // ---- streaming inputs (pgcn_stage_inputs): copy stream and its events
   cudaStream_t cps = nullptr;
   cudaEvent_t ev_x_free = nullptr, ev_lab_free = nullptr, ev_in_ready = nullptr;
@@ -227,7 +232,8 @@ int validate_cfg(const pgcn_config* c) {
   if (c->train_sparse != 0 && c->train_sparse != 1) return fail(PGCN_EINVAL, "train_sparse must be 0 or 1");
   if (c->spmm_tiles != 0 && c->spmm_tiles != 1) return fail(PGCN_EINVAL, "spmm_tiles must be 0 or 1");
   if (c->tile_min < 0 || c->tile_min > 128 * 64) return fail(PGCN_EINVAL, "tile_min out of range");
-  if (c->transport != 0 && c->transport != 1) return fail(PGCN_EINVAL, "transport must be 0 (LOCAL) or 1 (LOOPBACK)");
+  if (c->transport < 0 || c->transport > 2)
+    return fail(PGCN_EINVAL, "transport must be 0 (LOCAL), 1 (LOOPBACK) or 2 (PUSH)");
   if (c->halo_payload != 0 && c->halo_payload != 1) return fail(PGCN_EINVAL, "halo_payload must be 0 (fp32) or 1 (bf16)");
   return PGCN_OK;
 }
@@ -273,6 +279,12 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.inv_pos = A.take<int32_t>(p.n_send);
     p.halo_map = A.take<int32_t>(p.n_bd);
     p.msg_map = A.take<int32_t>(p.n_send);
+    if (C->xp == XP_PUSH) {
+      p.fpush_part = A.take<int32_t>(p.n_send);
+      p.fpush_row = A.take<int32_t>(p.n_send);
+      p.bpush_part = A.take<int32_t>(p.n_bd);
+      p.bpush_row = A.take<int32_t>(p.n_bd);
+    }
     p.X = A.take<float>(p.n_all * C->ld[0]);
     for (int l = 1; l < L; ++l)
       for (int b = 0; b < C->nb; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
@@ -424,12 +436,13 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
       return fail(PGCN_EUNSUPPORTED, "a single-process context hosts all %d partitions (got %d)", v0.n_parts, n_local);
     for (int i = 0; i < n_local; ++i)
       if (local[i] != i) return fail(PGCN_EINVAL, "local_parts must be 0..n_parts-1 in order");
-    C->xp = cfg->transport == 1 ? XP_LOOPBACK : XP_LOCAL;
+    C->xp = cfg->transport == 1 ? XP_LOOPBACK : (cfg->transport == 2 ? XP_PUSH : XP_LOCAL);
   }
   C->posted = C->xp != XP_LOCAL;
   C->p16 = cfg->halo_payload == 1;
   if (C->p16 && !C->posted)
     return fail(PGCN_EUNSUPPORTED, "bf16 exchange payloads need a posted transport (LOOPBACK or NCCL)");
+  if (C->p16 && C->xp == XP_PUSH) return fail(PGCN_EUNSUPPORTED, "the PUSH transport moves fp32 payloads");
   if (cfg->n_global != pgcn_partition_n_nodes(part)) return fail(PGCN_EINVAL, "cfg.n_global != partition N");
   C->cfg = *cfg;
   C->L = cfg->n_layers;
@@ -593,7 +606,7 @@ int transfer(pgcn_ctx* C, int64_t t, int l, bool fwd) {
   const int b = C->bi(t);
   if (C->hook_spin_ns > 0) spin_ns(C->cs, C->hook_spin_ns);
   if (C->hook_flags & PGCN_XH_NOCOMM) return PGCN_OK;
-  if (C->xp == XP_LOOPBACK) {
+  if (C->xp == XP_LOOPBACK || C->xp == XP_PUSH) {  // (PUSH: layers whose producer could not push)
     for (auto& pi : C->parts) {
       const int i = pi.part;
       for (auto& pj : C->parts) {
@@ -655,6 +668,36 @@ int transfer(pgcn_ctx* C, int64_t t, int l, bool fwd) {
 
 }  // namespace
 
+// N2 fused push (PUSH transport).  Forward: hosted partition p's layer-l output rows in S_{p,j} go
+// straight from the producing GEMM's epilogue into every receiver j's rows that layer l + 1 reads at
+// t + s (PIPE) / t (VANILLA) -- the same slots the transfer would fill (fwd_dst).  Backward: the
+// boundary rows of J^(l-1) go from the producing kernel into their owners' message rows of slot t.
+// All partitions are hosted by this context and the compute stream orders every producer before its
+// consumer and after the previous reader of the slot (the rotation argument of the posted exchange).
+bool fwd_push(pgcn_ctx* C, PartCtx& p, int64_t t, int l, PushSpec& ps) {
+  if (C->xp != XP_PUSH || l >= C->L || p.n_send == 0) return false;
+  ps = PushSpec{};
+  for (auto& q : C->parts) ps.base[q.part] = static_cast<float*>(fwd_dst(C, q, t, l + 1));
+  ps.ptr = p.inv_ptr;
+  ps.pos = p.inv_pos;
+  ps.part = p.fpush_part;
+  ps.row = p.fpush_row;
+  ps.mode = 1;
+  C->xbytes[0] += 4 * p.n_send * C->ld[l];
+  return true;
+}
+bool bwd_push(pgcn_ctx* C, PartCtx& p, int64_t t, int l, PushSpec& ps) {
+  if (C->xp != XP_PUSH || l < 2 || p.n_bd == 0) return false;
+  ps = PushSpec{};
+  for (auto& q : C->parts) ps.base[q.part] = static_cast<float*>(q.recv_b[l][C->bi(t)]);
+  ps.part = p.bpush_part;
+  ps.row = p.bpush_row;
+  ps.row0 = p.n_in;
+  ps.mode = 2;
+  C->xbytes[1] += 4 * p.n_bd * C->ld[l - 1];
+  return true;
+}
+
 // Alg. 1 l.9-13 for every hosted partition: consume the exchange of t - s (PIPE) and post this
 // iteration's, consumed at t + s (PIPE) or right away (VANILLA).  X is exchanged once (R10).
 // n_valid[i]: rows of partition i's layer input that hold data this iteration.
@@ -690,7 +733,9 @@ int post_fwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, int64_t* n_valid) 
     }
   }
   // post
-  if (l >= 2 || t == 1) {
+  if (l >= 2 && C->fpushed[l] == t) {  // PUSH: the producer of H^(l-1) already stored the rows (N2)
+    cudaEventRecord(C->ev_f_done[l][b], C->s);
+  } else if (l >= 2 || t == 1) {
     for (auto& p : C->parts) {
       if (p.n_send == 0) continue;
       const float* Hin = layer_in(p, l, b);
@@ -740,11 +785,15 @@ int post_bwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, bool* have) {
       Scope sc(C, PGCN_K_GATHER, 6.0 * C->F[l - 1] * p.n_bd);
       pack_rows_bf16(Lk, p.J[l - 1][b] + p.n_in * ldi, nullptr, p.n_bd, ldi, p.send_b[l][b]);
     }
-  cudaEventRecord(C->ev_b_ready[l], C->s);
-  cudaStreamWaitEvent(C->cs, C->ev_b_ready[l], 0);
-  int rc = transfer(C, t, l, false);
-  if (rc) return rc;
-  cudaEventRecord(C->ev_b_done[l][b], C->cs);
+  if (C->bpushed[l] == t) {  // PUSH: the producer of J^(l-1) already stored the boundary rows (N2)
+    cudaEventRecord(C->ev_b_done[l][b], C->s);
+  } else {
+    cudaEventRecord(C->ev_b_ready[l], C->s);
+    cudaStreamWaitEvent(C->cs, C->ev_b_ready[l], 0);
+    int rc = transfer(C, t, l, false);
+    if (rc) return rc;
+    cudaEventRecord(C->ev_b_done[l][b], C->cs);
+  }
   *have = !pipe || t > s;
   if (*have && !(C->hook_flags & PGCN_XH_SKIP_B_WAIT)) cudaStreamWaitEvent(C->s, C->ev_b_done[l][pipe ? C->bi(t - s) : b], 0);
   return PGCN_OK;
@@ -838,6 +887,29 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     cudaMemcpyAsync(p.inv_pos, v.inv_pos, sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.halo_map, hmap.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.msg_map, mmap.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+    std::vector<int32_t> fpp, fpr, bpp, bpr;
+    if (C->xp == XP_PUSH) {  // N2 destinations: send position k of peer j -> j's boundary row; boundary row
+      fpp.resize(p.n_send);  // r of owner j -> j's message row (send order)
+      fpr.resize(p.n_send);
+      bpp.resize(p.n_bd);
+      bpr.resize(p.n_bd);
+      for (int j = 0; j < C->n_parts; ++j) {
+        pgcn_part_view vj;
+        pgcn_partition_view(part, j, &vj);
+        for (int64_t k = v.send_off[j]; k < v.send_off[j + 1]; ++k) {
+          fpp[k] = j;
+          fpr[k] = (int32_t)(vj.halo_off[p.part] + (k - v.send_off[j]));
+        }
+        for (int64_t r = v.halo_off[j]; r < v.halo_off[j + 1]; ++r) {
+          bpp[r] = j;
+          bpr[r] = (int32_t)(vj.send_off[p.part] + (r - v.halo_off[j]));
+        }
+      }
+      cudaMemcpyAsync(p.fpush_part, fpp.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(p.fpush_row, fpr.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(p.bpush_part, bpp.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(p.bpush_row, bpr.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
+    }
     for (int w = 0; w < 2; ++w) {
       const TileSet* ts = p.ts[w];
       if (!ts) continue;
@@ -1095,8 +1167,10 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
                  (int64_t)nz, p.tiles(0), p.T16))) return poison(C, rc);
       }
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + Fo) + 4.0 * (Fi + 1) * Fo, 2.0 * p.n_in * (Fi + 1) * Fo);
+      PushSpec ps;
+      const bool psh = fwd_push(C, p, t, l, ps);
       if (tc_fwd_1seg(Lk, p.Z[l], p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], C->Fp[l], 0, C->F[l], out, ldo,
-                      bias, nullptr, 0, l < C->L, bf))
+                      bias, nullptr, 0, l < C->L, bf, psh ? &ps : nullptr))
         return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
       continue;
     }
@@ -1116,8 +1190,11 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       {
         Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (Fi + 2 * Fo), 2.0 * p.n_in * Fi * Fo);
+        PushSpec ps;
+        const bool psh = fwd_push(C, p, t, l, ps);
         if (tc_fwd_1seg(Lk, D, p.n_in, ldi, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], 2 * C->Fp[l],
-                        (int)(C->Fp[l] / kbk), C->F[l], out, ldo, bias, p.Z[l], ldo, l < C->L, bf))
+                        (int)(C->Fp[l] / kbk), C->F[l], out, ldo, bias, p.Z[l], ldo, l < C->L, bf,
+                        psh ? &ps : nullptr))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM (self) failed (layer %d)", l);
       }
       continue;
@@ -1148,8 +1225,10 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_GEMM_FWD, 4.0 * p.n_in * (2 * Fi + Fo) + 4.0 * (2 * Fi + 1) * Fo,
                2.0 * p.n_in * (2 * Fi + 1) * Fo);
       if (tcg) {
+        PushSpec ps;
+        const bool psh = fwd_push(C, p, t, l, ps);
         if (gemm_fwd_tc(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], bias, C->F[l], out, ldo,
-                        l < C->L, bf))
+                        l < C->L, bf, psh ? &ps : nullptr))
           return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
       } else {
         gemm_fwd_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], Wext, C->F[l], out, ldo, l < C->L);
@@ -1159,6 +1238,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   // X's last reader this iteration: layer 1's dropout (with p = 0 GraphSAGE reads X itself later, in
   // layer 1's weight gradient -- recorded in pgcn_layer_bwd)
   if (l == 1 && (C->cfg.dropout > 0.0 || C->gcn)) cudaEventRecord(C->ev_x_free, C->s);
+  // PUSH: layer l's output rows were stored into the receivers by its GEMM epilogue (GCN-sym transform-
+  // first layers produce H in the SpMM and SIMT GEMMs have no push: those layers keep pack + transfer)
+  if (C->xp == XP_PUSH && l < C->L && !(C->gcn && C->tf[l]) && C->cfg.gemm != 2) C->fpushed[l + 1] = t;
   rc = check_cuda(C, "pgcn_layer_fwd");
   if (rc) return rc;
   advance(C);
@@ -1241,8 +1323,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         }
         if (l >= 2) {
           Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_all * (Fo + Fi), 2.0 * p.n_all * Fo * Fi);
+          PushSpec ps;
+          const bool psh = bwd_push(C, p, t, l, ps);
           if (tc_fwd_mask(Lk, p.T[l], p.n_all, nullptr, 0, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
-                          C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, p.sym))
+                          C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, p.sym, psh ? &ps : nullptr))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
         }
         continue;
@@ -1263,8 +1347,11 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
         Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz + p.n_in, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) +
                                          4.0 * Fi * p.n_all + 12.0 * p.n_all));
+        PushSpec ps;
+        const bool psh = bwd_push(C, p, t, l, ps);
         if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, p.dA, ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l),
-                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16))) return poison(C, rc);
+                 C->work, p.sym, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16, nullptr,
+                 psh ? &ps : nullptr))) return poison(C, rc);
       }
       continue;
     }
@@ -1290,8 +1377,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       if (l >= 2) {
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * (p.n_all + p.n_in) * Fo + 4.0 * p.n_all * Fi,
                  2.0 * (p.n_all + p.n_in) * Fo * Fi);
+        PushSpec ps;
+        const bool psh = bwd_push(C, p, t, l, ps);
         if (tc_fwd_mask(Lk, p.T[l], p.n_all, p.M, p.n_in, ldo, C->F[l], C->WJ_hi[l], C->WJ_lo[l], C->Kq[l],
-                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, nullptr))
+                        C->F[l - 1], p.J[l - 1][b], ldi, p.gid, drop_spec(C, t, l), bf, nullptr, psh ? &ps : nullptr))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core input-gradient GEMM failed (layer %d)", l);
       }
       continue;
@@ -1323,12 +1412,15 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       Scope sc(C, PGCN_K_SPMM_BWD, sb(Fi, p.n_in, nz, cvt(Fi, p.n_in) + 4.0 * nz + 8.0 * (p.n_all + 1) + 4.0 * Fi * p.n_in +
                                        4.0 * Fi * p.n_all + 8.0 * p.n_all));
+      PushSpec ps;
+      const bool psh = bwd_push(C, p, t, l, ps);
       if ((rc = spmm_bwd(Lk, trp, tcol, p.dA, p.dA + ldi, 2 * ldi, p.n_in, p.n_all, p.J[l - 1][b], ldi, p.gid,
                drop_spec(C, t, l), C->work, nullptr, p.G16, (int64_t)nz, sp ? nullptr : p.tiles(1), p.T16,
-               cl ? p.tr_pos : nullptr))) return poison(C, rc);
+               cl ? p.tr_pos : nullptr, psh ? &ps : nullptr))) return poison(C, rc);
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)
+  if (l >= 2 && C->xp == XP_PUSH) C->bpushed[l] = t;  // every producer of J^(l-1) pushed its boundary rows
   if (l >= 2) {
     bool posted_have = false;
     if (C->posted && (rc = post_bwd(C, t, l, Lk, &posted_have))) return rc;

@@ -502,6 +502,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      // N2 fused push: copy this thread's finished row segment [n0, n0 + BN) to the peers that consume it
+      // (re-read from the just-written row, which keeps the push out of the register-bound store loop)
+      if (p.push.mode && (p.epi == EPI_ACT || p.epi == EPI_MASK) && row < p.M) {
+        const int64_t ld4 = p.ld_out / 4;
+        const float4* src = reinterpret_cast<const float4*>(p.out + (int64_t)row * p.ld_out);
+        const int64_t x1 = min((int64_t)(T.n0 + p.BN), p.ld_out) / 4;
+        for (int64_t x = T.n0 / 4; x < x1; ++x) push_f4(p.push, row, ld4, x, src[x]);
+      }
     }
   }
   tc_fence_before();
@@ -847,9 +855,11 @@ static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* 
 int64_t tc_kpad(int64_t K, int bf) { return bf ? (K + 63) / 64 * 64 : (K + 31) / 32 * 32; }
 
 int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const void* WT_hi,
-                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf) {
+                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf,
+                const PushSpec* push) {
   if (M <= 0) return 0;
   TcParams p{};
+  if (push) p.push = *push;
   const int64_t Fp = tc_kpad(F, bf);
   const float* A[2] = {Z, D};
   const int64_t rows[2] = {M, M};
@@ -864,9 +874,10 @@ int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M
 
 int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const void* WT_hi, const void* WT_lo,
                 int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
-                const float* addend, int64_t ld_add, int relu, int bf) {
+                const float* addend, int64_t ld_add, int relu, int bf, const PushSpec* push) {
   if (M <= 0) return 0;
   TcParams p{};
+  if (push) p.push = *push;
   const float* As[1] = {A};
   const int64_t rows[1] = {M};
   const int off[1] = {kb_off};
@@ -882,9 +893,10 @@ int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, con
 
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
                 const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d, int bf, const float* rscale) {
+                const int64_t* gid, const DropSpec& d, int bf, const float* rscale, const PushSpec* push) {
   if (M <= 0) return 0;
   TcParams p{};
+  if (push) p.push = *push;
   const float* A[2] = {Q, Mg};
   const int64_t rows[2] = {M, M_inner};
   const int off[2] = {0, (int)(Kq / (bf ? 64 : 32))};

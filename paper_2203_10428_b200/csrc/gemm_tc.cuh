@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "push.cuh"
+
 namespace pgcn {
 
 enum { TC_FWD = 0, TC_DA = 1, TC_DW = 2 };
@@ -29,6 +31,7 @@ struct alignas(64) TcParams {
   float scale;
   int width, mask_on;
   const float* rscale;  // EPI_MASK: optional per-row scale (GCN-sym d~^-1/2)
+  PushSpec push;        // EPI_ACT / EPI_MASK: N2 fused push of the rows peers consume (mode 0: off)
   int bf;  // 1: bf16 operands (kind::f16), 0: 3xTF32 (kind::tf32)
 };
 
@@ -56,7 +59,8 @@ int64_t tc_kpad(int64_t K, int bf);
 // Node-update GEMMs; bf = 0: 3xTF32 (B operand copies are tf32 hi/lo fp32 arrays), bf = 1: bf16
 // (B operand copy is bf16, *_lo unused).  Return 0 on success, < 0 on mapping / launch failure.
 int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const void* WT_hi,
-                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf);
+                const void* WT_lo, const float* bias, int64_t N, float* Y, int64_t ldY, int relu, int bf,
+                const PushSpec* push = nullptr);
 // dA = Mg W^T; halves = 2: [dZ' | dD] (GraphSAGE, first half scaled by inv_deg, row stride 2 ld),
 // halves = 1: inv_deg o (Mg W^T) (GCN-sym, row stride ld).
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
@@ -68,13 +72,13 @@ int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M,
 //   (kb_off = Fp / k-block) read from the WT operand copy (ldB = 2Fp columns).
 int tc_fwd_1seg(Launch L, const float* A, int64_t M, int64_t ldA, int64_t K, const void* WT_hi, const void* WT_lo,
                 int64_t ldB, int kb_off, int64_t N, float* out, int64_t ld_out, const float* bias,
-                const float* addend, int64_t ld_add, int relu, int bf);
+                const float* addend, int64_t ld_add, int relu, int bf, const PushSpec* push = nullptr);
 //   J[M x F] = mask o s o rscale o ([Q | Mg] [W_neigh | W_self]^T), Q rows M, Mg rows M_inner (rows
 //   beyond are zero), B = WJ [F x 2Kq]; mask / gid / key per DropSpec (R5).  GCN-sym: Mg = nullptr,
 //   J = mask o s o rscale o (Q W^T) with B = WJ [F x Kq]; rscale (per row) may be null.
 int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_inner, int64_t ld, int64_t K,
                 const void* WJ_hi, const void* WJ_lo, int64_t Kq, int64_t F, float* J, int64_t ldJ,
-                const int64_t* gid, const DropSpec& d, int bf, const float* rscale);
+                const int64_t* gid, const DropSpec& d, int bf, const float* rscale, const PushSpec* push = nullptr);
 //   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts;
 //   A1 == nullptr: G[(F+1) x N] = [A0^T B0 ; colsum(Mb)] (GCN-sym).
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,

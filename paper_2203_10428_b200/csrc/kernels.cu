@@ -174,7 +174,7 @@ __global__ void k_dropout(const float4* __restrict__ H, float4* __restrict__ D, 
 // Work item = (row, chunk): a group of G lanes owns NC*G float4 columns of one output row (for
 // every width used here one chunk covers the whole row) and keeps NC float4 accumulators; U
 // neighbour rows are in flight per step, so each lane has NC*U 16-byte loads outstanding.  The
-// (G, NC, U) table in spmm_shape() was measured with tools/spmm_lab.py on B200 (whole row per
+// (G, NC, U) table in spmm_shape() was measured with tools/ab_r1/spmm_lab.py on B200 (whole row per
 // group, ~8 loads in flight).  Neighbour ids are loaded G at a time (coalesced)
 // and broadcast with shuffles.  Sums run in CSR order, then the row is scaled by inv_deg (R16).
 // Work distribution: static grid-stride, or (work != nullptr) dynamic -- each group takes the
@@ -289,7 +289,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              int64_t n_all, int nchunk, float4* __restrict__ J,
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
                                                              unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                             int addend, const int32_t* __restrict__ dmap) {
+                                                             int addend, const int32_t* __restrict__ dmap,
+                                                             const __grid_constant__ PushSpec ps) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
       if (x >= ld4) continue;
       const float4 o = drop4(rs ? f4scale(acc[q], sr) : acc[q], x, kr, 1.f, d);  // mask of R5, J's own row
       __stcs(J + u0 * ld4 + x, o);
+      if (ps.mode) push_f4(ps, u0, ld4, x, o);  // N2: boundary-row gradient straight into its owner's message rows
     }
   }
 }
@@ -521,7 +523,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
                                                                float4* __restrict__ J, int64_t ld4,
                                                                const int64_t* __restrict__ gid, DropSpec d,
                                                                unsigned long long* work, int grabk, const float* __restrict__ rs,
-                                                               int addend, const int32_t* __restrict__ dmap) {
+                                                               int addend, const int32_t* __restrict__ dmap,
+                                                               const __grid_constant__ PushSpec ps) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
@@ -584,7 +587,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
         if (xf >= ld4) continue;
         float4 o = make_float4(acc[q][4 * h], acc[q][4 * h + 1], acc[q][4 * h + 2], acc[q][4 * h + 3]);
         if (rs) o = f4scale(o, sr);
-        __stcs(J + u0 * ld4 + xf, drop4(o, xf, kr, 1.f, d));
+        o = drop4(o, xf, kr, 1.f, d);
+        __stcs(J + u0 * ld4 + xf, o);
+        if (ps.mode) push_f4(ps, u0, ld4, xf, o);
       }
     }
   }
@@ -1089,7 +1094,7 @@ __global__ void k_opt(const float* __restrict__ grads, int64_t P, float* __restr
 
 // ---------------------------------------------------------------- SpMM dispatch
 // (G, NC, U, min blocks/SM) per row width, measured in the full Reddit-shaped step on B200
-// (tools/spmm_sweep.sh; tools/spmm_lab.py for the isolated kernel): rows of <= 32 float4 use one
+// (tools/ab_r1/spmm_sweep.sh; tools/ab_r1/spmm_lab.py for the isolated kernel): rows of <= 32 float4 use one
 // lane per float4 (G = next pow2, NC = 1, U = 8); wider rows use 32 lanes and NC = ceil(ld4/32)
 // float4 per lane, U ~ 8/NC rows in flight (whole row per warp); register caps chosen for 3-4
 // resident blocks (NC = 5: 3 blocks beat 2 by 15%; NC = 2: 4 blocks).
@@ -1152,7 +1157,7 @@ SpmmShape spmm_shape(int64_t ld4) {
     if (c >= nc) { pick = c; break; }
   s.NC = pick;
   // 256-wide rows (pick 2): 8 neighbours in flight x 2 float4 per lane, 2 blocks/SM (in-situ sweep
-  // after the 32-bit-addressing rewrite, tools/spmm_sweep5.sh: Reddit step 49.0 -> 46.5 ms).
+  // after the 32-bit-addressing rewrite, tools/ab_r1/spmm_sweep5.sh: Reddit step 49.0 -> 46.5 ms).
   s.U = pick == 2 ? 8 : (pick <= 4 ? 2 : 1);
   s.MB = pick == 2 ? 2 : (pick <= 6 ? 3 : (pick <= 8 ? 2 : 1));
   s.nchunk = (int)((ld4 + 32 * pick - 1) / (32 * pick));
@@ -1299,7 +1304,9 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
 int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const float* dZs, const float* dDs,
               int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld, const int64_t* gid,
               const DropSpec& d, unsigned long long* work, const float* rs, void* g16, int64_t nnz,
-              const TileDev* tiles, void* t16, const int32_t* dmap) {
+              const TileDev* tiles, void* t16, const int32_t* dmap, const PushSpec* push) {
+  PushSpec ps{};
+  if (push) ps = *push;
   if (n_all <= 0) return 0;
   const int tcu = tiles && tiles->n_tiles > 0 && tiles->n_rows == n_all;  // see spmm_fwd
   if (tcu) {
@@ -1331,7 +1338,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd16<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, G16, ld8, b, lda4, n_in, n_all,  \
-                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                     \
+                                                              sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap, ps);                                     \
   } else
       PGCN_SPMM16_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no bf16 spmm_bwd shape for ld8=%lld", (long long)ld8); }
 #undef X
@@ -1341,7 +1348,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
-                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap);                                       \
+                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap, ps);                                       \
   } else
       PGCN_SPMM_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no spmm_bwd shape for ld4=%lld", (long long)ld4); }
 #undef X

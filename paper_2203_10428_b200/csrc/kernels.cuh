@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "pgcn.h"
+#include "push.cuh"
 
 namespace pgcn {
 
@@ -78,7 +79,7 @@ int spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float
               const float* dDs, int64_t ld_dA, int64_t n_in, int64_t n_all, float* J, int64_t ld,
               const int64_t* gid, const DropSpec& d, unsigned long long* work, const float* rs = nullptr,
               void* g16 = nullptr, int64_t nnz = -1, const TileDev* tiles = nullptr, void* t16 = nullptr,
-              const int32_t* dmap = nullptr);
+              const int32_t* dmap = nullptr, const PushSpec* push = nullptr);
 // Both SpMMs return 0, or a PGCN_E* code (message set) when a launch cannot be made.
 // tiles (both SpMMs, optional): dense-tile decomposition of the pattern (tiles.h); its heavy tiles are
 // summed by spmm_tc into the output rows first and the gather kernel walks only the light CSR, adding

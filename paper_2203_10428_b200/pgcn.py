@@ -234,7 +234,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.train_sparse = int(bool(train_sparse))
     c.spmm_tiles = int(bool(spmm_tiles))
     c.tile_min = int(tile_min)
-    c.transport = {"local": 0, "loopback": 1}[transport]
+    c.transport = {"local": 0, "loopback": 1, "push": 2}[transport]
     c.halo_payload = {"f32": 0, "bf16": 1}[halo_payload]
     return c
 

@@ -107,6 +107,9 @@ def test_loopback_parity_and_bit_identity(P, mode, sf, sg, ema_init, depth):
     a, _ = run_ctx(P, g, widths, 3, T, params0, transport="loopback", **kw)
     b, _ = run_ctx(P, g, widths, 3, T, params0, transport="local", **kw)
     assert identical(a, b), "loopback and local transports must agree bit for bit"
+    c, ctxp = run_ctx(P, g, widths, 3, T, params0, transport="push", **kw)
+    assert identical(c, b), "the fused push (N2) must agree bit for bit with the local transport"
+    assert ctxp.exchange_bytes() == ctx.exchange_bytes()
 
 
 @pytest.mark.parametrize("model", ["sage", "gcn"])
@@ -126,6 +129,8 @@ def test_loopback_gcn_and_tiles(P, model):
     a, _ = run_ctx(P, g, widths, 2, T, params0, transport="loopback", **kw)
     b, _ = run_ctx(P, g, widths, 2, T, params0, transport="local", **kw)
     assert identical(a, b)
+    c, _ = run_ctx(P, g, widths, 2, T, params0, transport="push", **kw)  # GCN-sym tf layers: pack + copy
+    assert identical(c, b)
 
 
 DELAY_NS = 3_000_000  # 3 ms before every transfer: the comm stream falls far behind the compute

@@ -12,7 +12,9 @@ from synth.graphs import gen_graph, glorot_params  # noqa: E402
 
 RUNS = [dict(mode="pipe", smooth_f=True, smooth_g=True, depth=1), dict(mode="pipe", smooth_f=True, smooth_g=True, depth=2),
         dict(mode="vanilla"), dict(mode="pipe", smooth_g=True, halo_payload="bf16"),
-        dict(mode="vanilla", halo_payload="bf16"), dict(mode="pipe", spmm_tiles=True, tile_min=8, hook=1)]
+        dict(mode="vanilla", halo_payload="bf16"), dict(mode="pipe", spmm_tiles=True, tile_min=8, hook=1),
+        dict(mode="pipe", smooth_f=True, smooth_g=True, transport="push"), dict(mode="vanilla", transport="push"),
+        dict(mode="pipe", depth=2, model="gcn", transport="push")]
 for kw in RUNS:
     hook = kw.pop("hook", 0)
     dense = "tile_min" in kw
@@ -20,8 +22,8 @@ for kw in RUNS:
         gen_graph("cora", seed=1, n=700, nnz=3000, f0=37, classes=5)
     widths = [g.X.shape[1], 24, 20, 5]
     part = pgcn.partition(g.n, g.row_ptr, g.col_idx, 3)
-    cfg = pgcn.make_config(widths, dropout=0.5, loss="ce", opt="adam", n_global=g.n, n_train_global=g.n_train,
-                           transport="loopback", **kw)
+    kw.setdefault("transport", "loopback")
+    cfg = pgcn.make_config(widths, dropout=0.5, loss="ce", opt="adam", n_global=g.n, n_train_global=g.n_train, **kw)
     ctx = pgcn.Context(part, cfg)
     if hook:
         ctx.exchange_hook(200000, 0)
@@ -32,7 +34,7 @@ for kw in RUNS:
              torch.tensor(g.train_mask[gid]).pin_memory())
         host.append(h)
         ctx.set_inputs(i, *(a.cuda() for a in h))
-    theta = torch.tensor(pgcn.flatten_params(glorot_params(widths, 3))).cuda()
+    theta = torch.tensor(pgcn.flatten_params(glorot_params(widths, 3, model=kw.get("model", "sage")))).cuda()
     grads = torch.zeros_like(theta)
     opt = torch.zeros(2 * theta.numel(), device="cuda")
     loss = torch.zeros(1, device="cuda")
