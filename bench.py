@@ -327,8 +327,19 @@ def main():
                            tile_min=args.tile_min, depth=args.depth,
                            transport=transport if transport in ("loopback", "push") else "local",
                            halo_payload=args.halo_payload)
-    stream = torch.cuda.Stream()
     local_parts = list(range(parts)) if world == 1 else [rank]
+    transport_note = None
+    if transport in ("loopback", "push"):
+        # the posted exchange's message buffers must fit next to the activations; otherwise the local
+        # transport (no message buffers) hosts the partitions and the line says so
+        need = pgcn.workspace_bytes(part, cfg, local_parts)
+        free = torch.cuda.mem_get_info()[0]
+        if need > free - (2 << 30):
+            cfg.transport = 0
+            transport_note = "%s needs %.1f GB of workspace, %.1f GB free: local transport" % (
+                transport, need / 1e9, free / 1e9)
+            transport = "local"
+    stream = torch.cuda.Stream()
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
     with torch.cuda.stream(stream):
         ctx = pgcn.Context(part, cfg, local_parts=local_parts, comm=comm, stream=stream)
@@ -494,7 +505,8 @@ def main():
                       "global_batch": g.n,
                       "parallelism": ("partition x%d on one GPU (%s transport)" % (parts, transport)) if world == 1 else
                       ("partition x%d, one per GPU: NCCL p2p halo exchange on a comm stream + all-reduce" % world),
-                      "gemm": args.gemm, "gather": args.gather, "depth": args.depth,
+                      "gemm": args.gemm, "gather": args.gather, "depth": args.depth, "transport": transport,
+                      "transport_note": transport_note,
                       "train_sparse_last_layer": not args.no_train_sparse, "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,

@@ -33,7 +33,7 @@ int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const float* inv_d
                   int64_t n_rows, int64_t n_valid, float* Z, void* stream);
 
 /* Random-row gather microbenchmark (roofline denominator for DRAM-served aggregation): reads rows
- * idx[0 .. n_idx) (row_floats floats each, multiple of 4, <= 128) of tab in full, U rows in flight per
+ * idx[0 .. n_idx) (row_floats floats each, multiple of 4) of tab in full, U rows in flight per
  * lane group (variant 0: U = 8, 1: U = 16), and writes checksums to out[] (sm_count x 8 x 256 floats).
  * Bytes moved = n_idx x 4 x row_floats; the caller times it.                                       */
 int pgcn_dev_gather_read(const float* tab, int64_t row_floats, const int32_t* idx, int64_t n_idx, float* out,

@@ -252,6 +252,12 @@ bool staged_recv(const pgcn_ctx* C, int l) {
   return C->p16 || (C->cfg.smooth_f && C->cfg.mode == 1 && l >= 2);
 }
 
+// PUSH: whether layer l's output (layer l + 1's input) is stored into the receivers by its producer --
+// the node-update GEMM's epilogue; not GCN-sym transform-first layers (the SpMM produces H) or SIMT GEMMs.
+bool fwd_push_capable(const pgcn_ctx* C, int l) {
+  return C->xp == XP_PUSH && l < C->L && !(C->gcn && C->tf[l]) && C->cfg.gemm != 2;
+}
+
 // Lays out every buffer (dry run when A.base == nullptr).
 int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int32_t n_local, Arena& A) {
   const int L = C->L;
@@ -367,7 +373,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       for (int l = 1; l <= L; ++l)
         for (int b = 0; b < (l == 1 ? 1 : C->nb); ++b) {
           const int64_t ld = C->ld[l - 1];
-          p.send_f[l][b] = A.take<char>(eb * p.n_send * ld);
+          if (l == 1 || !fwd_push_capable(C, l - 1)) p.send_f[l][b] = A.take<char>(eb * p.n_send * ld);
           if (staged_recv(C, l)) p.recv_f[l][b] = A.take<char>(eb * p.n_bd * ld);
           if (l >= 2) {
             if (C->p16) p.send_b[l][b] = A.take<char>(eb * p.n_bd * ld);
@@ -1240,7 +1246,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   if (l == 1 && (C->cfg.dropout > 0.0 || C->gcn)) cudaEventRecord(C->ev_x_free, C->s);
   // PUSH: layer l's output rows were stored into the receivers by its GEMM epilogue (GCN-sym transform-
   // first layers produce H in the SpMM and SIMT GEMMs have no push: those layers keep pack + transfer)
-  if (C->xp == XP_PUSH && l < C->L && !(C->gcn && C->tf[l]) && C->cfg.gemm != 2) C->fpushed[l + 1] = t;
+  if (fwd_push_capable(C, l)) C->fpushed[l + 1] = t;
   rc = check_cuda(C, "pgcn_layer_fwd");
   if (rc) return rc;
   advance(C);

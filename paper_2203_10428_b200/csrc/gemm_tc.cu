@@ -777,11 +777,13 @@ static int dw_bn(int64_t N, int bf) {
 constexpr int kDwMaxWaves = 3;
 constexpr int kColsumSub = 16;  // max row chunks per split of the bias-row column sums
 static int dw_base(int64_t F, int64_t N) { return (int)(((F + 127) / 128) * ((N + dw_bn(N, 0) - 1) / dw_bn(N, 0))); }
-// Longest accumulation chain of one dW tile, in k-blocks of 32 rows (dev knob PGCN_DW_KMAX; 0 = none).
-// The tensor core's fp32 accumulation does not round to nearest, so its error grows with the chain
-// length instead of averaging out: a 13.9M-row dW in ~1000-k-block chains measured 1.3e-3 relative
-// error against fp64; splitting longer reductions into more tiles (summed in fp32 round-to-nearest by
-// the fixed-order second pass) keeps every chain short.
+// Longest accumulation chain of one dW tile, in k-blocks of 32 rows (dev knob PGCN_DW_KMAX; 0 = none;
+// default 128).  The tensor core's fp32 accumulation does not round to nearest, so its error grows with
+// the chain length instead of averaging out.  Measured on B200 against fp64 (tools/r2/dw_chain.py,
+// 13.9M x 48 x 48, 3xTF32): chains of 2935 / 1024 / 256 / 64 k-blocks -> 1.2e-3 / 2.0e-4 / 6.2e-5 /
+// 1.5e-5 relative error, at 4.84 / 5.04 / 5.09 / 6.08 ms; Reddit's 116K-row dW is unaffected (2.2e-5).
+// Splitting long reductions into more tiles (summed in fp32 round-to-nearest by the fixed-order second
+// pass) keeps every chain short.
 static int64_t dw_kmax() { return knobs().dw_kmax; }
 static int64_t zmin_for(int64_t kb) {
   const int64_t km = dw_kmax();

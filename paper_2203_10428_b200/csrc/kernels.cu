@@ -1567,14 +1567,16 @@ __global__ void __launch_bounds__(256) k_gather_read(const float4* __restrict__ 
   const int64_t n_grp = (int64_t)gridDim.x * blockDim.x / G;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t k0 = grp * U; k0 < n_idx; k0 += n_grp * U) {
-    float4 v[U];
+    for (int64_t x = lane; x < row4 || x == lane; x += G) {  // rows wider than G float4: several passes
+      float4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + u;
-      v[u] = (k < n_idx && lane < row4) ? __ldg(tab + (int64_t)__ldg(idx + k) * row4 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u;
+        v[u] = (k < n_idx && x < row4) ? __ldg(tab + (int64_t)__ldg(idx + k) * row4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc = f4add(acc, v[u]);
   }
   out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc.x + acc.y + acc.z + acc.w;
 }
@@ -1626,7 +1628,7 @@ extern "C" int pgcn_dev_spmm(const int64_t* row_ptr, const int32_t* col, const f
 
 extern "C" int pgcn_dev_gather_read(const float* tab, int64_t row_floats, const int32_t* idx, int64_t n_idx,
                                     float* out, int32_t variant, void* stream) {
-  if (!tab || !idx || !out || row_floats % 4 || row_floats <= 0 || row_floats > 4 * 32 || n_idx < 0) return -1;
+  if (!tab || !idx || !out || row_floats % 4 || row_floats <= 0 || n_idx < 0) return -1;
   const int64_t row4 = row_floats / 4;
   const int blocks = pgcn::sm_count() * 8;  // out holds blocks * 256 floats
   auto s = static_cast<cudaStream_t>(stream);

@@ -239,6 +239,14 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     return c
 
 
+def workspace_bytes(part: "Partitioning", cfg: Config, local_parts: Optional[Sequence[int]] = None) -> int:
+    """pgcn_workspace_bytes: device bytes a context hosting `local_parts` (default: all) needs."""
+    loc = np.ascontiguousarray(list(range(part.n_parts)) if local_parts is None else local_parts, dtype=np.int32)
+    nb = C.c_size_t()
+    _check(lib().pgcn_workspace_bytes(part.handle, _ptr(loc), len(loc), C.byref(cfg), C.byref(nb)))
+    return int(nb.value)
+
+
 def param_count(cfg: Config) -> int:
     return int(lib().pgcn_param_count(C.byref(cfg)))
 

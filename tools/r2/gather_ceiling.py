@@ -24,7 +24,8 @@ for F in (48, 128, 256):
     best = {}
     for variant in (0, 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        L.pgcn_dev_gather_read(tab.data_ptr(), F, idx.data_ptr(), n_idx, out.data_ptr(), variant, st.cuda_stream)
+        rc = L.pgcn_dev_gather_read(tab.data_ptr(), F, idx.data_ptr(), n_idx, out.data_ptr(), variant, st.cuda_stream)
+        assert rc == 0, rc
         e0.record()
         for _ in range(3):
             L.pgcn_dev_gather_read(tab.data_ptr(), F, idx.data_ptr(), n_idx, out.data_ptr(), variant, st.cuda_stream)
