@@ -253,13 +253,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
 #pragma unroll
           for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
-      for (; j < cnt; ++j) {
-        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
-        if (!CHK || c < nv) {
+      if (j < cnt) {  // remainder (< U edges): one predicated batch, every load in flight at once
+        float4 v[U][NC];
+        bool ok[U];
 #pragma unroll
-          for (int q = 0; q < NC; ++q)
-            f4acc(acc[q], __ldg(nbr(bq[q], c, row_bytes)));
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u < cnt ? j + u : j, G);
+          ok[u] = j + u < cnt && (!CHK || c < nv);
+#pragma unroll
+          for (int q = 0; q < NC; ++q) v[u][q] = ok[u] ? __ldg(nbr(bq[q], c, row_bytes)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u])
+#pragma unroll
+            for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
     }
     const float s = inv_deg[row];
@@ -336,11 +344,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
 #pragma unroll
           for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
-      for (; j < cnt; ++j) {
-        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
+      if (j < cnt) {  // remainder (< U edges): one predicated batch, every load in flight at once
+        float4 v[U][NC];
 #pragma unroll
-        for (int q = 0; q < NC; ++q)
-          f4acc(acc[q], __ldg(nbr(bq[q], c, row_bytes)));
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u < cnt ? j + u : j, G);
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = j + u < cnt ? __ldg(nbr(bq[q], c, row_bytes)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < cnt)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) f4acc(acc[q], v[u][q]);
       }
     }
     const uint64_t kr = row_key(d, gid[u0]);
@@ -480,12 +497,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
 #pragma unroll
           for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
       }
-      for (; j < cnt; ++j) {
-        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
-        if (!CHK || c < nv) {
+      if (j < cnt) {  // remainder (< U edges): one predicated batch, every load in flight at once
+        uint4 v[U][NC];
+        bool ok[U];
 #pragma unroll
-          for (int q = 0; q < NC; ++q) acc8(acc[q], __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))));
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u < cnt ? j + u : j, G);
+          ok[u] = j + u < cnt && (!CHK || c < nv);
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = ok[u] ? __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))) : make_uint4(0u, 0u, 0u, 0u);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u])
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
       }
     }
     const float s = inv_deg[row];
@@ -569,10 +596,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
 #pragma unroll
           for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
       }
-      for (; j < cnt; ++j) {
-        const uint32_t c = (uint32_t)__shfl_sync(gm, my, j, G);
+      if (j < cnt) {  // remainder (< U edges): one predicated batch, every load in flight at once
+        uint4 v[U][NC];
 #pragma unroll
-        for (int q = 0; q < NC; ++q) acc8(acc[q], __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))));
+        for (int u = 0; u < U; ++u) {
+          const uint32_t c = (uint32_t)__shfl_sync(gm, my, j + u < cnt ? j + u : j, G);
+#pragma unroll
+          for (int q = 0; q < NC; ++q)
+            v[u][q] = j + u < cnt ? __ldg(reinterpret_cast<const uint4*>(nbr(bq[q], c, row_bytes))) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < cnt)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc8(acc[q], v[u][q]);
       }
     }
     const uint64_t kr = row_key(d, gid[u0]);
@@ -1104,7 +1141,7 @@ struct SpmmShape {
 #define PGCN_SPMM_CASES(X)                                                                                     \
   X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
   X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
-  X(32, 4, 2, 3) X(32, 2, 8, 2)
+  X(32, 4, 2, 3) X(32, 2, 8, 2) X(16, 1, 8, 3) X(16, 1, 16, 2) X(16, 1, 16, 3)
 
 static bool dyn_enabled() { return knobs().spmm_dyn != 0; }
 
