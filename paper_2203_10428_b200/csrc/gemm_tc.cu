@@ -124,7 +124,9 @@ __device__ __forceinline__ uint32_t smix_top24(uint64_t z) {
   return (uint32_t)(z >> 40);
 }
 
-template <int BF>
+// PUSH (N2): the epilogue also stores the rows peers consume (p.push) -- a separate instantiation so the
+// push loop's registers do not weigh on the launches without it.
+template <int BF, int PUSH>
 __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant__ TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
                 o = make_float4(e[0], e[1], e[2], e[3]);
               }
               *reinterpret_cast<float4*>(out + n) = o;
+              if constexpr (PUSH) push_f4(p.push, row, p.ld_out / 4, n / 4, o);  // N2: rows peers consume
             }
           }
         } else if (p.epi == EPI_MASK) {  // dropout backward of the layer input (R5)
@@ -469,7 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
                 }
                 e[j] = x;
               }
-              *reinterpret_cast<float4*>(out + n) = make_float4(e[0], e[1], e[2], e[3]);
+              const float4 o = make_float4(e[0], e[1], e[2], e[3]);
+              *reinterpret_cast<float4*>(out + n) = o;
+              if constexpr (PUSH) push_f4(p.push, row, p.ld_out / 4, n / 4, o);  // N2: boundary rows to owners
             }
           }
         } else if (p.epi == EPI_DA) {
@@ -502,14 +507,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-      // N2 fused push: copy this thread's finished row segment [n0, n0 + BN) to the peers that consume it
-      // (re-read from the just-written row, which keeps the push out of the register-bound store loop)
-      if (p.push.mode && (p.epi == EPI_ACT || p.epi == EPI_MASK) && row < p.M) {
-        const int64_t ld4 = p.ld_out / 4;
-        const float4* src = reinterpret_cast<const float4*>(p.out + (int64_t)row * p.ld_out);
-        const int64_t x1 = min((int64_t)(T.n0 + p.BN), p.ld_out) / 4;
-        for (int64_t x = T.n0 / 4; x < x1; ++x) push_f4(p.push, row, ld4, x, src[x]);
-      }
     }
   }
   tc_fence_before();
@@ -715,11 +712,15 @@ int tc_tmem_cols(int BN) {
 static int gemm_ctas() { return knobs().tc_gemm_ctas; }
 
 cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
-  if (smem_attr_once((const void*)tc::k_umma_gemm<0>, 227 * 1024) || smem_attr_once((const void*)tc::k_umma_gemm<1>, 227 * 1024))
+  if (smem_attr_once((const void*)tc::k_umma_gemm<0, 0>, 227 * 1024) ||
+      smem_attr_once((const void*)tc::k_umma_gemm<1, 0>, 227 * 1024) ||
+      smem_attr_once((const void*)tc::k_umma_gemm<0, 1>, 227 * 1024) ||
+      smem_attr_once((const void*)tc::k_umma_gemm<1, 1>, 227 * 1024))
     return cudaErrorInvalidValue;
   TcParams p = p0;
   int ctas = 1;
-  if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW) {  // dW: split-K plan is sized for 148 CTAs
+  // (the PUSH instantiation needs > 85 registers per thread: one CTA of 384 threads per SM)
+  if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW && !p.push.mode) {  // dW: split-K plan sized for 148 CTAs
     const size_t stage = tc::geometry(p.bf, p.mode, p.BN).stage();
     int S = (int)((104 * 1024 - 1024 - 64) / stage);
     if (S >= 2) {
@@ -731,8 +732,14 @@ cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   const int cap = ctas * sms;
   int grid = p.n_tiles < cap ? p.n_tiles : cap;
   if (grid < 1) return cudaSuccess;
-  if (p.bf) tc::k_umma_gemm<1><<<grid, tc::kThreads, smem, s>>>(p);
-  else tc::k_umma_gemm<0><<<grid, tc::kThreads, smem, s>>>(p);
+  const bool push = p.push.mode != 0;
+  if (p.bf) {
+    if (push) tc::k_umma_gemm<1, 1><<<grid, tc::kThreads, smem, s>>>(p);
+    else tc::k_umma_gemm<1, 0><<<grid, tc::kThreads, smem, s>>>(p);
+  } else {
+    if (push) tc::k_umma_gemm<0, 1><<<grid, tc::kThreads, smem, s>>>(p);
+    else tc::k_umma_gemm<0, 0><<<grid, tc::kThreads, smem, s>>>(p);
+  }
   return cudaGetLastError();
 }
 

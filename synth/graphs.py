@@ -85,6 +85,10 @@ CONFIGS = {
     # (13.9M inner rows, ~200M local edges each) and fit one B200.
     "papers-q": dict(n=27764989, nnz=403921468, f0=128, classes=172, comm=128, train=0.011,
                      multilabel=False, feat="gauss", hidden=48, layers=3, dropout=0.0, lr=0.01),
+    # one eighth of papers100M (same degree, widths, train fraction and community size): the shape the ncu
+    # captures use -- papers-q's 170 GB workspace leaves no room for ncu's kernel replay buffers
+    "papers-e": dict(n=13882494, nnz=201960734, f0=128, classes=172, comm=64, train=0.011,
+                     multilabel=False, feat="gauss", hidden=48, layers=3, dropout=0.0, lr=0.01),
 }
 
 
