@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--smooth", default="", help="'', 'f', 'g' or 'gf'")
     ap.add_argument("--gemm", default="tc", choices=["tc", "simt", "bf16"])
     ap.add_argument("--gather", default="f32", choices=["f32", "bf16"],
-                    help="bf16: the bf16 gather tier (SpMM tables rounded to bf16, 2e-2 tier; SURVEY N1(iv))")
+                    help="bf16: the bf16 gather tier (SpMM tables rounded to bf16, 2e-2 tier; beyond SURVEY 8, not N1(iv))")
     ap.add_argument("--model", default="sage", choices=["sage", "gcn"],
                     help="GraphSAGE-mean (the paper's benchmark model) or GCN-sym (App. A.1, SURVEY N3)")
     ap.add_argument("--no-tiles", action="store_true",

@@ -160,7 +160,7 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *   model               0 GraphSAGE-mean (above); 1 GCN-sym (SURVEY N3, App. A.1 PAPER.md:637-647,
  *                       reading R26): Y = P D W + b with P = D~^-1/2 (A + I) D~^-1/2, D~ = d + 1
  *                       (full-graph degrees), W [F_{l-1} x F_l]; tensor-core GEMMs only (gemm 0/1).
- *   gather              0 fp32 aggregation tables (default); 1 bf16 gather tier (SURVEY N1(iv), 2e-2
+ *   gather              0 fp32 aggregation tables (default); 1 bf16 gather tier (2e-2
  *                       tier): every table an SpMM gathers (dropout output / T / dZ') is rounded to
  *                       bf16 first, the SpMMs gather bf16 rows and accumulate in fp32 -- half the
  *                       gathered bytes.  Everything else (H, J, exchange payloads, GEMM outputs)

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
   }
 }
 
-// ---------------------------------------------------------------- bf16 gather tier
+// ---------------------------------------------------------------- bf16 gather tier (pgcn_config.gather = 1)
 // The gathered table is first rounded to bf16 (k_to_bf16: rows of ld8 16-byte vectors = 8 columns,
 // padding columns 0); the SpMMs then gather half the bytes and accumulate in fp32 (exact bf16 ->
 // fp32 widening, FADD2 sums).  2e-2 tier (north_star), selected by pgcn_config.gather = 1.

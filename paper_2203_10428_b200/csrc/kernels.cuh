@@ -86,7 +86,7 @@ int spmm_bwd(Launch, const int64_t* t_row_ptr, const int32_t* t_col, const float
 // the tile sums (fwd: used only when n_valid >= n_cols and rows == nullptr).  t16 (fp32 tier with tiles):
 // scratch for the bf16 hi/lo split of the table, 2 x (table rows) x round_up(ld, 8) bf16.
 // nnz (both SpMMs): edges the launch visits (sizes the dynamic scheduler's grabs); -1 = one row per grab.
-// g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1, SURVEY N1(iv)) -- scratch of at least
+// g16 (both SpMMs): bf16 gather tier (pgcn_config.gather = 1) -- scratch of at least
 // (rows of the gathered table) x round_up(ld, 8) bf16; the table is rounded to bf16 there first and
 // the kernel gathers the bf16 rows (fp32 accumulation, fp32 output).  nullptr = fp32 gathers.
 
