@@ -1141,7 +1141,8 @@ struct SpmmShape {
 #define PGCN_SPMM_CASES(X)                                                                                     \
   X(32, 3, 2, 3) X(32, 8, 1, 2) X(32, 12, 1, 1) X(32, 16, 1, 1) X(32, 1, 8, 3) X(32, 2, 4, 3)             \
   X(32, 1, 8, 4) X(16, 1, 8, 4) X(8, 1, 8, 4) X(4, 1, 8, 4) X(32, 2, 4, 4) X(32, 5, 1, 3) X(32, 6, 1, 3) \
-  X(32, 4, 2, 3) X(32, 2, 8, 2) X(16, 1, 8, 3) X(16, 1, 16, 2) X(16, 1, 16, 3)
+  X(32, 4, 2, 3) X(32, 2, 8, 2) X(16, 1, 8, 3) X(4, 3, 4, 3) X(4, 3, 8, 2) X(4, 3, 2, 4) X(8, 2, 4, 3)          \
+  X(8, 2, 8, 2)
 
 static bool dyn_enabled() { return knobs().spmm_dyn != 0; }
 
