@@ -59,16 +59,21 @@ struct Geo {
   uint32_t a_raw, a_cvt, b_raw, b_cvt;
   __host__ __device__ uint32_t stage() const { return a_raw + a_cvt + b_raw + b_cvt; }
 };
-__host__ __device__ inline Geo geometry(int bf, int mode, int BN) {
+// DW with one f-tile of F <= 96 features stores only afeat (32 / 64 / 96) of the 128 A features per
+// stage: the MMA still reads 128 (its last atoms overlap the next buffer of the stage) but those TMEM
+// lanes are output rows >= F, never stored.  Smaller stages -> more of them in flight (the narrow dW of
+// papers-shaped layers, 48 x 48, is latency-bound on bytes in flight).
+__host__ __device__ inline Geo geometry(int bf, int mode, int BN, int afeat = BM) {
   Geo g;
   if (!bf) {
-    g.a_raw = BM * BK * 4;
-    g.a_cvt = BM * BK * 4;
+    const int af = mode == TC_DW ? afeat : BM;
+    g.a_raw = (uint32_t)af * BK * 4;
+    g.a_cvt = (uint32_t)af * BK * 4;
     g.b_raw = (uint32_t)BN * BK * 4;
     g.b_cvt = (uint32_t)BN * BK * 4;
   } else if (mode == TC_DW) {
-    g.a_raw = BM * 32 * 4;           // 128 features x 32 rows fp32
-    g.a_cvt = BM * 32 * 2;           // bf16 MN-major
+    g.a_raw = (uint32_t)afeat * 32 * 4;                // afeat features x 32 rows fp32
+    g.a_cvt = (uint32_t)((afeat + 63) / 64) * 64 * 32 * 2;  // bf16 MN-major, 64-feature atoms
     g.b_raw = (uint32_t)BN * 32 * 4;
     g.b_cvt = (uint32_t)BN * 32 * 2;
   } else {
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  const Geo geo = geometry(BF, p.mode, p.BN);
+  const Geo geo = geometry(BF, p.mode, p.BN, p.a_feat);
   const uint32_t a_bytes = geo.a_raw;
   const uint32_t b_bytes = geo.b_raw;
   const uint32_t stage_bytes = geo.stage();
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             mbar_expect_tx(&full[s], geo.a_raw + geo.b_raw);
             if (p.mode == TC_DW) {
               const int r0 = kb * 32;
-              for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+              for (int j = 0; j < p.a_feat / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
               for (int j = 0; j < p.BN / 32; ++j)
                 tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
             } else if (p.mode == TC_FWD) {
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
           if (p.mode == TC_DW) {
             const int r0 = kb * BK;
-            for (int j = 0; j < BM / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+            for (int j = 0; j < p.a_feat / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
             for (int j = 0; j < p.BN / 32; ++j)
               tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
           } else if (p.mode == TC_FWD) {
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             for (int part = 0; part < 2; ++part) {
               const uint8_t* raw = part == 0 ? base : base + geo.a_raw + geo.a_cvt;
               uint8_t* cvt = part == 0 ? base + geo.a_raw : base + geo.a_raw + geo.a_cvt + geo.b_raw;
-              const int nf = part == 0 ? BM : p.BN;
+              const int nf = part == 0 ? p.a_feat : p.BN;
               const int nch = nf / 8, items = nch * 32;
               for (int i = ct; i < items; i += kConvThreads) {
                 // chunk index fastest across a warp: its LDS.128s walk along 128-byte rows of the raw box
@@ -680,14 +685,15 @@ bool tc_map_table(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int
   return tc_map(m, base, bf16, cols, rows, ld, box_cols, box_rows, bf16 ? 1 : 2);
 }
 
-int tc_stages(int BN, int bf, int mode) {
-  const int stage = (int)tc::geometry(bf, mode, BN).stage();
+int tc_stages(int BN, int bf, int mode, int afeat) {
+  const int stage = (int)tc::geometry(bf, mode, BN, afeat).stage();
   int S = (200 * 1024) / stage;
-  return S > 4 ? 4 : (S < 2 ? 2 : S);
+  const int cap = mode == TC_DW ? 8 : 4;  // dW: stream of 32-row k-blocks, latency-bound on bytes in flight
+  return S > cap ? cap : (S < 2 ? 2 : S);
 }
 
-size_t tc_smem_bytes(int BN, int S, int bf, int mode) {
-  const size_t stage = tc::geometry(bf, mode, BN).stage();
+size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat) {
+  const size_t stage = tc::geometry(bf, mode, BN, afeat).stage();
   return 1024 + S * stage + (3 * S + 4) * 8 + 16;
 }
 
@@ -721,14 +727,14 @@ cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   int ctas = 1;
   // (the PUSH instantiation needs > 85 registers per thread: one CTA of 384 threads per SM)
   if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW && !p.push.mode) {  // dW: split-K plan sized for 148 CTAs
-    const size_t stage = tc::geometry(p.bf, p.mode, p.BN).stage();
+    const size_t stage = tc::geometry(p.bf, p.mode, p.BN, p.a_feat).stage();
     int S = (int)((104 * 1024 - 1024 - 64) / stage);
     if (S >= 2) {
       p.stages = S < p.stages ? S : p.stages;
       ctas = 2;
     }
   }
-  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode);
+  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode, p.a_feat);
   const int cap = ctas * sms;
   int grid = p.n_tiles < cap ? p.n_tiles : cap;
   if (grid < 1) return cudaSuccess;
@@ -765,7 +771,8 @@ void tc_wprep(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, floa
 static void tc_common(TcParams& p, int BN, int bf, int mode) {
   p.BN = BN;
   p.bf = bf;
-  p.stages = tc_stages(BN, bf, mode);
+  if (!p.a_feat) p.a_feat = tc::BM;
+  p.stages = tc_stages(BN, bf, mode, p.a_feat);
   p.tmem_cols = tc_tmem_cols(BN);
 }
 
@@ -969,6 +976,7 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   }
   TcParams p{};
   const int BN = dw_bn(N, bf);
+  p.a_feat = F <= 96 ? (int)((F + 31) / 32 * 32) : tc::BM;  // one f-tile of F <= 96: store only F features
   tc_common(p, BN, bf, TC_DW);
   int Zseg[2];
   dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg);

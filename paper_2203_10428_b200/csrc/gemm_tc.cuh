@@ -33,14 +33,15 @@ struct alignas(64) TcParams {
   const float* rscale;  // EPI_MASK: optional per-row scale (GCN-sym d~^-1/2)
   PushSpec push;        // EPI_ACT / EPI_MASK: N2 fused push of the rows peers consume (mode 0: off)
   int bf;  // 1: bf16 operands (kind::f16), 0: 3xTF32 (kind::tf32)
+  int a_feat;  // DW: A features stored per stage (32 / 64 / 96 / 128; see geometry()); other modes 128
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
                bool mn_major = false);
 bool tc_map_table(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int64_t rows, int64_t ld, int box_cols,
                   int box_rows);
-int tc_stages(int BN, int bf, int mode);
-size_t tc_smem_bytes(int BN, int S, int bf, int mode);
+int tc_stages(int BN, int bf, int mode, int afeat);
+size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat);
 void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, void* WT, void* Wp, void* WJ,
                    cudaStream_t s);
 int tc_bn(int64_t N);
