@@ -135,6 +135,59 @@ def max_over_ranks(x, dist):
     return float(t.item())
 
 
+def exchange_microbench(dist, view, widths, reps=10):
+    """SURVEY 8(d) all-to-all evidence for N > 1: the halo exchange of this partition at each distinct
+    layer-input width, as the grouped point-to-point send/recv the library posts (every peer j gets the
+    rows S_{rank,j}; this rank receives its boundary segments), fp32 rows padded to ld = round_up(F, 4).
+    Timed with CUDA events (NCCL) or the wall clock (gloo), max over ranks.  busBW = bytes sent per rank
+    / time x (n - 1) / n, the all-to-all convention, against 900 GB/s per direction of NVLink 5."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    nccl = dist.get_backend() == "nccl"
+    dev = "cuda" if nccl else "cpu"
+    out = []
+    for F in sorted(set(widths[:-1])):
+        ld = (F + 3) // 4 * 4
+        sends, recvs = {}, {}
+        for j in range(world):
+            if j == rank:
+                continue
+            ns = int(view["send_off"][j + 1] - view["send_off"][j])
+            nr = int(view["halo_off"][j + 1] - view["halo_off"][j])
+            sends[j] = torch.ones((ns, ld), device=dev)
+            recvs[j] = torch.empty((nr, ld), device=dev)
+
+        def once():
+            ops = [dist.P2POp(dist.isend, sends[j], j) for j in sends] + [dist.P2POp(dist.irecv, recvs[j], j)
+                                                                           for j in recvs]
+            for r in dist.batch_isend_irecv(ops) if ops else []:
+                r.wait()
+        once()
+        if nccl:
+            torch.cuda.synchronize()
+        dist.barrier()
+        if nccl:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                once()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+        else:
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                once()
+            ms = 1000.0 * (time.perf_counter() - t0) / reps
+        ms = max_over_ranks(ms, dist)
+        sent = sum(x.numel() * 4 for x in sends.values())
+        sent_max = max_over_ranks(float(sent), dist)
+        alg = sent_max / (ms / 1e3) / 1e9 if ms > 0 else None
+        out.append({"F": F, "bytes_sent_max_rank": int(sent_max), "ms": ms, "algbw_GBps": alg,
+                    "busbw_GBps": alg * (world - 1) / world if alg else None, "nvlink_GBps_per_dir": 900.0})
+    return out
+
+
 def build_workload(name, n_parts, model="sage"):
     import dataclasses
 
@@ -457,6 +510,9 @@ def main():
                "note": "pgcn_stage_inputs(host pinned X, labels, train mask) every iteration (library copy "
                        "stream, overlapped with the iteration in flight) + pgcn_step + loss read back each step"}
 
+    # (3b) N > 1: the exchange alone at each layer width (grouped send / recv, busBW)
+    comm_bench = exchange_microbench(dist, views[0], m.widths) if dist is not None else None
+
     # (4) exposed communication: the same iterations with the transfers skipped (PGCN_XH_NOCOMM;
     # timing only -- the halo state is stale afterwards).  exposed = T - T_nocomm.
     comm_info = None
@@ -510,7 +566,7 @@ def main():
                       "train_sparse_last_layer": not args.no_train_sparse, "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-           "comm": comm_info, "step_ms": [round(x, 3) for x in step_ms], "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
+           "comm": comm_info, "comm_bench": comm_bench, "step_ms": [round(x, 3) for x in step_ms], "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
            "setup_s": {"generate": t_gen, "partition": t_part},
            "workspace_GB": ctx.ws.numel() / 1e9}
     print(json.dumps(out))

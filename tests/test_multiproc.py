@@ -69,6 +69,10 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(allids, ids)
         ok_id = all(x == allids[0] for x in allids) and any(allids[0])
         mx = bench.max_over_ranks(float(rank + 1) * 10.0, dist)
+        # the bench's exchange microbenchmark (gloo here, NCCL on GPUs): runs, sizes match the views
+        cb = bench.exchange_microbench(dist, v, [4, 6, 3], reps=2)
+        assert [c["F"] for c in cb] == [4, 6]
+        assert all(c["bytes_sent_max_rank"] >= 0 and c["ms"] >= 0 for c in cb)
         q.put((rank, ok_f, ok_b, ok_id, mx, int(v["n_send"]), int(v["n_halo"])))
     finally:
         dist.destroy_process_group()
