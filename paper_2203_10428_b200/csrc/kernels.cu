@@ -4,6 +4,7 @@
 // Step numbers refer to SURVEY.md section 8(a); paper citations are in kernels.cuh / pgcn.h.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -215,9 +216,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
   int64_t cend = 0;
   if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
-    const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
+    // item -> (chunk, row), chunk-major: with several column chunks every row's chunk 0 is gathered
+    // before any chunk 1, so each phase's working set is 1/nchunk of the table (L2-resident when the
+    // launcher picks nchunk for that); rows: optional row list
+    const int64_t ch = nchunk > 1 ? it / n_rows : 0;
+    const int64_t ri = it - ch * n_rows;
     const int64_t row = rows ? (int64_t)rows[ri] : ri;
-    const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
+    const int64_t x0 = ch * (NC * G) + lane;
     // Lanes past the row end gather a clamped in-row column (same sectors as their neighbours,
     // no extra traffic) and never store, so the loop carries no column predicates.
     int xq[NC];
@@ -309,8 +314,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
   int64_t cend = 0;
   if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
-    const int64_t u0 = it / nchunk;
-    const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
+    const int64_t ch = nchunk > 1 ? it / n_all : 0;  // chunk-major, see k_spmm_fwd
+    const int64_t u0 = it - ch * n_all;
+    const int64_t x0 = ch * (NC * G) + lane;
     int xq[NC];
     const char* bq[NC];
 #pragma unroll
@@ -453,9 +459,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd16(const int64_t* __
   int64_t cend = 0;
   if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
-    const int64_t ri = it / nchunk;              // item -> (row, chunk); rows: optional row list
+    // item -> (chunk, row), chunk-major: with several column chunks every row's chunk 0 is gathered
+    // before any chunk 1, so each phase's working set is 1/nchunk of the table (L2-resident when the
+    // launcher picks nchunk for that); rows: optional row list
+    const int64_t ch = nchunk > 1 ? it / n_rows : 0;
+    const int64_t ri = it - ch * n_rows;
     const int64_t row = rows ? (int64_t)rows[ri] : ri;
-    const int64_t x0 = (it - ri * nchunk) * (NC * G) + lane;
+    const int64_t x0 = ch * (NC * G) + lane;
     const char* bq[NC];
     float acc[NC][8];
 #pragma unroll
@@ -561,8 +571,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd16(const int64_t* __
   int64_t cend = 0;
   if (work) first = next_item<G>(work, lane, gm, -1, 0, grabk, cend);
   for (int64_t it = first; it < n_items; it = next_item<G>(work, lane, gm, it, stride, grabk, cend)) {
-    const int64_t u0 = it / nchunk;
-    const int64_t x0 = (it - u0 * nchunk) * (NC * G) + lane;
+    const int64_t ch = nchunk > 1 ? it / n_all : 0;  // chunk-major, see k_spmm_fwd
+    const int64_t u0 = it - ch * n_all;
+    const int64_t x0 = ch * (NC * G) + lane;
     const char* bq[NC];
     float acc[NC][8];
 #pragma unroll
@@ -1227,6 +1238,23 @@ SpmmShape spmm16_shape(int64_t ld8) {
   return s;
 }
 
+// Column chunks for L2 residency: a gathered table larger than the
+// L2 budget (dev knob PGCN_SPMM_L2MB, MB; 0 = off) is processed in nchunk column chunks, chunk-major, so
+// the rows being gathered at any time span table_bytes / nchunk.  The shape is the one for the chunk
+// width; the row's other chunks are separate items.
+SpmmShape chunked(SpmmShape (*shape)(int64_t), int64_t w, double table_bytes) {
+  const double budget = (double)knobs().spmm_l2mb * 1048576.0;
+  if (budget <= 0.0 || table_bytes <= budget) return shape(w);
+  int64_t nch = (int64_t)std::ceil(table_bytes / budget);
+  int64_t cw = (w + nch - 1) / nch;
+  cw = (cw + 3) / 4 * 4;  // chunk width in vectors: a multiple of 4 (whole 64-byte fp32 / bf16 segments)
+  if (cw >= w) return shape(w);
+  SpmmShape sh = shape(cw);
+  sh.nchunk = (int)((w + (int64_t)sh.G * sh.NC - 1) / ((int64_t)sh.G * sh.NC));
+  return sh;
+}
+
+
 }  // namespace
 
 // Items per atomic grab of the dynamic SpMM scheduler: ~128 edges per grab, 1..64 rows (sweep
@@ -1286,7 +1314,7 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
   auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add) -> int {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     if (b16) {
-      const SpmmShape sh = spmm16_shape(ld8);
+      const SpmmShape sh = chunked(spmm16_shape, ld8, (double)n_valid * ld8 * 16);
       const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
@@ -1302,7 +1330,7 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
       PGCN_SPMM16_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no bf16 spmm_fwd shape for ld8=%lld", (long long)ld8); }
 #undef X
     } else {
-      const SpmmShape sh = spmm_shape(ld4);
+      const SpmmShape sh = chunked(spmm_shape, ld4, (double)n_valid * ld4 * 16);
       const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
@@ -1371,7 +1399,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     auto b = reinterpret_cast<const float4*>(dD);
     if (b16) {
-      const SpmmShape sh = spmm16_shape(ld8);
+      const SpmmShape sh = chunked(spmm16_shape, ld8, (double)n_in * ld8 * 16);
       const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
@@ -1381,7 +1409,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
       PGCN_SPMM16_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no bf16 spmm_bwd shape for ld8=%lld", (long long)ld8); }
 #undef X
     } else {
-      const SpmmShape sh = spmm_shape(ld4);
+      const SpmmShape sh = chunked(spmm_shape, ld4, (double)n_in * ld4 * 16);
       const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, sm_count() * 64);
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
