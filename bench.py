@@ -199,7 +199,7 @@ def build_workload(name, n_parts, model="sage"):
     return g, m, params0, time.time() - t0
 
 
-def cpu_baseline(name, parts, mode, smooth, sample_n=4000, iters=2, model="sage"):
+def cpu_baseline(name, parts, mode, smooth, sample_n=16000, iters=2, model="sage"):
     """The oracle (oracle/, numpy/scipy fp64) as it stands, on a bounded sample of the same workload:
     the same generator recipe, degree, widths, dropout and partition count at N = sample_n, timed
     for `iters` PipeGCN iterations; per-epoch time extrapolated linearly in N (every term of the

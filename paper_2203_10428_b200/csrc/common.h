@@ -25,7 +25,7 @@ struct DevKnobs {
   int tc_spmm_bn = 0, tc_spmm_order = 1, tc_spmm_dbg = 0, tc_spmm_nacc1 = 0, tc_spmm_ts = 1, tc_spmm_ctas = 2,
       tc_spmm_box64 = 1, tc_bnmax = 256, tc_gemm_ctas = 2, spmm_dyn = 1, tf_off = 0;
   long long dw_kmax = 128;
-  int spmm_l2mb = 0;
+  int spmm_l2mb = 96;
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

@@ -1242,10 +1242,13 @@ SpmmShape spmm16_shape(int64_t ld8) {
 // L2 budget (dev knob PGCN_SPMM_L2MB, MB; 0 = off) is processed in nchunk column chunks, chunk-major, so
 // the rows being gathered at any time span table_bytes / nchunk.  The shape is the one for the chunk
 // width; the row's other chunks are separate items.
+// Only two halves, and only for tables up to 3x the budget: measured on B200 (PGCN_SPMM_L2MB sweep,
+// profiles/r2_spmm_chunks.md) the Reddit-shaped step gains 3 % at 96 MB (its 238 MB forward and 119 MB
+// transposed tables), while splitting GB-sized tables (products) into many narrow chunks loses 70 %.
 SpmmShape chunked(SpmmShape (*shape)(int64_t), int64_t w, double table_bytes) {
   const double budget = (double)knobs().spmm_l2mb * 1048576.0;
-  if (budget <= 0.0 || table_bytes <= budget) return shape(w);
-  int64_t nch = (int64_t)std::ceil(table_bytes / budget);
+  if (budget <= 0.0 || table_bytes <= budget || table_bytes > 3.0 * budget) return shape(w);
+  const int64_t nch = 2;
   int64_t cw = (w + nch - 1) / nch;
   cw = (cw + 3) / 4 * 4;  // chunk width in vectors: a multiple of 4 (whole 64-byte fp32 / bf16 segments)
   if (cw >= w) return shape(w);
