@@ -379,134 +379,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
   }
 }
 
-// ---------------------------------------------------------------- narrow rows: several edges per warp
-// Rows of W <= 16 float4 (papers-shaped 48 wide, Reddit's 41-wide last layer): the group-per-row kernels
-// above give each row G = 16 lanes, so two rows with different degrees share a warp and their loops
-// diverge.  Here one warp owns one output row: lane = (edge slot e, column x), E = 32 / W slots, each
-// slot gathers every E-th edge of a 32-edge chunk (U per slot in flight), and the slots' partial sums are
-// combined with shuffles before the epilogue.  Sum order (reading R29): per slot in CSR order, then the
-// slots pairwise -- a reassociation of Eq. 3's sum like the tile path's (R28).
-__device__ __forceinline__ float4 shfl_down4(const float4 v, int d) {
-  return make_float4(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d),
-                     __shfl_down_sync(0xffffffffu, v.z, d), __shfl_down_sync(0xffffffffu, v.w, d));
-}
-
-// acc (slot e, column x) += the table rows of the edges [beg, end) that fall to slot e
-template <int U, bool CHK>
-__device__ __forceinline__ void me_gather(const int32_t* __restrict__ col, int64_t beg, int64_t end, int lane, int e,
-                                          int E, bool act, const char* bq, uint32_t row_bytes, uint32_t nv,
-                                          float4& acc) {
-  for (int64_t e0 = beg; e0 < end; e0 += 32) {
-    const int cnt = (int)((end - e0) < 32 ? (end - e0) : 32);
-    const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
-    for (int j = 0; j < cnt; j += E * U) {
-      float4 v[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = j + u * E + e;
-        const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, my, k < cnt ? k : 0);
-        ok[u] = act && k < cnt && (!CHK || c < nv);
-        v[u] = ok[u] ? __ldg(nbr(bq, c, row_bytes)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (ok[u]) f4acc(acc, v[u]);
-    }
-  }
-}
-
-// slot 0 of each column ends up with the sum over all slots
-__device__ __forceinline__ void me_combine(float4& acc, int e, int E, int W) {
-  for (int sft = 1; sft < E; sft <<= 1) {
-    const float4 o = shfl_down4(acc, sft * W);
-    if ((e & (2 * sft - 1)) == 0 && e + sft < E) f4acc(acc, o);
-  }
-}
-
-template <int U, int MINB, bool CHK>
-__global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd_me(const int64_t* __restrict__ rp,
-                                                                const int32_t* __restrict__ col,
-                                                                const float* __restrict__ inv_deg,
-                                                                const float4* __restrict__ D, int64_t ld4,
-                                                                int64_t n_rows, int64_t n_valid, float4* __restrict__ Z,
-                                                                unsigned long long* work, int grabk, int self,
-                                                                const float* __restrict__ bias, int64_t n_bias,
-                                                                int relu, const int32_t* __restrict__ rows, int addend,
-                                                                int compact) {
-  const int lane = threadIdx.x & 31;
-  const int W = (int)ld4, E = 32 / W;
-  const int e = lane / W, x = lane - e * W;
-  const bool act = e < E;
-  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / 32);
-  const uint32_t row_bytes = (uint32_t)ld4 * 16u;
-  const char* bq = reinterpret_cast<const char*>(D + (act ? x : 0));
-  int64_t first = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int64_t cend = 0;
-  if (work) first = next_item<32>(work, lane, 0xffffffffu, -1, 0, grabk, cend);
-  for (int64_t ri = first; ri < n_rows; ri = next_item<32>(work, lane, 0xffffffffu, ri, stride, grabk, cend)) {
-    const int64_t row = rows ? (int64_t)rows[ri] : ri;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (act && e == 0) {
-      if (self) acc = __ldg(D + row * ld4 + x);                  // GCN-sym self loop (R26)
-      if (addend) f4acc(acc, __ldcs(Z + row * ld4 + x));         // heavy-tile sums, in place
-    }
-    me_gather<U, CHK>(col, rp[row], rp[row + 1], lane, e, E, act, bq, row_bytes, (uint32_t)n_valid, acc);
-    me_combine(acc, e, E, W);
-    if (act && e == 0) {
-      float4 o = f4scale(acc, inv_deg[row]);
-      if (bias) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float v = comp(o, j) + (4 * x + j < n_bias ? bias[4 * x + j] : 0.f);
-          set_comp(o, j, relu ? fmaxf(v, 0.f) : v);
-        }
-      }
-      __stcs(Z + (compact ? ri : row) * ld4 + x, o);
-    }
-  }
-}
-
-template <int U, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd_me(const int64_t* __restrict__ trp,
-                                                                const int32_t* __restrict__ tcol,
-                                                                const float4* __restrict__ dZs,
-                                                                const float4* __restrict__ dDs, int64_t ldA4, int64_t n_in,
-                                                                int64_t n_all, float4* __restrict__ J, int64_t ld4,
-                                                                const int64_t* __restrict__ gid, DropSpec d,
-                                                                unsigned long long* work, int grabk,
-                                                                const float* __restrict__ rs, int addend,
-                                                                const int32_t* __restrict__ dmap,
-                                                                const __grid_constant__ PushSpec ps) {
-  const int lane = threadIdx.x & 31;
-  const int W = (int)ld4, E = 32 / W;
-  const int e = lane / W, x = lane - e * W;
-  const bool act = e < E;
-  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / 32);
-  const uint32_t row_bytes = (uint32_t)ldA4 * 16u;
-  const char* bq = reinterpret_cast<const char*>(dZs + (act ? x : 0));
-  int64_t first = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int64_t cend = 0;
-  if (work) first = next_item<32>(work, lane, 0xffffffffu, -1, 0, grabk, cend);
-  for (int64_t u0 = first; u0 < n_all; u0 = next_item<32>(work, lane, 0xffffffffu, u0, stride, grabk, cend)) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (act && e == 0) {
-      const int64_t du = dmap ? (u0 < n_in ? (int64_t)dmap[u0] : -1) : (u0 < n_in ? u0 : -1);
-      if (dDs && du >= 0) acc = __ldcs(dDs + du * ldA4 + x);
-      if (addend) f4acc(acc, __ldcs(J + u0 * ld4 + x));
-    }
-    me_gather<U, false>(tcol, trp[u0], trp[u0 + 1], lane, e, E, act, bq, row_bytes, 0u, acc);
-    me_combine(acc, e, E, W);
-    if (act && e == 0) {
-      const uint64_t kr = row_key(d, gid[u0]);
-      const float sr = rs ? rs[u0] : 1.f;
-      const float4 o = drop4(rs ? f4scale(acc, sr) : acc, x, kr, 1.f, d);
-      __stcs(J + u0 * ld4 + x, o);
-      if (ps.mode) push_f4(ps, u0, ld4, x, o);
-    }
-  }
-}
-
 // ---------------------------------------------------------------- bf16 gather tier (pgcn_config.gather = 1)
 // The gathered table is first rounded to bf16 (k_to_bf16: rows of ld8 16-byte vectors = 8 columns,
 // padding columns 0); the SpMMs then gather half the bytes and accumulate in fp32 (exact bf16 ->
@@ -1453,22 +1325,6 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
   }
   auto gather = [&](cudaStream_t st, unsigned long long* wk, int slf, int add) -> int {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
-    const int me = knobs().spmm_me;
-    if (!b16 && ld4 <= 16 && me) {  // narrow rows: one warp per row, several edges per warp
-      const int grid = grid_for(n_rows, kThreads / 32, sm_count() * 64);
-      const int Kw = grab_items(nnz, n_rows);
-#define ME(U_)                                                                                                   \
-  if (chk)                                                                                                       \
-    k_spmm_fwd_me<U_, 4, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, Z4, wk, \
-                                                         Kw, slf, bias, n_bias, relu, rows, add, compact);         \
-  else                                                                                                           \
-    k_spmm_fwd_me<U_, 4, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows, n_valid, Z4, wk, \
-                                                          Kw, slf, bias, n_bias, relu, rows, add, compact);
-      if (me == 4) { ME(4) } else { ME(8) }
-#undef ME
-      count(L);
-      return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
-    }
     if (b16) {
       const SpmmShape sh = chunked(spmm16_shape, ld8, (double)n_valid * ld8 * 16);
       const int grid = grid_for(n_rows * sh.nchunk, kThreads / sh.G, sm_count() * 64);
@@ -1554,18 +1410,6 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
   auto gather = [&](cudaStream_t st, unsigned long long* wk, const float* dD, int add) -> int {
     if (wk) cudaMemsetAsync(wk, 0, sizeof(unsigned long long), st);
     auto b = reinterpret_cast<const float4*>(dD);
-    const int me = knobs().spmm_me;
-    if (!b16 && ld4 <= 16 && me) {  // narrow rows: one warp per row, several edges per warp
-      const int grid = grid_for(n_all, kThreads / 32, sm_count() * 64);
-      if (me == 4)
-        k_spmm_bwd_me<4, 4><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, J4, ld4, gid, d, wk,
-                                                       K, rs, add, dmap, ps);
-      else
-        k_spmm_bwd_me<8, 4><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all, J4, ld4, gid, d, wk,
-                                                       K, rs, add, dmap, ps);
-      count(L);
-      return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
-    }
     if (b16) {
       const SpmmShape sh = chunked(spmm16_shape, ld8, (double)n_in * ld8 * 16);
       const int grid = grid_for(n_all * sh.nchunk, kThreads / sh.G, sm_count() * 64);

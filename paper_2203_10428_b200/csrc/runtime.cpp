@@ -68,8 +68,6 @@ const DevKnobs& knobs() {
     k.spmm_table = std::getenv("PGCN_SPMM_TABLE");
     k.tf_off = env_int("PGCN_TF_OFF", 0);
     k.spmm_l2mb = env_int("PGCN_SPMM_L2MB", 96);
-    k.spmm_me = env_int("PGCN_SPMM_ME", 8);
-    if (k.spmm_me != 0 && k.spmm_me != 4) k.spmm_me = 8;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
     if (k.dw_kmax < 0) k.dw_kmax = 128;
   });
