@@ -203,17 +203,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
                                                              int64_t n_valid, int nchunk, float4* __restrict__ Z,
                                                              unsigned long long* work, int grabk, int self,
                                                              const float* __restrict__ bias, int64_t n_bias, int relu,
-                                                             const int32_t* __restrict__ rows, int addend, int compact,
-                                                             int64_t nnz_total) {
+                                                             const int32_t* __restrict__ rows, int addend, int compact) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_rows * nchunk;
-  // Row prefetch: items of one grab are consecutive rows, so while row r is gathered the group already
-  // loads r + 1's end pointer and first column chunk -- two of the four dependent latencies of a short
-  // row (row pointer, column indices, gathers) leave the critical path (papers-shaped rows: ~15 edges).
-  const bool pf_ok = work && !rows && nchunk == 1 && nnz_total > 0;
-  int64_t pf_it = -1, pf_beg = 0, pf_end = 0;
-  int pf_my = 0;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   // Hot-loop addressing is 32-bit: neighbour row c sits at lane_base + c * row_bytes (one
   // IMAD.WIDE per edge; the launcher guarantees ld4 * 16 < 2^32 and ids < 2^31).
@@ -245,26 +238,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_fwd(const int64_t* __re
       acc[q] = self ? __ldg(D + row * ld4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (addend) f4acc(acc[q], __ldcs(Z + row * ld4 + xq[q]));  // heavy-tile sums (spmm_tc) of this row, in place
     }
-    int64_t beg, end;
-    int my0;
-    if (it == pf_it) {
-      beg = pf_beg;
-      end = pf_end;
-      my0 = pf_my;
-    } else {
-      beg = rp[row];
-      end = rp[row + 1];
-      my0 = lane < end - beg ? __ldg(col + beg + lane) : 0;
-    }
-    if (pf_ok && it + 1 < cend && it + 1 < n_items) {
-      pf_it = it + 1;
-      pf_beg = end;
-      pf_end = rp[row + 2];
-      pf_my = end + lane < nnz_total ? __ldg(col + end + lane) : 0;
-    }
+    const int64_t beg = rp[row], end = rp[row + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
-      const int my = e0 == beg ? my0 : (lane < cnt ? __ldg(col + e0 + lane) : 0);
+      const int my = lane < cnt ? __ldg(col + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
         float4 v[U][NC];
@@ -326,13 +303,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
                                                              int64_t ld4, const int64_t* __restrict__ gid, DropSpec d,
                                                              unsigned long long* work, int grabk, const float* __restrict__ rs,
                                                              int addend, const int32_t* __restrict__ dmap,
-                                                             const __grid_constant__ PushSpec ps, int64_t nnz_total) {
+                                                             const __grid_constant__ PushSpec ps) {
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t n_items = n_all * nchunk;
-  const bool pf_ok = work && nchunk == 1 && nnz_total > 0;  // row prefetch, see k_spmm_fwd
-  int64_t pf_it = -1, pf_beg = 0, pf_end = 0;
-  int pf_my = 0;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   const uint32_t row_bytes = (uint32_t)ldA4 * 16u;  // 32-bit hot-loop addressing (see k_spmm_fwd)
   const char* base = reinterpret_cast<const char*>(dZs);
@@ -358,26 +332,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_bwd(const int64_t* __re
       acc[q] = (dDs && du >= 0) ? __ldcs(dDs + du * ldA4 + xq[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (addend) f4acc(acc[q], __ldcs(J + u0 * ld4 + xq[q]));  // heavy-tile sums (spmm_tc) of this row, in place
     }
-    int64_t beg, end;
-    int my0;
-    if (it == pf_it) {
-      beg = pf_beg;
-      end = pf_end;
-      my0 = pf_my;
-    } else {
-      beg = trp[u0];
-      end = trp[u0 + 1];
-      my0 = lane < end - beg ? __ldg(tcol + beg + lane) : 0;
-    }
-    if (pf_ok && it + 1 < cend && it + 1 < n_items) {
-      pf_it = it + 1;
-      pf_beg = end;
-      pf_end = trp[u0 + 2];
-      pf_my = end + lane < nnz_total ? __ldg(tcol + end + lane) : 0;
-    }
+    const int64_t beg = trp[u0], end = trp[u0 + 1];
     for (int64_t e0 = beg; e0 < end; e0 += G) {
       const int cnt = (int)((end - e0) < G ? (end - e0) : G);
-      const int my = e0 == beg ? my0 : (lane < cnt ? __ldg(tcol + e0 + lane) : 0);
+      const int my = lane < cnt ? __ldg(tcol + e0 + lane) : 0;
       int j = 0;
       for (; j + U <= cnt; j += U) {
         float4 v[U][NC];
@@ -1391,11 +1349,11 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
     if (chk)                                                                                                   \
       k_spmm_fwd<G_, NC_, U_, MB_, true><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,      \
                                                                     n_valid, sh.nchunk, Z4, wk, K, slf, bias,     \
-                                                                    n_bias, relu, rows, add, compact, nnz);       \
+                                                                    n_bias, relu, rows, add, compact);            \
     else                                                                                                       \
       k_spmm_fwd<G_, NC_, U_, MB_, false><<<grid, kThreads, 0, st>>>(row_ptr, col, inv_deg, D4, ld4, n_rows,     \
                                                                      n_valid, sh.nchunk, Z4, wk, K, slf, bias,    \
-                                                                     n_bias, relu, rows, add, compact, nnz);      \
+                                                                     n_bias, relu, rows, add, compact);           \
   } else
       PGCN_SPMM_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no spmm_fwd shape for ld4=%lld", (long long)ld4); }
 #undef X
@@ -1468,7 +1426,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
 #define X(G_, NC_, U_, MB_)                                                                                     \
   if (sh.G == G_ && sh.NC == NC_ && sh.U == U_ && sh.MB == MB_) {                                              \
     k_spmm_bwd<G_, NC_, U_, MB_><<<grid, kThreads, 0, st>>>(t_row_ptr, t_col, a, b, lda4, n_in, n_all,          \
-                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap, ps, nnz);                                       \
+                                                            sh.nchunk, J4, ld4, gid, d, wk, K, rs, add, dmap, ps);                                       \
   } else
       PGCN_SPMM_CASES(X) { return fail(PGCN_EUNSUPPORTED, "no spmm_bwd shape for ld4=%lld", (long long)ld4); }
 #undef X
