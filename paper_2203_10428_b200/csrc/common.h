@@ -26,6 +26,7 @@ struct DevKnobs {
       tc_spmm_box64 = 1, tc_bnmax = 256, tc_gemm_ctas = 2, spmm_dyn = 1, tf_off = 0;
   long long dw_kmax = 128;
   int spmm_l2mb = 96;
+  int dw_merge = 1;
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

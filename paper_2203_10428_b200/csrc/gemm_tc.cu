@@ -190,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             mbar_expect_tx(&full[s], geo.a_raw + geo.b_raw);
             if (p.mode == TC_DW) {
               const int r0 = kb * 32;
-              for (int j = 0; j < p.a_feat / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+              for (int j = 0; j < p.a_feat / 32; ++j)
+                tma_load_2d(A + j * 4096, &p.map_a[p.merged ? (j >> 1) : T.seg], &full[s],
+                            p.merged ? 32 * (j & 1) : T.m0 + 32 * j, r0);
               for (int j = 0; j < p.BN / 32; ++j)
                 tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
             } else if (p.mode == TC_FWD) {
@@ -208,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
           if (p.mode == TC_DW) {
             const int r0 = kb * BK;
-            for (int j = 0; j < p.a_feat / 32; ++j) tma_load_2d(A + j * 4096, &p.map_a[T.seg], &full[s], T.m0 + 32 * j, r0);
+            for (int j = 0; j < p.a_feat / 32; ++j)
+              tma_load_2d(A + j * 4096, &p.map_a[p.merged ? (j >> 1) : T.seg], &full[s],
+                          p.merged ? 32 * (j & 1) : T.m0 + 32 * j, r0);
             for (int j = 0; j < p.BN / 32; ++j)
               tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
           } else if (p.mode == TC_FWD) {
@@ -497,8 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             }
           }
         } else {  // EPI_PART: dW partial of split z, row stride ld_out = round_up(N, 4)
-          if (row < p.F) {
-            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)p.out_row_off[T.seg] + row) * p.ld_out;
+          const int sg = p.merged ? (row >> 6) : T.seg, r = p.merged ? (row & 63) : row;  // merged: lanes 64+ = seg 1
+          if (r < p.F) {
+            float* out = p.out + ((int64_t)T.z * p.K_out + (int64_t)p.out_row_off[sg] + r) * p.ld_out;
 #pragma unroll
             for (int g4 = 0; g4 < 4; ++g4) {
               const int n = T.n0 + c0 + 4 * g4;
@@ -976,10 +981,19 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   }
   TcParams p{};
   const int BN = dw_bn(N, bf);
-  p.a_feat = F <= 96 ? (int)((F + 31) / 32 * 32) : tc::BM;  // one f-tile of F <= 96: store only F features
+  // Two segments over the same rows and the same B (aggregate-first GraphSAGE: [Z | D]^T M) with F <= 64
+  // share one 128-row M tile: B (M) is streamed once instead of once per segment and the k-block loop
+  // runs once (papers-shaped 48-wide layers).
+  p.merged = nseg == 2 && rows0 == rows1 && B0 == B1 && F <= 64 && knobs().dw_merge;
+  p.a_feat = p.merged ? tc::BM : (F <= 96 ? (int)((F + 31) / 32 * 32) : tc::BM);
   tc_common(p, BN, bf, TC_DW);
   int Zseg[2];
-  dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg);
+  if (p.merged) {
+    dw_plan((rows0 + 31) / 32, 0, 1, dw_base(F, N), Zseg);
+    Zseg[1] = Zseg[0];
+  } else {
+    dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg);
+  }
   const int Zs = std::max(Zseg[0], Zseg[1]);
   const int64_t NP = (N + 3) / 4 * 4;  // partial row stride (16-byte aligned epilogue stores)
   if ((int64_t)Zs * K * NP > ws_floats) return -3;
@@ -993,7 +1007,7 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   if (!ok) return -1;
   p.mode = TC_DW;
   p.epi = EPI_PART;
-  p.nseg = nseg;
+  p.nseg = p.merged ? 1 : nseg;
   p.Z = Zs;
   for (int s = 0; s < nseg; ++s) {
     p.Zseg[s] = Zseg[s];
@@ -1004,7 +1018,7 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   }
   p.n_ftiles = (int)((F + 127) / 128);
   p.n_ntiles = (int)((N + BN - 1) / BN);
-  p.n_tiles = (Zseg[0] + (nseg > 1 ? Zseg[1] : 0)) * p.n_ftiles * p.n_ntiles;
+  p.n_tiles = (Zseg[0] + (nseg > 1 && !p.merged ? Zseg[1] : 0)) * p.n_ftiles * p.n_ntiles;
   p.M = (int)rmax;
   p.N = (int)N;
   p.F = (int)F;

@@ -34,6 +34,8 @@ struct alignas(64) TcParams {
   PushSpec push;        // EPI_ACT / EPI_MASK: N2 fused push of the rows peers consume (mode 0: off)
   int bf;  // 1: bf16 operands (kind::f16), 0: 3xTF32 (kind::tf32)
   int a_feat;  // DW: A features stored per stage (32 / 64 / 96 / 128; see geometry()); other modes 128
+  int merged;  // DW with two segments over the same rows and operand B, F <= 64: one M tile holds both
+               // (A atoms 0-1 = segment 0's features, 2-3 = segment 1's; TMEM lanes 0-63 / 64-127)
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
