@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--halo-payload", default="f32", choices=["f32", "bf16"],
                     help="bf16: exchange payloads rounded to bf16 (SURVEY N1(iv), 2e-2 tier)")
     ap.add_argument("--depth", type=int, default=1, help="pipeline depth s (R27)")
+    ap.add_argument("--lean", action="store_true",
+                    help="lean-memory mode (SURVEY N1(iii)): Z recomputed in the backward, shared Z / T scratches, "
+                         "one slot for J and the feature messages; bit-identical results")
     ap.add_argument("--no-ablation", action="store_true", help="skip the no-communication timing ablation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -379,7 +382,7 @@ def main():
                            train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles,
                            tile_min=args.tile_min, depth=args.depth,
                            transport=transport if transport in ("loopback", "push") else "local",
-                           halo_payload=args.halo_payload)
+                           halo_payload=args.halo_payload, lean=args.lean)
     local_parts = list(range(parts)) if world == 1 else [rank]
     transport_note = None
     if transport in ("loopback", "push"):
@@ -387,6 +390,8 @@ def main():
         # transport (no message buffers) hosts the partitions and the line says so
         need = pgcn.workspace_bytes(part, cfg, local_parts)
         free = torch.cuda.mem_get_info()[0]
+        if need > free - (2 << 30) and args.lean:
+            raise SystemExit("bench: lean %s needs %.1f GB of workspace, %.1f GB free" % (transport, need / 1e9, free / 1e9))
         if need > free - (2 << 30):
             cfg.transport = 0
             transport_note = "%s needs %.1f GB of workspace, %.1f GB free: local transport" % (
@@ -562,6 +567,7 @@ def main():
                       "parallelism": ("partition x%d on one GPU (%s transport)" % (parts, transport)) if world == 1 else
                       ("partition x%d, one per GPU: NCCL p2p halo exchange on a comm stream + all-reduce" % world),
                       "gemm": args.gemm, "gather": args.gather, "depth": args.depth, "transport": transport,
+                      "lean": bool(args.lean),
                       "transport_note": transport_note,
                       "train_sparse_last_layer": not args.no_train_sparse, "spmm_tiles": not args.no_tiles,
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},

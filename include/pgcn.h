@@ -204,6 +204,21 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       (SURVEY N1(iv), 2e-2 tier): the packed boundary features and the boundary-row
  *                       gradients are rounded to bf16 (round to nearest even) for the transfer and
  *                       widened on receipt (EMA and sums in fp32) -- half the exchanged bytes.
+ *   lean                1: lean-memory mode (same results bit for bit, fewer bytes of
+ *                       workspace): (a) the aggregation Z of every layer lives in one shared scratch and
+ *                       is recomputed by the backward before the weight gradient (one more forward SpMM
+ *                       per aggregate-first layer); (b) T = D W_neigh of transform-first layers shares one
+ *                       scratch (it is dead between a layer's forward and its backward); (c) J^(l) and
+ *                       the packed feature messages keep one slot instead of s + 1 -- the backward of
+ *                       layer l+1 at t waits for the transfer of t-1 to have read J^(l)'s boundary rows,
+ *                       the pack at t for the transfer of t-1 (s = 1: already implied by Alg. 1's wait);
+ *                       (d) with the compact last layer (train_sparse, aggregate-first GraphSAGE) the
+ *                       last layer's logits / M / D_tr rows are sized by min(n_inner, n_train_global)
+ *                       and Y^(L) of non-train rows is not stored at all (pgcn_tensor of the last
+ *                       layer's H is then unavailable; pgcn_set_inputs fails with PGCN_EINVAL if a
+ *                       partition holds more train rows than n_train_global).  Needs a posted transport
+ *                       (LOOPBACK, PUSH, NCCL) when n_parts > 1: LOCAL reads the peers' gradient rows of
+ *                       an earlier slot in place.
  * ---------------------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_layers;
@@ -231,6 +246,7 @@ typedef struct {
   int32_t tile_min;
   int32_t transport;
   int32_t halo_payload;
+  int32_t lean;
 } pgcn_config;
 
 /* Cross-process transport.  NULL (or nranks == 1) = every partition is hosted by this

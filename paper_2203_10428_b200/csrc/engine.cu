@@ -239,6 +239,7 @@ int validate_cfg(const pgcn_config* c) {
   if (c->transport < 0 || c->transport > 2)
     return fail(PGCN_EINVAL, "transport must be 0 (LOCAL), 1 (LOOPBACK) or 2 (PUSH)");
   if (c->halo_payload != 0 && c->halo_payload != 1) return fail(PGCN_EINVAL, "halo_payload must be 0 (fp32) or 1 (bf16)");
+  if (c->lean != 0 && c->lean != 1) return fail(PGCN_EINVAL, "lean must be 0 or 1");
   return PGCN_OK;
 }
 
@@ -298,24 +299,41 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.X = A.take<float>(p.n_all * C->ld[0]);
     for (int l = 1; l < L; ++l)
       for (int b = 0; b < C->nb; ++b) p.H[l][b] = A.take<float>(p.n_all * C->ld[l]);
-    p.logits = A.take<float>(p.n_in * C->ld[L]);
+    // lean (N1(iii)): with the compact last layer only the train rows' logits exist (Y_tr in M)
+    const bool lean = C->cfg.lean != 0;
+    const int64_t n_trb = std::min(p.n_in, (int64_t)C->cfg.n_train_global);  // bound on a partition's train rows
+    if (!(lean && C->cl)) p.logits = A.take<float>(p.n_in * C->ld[L]);
+    int64_t zw = 0, tw = 0;  // lean: widths of the shared Z and T scratches
     for (int l = 1; l <= L; ++l) {
       if (C->cfg.dropout > 0.0 || C->cfg.model == 1) p.D[l] = A.take<float>(p.n_all * C->ld[l - 1]);
+      zw = std::max(zw, C->tf[l] ? C->ld[l] : C->ld[l - 1]);
+      if (C->tf[l]) tw = std::max(tw, C->ld[l]);
+      if (lean) continue;
       p.Z[l] = A.take<float>(p.n_in * (C->tf[l] ? C->ld[l] : C->ld[l - 1]));   // Z, or S = inv_deg P T
       if (C->tf[l]) p.T[l] = A.take<float>(p.n_all * C->ld[l]);                 // T = D W_neigh, then Q
+    }
+    if (lean) {  // one Z scratch (recomputed by the backward) and one T scratch (dead between fwd and bwd)
+      float* zs = A.take<float>(p.n_in * zw);
+      float* tsc = tw ? A.take<float>(p.n_all * tw) : nullptr;
+      for (int l = 1; l <= L; ++l) {
+        p.Z[l] = zs;
+        if (C->tf[l]) p.T[l] = tsc;
+      }
     }
     // M: J^(l) o ReLU' at width F_l (l >= 1); dA: scale_rows output of transform-first layers (width
     // F_l) or dA = M W^T of aggregate-first layers l >= 2 (width 2 F_{l-1}, F_{l-1} for GCN-sym)
     int64_t ld_m = 0, ld_da = 0;
     for (int l = 1; l <= L; ++l) {
-      ld_m = std::max(ld_m, C->ld[l]);
+      if (!(lean && C->cl && l == L)) ld_m = std::max(ld_m, C->ld[l]);
       if (C->tf[l]) ld_da = std::max(ld_da, C->ld[l]);
       else if (l >= 2) ld_da = std::max(ld_da, (C->cfg.model == 1 ? 1 : 2) * C->ld[l - 1]);
     }
-    p.M = A.take<float>(p.n_in * ld_m);
+    // lean + compact last layer: M^(L) / Y_tr has at most n_trb rows
+    p.M = A.take<float>(lean && C->cl ? std::max(p.n_in * ld_m, n_trb * C->ld[L]) : p.n_in * ld_m);
     if (ld_da > 0) p.dA = A.take<float>(p.n_in * ld_da);
     for (int l = 1; l < L; ++l) {
-      for (int b = 0; b < C->nb; ++b) p.J[l][b] = A.take<float>(p.n_all * C->ld[l]);
+      for (int b = 0; b < C->nb; ++b)  // lean: one slot (the next writer waits for the transfer, see layer_bwd)
+        p.J[l][b] = (lean && b > 0) ? p.J[l][0] : A.take<float>(p.n_all * C->ld[l]);
       if (C->cfg.smooth_g) p.emaG[l] = A.take<float>(p.n_send * C->ld[l]);
     }
     p.labels = C->cfg.loss == 0 ? (void*)A.take<int32_t>(p.n_in) : (void*)A.take<uint8_t>(p.n_in * C->F[L]);
@@ -354,9 +372,10 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       if (C->cl) {  // Y_tr lives in M (free until the loss, which turns it into M_tr in place); D_tr in dA
         p.tr_pos = A.take<int32_t>(p.n_in);
         p.Ytr = p.M;
-        p.Dtr = (p.dA && ld_da >= C->ld[L - 1]) ? p.dA : A.take<float>(p.n_in * C->ld[L - 1]);
-        p.lab_tr = C->cfg.loss == 0 ? (void*)A.take<int32_t>(p.n_in) : (void*)A.take<uint8_t>(p.n_in * C->F[L]);
-        p.invdeg_tr = A.take<float>(p.n_in);
+        const int64_t ntr = lean ? n_trb : p.n_in;
+        p.Dtr = (p.dA && ld_da >= C->ld[L - 1]) ? p.dA : A.take<float>(ntr * C->ld[L - 1]);
+        p.lab_tr = C->cfg.loss == 0 ? (void*)A.take<int32_t>(ntr) : (void*)A.take<uint8_t>(ntr * C->F[L]);
+        p.invdeg_tr = A.take<float>(ntr);
       }
       const size_t tb = train_rows_tmp_bytes(p.n_in, p.n_all);
       if ((int64_t)tb > C->sp_tmp_bytes) C->sp_tmp_bytes = (int64_t)tb;
@@ -377,7 +396,8 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       for (int l = 1; l <= L; ++l)
         for (int b = 0; b < (l == 1 ? 1 : C->nb); ++b) {
           const int64_t ld = C->ld[l - 1];
-          if (l == 1 || !fwd_push_capable(C, l - 1)) p.send_f[l][b] = A.take<char>(eb * p.n_send * ld);
+          if (l == 1 || !fwd_push_capable(C, l - 1))  // lean: one slot (the pack waits for the previous send)
+            p.send_f[l][b] = (C->cfg.lean && b > 0) ? p.send_f[l][0] : A.take<char>(eb * p.n_send * ld);
           if (staged_recv(C, l)) p.recv_f[l][b] = A.take<char>(eb * p.n_bd * ld);
           if (l >= 2) {
             if (C->p16) p.send_b[l][b] = A.take<char>(eb * p.n_bd * ld);
@@ -453,6 +473,9 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
   if (C->p16 && !C->posted)
     return fail(PGCN_EUNSUPPORTED, "bf16 exchange payloads need a posted transport (LOOPBACK or NCCL)");
   if (C->p16 && C->xp == XP_PUSH) return fail(PGCN_EUNSUPPORTED, "the PUSH transport moves fp32 payloads");
+  if (cfg->lean && !C->posted && v0.n_parts > 1)
+    return fail(PGCN_EUNSUPPORTED, "lean mode needs a posted transport (LOOPBACK, PUSH or NCCL): LOCAL reads the "
+                                   "peers' gradient rows of an earlier slot in place");
   if (cfg->n_global != pgcn_partition_n_nodes(part)) return fail(PGCN_EINVAL, "cfg.n_global != partition N");
   C->cfg = *cfg;
   C->L = cfg->n_layers;
@@ -746,6 +769,8 @@ int post_fwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, int64_t* n_valid) 
   if (l >= 2 && C->fpushed[l] == t) {  // PUSH: the producer of H^(l-1) already stored the rows (N2)
     cudaEventRecord(C->ev_f_done[l][b], C->s);
   } else if (l >= 2 || t == 1) {
+    // lean: one send slot -- the transfer of t - 1 must have read it (PIPE s = 1 already waited above)
+    if (C->cfg.lean && l >= 2 && t > 1) cudaStreamWaitEvent(C->s, C->ev_f_done[l][C->bi(t - 1)], 0);
     for (auto& p : C->parts) {
       if (p.n_send == 0) continue;
       const float* Hin = layer_in(p, l, b);
@@ -1021,6 +1046,9 @@ extern "C" int pgcn_set_inputs(pgcn_ctx* C, int32_t local, const float* X, const
     cudaStreamSynchronize(C->s);  // sizes of the last layer's launches (documented: synchronous here)
     p.n_tr = h[0];
     p.nnz_tr = h[1];
+    if (C->cfg.lean && C->cl && p.n_tr > std::min(p.n_in, (int64_t)C->cfg.n_train_global))
+      return fail(PGCN_EINVAL, "lean mode: partition %d has %lld train rows > n_train_global %lld", p.part,
+                  (long long)p.n_tr, (long long)C->cfg.n_train_global);
     p.last_sparse = C->cl || !(p.ts[0] && p.ts[1] && 4 * p.n_tr > p.n_in);
     if (C->cl) {  // compact train rows: positions, P_i^T restricted columns -> positions, labels, inv_deg
       compact_train_setup(Lk, p.tr_list, p.n_tr, p.n_in, p.tr_pos, p.tcol_tr, p.nnz_tr);
@@ -1228,7 +1256,7 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       if (p.n_tr > 0 && gemm_fwd_tc(Lk, p.Z[l], p.Dtr, ldi, p.n_tr, C->F[l - 1], C->WT_hi[l], C->WT_lo[l], bias,
                                     C->F[l], p.Ytr, ldo, 0, bf))
         return fail(PGCN_ECUDA, "pgcn_layer_fwd: tensor-core GEMM launch failed (layer %d)", l);
-      scatter_rows(Lk, p.Ytr, p.tr_list, p.n_tr, ldo, p.logits);
+      if (p.logits) scatter_rows(Lk, p.Ytr, p.tr_list, p.n_tr, ldo, p.logits);  // (lean: train rows only, in Y_tr)
       continue;
     }
     // S4: Y = [Z | D] W + b, ReLU on hidden layers
@@ -1301,6 +1329,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   // the rounding pass over the table (read fp32, write bf16)
   auto gat = [&](double F, double e) { return (C->cfg.gather ? 2.0 : 4.0) * F * e; };
   auto cvt = [&](double F, double rows) { return C->cfg.gather ? 6.0 * F * rows : 0.0; };
+  // lean (N1(iii)): J^(l-1) has one slot; its boundary rows posted at t - 1 must have been read by the
+  // transfer before this iteration rewrites them (bf16 payloads travel from send_b, PUSH from epilogues)
+  if (C->cfg.lean && C->posted && !C->p16 && l >= 2 && t > 1)
+    cudaStreamWaitEvent(C->s, C->ev_b_done[l][C->bi(t - 1)], 0);
   // phase A: S6 (G_i^(l), Alg. 1 l.18), S7 + S8 (J^(l-1) for inner and boundary rows, l.20)
   for (auto& p : C->parts) {
     const double Fi = (double)C->F[l - 1], Fo = (double)C->F[l];
@@ -1312,6 +1344,19 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
     auto sb = [&](double F, double nv, double e, double rest) { return SpmmBytes{gat(F, nv) + rest, gat(F, e) + rest}; };
     const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
+    if (C->cfg.lean && !C->tf[l]) {
+      // N1(iii): Z^(l) was not kept (one scratch for every layer) -- recompute it with the forward's own
+      // launch (same inputs: D^(l) and the boundary rows of slot t are untouched until t + 1), bit for bit
+      const bool spf = C->cfg.train_sparse && l == C->L && p.last_sparse;
+      const int64_t nrf = spf ? p.n_tr : p.n_in, nvf = p.n_valid[l];
+      const double nzf = spf ? (double)p.nnz_tr : (double)p.nnz;
+      Scope sc(C, PGCN_K_SPMM_FWD, sb(Fi, nvf, nzf + (C->gcn ? nrf : 0), cvt(Fi, nvf) + 4.0 * nzf + 8.0 * (nrf + 1) +
+                                       4.0 * nrf + 4.0 * Fi * nrf));
+      if ((rc = spmm_fwd(Lk, p.rp, p.col, C->gcn ? p.sym : p.inv_deg, D, ldi, nrf, nvf, p.Z[l], C->work, C->gcn ? 1 : 0,
+                         nullptr, 0, 0, p.n_all, p.G16, spf ? p.tr_list : nullptr, (int64_t)nzf, p.tiles(0), p.T16,
+                         C->cl && l == C->L)))
+        return poison(C, rc);
+    }
     if (C->gcn) {
       // GCN-sym backward (App. A.1 PAPER.md:651-657 with P = S (A + I) S, S = diag(d~^-1/2), R26)
       if (C->tf[l]) {
@@ -1556,7 +1601,9 @@ extern "C" int pgcn_layer_fwd_io(pgcn_ctx* C, int64_t t, int32_t l, const float*
   if (h_out)
     for (size_t k = 0; k < C->parts.size(); ++k) {
       PartCtx& p = C->parts[k];
-      if (h_out[k]) copy_rows(C, h_out[k], ld_out, l < C->L ? p.H[l][bb] : p.logits, C->ld[l], C->F[l], p.n_in);
+      if (!h_out[k]) continue;
+      if (l == C->L && !p.logits) return fail(PGCN_EUNSUPPORTED, "lean mode: the last layer's output rows are not kept");
+      copy_rows(C, h_out[k], ld_out, l < C->L ? p.H[l][bb] : p.logits, C->ld[l], C->F[l], p.n_in);
     }
   return check_cuda(C, "pgcn_layer_fwd_io");
 }
@@ -1627,7 +1674,7 @@ extern "C" int pgcn_tensor(pgcn_ctx* C, int32_t local, int32_t kind, int32_t l, 
   const bool lok = l >= 1 && l <= C->L;
   switch (kind) {
     case PGCN_T_H:
-      if (!lok) break;
+      if (!lok || (l == C->L && !p.logits)) break;  // (lean + compact last layer: logits not kept)
       *o = {l < C->L ? (void*)p.H[l][b] : (void*)p.logits, p.n_in, C->F[l], C->ld[l]};
       return PGCN_OK;
     case PGCN_T_HIN:

@@ -53,7 +53,7 @@ class Config(C.Structure):
                 ("eps", C.c_double), ("transform_first", C.c_int32), ("staleness_stats", C.c_int32),
                 ("model", C.c_int32), ("depth", C.c_int32), ("gather", C.c_int32),
                 ("train_sparse", C.c_int32), ("spmm_tiles", C.c_int32), ("tile_min", C.c_int32),
-                ("transport", C.c_int32), ("halo_payload", C.c_int32)]
+                ("transport", C.c_int32), ("halo_payload", C.c_int32), ("lean", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -211,7 +211,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
                 opt="adam", lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, dump_j=False,
                 transform_first=True, staleness_stats=False, model="sage", depth=1,
                 gather="f32", train_sparse=False, spmm_tiles=True, tile_min=0, transport="local",
-                halo_payload="f32") -> Config:
+                halo_payload="f32", lean=False) -> Config:
     c = Config()
     c.n_layers = len(widths) - 1
     for i, w in enumerate(widths):
@@ -236,6 +236,7 @@ def make_config(widths: Sequence[int], *, mode="pipe", smooth_f=False, smooth_g=
     c.tile_min = int(tile_min)
     c.transport = {"local": 0, "loopback": 1, "push": 2}[transport]
     c.halo_payload = {"f32": 0, "bf16": 1}[halo_payload]
+    c.lean = int(bool(lean))
     return c
 
 

@@ -103,3 +103,28 @@ def test_contiguous_map_matches_header_rule():
     # lo_p = floor(p * N / n) (include/pgcn.h, reading R19)
     m = contiguous_map(10, 3)
     assert m.tolist() == [0, 0, 0, 1, 1, 1, 2, 2, 2, 2]
+
+
+def test_lean_workspace_host_query(P):
+    """N1(iii) lean-memory mode through the host-only workspace query: a papers-shaped layer stack
+    (transform-first layer 1, compact last layer) needs fewer bytes with lean = 1, exactly the dropped
+    buffers' worth at least the shared Z / J slots; lean with the LOCAL transport and several
+    partitions is rejected (PGCN_EUNSUPPORTED)."""
+    g = gen_graph("papers", seed=3, n=20000, nnz=180000, f0=64, classes=40)
+    widths = [64, 16, 16, 40]
+    part = P.partition(g.n, g.row_ptr, g.col_idx, 2)
+    kw = dict(n_global=g.n, n_train_global=g.n_train, train_sparse=True, transport="loopback")
+    full = P.workspace_bytes(part, P.make_config(widths, **kw))
+    lean = P.workspace_bytes(part, P.make_config(widths, lean=True, **kw))
+    v = [part.view(i) for i in range(2)]
+    n_in = [int(x["n_inner"]) for x in v]
+    n_all = [int(x["n_inner"] + x["n_halo"]) for x in v]
+    # at least: the last layer's logits (n_in x 40) and two of the three Z buffers (n_in x 16), one J slot
+    # per hidden layer (n_all x 16) are gone; M shrinks from width 40 to 16
+    dropped = sum(4 * (ni * 40 + 2 * ni * 16 + 2 * na * 16 + ni * 24) for ni, na in zip(n_in, n_all))
+    assert full - lean >= 0.95 * dropped, (full, lean, dropped)
+    with pytest.raises(P.PgcnError):
+        P.workspace_bytes(part, P.make_config(widths, lean=True, **dict(kw, transport="local")))
+    # one partition: nothing is exchanged, LOCAL is fine
+    part1 = P.partition(g.n, g.row_ptr, g.col_idx, 1)
+    assert P.workspace_bytes(part1, P.make_config(widths, lean=True, **dict(kw, transport="local"))) > 0
