@@ -27,6 +27,7 @@ struct DevKnobs {
   long long dw_kmax = 128;
   int spmm_l2mb = 96;
   int dw_merge = 1;
+  int presplit = 0;
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

@@ -54,6 +54,7 @@ struct PartCtx {
   float* T[PGCN_MAX_LAYERS + 1] = {};
   int64_t n_valid[PGCN_MAX_LAYERS + 1] = {};  // rows of the layer input valid this iteration
   float* M = nullptr;
+  float* Mlo = nullptr;  // 3xTF32 tier: lo = M - trunc_tf32(M), written with M (the GEMMs reading M load it)
   float* dA = nullptr;
   float* J[PGCN_MAX_LAYERS + 1][kMaxBuf] = {};
   float* emaG[PGCN_MAX_LAYERS + 1] = {};
@@ -182,6 +183,7 @@ struct pgcn_ctx {
   cudaEvent_t ev_x_free = nullptr, ev_lab_free = nullptr, ev_in_ready = nullptr;
   int in_pending = 0, inputs_set = 0;
   int force_write_j = 0;  // pgcn_layer_bwd_io with j_in: the stale-gradient accumulate writes J^(l-1) inner rows
+  int mlo_stale = 0;      // pgcn_layer_bwd_io(layer L, j_out): M came from the caller, Mlo was not written
 #ifdef PGCN_WITH_NCCL
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
@@ -329,7 +331,17 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
       else if (l >= 2) ld_da = std::max(ld_da, (C->cfg.model == 1 ? 1 : 2) * C->ld[l - 1]);
     }
     // lean + compact last layer: M^(L) / Y_tr has at most n_trb rows
-    p.M = A.take<float>(lean && C->cl ? std::max(p.n_in * ld_m, n_trb * C->ld[L]) : p.n_in * ld_m);
+    const int64_t m_floats = lean && C->cl ? std::max(p.n_in * ld_m, n_trb * C->ld[L]) : p.n_in * ld_m;
+    p.M = A.take<float>(m_floats);
+    // M's lo term: where GEMMs read M in several tiles (widths >= 128; narrow layers read it about once) and
+    // not for the compact last layer (n_tr rows); lean: the converters split M
+    int64_t ld_mlo = 0;
+    for (int l = 1; l <= L; ++l)
+      if (!(C->cl && l == L)) ld_mlo = std::max(ld_mlo, C->ld[l]);
+    // Dev knob PGCN_PRESPLIT=1 (default off): measured on B200 (profiles/r2p_presplit.md) the GEMMs gain
+    // 1.6 ms per Yelp-shaped step (dW 16.2 -> 15.0, dA 10.1 -> 9.6) and the M_lo stores cost 0.8 ms in the
+    // stale-gradient accumulate -- the converter warps are not what bounds these GEMMs
+    if (C->cfg.gemm == 0 && !lean && ld_mlo >= 128 && knobs().presplit) p.Mlo = A.take<float>(p.n_in * ld_mlo);
     if (ld_da > 0) p.dA = A.take<float>(p.n_in * ld_da);
     for (int l = 1; l < L; ++l) {
       for (int b = 0; b < C->nb; ++b)  // lean: one slot (the next writer waits for the transfer, see layer_bwd)
@@ -1301,9 +1313,9 @@ extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
       reduce_sum(Lk, p.row_loss, p.n_tr, C->part_loss + i);
       continue;
     }
-    Scope sc(C, PGCN_K_LOSS, 8.0 * p.n_in * C->F[L] + 5.0 * p.n_in);
+    Scope sc(C, PGCN_K_LOSS, (p.Mlo ? 12.0 : 8.0) * p.n_in * C->F[L] + 5.0 * p.n_in);
     loss_rows(Lk, C->cfg.loss, p.logits, p.n_in, C->F[L], C->ld[L], p.labels, p.train,
-              (double)C->cfg.n_train_global, p.M, p.row_loss);
+              (double)C->cfg.n_train_global, p.M, p.row_loss, p.Mlo);
     reduce_sum(Lk, p.row_loss, p.n_in, C->part_loss + i);
   }
   if (loss_dev) reduce_sum(Lk, C->part_loss, (int64_t)C->parts.size(), loss_dev);
@@ -1344,6 +1356,8 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     const double nz = sp ? (double)p.nnz_tr : (double)p.nnz;
     auto sb = [&](double F, double nv, double e, double rest) { return SpmmBytes{gat(F, nv) + rest, gat(F, e) + rest}; };
     const float* D = (C->cfg.dropout > 0.0 || C->gcn) ? p.D[l] : layer_in(p, l, b);
+    // M's producer-written lo term (3xTF32 tier; not for the compact last layer's M_tr)
+    const float* mlo = (C->mlo_stale || (C->cl && l == C->L)) ? nullptr : p.Mlo;
     if (C->cfg.lean && !C->tf[l]) {
       // N1(iii): Z^(l) was not kept (one scratch for every layer) -- recompute it with the forward's own
       // launch (same inputs: D^(l) and the boundary rows of slot t are untouched until t + 1), bit for bit
@@ -1390,14 +1404,14 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * p.n_in * (Fi + Fo), 2.0 * p.n_in * (Fi + 1) * Fo);
         if (tc_dw_general(Lk, p.Z[l], p.M, p.n_in, nullptr, nullptr, 0, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
-                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf))
+                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf, mlo))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       }
       if (l >= 2) {
         {  // dZs = S (M W^T)
           Scope sc(C, PGCN_K_GEMM_DA, 4.0 * p.n_in * (Fi + Fo) + 4.0 * p.n_in, 2.0 * p.n_in * Fo * Fi);
           if (gemm_da_tc(Lk, p.M, ldo, p.n_in, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1], p.sym, p.dA,
-                         ldi, bf, 1))
+                         ldi, bf, 1, mlo))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         }
         // J^(l-1)_u = mask o s o d~_u^-1/2 ((A + I)^T dZs)_u over inner + boundary rows
@@ -1427,7 +1441,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       {
         Scope sc(C, PGCN_K_GEMM_DW, 4.0 * (nv + p.n_in) * (Fi + Fo), 2.0 * (nv + p.n_in) * Fi * Fo);
         if (tc_dw_general(Lk, D, p.T[l], nv, D, p.M, p.n_in, ldi, ldo, C->F[l - 1], C->F[l], p.M, p.n_in,
-                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf))
+                          p.G + C->woff[l], C->dw_ws, C->dw_ws_floats, bf, nullptr, mlo))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       }
       if (l >= 2) {
@@ -1448,7 +1462,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       Scope sc(C, PGCN_K_GEMM_DW, 4.0 * mr * (2 * Fi + Fo), 2.0 * mr * (2 * Fi + 1) * Fo);
       if (C->cfg.gemm != 2) {
         if (gemm_dw_tc(Lk, p.Z[l], D, ldi, mr, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
-                       C->dw_ws_floats, bf))
+                       C->dw_ws_floats, bf, mlo))
           return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dW GEMM failed (layer %d)", l);
       } else {
         gemm_dw_f32(Lk, p.Z[l], D, ldi, p.n_in, C->F[l - 1], p.M, ldo, C->F[l], p.G + C->woff[l], C->dw_ws,
@@ -1460,7 +1474,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
         Scope sc(C, PGCN_K_GEMM_DA, 4.0 * mr * (2 * Fi + Fo) + 4.0 * mr, 2.0 * mr * Fo * 2 * Fi);
         if (C->cfg.gemm != 2) {
           if (mr > 0 && gemm_da_tc(Lk, p.M, ldo, mr, C->F[l], C->Wp_hi[l], C->Wp_lo[l], C->Kp[l], C->F[l - 1],
-                                   cl ? p.invdeg_tr : p.inv_deg, p.dA, ldi, bf, 2))
+                                   cl ? p.invdeg_tr : p.inv_deg, p.dA, ldi, bf, 2, mlo))
             return fail(PGCN_ECUDA, "pgcn_layer_bwd: tensor-core dA GEMM failed (layer %d)", l);
         } else {
           gemm_da_f32(Lk, p.M, ldo, p.n_in, C->F[l], Wext, C->F[l - 1], p.inv_deg, p.dA, ldi);
@@ -1504,10 +1518,10 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
       }
       const int m16 = C->posted && C->p16;
       const double Fi = (double)C->F[l - 1];
-      Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j) + 8.0 * p.n_in +
+      Scope sc(C, PGCN_K_GRAD_REDUCE, 4.0 * Fi * p.n_in * (3 + C->cfg.dump_j + (p.Mlo ? 1 : 0)) + 8.0 * p.n_in +
                                           (msg.n_seg ? ((m16 ? 2.0 : 4.0) * Fi + 4.0 + (use_ema ? 8.0 * Fi : 0.0)) * p.n_send : 0.0));
       grad_reduce(Lk, p.inv_ptr, p.inv_pos, msg, row_map, p.emaG[l - 1], (float)C->cfg.gamma, use_ema, first,
-                  p.J[l - 1][b], C->cfg.dump_j || C->force_write_j, p.H[l - 1][b], p.M, p.n_in, ldi, m16);
+                  p.J[l - 1][b], C->cfg.dump_j || C->force_write_j, p.H[l - 1][b], p.M, p.n_in, ldi, m16, p.Mlo);
       if (C->cfg.staleness_stats && C->xp != XP_NCCL && C->n_parts > 1 && p.n_send > 0) {
         // N4: ||gradient messages used - fresh ones||^2 (fresh = peers' boundary rows of this iteration;
         // used = the smoothed state, the stale messages, or 0 when nothing was received)
@@ -1629,12 +1643,14 @@ extern "C" int pgcn_layer_bwd_io(pgcn_ctx* C, int64_t t, int32_t l, const float*
         copy_rows(C, p.J[l][bb], C->ld[l], j_out[k], ld_jo, C->F[l], p.n_in);
         SegTable none{};
         grad_reduce(Lk, p.inv_ptr, p.inv_pos, none, nullptr, nullptr, 0.f, 0, 0, p.J[l][bb], 0, p.H[l][bb], p.M,
-                    p.n_in, C->ld[l]);
+                    p.n_in, C->ld[l], 0, p.Mlo);
       }
     }
   C->force_write_j = j_in != nullptr && l >= 2;
+  C->mlo_stale = j_out != nullptr && l == C->L;  // M^(L) copied from the caller: the GEMMs split it themselves
   rc = pgcn_layer_bwd(C, t, l, C->theta_io);
   C->force_write_j = 0;
+  C->mlo_stale = 0;
   if (rc) return rc;
   if (j_in && l >= 2)
     for (size_t k = 0; k < C->parts.size(); ++k) {

@@ -207,14 +207,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
               tma_load_2d(B, &p.map_b[0], &full[s], kb * 64, T.half * p.F + T.n0);
             }
           } else {
-          mbar_expect_tx(&full[s], a_bytes + (split_b ? b_bytes : 2 * b_bytes));
+          const bool pb = split_b && ((p.pre_b >> T.seg) & 1), pa = p.mode == TC_DA && p.pre_a;
+          mbar_expect_tx(&full[s], (pa ? 2 : 1) * a_bytes + (split_b && !pb ? b_bytes : 2 * b_bytes));
           if (p.mode == TC_DW) {
             const int r0 = kb * BK;
             for (int j = 0; j < p.a_feat / 32; ++j)
               tma_load_2d(A + j * 4096, &p.map_a[p.merged ? (j >> 1) : T.seg], &full[s],
                           p.merged ? 32 * (j & 1) : T.m0 + 32 * j, r0);
-            for (int j = 0; j < p.BN / 32; ++j)
+            for (int j = 0; j < p.BN / 32; ++j) {
               tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
+              if (pb) tma_load_2d(Blo + j * 4096, &p.map_lo[T.seg], &full[s], T.n0 + 32 * j, r0);
+            }
           } else if (p.mode == TC_FWD) {
             const int seg = kb < p.kb_seg[0] ? 0 : 1;
             const int kl = kb - (seg ? p.kb_seg[0] : 0);
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kcol, T.n0);
           } else {  // TC_DA
             tma_load_2d(A, &p.map_a[0], &full[s], kb * BK, T.m0);
+            if (pa) tma_load_2d(A + a_bytes, &p.map_lo[0], &full[s], kb * BK, T.m0);
             const int brow = T.half * p.F + T.n0;
             tma_load_2d(B, &p.map_b[0], &full[s], kb * BK, brow);
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * BK, brow);
@@ -355,11 +359,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
         float4* A = reinterpret_cast<float4*>(stA + (size_t)s * stage_bytes);
         float4* Alo = A + a_bytes / 16;
 #if PGCN_TF32_TRUNC_HI
-        for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
-          const float4 x = A[i];
-          Alo[i] = make_float4(tf32_lo_trunc(x.x), tf32_lo_trunc(x.y), tf32_lo_trunc(x.z), tf32_lo_trunc(x.w));
-        }
-        if (split_b) {
+        // (operands whose lo arrived by TMA -- p.pre_a / p.pre_b -- are not converted)
+        if (!(p.mode == TC_DA && p.pre_a))
+          for (int i = ct; i < (int)(a_bytes / 16); i += kConvThreads) {
+            const float4 x = A[i];
+            Alo[i] = make_float4(tf32_lo_trunc(x.x), tf32_lo_trunc(x.y), tf32_lo_trunc(x.z), tf32_lo_trunc(x.w));
+          }
+        if (split_b && !((p.pre_b >> T.seg) & 1)) {
           const float4* B = A + 2 * (a_bytes / 16);
           float4* Blo = A + 2 * (a_bytes / 16) + b_bytes / 16;
           for (int i = ct; i < (int)(b_bytes / 16); i += kConvThreads) {
@@ -721,6 +727,8 @@ int tc_tmem_cols(int BN) {
 // two independent pipelines per SM hide more of it (papers-q forward GEMMs 18.9 -> 15.7 ms per step;
 // the dW GEMM measured slower, its split-K plan fills 148-CTA waves).  Dev knob PGCN_TC_GEMM_CTAS=1.
 static int gemm_ctas() { return knobs().tc_gemm_ctas; }
+// dev knob PGCN_PRESPLIT=1: the engine allocates M_lo and the GEMMs load it (default 0, see engine.cu)
+static bool presplit_enabled() { return knobs().presplit != 0; }
 
 cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   if (smem_attr_once((const void*)tc::k_umma_gemm<0, 0>, 227 * 1024) ||
@@ -938,13 +946,16 @@ int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_
 }
 
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves) {
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves,
+               const float* Mlo) {
   if (M <= 0) return 0;
   if (halves != 1 && halves != 2) return -1;
   TcParams p{};
   const int BN = tc_bn(F);
   tc_common(p, BN, bf, TC_DA);
   bool ok = tc_map(&p.map_a[0], Mg, false, N, M, ldM, 32, 128, bf ? 0 : 1);
+  p.pre_a = !bf && Mlo && PGCN_TF32_TRUNC_HI && presplit_enabled();
+  if (p.pre_a) ok = ok && tc_map(&p.map_lo[0], Mlo, false, N, M, ldM, 32, 128, 1);
   if (bf) ok = ok && tc_map(&p.map_b[0], Wp_hi, true, N, halves * F, Kp, 64, BN, 1);
   else
     ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, halves * F, Kp, 32, BN, 1) &&
@@ -970,7 +981,7 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
 
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
-                  float* G, float* ws, int64_t ws_floats, int bf) {
+                  float* G, float* ws, int64_t ws_floats, int bf, const float* B0lo, const float* B1lo) {
   const int nseg = A1 ? 2 : 1;  // GCN-sym: G = [A0^T B0 ; colsum(Mb)]
   if (!A1) rows1 = 0;
   const int64_t K = nseg * F + 1;
@@ -1000,10 +1011,16 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const float* As[2] = {A0, A1};
   const float* Bs[2] = {B0, B1};
   const int64_t rows[2] = {rows0, rows1};
+  const float* Blos[2] = {B0lo, B1lo};
   bool ok = true;
-  for (int s = 0; s < nseg && ok; ++s)
+  for (int s = 0; s < nseg && ok; ++s) {
     ok = tc_map(&p.map_a[s], As[s], false, F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, bf ? 0 : 2) &&
          tc_map(&p.map_b[s], Bs[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, bf ? 0 : 2);
+    if (ok && !bf && Blos[s] && PGCN_TF32_TRUNC_HI && presplit_enabled()) {
+      ok = tc_map(&p.map_lo[s], Blos[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, 2);
+      p.pre_b |= 1 << s;
+    }
+  }
   if (!ok) return -1;
   p.mode = TC_DW;
   p.epi = EPI_PART;
@@ -1057,8 +1074,8 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
 }
 
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
-               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf) {
-  return tc_dw_general(L, Z, Mg, M, D, Mg, M, ldA, ldM, F, N, Mg, M, G, ws, ws_floats, bf);
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf, const float* Mlo) {
+  return tc_dw_general(L, Z, Mg, M, D, Mg, M, ldA, ldM, F, N, Mg, M, G, ws, ws_floats, bf, Mlo, Mlo);
 }
 
 }  // namespace pgcn

@@ -36,6 +36,11 @@ struct alignas(64) TcParams {
   int a_feat;  // DW: A features stored per stage (32 / 64 / 96 / 128; see geometry()); other modes 128
   int merged;  // DW with two segments over the same rows and operand B, F <= 64: one M tile holds both
                // (A atoms 0-1 = segment 0's features, 2-3 = segment 1's; TMEM lanes 0-63 / 64-127)
+  // 3xTF32 operands whose lo = x - trunc_tf32(x) was written by their producer (the loss / the stale-
+  // gradient accumulate write M and M_lo): TMA loads lo from map_lo instead of the converter warps
+  // computing it once per tile that reads the operand.  pre_a: DA's A (M); pre_b: bit s = DW segment s's B.
+  CUtensorMap map_lo[2];
+  int pre_a, pre_b;
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
@@ -66,10 +71,12 @@ int gemm_fwd_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M
                 const PushSpec* push = nullptr);
 // dA = Mg W^T; halves = 2: [dZ' | dD] (GraphSAGE, first half scaled by inv_deg, row stride 2 ld),
 // halves = 1: inv_deg o (Mg W^T) (GCN-sym, row stride ld).
+// Mlo (optional, 3xTF32 only): the producer-written lo = x - trunc_tf32(x) of Mg, same layout.
 int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, const void* Wp_hi, const void* Wp_lo,
-               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves);
+               int64_t Kp, int64_t F, const float* inv_deg, float* dA, int64_t ld, int bf, int halves,
+               const float* Mlo = nullptr);
 int gemm_dw_tc(Launch L, const float* Z, const float* D, int64_t ldA, int64_t M, int64_t F, const float* Mg,
-               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf);
+               int64_t ldM, int64_t N, float* G, float* ws, int64_t ws_floats, int bf, const float* Mlo = nullptr);
 // Transform-before-aggregate pieces (N1: P(DW) = (PD)W for F_out < F_in):
 //   out[M x N] = act(A[M x K] W_seg^T + addend + bias), W_seg = W_neigh (kb_off 0) or W_self
 //   (kb_off = Fp / k-block) read from the WT operand copy (ldB = 2Fp columns).
@@ -84,8 +91,10 @@ int tc_fwd_mask(Launch L, const float* Q, int64_t M, const float* Mg, int64_t M_
                 const int64_t* gid, const DropSpec& d, int bf, const float* rscale, const PushSpec* push = nullptr);
 //   G[(2F+1) x N] = [A0^T B0 ; A1^T B1 ; colsum(Mb)], A_s/B_s over their own row counts;
 //   A1 == nullptr: G[(F+1) x N] = [A0^T B0 ; colsum(Mb)] (GCN-sym).
+//   B0lo / B1lo (optional, 3xTF32): producer-written lo of B0 / B1.
 int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, const float* A1, const float* B1,
                   int64_t rows1, int64_t ldA, int64_t ldB, int64_t F, int64_t N, const float* Mb, int64_t rowsMb,
-                  float* G, float* ws, int64_t ws_floats, int bf);
+                  float* G, float* ws, int64_t ws_floats, int bf, const float* B0lo = nullptr,
+                  const float* B1lo = nullptr);
 
 }  // namespace pgcn

@@ -727,12 +727,20 @@ __global__ void k_spin(int64_t ns) {
   } while ((int64_t)(t - t0) < ns);
 }
 
+// lo = x - trunc_tf32(x) (exact): the 3xTF32 GEMMs' second operand term (tc_ptx.cuh tf32_lo_trunc, the
+// converter warps' split -- kind::tf32 reads the raw word's top 19 bits as hi), written by the producers
+// of M so the GEMMs that read M load it instead of recomputing it per tile (gemm_tc.cu pre_a / pre_b).
+__device__ __forceinline__ float lo_tf32(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ float4 lo_tf32(float4 v) {
+  return make_float4(lo_tf32(v.x), lo_tf32(v.y), lo_tf32(v.z), lo_tf32(v.w));
+}
+
 // ---------------------------------------------------------------- stale gradient accumulate + M (S9)
 __global__ void k_grad_reduce(const int64_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv_pos,
                               const __grid_constant__ SegTable msg, const int32_t* __restrict__ row_map,
                               float4* __restrict__ ema, float gamma, int use_ema, int first, float4* __restrict__ J,
                               int write_j, const float4* __restrict__ Hprev, float4* __restrict__ M, int64_t n_in,
-                              int64_t ld4, int msg16) {
+                              int64_t ld4, int msg16, float4* __restrict__ Mlo) {
   const int64_t total = n_in * ld4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i / ld4, x = i - v * ld4;
@@ -758,8 +766,10 @@ __global__ void k_grad_reduce(const int64_t* __restrict__ inv_ptr, const int32_t
     }
     if (write_j) J[i] = acc;
     const float4 h = Hprev[v * ld4 + x];
-    M[i] = make_float4(h.x > 0.f ? acc.x : 0.f, h.y > 0.f ? acc.y : 0.f, h.z > 0.f ? acc.z : 0.f,
-                       h.w > 0.f ? acc.w : 0.f);
+    const float4 m = make_float4(h.x > 0.f ? acc.x : 0.f, h.y > 0.f ? acc.y : 0.f, h.z > 0.f ? acc.z : 0.f,
+                                 h.w > 0.f ? acc.w : 0.f);
+    M[i] = m;
+    if (Mlo) Mlo[i] = lo_tf32(m);
   }
 }
 
@@ -777,14 +787,18 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // Y and M may alias (compact train rows: the logits become J^(L) in place, each row read before written)
 __global__ void k_loss_ce(const float* Y, int64_t n, int64_t C, int64_t ld, const int32_t* __restrict__ lab,
-                          const uint8_t* __restrict__ train, float inv_nt, float* M, float* __restrict__ rl) {
+                          const uint8_t* __restrict__ train, float inv_nt, float* M, float* __restrict__ rl,
+                          float* __restrict__ Mlo) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
     const float* y = Y + v * ld;
     float* m = M + v * ld;
     if (train && !train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
-      for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t c = lane; c < ld / 4; c += 32) {
+        reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (Mlo) reinterpret_cast<float4*>(Mlo + v * ld)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       if (lane == 0) rl[v] = 0.f;
       continue;
     }
@@ -802,13 +816,15 @@ __global__ void k_loss_ce(const float* Y, int64_t n, int64_t C, int64_t ld, cons
       float g = 0.f;
       if (c < C) g = (expf(y[c] - mx) / s - (c == t ? 1.f : 0.f)) * inv_nt;
       m[c] = g;
+      if (Mlo) Mlo[v * ld + c] = lo_tf32(g);
     }
     if (lane == 0) rl[v] = (ls + mx - yt) * inv_nt;
   }
 }
 
 __global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, const uint8_t* __restrict__ lab,
-                           const uint8_t* __restrict__ train, float inv_ntc, float* M, float* __restrict__ rl) {
+                           const uint8_t* __restrict__ train, float inv_ntc, float* M, float* __restrict__ rl,
+                           float* __restrict__ Mlo) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
@@ -816,7 +832,10 @@ __global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, con
     float* m = M + v * ld;
     const bool tr = !train || train[v] != 0;
     if (!tr) {
-      for (int64_t c = lane; c < ld / 4; c += 32) reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t c = lane; c < ld / 4; c += 32) {
+        reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (Mlo) reinterpret_cast<float4*>(Mlo + v * ld)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       if (lane == 0) rl[v] = 0.f;
       continue;
     }
@@ -829,6 +848,7 @@ __global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, con
         l += fmaxf(yc, 0.f) + log1pf(expf(-fabsf(yc))) - lb * yc;
       }
       m[c] = g;
+      if (Mlo) Mlo[v * ld + c] = lo_tf32(g);
     }
     l = warp_sum(l);
     if (lane == 0) rl[v] = l * inv_ntc;
@@ -1465,13 +1485,13 @@ void gather_rows(Launch L, const SegTable& src, const int32_t* row_map, int64_t 
 
 void grad_reduce(Launch L, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg, const int32_t* row_map,
                  float* ema, float gamma, int use_ema, int first, float* J, int write_j, const float* Hprev, float* M,
-                 int64_t n_in, int64_t ld, int msg16) {
+                 int64_t n_in, int64_t ld, int msg16, float* Mlo) {
   if (n_in <= 0) return;
   const int64_t ld4 = ld / 4;
   k_grad_reduce<<<grid_for(n_in * ld4, kThreads), kThreads, 0, L.s>>>(
       inv_ptr, inv_pos, msg, row_map, reinterpret_cast<float4*>(ema), gamma, use_ema, first,
       reinterpret_cast<float4*>(J), write_j, reinterpret_cast<const float4*>(Hprev), reinterpret_cast<float4*>(M), n_in,
-      ld4, msg16);
+      ld4, msg16, reinterpret_cast<float4*>(Mlo));
   count(L);
 }
 
@@ -1526,15 +1546,15 @@ void gather_bytes(Launch L, const void* src, const int32_t* list, int64_t n, int
 }
 
 void loss_rows(Launch L, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
-               const uint8_t* train, double n_train, float* M, float* row_loss) {
+               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo) {
   if (n <= 0) return;
   const int grid = grid_for(n, kThreads / 32, sm_count() * 32);
   if (kind == 0)
     k_loss_ce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const int32_t*>(labels), train,
-                                          (float)(1.0 / n_train), M, row_loss);
+                                          (float)(1.0 / n_train), M, row_loss, Mlo);
   else
     k_loss_bce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const uint8_t*>(labels), train,
-                                           (float)(1.0 / (n_train * (double)C)), M, row_loss);
+                                           (float)(1.0 / (n_train * (double)C)), M, row_loss, Mlo);
   count(L);
 }
 

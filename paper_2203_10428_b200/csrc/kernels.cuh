@@ -123,7 +123,8 @@ void gather_rows(Launch, const SegTable& src, const int32_t* row_map, int64_t n_
 // msg16: the message rows are bf16 (halo_payload = 1; 4 bf16 per float4 of the row, row stride ld).
 void grad_reduce(Launch, const int64_t* inv_ptr, const int32_t* inv_pos, const SegTable& msg,
                  const int32_t* row_map, float* ema, float gamma, int use_ema, int first, float* J,
-                 int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld, int msg16 = 0);
+                 int write_j, const float* Hprev, float* M, int64_t n_in, int64_t ld, int msg16 = 0,
+                 float* Mlo = nullptr);
 
 // bf16 exchange payloads (pgcn_config.halo_payload = 1).  Rows of ld bf16 (ld % 4 == 0).
 // pack:    dst[r] = bf16_rn(src[row_map ? row_map[r] : r])                     (S2 / S10 pack)
@@ -137,8 +138,9 @@ void spin_ns(cudaStream_t s, int64_t ns);
 // S5: CE (labels int32) or BCE (labels uint8 [n x C]) on rows with train[v] != 0 (train == nullptr:
 // every row is a train row).
 // M = J^(L) (zero outside the train set), row_loss[v] = loss term of v (already / n_train).
+// Mlo (optional; also grad_reduce): M's 3xTF32 lo term, x - trunc_tf32(x), for the GEMMs that read M.
 void loss_rows(Launch, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
-               const uint8_t* train, double n_train, float* M, float* row_loss);
+               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo = nullptr);
 // out[0] = sum of x[0..n) (single block, fixed order -> deterministic)
 void reduce_sum(Launch, const float* x, int64_t n, float* out);
 

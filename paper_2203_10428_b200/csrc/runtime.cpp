@@ -69,6 +69,7 @@ const DevKnobs& knobs() {
     k.tf_off = env_int("PGCN_TF_OFF", 0);
     k.spmm_l2mb = env_int("PGCN_SPMM_L2MB", 96);
     k.dw_merge = env_int("PGCN_DW_MERGE", 1);
+    k.presplit = env_int("PGCN_PRESPLIT", 0);
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
     if (k.dw_kmax < 0) k.dw_kmax = 128;
   });
