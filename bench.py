@@ -202,6 +202,49 @@ def build_workload(name, n_parts, model="sage"):
     return g, m, params0, time.time() - t0
 
 
+class RankGraph:
+    """The slice of a huge synthetic graph one rank materialises (papers100M-shaped multi-GPU runs): the
+    full CSR structure is generated (and partitioned) on every rank, but X, labels and the train mask only
+    for the rank's own rows (synth.graphs.rows_inputs, counter-based per row); n_train is the global count
+    (all-reduced)."""
+
+    def __init__(self, n, nnz, X, labels, train_mask, n_train):
+        self.n, self.nnz, self.X, self.labels, self.train_mask, self._n_train = n, nnz, X, labels, train_mask, n_train
+
+    @property
+    def n_train(self):
+        return self._n_train
+
+
+def build_rank_workload(name, parts, rank, dist, pgcn, model="sage", n=None, nnz=None):
+    """Per-rank workload of a huge config: structure + partition on every rank, inputs of the rank's rows
+    only.  Returns (RankGraph, model cfg, params0, partitioning, seconds).  Host memory per rank: the CSR
+    (7.3 GB at papers100M) + the partition arrays + this rank's X rows."""
+    import dataclasses
+
+    import numpy as np
+    from synth.graphs import CONFIGS, gen_structure, glorot_params, model_for, rows_inputs
+    t0 = time.time()
+    row_ptr, col = gen_structure(name, seed=1, n=n, nnz=nnz)
+    n, nnz = len(row_ptr) - 1, int(row_ptr[-1])
+    part = pgcn.partition(n, row_ptr, col, parts)
+    del row_ptr, col
+    gid = part.view(rank)["inner_gid"]
+    X, lab, tm = rows_inputs(name, gid, n=n)
+    cnt = np.array([int(tm.sum())], dtype=np.int64)
+    if dist is not None:
+        import torch
+        tt = torch.from_numpy(cnt).to("cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt)
+        cnt = tt.cpu().numpy()
+    m = dataclasses.replace(model_for(name), model=model)
+    params0 = glorot_params(m.widths, 3, model=model)
+    return RankGraph(n, nnz, X, lab, tm, int(cnt[0])), m, params0, part, time.time() - t0
+
+
+SHARDED_N = 50_000_000  # configs above this many nodes build per-rank inputs (build_rank_workload)
+
+
 def cpu_baseline(name, parts, mode, smooth, sample_n=16000, iters=2, model="sage"):
     """The oracle (oracle/, numpy/scipy fp64) as it stands, on a bounded sample of the same workload:
     the same generator recipe, degree, widths, dropout and partition count at N = sample_n, timed
@@ -371,10 +414,16 @@ def main():
     parts = args.parts or (max(2, args.gpus) if world == 1 else world)
     if world > 1 and parts != world:
         raise SystemExit("multi-GPU runs host one partition per rank (--parts must equal WORLD_SIZE)")
-    g, m, params0, t_gen = build_workload(args.config, parts, args.model)
-    t0 = time.time()
-    part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
-    t_part = time.time() - t0
+    from synth.graphs import CONFIGS
+    sharded = world > 1 and CONFIGS[args.config]["n"] > SHARDED_N
+    if sharded:  # papers100M-shaped: every rank materialises only its own rows' inputs
+        g, m, params0, part, t_gen = build_rank_workload(args.config, parts, rank, dist, pgcn, args.model)
+        t_part = 0.0
+    else:
+        g, m, params0, t_gen = build_workload(args.config, parts, args.model)
+        t0 = time.time()
+        part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
+        t_part = time.time() - t0
     transport = args.transport if world == 1 else "nccl"
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
@@ -385,18 +434,31 @@ def main():
                            halo_payload=args.halo_payload, lean=args.lean)
     local_parts = list(range(parts)) if world == 1 else [rank]
     transport_note = None
-    if transport in ("loopback", "push"):
-        # the posted exchange's message buffers must fit next to the activations; otherwise the local
-        # transport (no message buffers) hosts the partitions and the line says so
+    # Fit the workspace to this GPU: the posted exchange's message buffers must fit next to the activations,
+    # else the local transport (no message buffers) hosts the partitions; a layout that still does not fit
+    # runs in the lean-memory mode (N1(iii): same results, needs a posted transport -- NCCL, or loopback on
+    # one GPU).  The line says which (config.transport_note).
+    def fits(c):
+        return pgcn.workspace_bytes(part, c, local_parts) <= torch.cuda.mem_get_info()[0] - (2 << 30)
+    if not fits(cfg):
         need = pgcn.workspace_bytes(part, cfg, local_parts)
-        free = torch.cuda.mem_get_info()[0]
-        if need > free - (2 << 30) and args.lean:
-            raise SystemExit("bench: lean %s needs %.1f GB of workspace, %.1f GB free" % (transport, need / 1e9, free / 1e9))
-        if need > free - (2 << 30):
+        if args.lean:
+            raise SystemExit("bench: lean layout needs %.1f GB of workspace, %.1f GB free" % (
+                need / 1e9, torch.cuda.mem_get_info()[0] / 1e9))
+        if transport in ("loopback", "push"):
             cfg.transport = 0
-            transport_note = "%s needs %.1f GB of workspace, %.1f GB free: local transport" % (
-                transport, need / 1e9, free / 1e9)
-            transport = "local"
+            if fits(cfg):
+                transport_note = "%s needs %.1f GB of workspace: local transport" % (transport, need / 1e9)
+                transport = "local"
+            else:
+                cfg.transport = 1 if transport == "loopback" else 2
+        if transport != "local":
+            cfg.lean = 1
+            if not fits(cfg):
+                raise SystemExit("bench: even the lean layout needs %.1f GB of workspace" % (
+                    pgcn.workspace_bytes(part, cfg, local_parts) / 1e9))
+            args.lean = True
+            transport_note = "default layout needs %.1f GB of workspace: lean-memory mode" % (need / 1e9)
     stream = torch.cuda.Stream()
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
     with torch.cuda.stream(stream):
@@ -405,9 +467,12 @@ def main():
     host = []
     for i, v in enumerate(views):
         gid = v["inner_gid"]
-        X = torch.from_numpy(np.ascontiguousarray(g.X[gid])).pin_memory()
-        lab = torch.from_numpy(np.ascontiguousarray(g.labels[gid])).pin_memory()
-        tm = torch.from_numpy(np.ascontiguousarray(g.train_mask[gid])).pin_memory()
+        if sharded:  # the rank's rows, already in V_i order
+            X, lab, tm = (torch.from_numpy(a).pin_memory() for a in (g.X, g.labels, g.train_mask))
+        else:
+            X = torch.from_numpy(np.ascontiguousarray(g.X[gid])).pin_memory()
+            lab = torch.from_numpy(np.ascontiguousarray(g.labels[gid])).pin_memory()
+            tm = torch.from_numpy(np.ascontiguousarray(g.train_mask[gid])).pin_memory()
         host.append((X, lab, tm))
     nloc = len(local_parts)
     for i in range(nloc):  # one partition at a time: the device staging copy is freed right after
@@ -573,7 +638,7 @@ def main():
                       "l2": "inputs larger than L2 (X %.0f MB, CSR %.0f MB)" % (g.X.nbytes / 1e6, g.nnz * 8 / 1e6)},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
            "comm": comm_info, "comm_bench": comm_bench, "step_ms": [round(x, 3) for x in step_ms], "breakdown": breakdown, "ms_per_step_instrumented": ms_instr, "loss": loss_v,
-           "setup_s": {"generate": t_gen, "partition": t_part},
+           "setup_s": {"generate": t_gen, "partition": t_part, "per_rank_inputs": sharded},
            "workspace_GB": ctx.ws.numel() / 1e9}
     print(json.dumps(out))
 

@@ -140,12 +140,12 @@ class Partitioning:
     """pgcn_partition (Alg. 1 l.1-5) over a CSR graph."""
 
     def __init__(self, n, row_ptr, col_idx, n_parts, part_of=None, n_threads=0):
-        self._row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
-        self._col = np.ascontiguousarray(col_idx, dtype=np.int32)
-        self._part_of = None if part_of is None else np.ascontiguousarray(part_of, dtype=np.int32)
+        # the CSR is borrowed for the duration of the call only (the handle owns copies of what it needs)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(col_idx, dtype=np.int32)
+        po = None if part_of is None else np.ascontiguousarray(part_of, dtype=np.int32)
         h = C.c_void_p()
-        _check(lib().pgcn_partition(int(n), _ptr(self._row_ptr), _ptr(self._col), int(n_parts),
-                                    _ptr(self._part_of), int(n_threads), C.byref(h)))
+        _check(lib().pgcn_partition(int(n), _ptr(rp), _ptr(col), int(n_parts), _ptr(po), int(n_threads), C.byref(h)))
         self.handle = h
         self.n = int(n)
         self.n_parts = int(n_parts)

@@ -130,6 +130,34 @@ int64_t synth_edges(int64_t n, int32_t n_comm, double stubs_mean, double scale, 
   return nnz;
 }
 
+// Per-row inputs for huge graphs (papers100M-shaped), generated only for the rows a rank owns: every value
+// is a counter-based hash of (seed, stream, gid, column), so any subset of rows is reproducible on its own
+// (synth/graphs.py rows_inputs).  Same distributions as gen_graph's numpy draws: X = N(0,1) + 1 at column
+// (community mod f0); label = community mod classes w.p. 0.8 else uniform; train = U(0,1) < train_frac.
+void synth_rows(uint64_t seed, int64_t n, int32_t n_comm, int32_t f0, int32_t classes, double train_frac,
+                const int64_t* gids, int64_t m, int32_t n_threads, float* X, int32_t* labels, uint8_t* train) {
+  int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  const int64_t csize = std::max<int64_t>(n / n_comm, 1);
+  parallel_for(m, nt, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t r = lo; r < hi; ++r) {
+      const uint64_t g = (uint64_t)gids[r];
+      const int64_t c = std::min<int64_t>((int64_t)g / csize, n_comm - 1);
+      float* x = X + r * f0;
+      for (int32_t j = 0; j < f0; j += 2) {  // Box-Muller pairs
+        const uint64_t k = g * (uint64_t)(f0 + 1) + (uint64_t)j;
+        const double u1 = u01(h3(seed, 11, k)), u2 = u01(h3(seed, 12, k));
+        const double rad = std::sqrt(-2.0 * std::log(1.0 - u1)), th = 6.283185307179586 * u2;
+        x[j] = (float)(rad * std::cos(th));
+        if (j + 1 < f0) x[j + 1] = (float)(rad * std::sin(th));
+      }
+      x[c % f0] += 1.0f;
+      const bool keep = u01(h3(seed, 13, g)) < 0.8;
+      labels[r] = keep ? (int32_t)(c % classes) : (int32_t)(h3(seed, 14, g) % (uint64_t)classes);
+      train[r] = u01(h3(seed, 15, g)) < train_frac ? 1 : 0;
+    }
+  });
+}
+
 void synth_free(void* p) { std::free(p); }
 
 }  // extern "C"

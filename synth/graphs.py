@@ -127,6 +127,10 @@ def _lib():
                                     ctypes.c_double, ctypes.c_uint64, ctypes.c_int32,
                                     ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
         lib.synth_free.argtypes = [ctypes.c_void_p]
+        lib.synth_rows.restype = None
+        lib.synth_rows.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.c_double, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _LIB = lib
     return _LIB
 
@@ -145,6 +149,51 @@ def _draw_edges(n, n_comm, stubs_mean, scale, cross, seed):
         ctypes.memmove(col.ctypes.data, colp.value, 4 * nnz)
     lib.synth_free(colp)
     return row_ptr, col
+
+
+def gen_structure(name: str, seed: int = 1, n: Optional[int] = None, nnz: Optional[int] = None,
+                  comm: Optional[int] = None, cross: float = 0.10):
+    """The CSR structure of gen_graph(name, ...) alone (same edge draw and nnz refit, no inputs):
+    (row_ptr int64 [n+1], col_idx int32 [nnz])."""
+    c = dict(CONFIGS[name])
+    n = c["n"] if n is None else n
+    nnz_t = c["nnz"] if nnz is None else nnz
+    n_comm = min(c["comm"] if comm is None else comm, n)
+    stubs_mean = nnz_t / (2.0 * n)
+    scale = 1.0
+    for _ in range(6):
+        row_ptr, col = _draw_edges(n, n_comm, stubs_mean, scale, cross, seed)
+        got = int(row_ptr[-1])
+        if got == 0 or abs(got - nnz_t) <= 0.01 * nnz_t:
+            break
+        scale *= nnz_t / got
+    return row_ptr, col
+
+
+def rows_inputs(name: str, gids, seed: int = 1, n: Optional[int] = None, f0: Optional[int] = None,
+                classes: Optional[int] = None, comm: Optional[int] = None):
+    """Inputs of the rows `gids` only, for graphs too large to materialise X on every rank (the
+    papers100M-shaped multi-GPU run: each rank builds its own partition's rows).  Counter-based per row
+    (synth_rows in gen.cpp): any subset of rows is reproducible on its own.  Same distributions as
+    gen_graph's single-label recipe (X ~ N(0,1) + 1 at column (community mod F), label = community mod C
+    w.p. 0.8, train ~ U(0,1) < train_frac), different random values.  Returns (X float32 [m, f0],
+    labels int32 [m], train_mask uint8 [m])."""
+    import ctypes
+    c = dict(CONFIGS[name])
+    if c["multilabel"]:
+        raise ValueError("rows_inputs: single-label configs only")
+    n = c["n"] if n is None else n
+    f0 = c["f0"] if f0 is None else f0
+    classes = c["classes"] if classes is None else classes
+    n_comm = min(c["comm"] if comm is None else comm, n)
+    gids = np.ascontiguousarray(gids, dtype=np.int64)
+    m = len(gids)
+    X = np.empty((m, f0), dtype=np.float32)
+    lab = np.empty(m, dtype=np.int32)
+    tm = np.empty(m, dtype=np.uint8)
+    _lib().synth_rows(ctypes.c_uint64(seed * 1000003 + 2), n, n_comm, f0, classes, float(c["train"]),
+                      gids.ctypes.data, m, 0, X.ctypes.data, lab.ctypes.data, tm.ctypes.data)
+    return X, lab, tm
 
 
 def gen_graph(name: str, seed: int = 1, n: Optional[int] = None, nnz: Optional[int] = None,

@@ -97,3 +97,51 @@ def test_two_process_index_round_trip(world):
         assert ok_id
         assert mx == 10.0 * world
         assert n_send > 0 and n_halo > 0
+
+
+def _rank_workload_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_10428_b200 import pgcn
+        from synth.graphs import rows_inputs
+        import bench
+        g, m, params0, part, _ = bench.build_rank_workload("papers", world, rank, dist, pgcn, n=20000, nnz=180000)
+        gid = part.view(rank)["inner_gid"]
+        # the rank's rows are the rows of any larger request (per-row counter-based inputs)
+        lo = max(int(gid[0]) - 100, 0)
+        Xs, ls, ts = rows_inputs("papers", np.arange(lo, int(gid[-1]) + 1), n=g.n)
+        ok_rows = (np.array_equal(g.X, Xs[gid - lo]) and np.array_equal(g.labels, ls[gid - lo]) and
+                   np.array_equal(g.train_mask, ts[gid - lo]))
+        q.put((rank, gid.tolist(), int(g.train_mask.sum()), g.n_train, ok_rows, m.widths, g.n))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_sharded_workload():
+    """papers100M-shaped multi-GPU runs build per-rank inputs (bench.build_rank_workload): the ranks'
+    rows partition the node set, each rank's X / labels / train mask rows equal the per-row generator's
+    rows of any request containing them, and n_train_global is the all-reduced train count."""
+    from paper_2203_10428_b200 import build
+    build.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_workload_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = res[0][6]
+    allg = sorted(x for r in res for x in r[1])
+    assert allg == list(range(n))
+    total = sum(r[2] for r in res)
+    assert total > 0 and all(r[3] == total for r in res)
+    assert all(r[4] for r in res)
+    assert res[0][5] == [128, 48, 48, 172]
