@@ -28,6 +28,7 @@ struct DevKnobs {
   int spmm_l2mb = 96;
   int dw_merge = 1;
   int presplit = 0;
+  int spmm_nch = 2;  // column chunks of an L2-chunked gather (PGCN_SPMM_NCH)
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

@@ -1277,7 +1277,7 @@ SpmmShape spmm16_shape(int64_t ld8) {
 SpmmShape chunked(SpmmShape (*shape)(int64_t), int64_t w, double table_bytes) {
   const double budget = (double)knobs().spmm_l2mb * 1048576.0;
   if (budget <= 0.0 || table_bytes <= budget || table_bytes > 3.0 * budget) return shape(w);
-  const int64_t nch = 2;
+  const int64_t nch = knobs().spmm_nch;  // (dev knob PGCN_SPMM_NCH, default 2)
   int64_t cw = (w + nch - 1) / nch;
   cw = (cw + 3) / 4 * 4;  // chunk width in vectors: a multiple of 4 (whole 64-byte fp32 / bf16 segments)
   if (cw >= w) return shape(w);

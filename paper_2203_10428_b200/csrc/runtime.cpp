@@ -70,6 +70,8 @@ const DevKnobs& knobs() {
     k.spmm_l2mb = env_int("PGCN_SPMM_L2MB", 96);
     k.dw_merge = env_int("PGCN_DW_MERGE", 1);
     k.presplit = env_int("PGCN_PRESPLIT", 0);
+    k.spmm_nch = env_int("PGCN_SPMM_NCH", 2);
+    if (k.spmm_nch < 2 || k.spmm_nch > 8) k.spmm_nch = 2;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
     if (k.dw_kmax < 0) k.dw_kmax = 128;
   });

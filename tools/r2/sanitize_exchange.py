@@ -1,6 +1,7 @@
 """compute-sanitizer driver for the posted exchange (LOOPBACK transport): 3 partitions, PIPE-GF at
 depth 1 and 2, VANILLA, fp32 and bf16 payloads, tile aggregation on a dense-community graph, the delay
-hook, and the streaming input re-upload (pgcn_stage_inputs), 4 iterations each."""
+hook, the streaming input re-upload (pgcn_stage_inputs), the PUSH transport and the lean-memory mode
+(one J / message slot guarded by waits), 4 iterations each."""
 import os
 import sys
 
@@ -14,7 +15,9 @@ RUNS = [dict(mode="pipe", smooth_f=True, smooth_g=True, depth=1), dict(mode="pip
         dict(mode="vanilla"), dict(mode="pipe", smooth_g=True, halo_payload="bf16"),
         dict(mode="vanilla", halo_payload="bf16"), dict(mode="pipe", spmm_tiles=True, tile_min=8, hook=1),
         dict(mode="pipe", smooth_f=True, smooth_g=True, transport="push"), dict(mode="vanilla", transport="push"),
-        dict(mode="pipe", depth=2, model="gcn", transport="push")]
+        dict(mode="pipe", depth=2, model="gcn", transport="push"),
+        dict(mode="pipe", smooth_f=True, smooth_g=True, lean=True, train_sparse=True),
+        dict(mode="pipe", depth=2, lean=True, hook=1), dict(mode="vanilla", lean=True, transport="push")]
 for kw in RUNS:
     hook = kw.pop("hook", 0)
     dense = "tile_min" in kw
