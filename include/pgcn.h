@@ -385,8 +385,14 @@ int64_t pgcn_launch_count(const pgcn_ctx* ctx);
 enum {
   PGCN_K_SPMM_FWD = 0, PGCN_K_SPMM_BWD = 1, PGCN_K_GEMM_FWD = 2, PGCN_K_GEMM_DW = 3, PGCN_K_GEMM_DA = 4,
   PGCN_K_DROPOUT = 5, PGCN_K_GATHER = 6, PGCN_K_GRAD_REDUCE = 7, PGCN_K_LOSS = 8, PGCN_K_UPDATE = 9,
-  PGCN_K_COUNT = 10
+  PGCN_K_SPMM_TILE_FWD = 10, PGCN_K_SPMM_TILE_BWD = 11,
+  PGCN_K_COUNT = 12
 };
+/* PGCN_K_SPMM_TILE_FWD / _BWD are sub-intervals of PGCN_K_SPMM_FWD / _BWD: the tensor-core tile part of an
+ * aggregation launch on the tile path (bf16 split of the table + k_spmm_tc), charged with the MMA flops it
+ * executes (2 x 128 x 64 x round_up(width, 64) per heavy tile and table: the 0/1 tile times the table's
+ * 64 rows, zeros included) and the bytes its TMA loads (64 table rows per tile and table + the 1 KB mask).
+ * The rest of the SPMM interval is the gather kernel (light edges and the epilogue).                */
 int pgcn_timing_enable(pgcn_ctx* ctx, int32_t on); /* also resets the accumulators */
 int pgcn_timing_read(pgcn_ctx* ctx, int32_t kind, double* ms, int64_t* launches, double* alg_bytes,
                      double* alg_flops);

@@ -188,7 +188,7 @@ struct pgcn_ctx {
   ncclComm_t ch = nullptr, cr = nullptr;  // halo exchange / weight-gradient all-reduce
 #endif
   cudaStream_t cs = nullptr;              // comm stream (high priority)
-  pgcn::Launch launch() { return pgcn::Launch{s, &launches}; }
+  pgcn::Launch launch();
   cudaEvent_t ev_f_pack[PGCN_MAX_LAYERS + 1] = {}, ev_b_ready[PGCN_MAX_LAYERS + 1] = {};
   cudaEvent_t ev_f_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {}, ev_b_done[PGCN_MAX_LAYERS + 1][pgcn::kMaxBuf] = {};
   int nb = 2;                                              // buffers in rotation = depth + 1
@@ -218,6 +218,29 @@ struct pgcn_ctx {
 
 namespace pgcn {
 namespace {
+
+// Launch::mark of a timed context: the tile part of an aggregation launch as its own timing kind
+void tile_mark(void* mctx, int kind, int begin, double flops, double bytes) {
+  pgcn_ctx* C = static_cast<pgcn_ctx*>(mctx);
+  KTimer& t = C->kt[kind];
+  if (begin) {
+    if (t.used + 2 > t.ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      t.ev.push_back(a);
+      t.ev.push_back(b);
+    }
+    cudaEventRecord(t.ev[t.used], C->s);
+    t.n += 1;
+    t.flops += flops;
+    t.bytes += bytes;
+    t.gbytes += bytes;
+  } else {
+    cudaEventRecord(t.ev[t.used + 1], C->s);
+    t.used += 2;
+  }
+}
 
 int validate_cfg(const pgcn_config* c) {
   if (!c) return fail(PGCN_EINVAL, "config is NULL");
@@ -850,6 +873,15 @@ int post_bwd(pgcn_ctx* C, int64_t t, int l, const Launch& Lk, bool* have) {
 }  // namespace pgcn
 
 using namespace pgcn;
+
+pgcn::Launch pgcn_ctx::launch() {
+  pgcn::Launch L{s, &launches};
+  if (timing) {
+    L.mark = tile_mark;
+    L.mctx = this;
+  }
+  return L;
+}
 
 extern "C" int64_t pgcn_param_count(const pgcn_config* cfg) { return cfg ? param_count(cfg) : -1; }
 

@@ -1311,6 +1311,22 @@ void dropout_fwd(Launch L, const float* H, float* D, int64_t ld, int64_t n_rows,
   count(L);
 }
 
+// Sub-interval timing of the tile part (Launch::mark): executed MMA flops (0/1 tile x 64 table rows per
+// heavy tile, every table, columns rounded to whole 64-column atoms) and TMA bytes (64 rows per tile and
+// table + the 1 KB bitmask).
+struct TileMark {
+  const Launch& L;
+  int kind;
+  TileMark(const Launch& l, int k, const TileDev& T, int64_t width, bool b16) : L(l), kind(k) {
+    if (!L.mark) return;
+    const double nt = b16 ? 1.0 : 2.0, cols = (double)((width + 63) / 64 * 64), tiles = (double)T.n_tiles;
+    L.mark(L.mctx, kind, 1, 2.0 * 128.0 * 64.0 * cols * nt * tiles, tiles * (64.0 * cols * 2.0 * nt + 1024.0));
+  }
+  ~TileMark() {
+    if (L.mark) L.mark(L.mctx, kind, 0, 0.0, 0.0);
+  }
+};
+
 // Tile path (tiles != nullptr, every neighbour row valid): the heavy tiles go to the tensor cores
 // (spmm_tc, writing the tile sums into the output rows) and the gather kernel then walks the light
 // edges on top of them (addend) and applies the epilogue.  (Running the light gather concurrently
@@ -1384,6 +1400,7 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
   if (!tcu) return gather(L.s, work, self, 0);
   auto tile = [&](float* out) -> int {
     int rc;
+    TileMark tm(L, PGCN_K_SPMM_TILE_FWD, *tiles, ld, b16);
     if (b16) {
       rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_valid, ld8 * 8, out, ld, ld);
     } else {  // fp32 tier: bf16 hi/lo split of the table, then the tile sums (2 MMAs per k-step)
@@ -1457,6 +1474,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
   if (!tcu) return gather(L.s, work, dDs, 0);
   auto tile = [&](float* out) -> int {
     int rc;
+    TileMark tm(L, PGCN_K_SPMM_TILE_BWD, *tiles, ld, b16);
     if (b16) {
       rc = spmm_tc(L, *tiles, G16, nullptr, ld8 * 8, n_in, ld8 * 8, out, ld, ld);
     } else {  // fp32 tier: bf16 hi/lo split of dZs, then the tile sums

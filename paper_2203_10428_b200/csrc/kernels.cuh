@@ -31,6 +31,10 @@ struct DropSpec {
 struct Launch {
   cudaStream_t s;
   int64_t* count;
+  // optional sub-interval timing (engine, pgcn_timing_*): mark(mctx, kind, begin, flops, bytes) brackets the
+  // tensor-core tile part of an aggregation launch (kind PGCN_K_SPMM_TILE_FWD / _BWD)
+  void (*mark)(void* mctx, int kind, int begin, double flops, double bytes) = nullptr;
+  void* mctx = nullptr;
 };
 
 // Device copy of a dense-tile decomposition (tiles.h) of an SpMM pattern.

@@ -23,7 +23,7 @@ OK, EINVAL, ESTATE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, 
 T_H, T_HIN, T_Z, T_J, T_G = 0, 1, 2, 3, 4
 XH_SKIP_F_WAIT, XH_SKIP_B_WAIT, XH_NOCOMM = 1, 2, 4  # pgcn_dev_exchange_hook flags (include/pgcn_dev.h)
 KERNELS = ["spmm_fwd", "spmm_bwd", "gemm_fwd", "gemm_dw", "gemm_da", "dropout", "gather", "grad_reduce", "loss",
-           "update"]
+           "update", "spmm_tile_fwd", "spmm_tile_bwd"]
 
 
 class PgcnError(RuntimeError):
