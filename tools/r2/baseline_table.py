@@ -17,18 +17,21 @@ ROWS = [
     ("reddit_gcn", "Reddit-shaped, GCN-sym (N3)", "fp32", "PIPE / loopback"),
     ("reddit_bf16gather", "Reddit-shaped", "bf16 gather", "PIPE / loopback"),
     ("reddit_bf16all", "Reddit-shaped", "bf16 gather + bf16 GEMM", "PIPE / loopback"),
+    ("reddit_lean", "Reddit-shaped, lean-memory mode (N1(iii))", "fp32", "PIPE / loopback"),
     ("products_pipe", "products-shaped (2.45M, 61.8M nnz, 100-128-128-47)", "fp32", "PIPE / loopback"),
     ("products_bf16gather", "products-shaped", "bf16 gather", "PIPE / loopback"),
     ("yelp_pipe_gf", "Yelp-shaped (717K, 7.0M nnz, 300-512×3-100, BCE)", "fp32", "PIPE-GF / loopback"),
     ("yelp_bf16all_gf", "Yelp-shaped", "bf16 gather + bf16 GEMM", "PIPE-GF / loopback"),
     ("papers_q", "papers-q (papers100M recipe at ¼: 27.8M, 404M nnz, 128-48-48-172)", "fp32", "PIPE / %s"),
+    ("papers_q_lean", "papers-q, lean-memory mode (N1(iii))", "fp32", "PIPE / %s"),
     ("cora_pipe", "Cora-shaped (2.7K, 10.6K nnz, 1433-16-7)", "fp32", "PIPE / loopback"),
 ]
 
 
 def main():
     src = sys.argv[1]
-    out = ["| config | tier | mode / transport | ep/s | ms/epoch | top kernel (ms/step) | roofline frac | exposed comm ms | e2e ep/s |",
+    out = ["| config | tier | mode / transport | ep/s | ms/epoch | dominant kernel (ms/step): roofline frac | "
+           "aggregation: B_min/HBM frac | exposed comm ms | e2e ep/s |",
            "|---|---|---|---|---|---|---|---|---|"]
     for name, cfg, tier, mode in ROWS:
         p = os.path.join(src, name + ".json")
@@ -38,14 +41,15 @@ def main():
             d = json.loads(open(p).read().strip().splitlines()[-1])
         except Exception:
             continue
-        b = d["breakdown"]
-        top = max(b.items(), key=lambda kv: kv[1]["ms_per_step"])
         exp = d["comm"] and d["comm"].get("exposed_ms_per_step")
         r = d["roofline"]
+        ra = d.get("roofline_aggregation")
+        ms_k = d["kernels"][r["kernel"]]["ms_per_step"] if "kernels" in d else d["breakdown"][r["kernel"]]["ms_per_step"]
         if "%s" in mode:
             mode = mode % d["config"].get("transport")
-        out.append("| %s | %s | %s | %.2f | %.2f | %s (%.2f) | %s %.3f | %s | %s |" % (
-            cfg, tier, mode, d["value"], d["ms_per_step"], top[0], top[1]["ms_per_step"], r["bound"], r["frac"],
+        out.append("| %s | %s | %s | %.2f | %.2f | %s (%.2f): %s %.3f | %s | %s | %s |" % (
+            cfg, tier, mode, d["value"], d["ms_per_step"], r["kernel"], ms_k, r["bound"], r["frac"],
+            ("%.3f" % ra["frac"]) if ra else "—",
             ("%.2f" % exp) if exp is not None else "—", ("%.2f" % d["e2e"]["value"]) if d.get("e2e") else "—"))
     ref = os.path.join(src, "reference_reddit.json")
     if os.path.exists(ref):
