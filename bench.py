@@ -395,14 +395,27 @@ def kernel_roofline(name, kd, pk, args, kern, l2p):
     n = max(kd["launches"], 1)
     sec = kd["ms"] / 1e3 / n
     if name == "k_umma_gemm":
+        # the binding roof at these GEMMs' arithmetic intensity (narrow layers sit below the
+        # ridge): tensor if AI x HBM >= the dtype's tensor peak, else HBM with the algorithmic operand bytes
         mult = 1.0 if args.gemm == "bf16" else 3.0
         peak = pk["bf16_tflops"] * (1.0 if args.gemm == "bf16" else 0.5)
         ach = mult * kd["flops"] / n / sec / 1e12
-        return {"kernel": name, "launches_timed": kd["launches"], "ms_per_launch": kd["ms"] / n, "bound": "tensor",
-                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops%s" % ("" if args.gemm == "bf16" else " x 1/2 (tf32)"),
-                "traffic": None, "flops_per_launch": kd["flops"] / n, "tensor_flop_multiplier": mult,
-                "note": "all node-update GEMM launches (fwd, dW, dA); fp32 products x 2 x the tensor MMAs per product"}
+        ai = mult * kd["flops"] / kd["bytes"] if kd["bytes"] > 0 else float("inf")
+        common = {"kernel": name, "launches_timed": kd["launches"], "ms_per_launch": kd["ms"] / n, "traffic": None,
+                  "flops_per_launch": kd["flops"] / n, "bytes_per_launch": kd["bytes"] / n,
+                  "tensor_flop_multiplier": mult, "ai_flop_per_byte": ai,
+                  "ridge_flop_per_byte": peak * 1e12 / (pk["hbm_gbs"] * 1e9),
+                  "tensor": {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                             "peak_source": "MEASURED_PEAKS.json bf16_tflops%s" % (
+                                 "" if args.gemm == "bf16" else " x 1/2 (tf32)")},
+                  "note": "all node-update GEMM launches (fwd, dW, dA); flops = fp32 products x 2 x the tensor MMAs "
+                          "per product; bytes = operand reads + output writes (algorithmic)"}
+        if ai * pk["hbm_gbs"] * 1e9 >= peak * 1e12:
+            return dict(common, bound="tensor", achieved=ach, peak=peak, unit="TFLOP/s", frac=ach / peak,
+                        peak_source=common["tensor"]["peak_source"])
+        gbs = kd["bytes"] / n / sec / 1e9
+        return dict(common, bound="hbm", achieved=gbs, peak=pk["hbm_gbs"], unit="GB/s", frac=gbs / pk["hbm_gbs"],
+                    peak_source="MEASURED_PEAKS.json hbm_gbs (AI below the tensor ridge)")
     if name == "k_spmm_tc":
         peak = pk["bf16_tflops"]
         ach = kd["flops"] / n / sec / 1e12
