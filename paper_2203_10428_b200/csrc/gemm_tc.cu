@@ -63,14 +63,15 @@ struct Geo {
 // stage: the MMA still reads 128 (its last atoms overlap the next buffer of the stage) but those TMEM
 // lanes are output rows >= F, never stored.  Smaller stages -> more of them in flight (the narrow dW of
 // papers-shaped layers, 48 x 48, is latency-bound on bytes in flight).
-__host__ __device__ inline Geo geometry(int bf, int mode, int BN, int afeat = BM) {
+__host__ __device__ inline Geo geometry(int bf, int mode, int BN, int afeat = BM, int kbw = BK) {
   Geo g;
   if (!bf) {
     const int af = mode == TC_DW ? afeat : BM;
-    g.a_raw = (uint32_t)af * BK * 4;
-    g.a_cvt = (uint32_t)af * BK * 4;
-    g.b_raw = (uint32_t)BN * BK * 4;
-    g.b_cvt = (uint32_t)BN * BK * 4;
+    const int kw = (mode == TC_DW || kbw <= 0) ? BK : kbw;
+    g.a_raw = (uint32_t)af * kw * 4;
+    g.a_cvt = (uint32_t)af * kw * 4;
+    g.b_raw = (uint32_t)BN * kw * 4;
+    g.b_cvt = (uint32_t)BN * kw * 4;
   } else if (mode == TC_DW) {
     g.a_raw = (uint32_t)afeat * 32 * 4;                // afeat features x 32 rows fp32
     g.a_cvt = (uint32_t)((afeat + 63) / 64) * 64 * 32 * 2;  // bf16 MN-major, 64-feature atoms
@@ -136,7 +137,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  const Geo geo = geometry(BF, p.mode, p.BN, p.a_feat);
+  const Geo geo = geometry(BF, p.mode, p.BN, p.a_feat, p.kbw);
+  const int kw = p.kbw > 0 ? p.kbw : BK;  // tf32 FWD / DA k-block width (fp32 elements)
   const uint32_t a_bytes = geo.a_raw;
   const uint32_t b_bytes = geo.b_raw;
   const uint32_t stage_bytes = geo.stage();
@@ -221,16 +223,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           } else if (p.mode == TC_FWD) {
             const int seg = kb < p.kb_seg[0] ? 0 : 1;
             const int kl = kb - (seg ? p.kb_seg[0] : 0);
-            tma_load_2d(A, &p.map_a[seg], &full[s], kl * BK, T.m0);
-            const int kcol = (p.kb_off_b[seg] + kl) * BK;
+            tma_load_2d(A, &p.map_a[seg], &full[s], kl * kw, T.m0);
+            const int kcol = p.kb_off_b[seg] * BK + kl * kw;  // (kb_off_b in 32-element units)
             tma_load_2d(B, &p.map_b[0], &full[s], kcol, T.n0);
             tma_load_2d(Blo, &p.map_b_lo, &full[s], kcol, T.n0);
           } else {  // TC_DA
-            tma_load_2d(A, &p.map_a[0], &full[s], kb * BK, T.m0);
-            if (pa) tma_load_2d(A + a_bytes, &p.map_lo[0], &full[s], kb * BK, T.m0);
+            tma_load_2d(A, &p.map_a[0], &full[s], kb * kw, T.m0);
+            if (pa) tma_load_2d(A + a_bytes, &p.map_lo[0], &full[s], kb * kw, T.m0);
             const int brow = T.half * p.F + T.n0;
-            tma_load_2d(B, &p.map_b[0], &full[s], kb * BK, brow);
-            tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * BK, brow);
+            tma_load_2d(B, &p.map_b[0], &full[s], kb * kw, brow);
+            tma_load_2d(Blo, &p.map_b_lo, &full[s], kb * kw, brow);
           }
           }
           if (++s == S) { s = 0; ph ^= 1; }
@@ -280,6 +282,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             continue;
           }
           const uint32_t Alo = A + a_bytes, B = A + 2 * a_bytes, Blo = B + b_bytes;
+          if (p.mode != TC_DW && kw == 16) {  // K-major SW64: 64-byte rows, 8-row groups 512 B apart, 2 k-steps
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint64_t ah = make_desc(A + kk * 32, 16, 512, 4), al = make_desc(Alo + kk * 32, 16, 512, 4);
+              const uint64_t bh = make_desc(B + kk * 32, 16, 512, 4), bl = make_desc(Blo + kk * 32, 16, 512, 4);
+              mma_tf32(d, ah, bh, idesc, accum);
+              mma_tf32(d, ah, bl, idesc, 1u);
+              mma_tf32(d, al, bh, idesc, 1u);
+              accum = 1u;
+            }
+            tc_commit(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             uint64_t ah, al, bh, bl;
@@ -667,7 +683,8 @@ EncodeFn encode_fn() {
 }
 }  // namespace
 
-// swz: 0 none, 1 128B (K-major UMMA operands), 2 128B_ATOM_32B (tf32 MN-major operands).
+// swz: 0 none, 1 128B (K-major UMMA operands), 2 128B_ATOM_32B (tf32 MN-major operands), 3 64B (K-major
+// tf32 operands in 16-element k-blocks).
 static bool tc_map(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int64_t rows, int64_t ld, int box_cols,
                    int box_rows, int swz) {
   EncodeFn f = encode_fn();
@@ -678,7 +695,8 @@ static bool tc_map(CUtensorMap* m, const void* base, bool bf16, int64_t cols, in
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   const CUtensorMapSwizzle sw = swz == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE
-                                         : (swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+                                         : (swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                     : (swz == 3 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   return f(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -696,15 +714,15 @@ bool tc_map_table(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int
   return tc_map(m, base, bf16, cols, rows, ld, box_cols, box_rows, bf16 ? 1 : 2);
 }
 
-int tc_stages(int BN, int bf, int mode, int afeat) {
-  const int stage = (int)tc::geometry(bf, mode, BN, afeat).stage();
+int tc_stages(int BN, int bf, int mode, int afeat, int kbw) {
+  const int stage = (int)tc::geometry(bf, mode, BN, afeat, kbw).stage();
   int S = (200 * 1024) / stage;
   const int cap = mode == TC_DW ? 8 : 4;  // dW: stream of 32-row k-blocks, latency-bound on bytes in flight
   return S > cap ? cap : (S < 2 ? 2 : S);
 }
 
-size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat) {
-  const size_t stage = tc::geometry(bf, mode, BN, afeat).stage();
+size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat, int kbw) {
+  const size_t stage = tc::geometry(bf, mode, BN, afeat, kbw).stage();
   return 1024 + S * stage + (3 * S + 4) * 8 + 16;
 }
 
@@ -740,14 +758,14 @@ cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   int ctas = 1;
   // (the PUSH instantiation needs > 85 registers per thread: one CTA of 384 threads per SM)
   if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW && !p.push.mode) {  // dW: split-K plan sized for 148 CTAs
-    const size_t stage = tc::geometry(p.bf, p.mode, p.BN, p.a_feat).stage();
+    const size_t stage = tc::geometry(p.bf, p.mode, p.BN, p.a_feat, p.kbw).stage();
     int S = (int)((104 * 1024 - 1024 - 64) / stage);
     if (S >= 2) {
       p.stages = S < p.stages ? S : p.stages;
       ctas = 2;
     }
   }
-  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode, p.a_feat);
+  const size_t smem = tc_smem_bytes(p.BN, p.stages, p.bf, p.mode, p.a_feat, p.kbw);
   const int cap = ctas * sms;
   int grid = p.n_tiles < cap ? p.n_tiles : cap;
   if (grid < 1) return cudaSuccess;
@@ -785,7 +803,9 @@ static void tc_common(TcParams& p, int BN, int bf, int mode) {
   p.BN = BN;
   p.bf = bf;
   if (!p.a_feat) p.a_feat = tc::BM;
-  p.stages = tc_stages(BN, bf, mode, p.a_feat);
+  // 3xTF32 K-major modes with 256-wide n-tiles: 16-element k-blocks (half the 96 KB stage, four in flight)
+  if (!bf && mode != TC_DW && BN > 128 && knobs().tc_bk16) p.kbw = 16;
+  p.stages = tc_stages(BN, bf, mode, p.a_feat, p.kbw);
   p.tmem_cols = tc_tmem_cols(BN);
 }
 
@@ -793,7 +813,8 @@ static void tc_common(TcParams& p, int BN, int bf, int mode) {
 static int dw_bn(int64_t N, int bf) {
   const int64_t atom = bf ? 64 : 32;
   int64_t bn = (N + atom - 1) / atom * atom;
-  return (int)(bn > 256 ? 256 : bn);
+  const int64_t cap = bf ? 256 : knobs().tc_dw_bnmax;  // (dev knob PGCN_TC_DW_BNMAX, 3xTF32 A/B tests)
+  return (int)(bn > cap ? cap : bn);
 }
 
 // Split-K plan of the dW GEMM: each of the n_seg segments (row counts kb_s k-blocks of 32 rows) is cut
@@ -860,13 +881,14 @@ static int launch_fwd(Launch L, int nseg, const float* const* A, const int64_t* 
   const int BN = tc_bn(N);
   tc_common(p, BN, bf, TC_FWD);
   bool ok;
+  const int kw = p.kbw > 0 ? p.kbw : 32, sw = kw == 16 ? 3 : 1;  // tf32 k-block width and its swizzle
   if (bf) ok = tc_map(&p.map_b[0], B_hi, true, ldB, N, ldB, 64, BN, 1);
   else
-    ok = tc_map(&p.map_b[0], B_hi, false, ldB, N, ldB, 32, BN, 1) && tc_map(&p.map_b_lo, B_lo, false, ldB, N, ldB, 32, BN, 1);
+    ok = tc_map(&p.map_b[0], B_hi, false, ldB, N, ldB, kw, BN, sw) && tc_map(&p.map_b_lo, B_lo, false, ldB, N, ldB, kw, BN, sw);
   for (int s = 0; s < nseg && ok; ++s)
-    ok = tc_map(&p.map_a[s], A[s], false, K, rowsA[s] > 0 ? rowsA[s] : 1, ldA, 32, 128, bf ? 0 : 1);
+    ok = tc_map(&p.map_a[s], A[s], false, K, rowsA[s] > 0 ? rowsA[s] : 1, ldA, bf ? 32 : kw, 128, bf ? 0 : sw);
   if (!ok) return -1;
-  const int kbk = bf ? 64 : 32;
+  const int kbk = bf ? 64 : kw;
   p.mode = TC_FWD;
   p.nseg = nseg;
   for (int s = 0; s < nseg; ++s) {
@@ -953,13 +975,14 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   TcParams p{};
   const int BN = tc_bn(F);
   tc_common(p, BN, bf, TC_DA);
-  bool ok = tc_map(&p.map_a[0], Mg, false, N, M, ldM, 32, 128, bf ? 0 : 1);
+  const int kw = p.kbw > 0 ? p.kbw : 32, sw = kw == 16 ? 3 : 1;  // tf32 k-block width and its swizzle
+  bool ok = tc_map(&p.map_a[0], Mg, false, N, M, ldM, bf ? 32 : kw, 128, bf ? 0 : sw);
   p.pre_a = !bf && Mlo && PGCN_TF32_TRUNC_HI && presplit_enabled();
-  if (p.pre_a) ok = ok && tc_map(&p.map_lo[0], Mlo, false, N, M, ldM, 32, 128, 1);
+  if (p.pre_a) ok = ok && tc_map(&p.map_lo[0], Mlo, false, N, M, ldM, kw, 128, sw);
   if (bf) ok = ok && tc_map(&p.map_b[0], Wp_hi, true, N, halves * F, Kp, 64, BN, 1);
   else
-    ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, halves * F, Kp, 32, BN, 1) &&
-         tc_map(&p.map_b_lo, Wp_lo, false, N, halves * F, Kp, 32, BN, 1);
+    ok = ok && tc_map(&p.map_b[0], Wp_hi, false, N, halves * F, Kp, kw, BN, sw) &&
+         tc_map(&p.map_b_lo, Wp_lo, false, N, halves * F, Kp, kw, BN, sw);
   if (!ok) return -1;
   p.mode = TC_DA;
   p.epi = EPI_DA;
@@ -967,7 +990,7 @@ int gemm_da_tc(Launch L, const float* Mg, int64_t ldM, int64_t M, int64_t N, con
   p.n_ntiles_half = (int)((F + BN - 1) / BN);
   p.n_ntiles = halves * p.n_ntiles_half;
   p.n_tiles = (int)((M + 127) / 128) * p.n_ntiles;
-  p.kb_seg[0] = (int)((N + (bf ? 63 : 31)) / (bf ? 64 : 32));
+  p.kb_seg[0] = (int)((N + (bf ? 64 : kw) - 1) / (bf ? 64 : kw));
   p.M = (int)M;
   p.N = (int)N;
   p.F = (int)F;

@@ -41,14 +41,17 @@ struct alignas(64) TcParams {
   // computing it once per tile that reads the operand.  pre_a: DA's A (M); pre_b: bit s = DW segment s's B.
   CUtensorMap map_lo[2];
   int pre_a, pre_b;
+  // 3xTF32 FWD / DA: fp32 elements per k-block, 32 (one 128-byte SW128 row; 0 = 32) or 16 (one 64-byte SW64
+  // row): half-size stages, twice as many in flight, for the 256-wide n-tiles whose 96 KB stages fit twice
+  int kbw;
 };
 
 bool tc_map_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_cols, int box_rows,
                bool mn_major = false);
 bool tc_map_table(CUtensorMap* m, const void* base, bool bf16, int64_t cols, int64_t rows, int64_t ld, int box_cols,
                   int box_rows);
-int tc_stages(int BN, int bf, int mode, int afeat);
-size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat);
+int tc_stages(int BN, int bf, int mode, int afeat, int kbw = 32);
+size_t tc_smem_bytes(int BN, int S, int bf, int mode, int afeat, int kbw = 32);
 void tc_wprep_bf16(const float* W, int F, int N, int Fp, int Kp, int Kq, int ns, void* WT, void* Wp, void* WJ,
                    cudaStream_t s);
 int tc_bn(int64_t N);
