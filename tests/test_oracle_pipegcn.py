@@ -353,3 +353,40 @@ def test_depth_ema_gamma0_is_identity():
     b = pipegcn.run(g, parts, params, c, 5, mode="pipe", depth=2, smooth_f=True, smooth_g=True, gamma=0.0)
     for ra, rb in zip(a, b):
         assert ra["loss"] == rb["loss"]
+
+
+@pytest.mark.parametrize("ema_init", ["first", "zero"])
+@pytest.mark.parametrize("depth", [1, 2])
+def test_ema_f_transient_closed_form(ema_init, depth):
+    """EMA-F transient values (Sec. 3.4; readings R12, R14, R27), pinned by the EMA
+    recursion's closed form.  With eta = 0 and p = 0 the owners' layer-1 rows take two values only:
+    a = H1 computed with zero X boundary rows (t <= s, Alg. 1 l.6) and b = the full-graph H1 once X's
+    boundary rows are installed (t > s; O1, oracle/sage.py).  The layer-2 boundary rows consumed at t carry
+    the rows sent at t - s, so the messages are a for t in [s+1, 2s] and b afterwards, and the smoothed
+    rows are
+      t in [s+1, 2s]: first-receipt init a;  zero init (1 - gamma^(t-s)) a
+      t >= 2s:        gamma^(t-2s) c + (1 - gamma^(t-2s)) b,  c = a (first) or (1 - gamma^s) a (zero).
+    A swapped gamma / 1 - gamma, a late or early first receipt, or smoothing the fresh instead of the
+    stale rows fails it."""
+    g = small_graph(seed=11)
+    widths = [9, 8, 4]
+    gamma = 0.7
+    c = cfg(widths, p=0.0, lr=0.0, gamma=gamma)
+    params = glorot_params(widths, 3)
+    parts = partition(g.n, g.row_ptr, g.col_idx, 3)
+    T = 2 * depth + 5
+    recs = pipegcn.run(g, parts, params, c, T, mode="pipe", smooth_f=True, ema_init=ema_init, depth=depth)
+    a = assemble(parts, recs[0]["H"][1], g.n, widths[1])      # t = 1: zero X boundary rows
+    b = sage.forward_backward(g, params, 1, c)["H"][1]        # full graph (p = 0: no mask)
+    assert np.abs(a - b).max() > 1e-3                         # the transient is not trivial
+    s = depth
+    for t in range(s + 1, T + 1):
+        if t <= 2 * s:
+            exp = a if ema_init == "first" else (1.0 - gamma ** (t - s)) * a
+        else:
+            c0 = a if ema_init == "first" else (1.0 - gamma ** s) * a
+            k = t - 2 * s
+            exp = gamma ** k * c0 + (1.0 - gamma ** k) * b
+        for i, P in enumerate(parts):
+            got = recs[t - 1]["halo"][2][i]
+            assert close(got, exp[P["halo_gid"]], 1e-12), (t, i)
