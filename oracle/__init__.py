@@ -18,8 +18,8 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`): SplitMix64 published vectors, bru
 definitions and dense-P brute force on tiny graphs, hand-derived golden values
 (tests/golden/), float64 central finite differences, O2 == O1, O3(t=1) == O1 on P_in,
 O3 == O2 once eta = 0 halos settle, EMA gamma=0 identity and geometric convergence, the
-EMA-F transient against the recursion's closed form at eta = 0 (first-receipt and zero init),
+EMA-F / EMA-G transients against the recursion's closed form at eta = 0,
 Adam against torch.optim.Adam.  Readings of ambiguous passages: DESIGN.md "Readings".
 Parity unpinned: exact per-step values of O3 in the eta > 0 transient beyond the pins
-above, and the EMA-G transient values (R12).
+above, and zero-init EMA-G (R12).
 """

@@ -390,3 +390,30 @@ def test_ema_f_transient_closed_form(ema_init, depth):
         for i, P in enumerate(parts):
             got = recs[t - 1]["halo"][2][i]
             assert close(got, exp[P["halo_gid"]], 1e-12), (t, i)
+
+
+def test_ema_g_transient_closed_form():
+    """EMA-G transient (Sec. 3.4; readings R12, R13), first-receipt init, eta = 0, p = 0,
+    L = 2, no feature smoothing.  The forward is constant from t = 3 on (layer-2 halos = the full-graph H1
+    sent at t >= 2), so the raw gradient messages consumed at t are m1 (t = 2), m2 (t = 3) and m* (t >= 4),
+    and the smoothed run differs from the plain one only through C_hat - C summed per row (S):
+      t = 2: 0;   t = 3: gamma S(m1 - m2);   t >= 4: gamma^(t-3) (gamma S(m1 - m2) + S(m2 - m*)),
+    where S(m2 - m*) = J_plain(3) - J_plain(4) (same local term from t = 3 on).  So the accumulated J^(1)
+    must satisfy J_g(t) - J_p(t) = gamma^(t-3) [(J_g(3) - J_p(3)) + (J_p(3) - J_p(4))] for t >= 4."""
+    g = small_graph(seed=12)
+    widths = [9, 8, 4]
+    gamma = 0.6
+    c = cfg(widths, p=0.0, lr=0.0, gamma=gamma)
+    params = glorot_params(widths, 3)
+    parts = partition(g.n, g.row_ptr, g.col_idx, 3)
+    T = 8
+    plain = pipegcn.run(g, parts, params, c, T, mode="pipe")
+    smooth = pipegcn.run(g, parts, params, c, T, mode="pipe", smooth_g=True)
+    Jp = [assemble(parts, r["J"][1], g.n, widths[1]) for r in plain]
+    Jg = [assemble(parts, r["J"][1], g.n, widths[1]) for r in smooth]
+    assert close(Jg[1], Jp[1], 1e-13)                      # t = 2: the first receipt is the message itself
+    d3 = Jg[2] - Jp[2]
+    assert np.abs(d3).max() > 1e-6 * np.abs(Jp[2]).max()     # the transient is not trivial
+    base = d3 + (Jp[2] - Jp[3])
+    for t in range(4, T + 1):
+        assert np.allclose(Jg[t - 1] - Jp[t - 1], gamma ** (t - 3) * base, rtol=0, atol=1e-12 * np.abs(Jp[2]).max()), t
