@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2 final evidence pass: GPU tests, smoke, sanitizers, the default bench + reference arm, ncu launch
 # lists and full captures (exported to CSV on the box), all configs for BASELINE.md
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out/final
 O=gpurun_out/final
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt

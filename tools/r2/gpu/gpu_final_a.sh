@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-2 final evidence, part A: GPU tests, smoke, the default bench (twice) + reference arm, ncu launch list of
 # the default bench and full captures of its top kernels (exported to CSV on the box)
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/fa; mkdir -p $O
 nvidia-smi -L > $O/gpu.txt; nproc >> $O/gpu.txt; free -g >> $O/gpu.txt
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt

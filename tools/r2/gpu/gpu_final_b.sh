@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-2 final evidence, part B: every config of BASELINE.md, ncu launch lists of papers-e and products,
 # compute-sanitizer on the exchange transports and the lean mode
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/fb; mkdir -p $O
 bash tools/r2/all_configs.sh $O/all
 for cfg in reddit yelp; do

@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2, second GPU pass: GPU tests (incl. exchange, full-size step parity, large dW), sanitizer on the
 # loopback exchange, three bench runs (mode study), launch list and full ncu captures of the top kernels
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 2400 python -m pytest tests -m gpu -q -s -p no:cacheprovider > gpurun_out/r2b_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2b_pytest.txt
 for T in memcheck racecheck synccheck; do

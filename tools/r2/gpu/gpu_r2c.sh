@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2: papers-q shape (the north_star flagship per-GPU shape) -- bench, launch list with DRAM bytes,
 # full ncu capture of the aggregation kernels, and the random-row gather ceiling
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 for K in 0 1024 256 64; do PGCN_DW_KMAX=$K timeout 600 python tools/r2/dw_chain.py >> gpurun_out/r2c_dw_chain.jsonl 2>> gpurun_out/r2c_dw_chain.err; done
 timeout 600 python tools/r2/gather_ceiling.py > gpurun_out/r2c_gather_ceiling.jsonl 2> gpurun_out/r2c_gather_ceiling.err

@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: PUSH transport tests + sanitizer, transports A/B on Reddit, papers-q bench + ncu, gather ceiling
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 1500 python -m pytest -q -s -p no:cacheprovider tests/test_gpu_exchange.py "tests/test_gpu_fullsize_step.py::test_full_size_two_iterations[products]" tests/test_gpu_gemm.py -k "exchange or products or full_size" > gpurun_out/r2d_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2d_pytest.txt
 for T in memcheck racecheck; do

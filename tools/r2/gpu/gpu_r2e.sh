@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: predicated-remainder SpMM + papers-q shape sweep (ld4 = 12: G, NC, U, min blocks/SM), Reddit check
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 900 python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_tiles.py tests/test_gpu_train_sparse.py > gpurun_out/r2e_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2e_pytest.txt
 for sh in default 16,1,8,3 16,1,16,2 16,1,16,3; do

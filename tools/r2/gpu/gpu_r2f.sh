@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: papers-e SpMM shape sweep (ld4 = 12), steady-state ncu capture of the papers aggregation, all configs
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 for sh in default 4,3,4,3 4,3,8,2 4,3,2,4 8,2,4,3 8,2,8,2; do
   if [ $sh = default ]; then unset PGCN_SPMM_TABLE; else export PGCN_SPMM_TABLE="12=$sh"; fi

@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2: dW stage change validation + timing, papers-e SpMM shape sweep, steady-state ncu of the papers
 # aggregation and GEMMs (exported to CSV on the box: full reports exceed the copy-back limit), all configs
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 1200 python -m pytest -q -p no:cacheprovider tests/test_gpu_gemm.py "tests/test_gpu_fullsize_step.py" > gpurun_out/r2g_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2g_pytest.txt
 timeout 600 python tools/r2/dw_chain.py > gpurun_out/r2g_dw_chain.jsonl 2> gpurun_out/r2g_dw_chain.err

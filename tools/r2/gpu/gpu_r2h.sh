@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: column-chunked (L2-resident) gathers -- parity with chunking forced on small graphs, Reddit sweep
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 PGCN_SPMM_L2MB=1 timeout 1200 python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_tiles.py tests/test_gpu_train_sparse.py tests/test_gpu_gcn.py tests/test_gpu_bf16_gather.py > gpurun_out/r2h_pytest_chunked.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2h_pytest_chunked.txt
 for mb in 0 96 64 32 16; do

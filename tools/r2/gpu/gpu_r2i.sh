@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: Reddit last-layer variants (train-sparse gather vs all-row tile path; 44-wide row shapes), papers-q shape
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 run() { name=$1; shift; timeout 900 python bench.py --no-cpu --no-e2e --no-ablation "$@" > gpurun_out/r2i_$name.json 2> gpurun_out/r2i_$name.err; }
 run reddit_default

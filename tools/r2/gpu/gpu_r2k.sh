@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2: narrow-row gather kernels -- GPU parity suite, papers-q / Reddit / products with U = 8, 4, off
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 1800 python -m pytest -q -x -p no:cacheprovider tests -m gpu --deselect tests/test_gpu_fullsize_step.py > gpurun_out/r2k_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2k_pytest.txt
 for me in 8 4 0; do

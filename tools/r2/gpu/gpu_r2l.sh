@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 mkdir -p gpurun_out
 timeout 1500 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_tiles.py tests/test_gpu_train_sparse.py tests/test_gpu_exchange.py tests/test_gpu_gcn.py > gpurun_out/r2l_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/r2l_pytest.txt
 run() { name=$1; shift; timeout 900 python bench.py --no-cpu --no-e2e --no-ablation "$@" > gpurun_out/r2l_$name.json 2> gpurun_out/r2l_$name.err; }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # re-entry check of HEAD: GPU tests, smoke, default bench twice
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2n; mkdir -p $O
 nvidia-smi -L > $O/gpu.txt; nproc >> $O/gpu.txt
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt

@@ -1,6 +1,6 @@
 #!/bin/bash
 # lean-memory mode (N1(iii)): GPU tests, papers-q lean vs default, Reddit lean
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2o; mkdir -p $O
 free -g > $O/host.txt; nproc >> $O/host.txt
 timeout 1500 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_lean.py tests/test_gpu_multigpu.py > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/pytest.txt

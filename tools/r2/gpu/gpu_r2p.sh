@@ -1,6 +1,6 @@
 #!/bin/bash
 # producer-written M_lo (3xTF32 pre-split operand): GPU tests, bench A/B (PGCN_PRESPLIT=0 vs 1) on Reddit / Yelp
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2p; mkdir -p $O
 timeout 2400 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_lean.py tests/test_gpu_parity.py tests/test_gpu_gcn.py tests/test_gpu_train_sparse.py tests/test_gpu_exchange.py tests/test_gpu_gemm.py tests/test_gpu_fullsize_step.py > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/pytest.txt
 for ps in 1 0; do

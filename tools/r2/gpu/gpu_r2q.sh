@@ -1,6 +1,6 @@
 #!/bin/bash
 # column-chunk count A/B for the L2-chunked gathers (Reddit-shaped: 238 MB forward / 119 MB transposed tables)
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2q; mkdir -p $O
 for rep in 1 2; do
 for nch in 2 3 4; do

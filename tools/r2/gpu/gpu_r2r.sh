@@ -1,6 +1,6 @@
 #!/bin/bash
 # 16-element k-blocks (SW64) for the 3xTF32 K-major GEMMs with 256-wide n-tiles: tests + bench A/B
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2r; mkdir -p $O
 timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_gemm.py > $O/pytest_gemm.txt 2>&1; echo "rc=$?" >> $O/pytest_gemm.txt
 tail -2 $O/pytest_gemm.txt

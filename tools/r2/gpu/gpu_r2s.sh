@@ -1,6 +1,6 @@
 #!/bin/bash
 # 16-element k-blocks for every 3xTF32 K-major GEMM (PGCN_TC_BK16=2) vs only 256-wide n-tiles (1): tests + A/B
-cd "$(dirname "$0")/../.."
+cd "$(dirname "$0")/../../.."
 O=gpurun_out/r2s; mkdir -p $O
 PGCN_TC_BK16=2 timeout 900 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_gemm.py tests/test_gpu_parity.py > $O/pytest_bk2.txt 2>&1; echo "rc=$?" >> $O/pytest_bk2.txt
 tail -2 $O/pytest_bk2.txt
