@@ -30,7 +30,7 @@ struct DevKnobs {
   int presplit = 0;
   int spmm_nch = 2;  // column chunks of an L2-chunked gather (PGCN_SPMM_NCH)
   int tc_dw_bnmax = 256;
-  int tc_bk16 = 1;  // 3xTF32 K-major GEMMs with 256-wide n-tiles: 16-element k-blocks (PGCN_TC_BK16)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
+  int tc_bk16 = 2;  // 3xTF32 K-major GEMMs: 16-element k-blocks (PGCN_TC_BK16: 0 off, 1 n-tiles > 128, 2 all)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

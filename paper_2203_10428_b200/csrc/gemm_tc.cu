@@ -803,8 +803,11 @@ static void tc_common(TcParams& p, int BN, int bf, int mode) {
   p.BN = BN;
   p.bf = bf;
   if (!p.a_feat) p.a_feat = tc::BM;
-  // 3xTF32 K-major modes with 256-wide n-tiles: 16-element k-blocks (half the 96 KB stage, four in flight)
-  if (!bf && mode != TC_DW && BN > 128 && knobs().tc_bk16) p.kbw = 16;
+  // 3xTF32 K-major modes: 16-element k-blocks -- half-size stages, twice as many in flight (256-wide n-tiles:
+  // four 48 KB stages instead of two 96 KB ones; narrow n-tiles: enough stages for two CTAs per SM).
+  // Dev knob PGCN_TC_BK16: 0 off, 1 n-tiles > 128 only, 2 (default) every n-tile (profiles/r2r_bk16.md)
+  const int bk16 = knobs().tc_bk16;
+  if (!bf && mode != TC_DW && (bk16 == 2 || (bk16 == 1 && BN > 128))) p.kbw = 16;
   p.stages = tc_stages(BN, bf, mode, p.a_feat, p.kbw);
   p.tmem_cols = tc_tmem_cols(BN);
 }

@@ -72,7 +72,7 @@ const DevKnobs& knobs() {
     k.presplit = env_int("PGCN_PRESPLIT", 0);
     k.spmm_nch = env_int("PGCN_SPMM_NCH", 2);
     k.tc_dw_bnmax = env_int("PGCN_TC_DW_BNMAX", 256);
-    k.tc_bk16 = env_int("PGCN_TC_BK16", 1);
+    k.tc_bk16 = env_int("PGCN_TC_BK16", 2);
     if (k.tc_dw_bnmax < 32 || k.tc_dw_bnmax > 256 || k.tc_dw_bnmax % 32) k.tc_dw_bnmax = 256;
     if (k.spmm_nch < 2 || k.spmm_nch > 8) k.spmm_nch = 2;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
