@@ -30,7 +30,8 @@ struct DevKnobs {
   int presplit = 0;
   int spmm_nch = 2;  // column chunks of an L2-chunked gather (PGCN_SPMM_NCH)
   int tc_dw_bnmax = 256;
-  int tc_bk16 = 2;  // 3xTF32 K-major GEMMs: 16-element k-blocks (PGCN_TC_BK16: 0 off, 1 n-tiles > 128, 2 all)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
+  int tc_bk16 = 2;
+  int tc_dw16 = 0;  // 3xTF32 dW: 16-row k-blocks (PGCN_TC_DW16; measured slower, profiles/r2r_bk16.md)  // 3xTF32 K-major GEMMs: 16-element k-blocks (PGCN_TC_BK16: 0 off, 1 n-tiles > 128, 2 all)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

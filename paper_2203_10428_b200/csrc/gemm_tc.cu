@@ -67,7 +67,7 @@ __host__ __device__ inline Geo geometry(int bf, int mode, int BN, int afeat = BM
   Geo g;
   if (!bf) {
     const int af = mode == TC_DW ? afeat : BM;
-    const int kw = (mode == TC_DW || kbw <= 0) ? BK : kbw;
+    const int kw = kbw <= 0 ? BK : kbw;  // (DW: rows per k-block)
     g.a_raw = (uint32_t)af * kw * 4;
     g.a_cvt = (uint32_t)af * kw * 4;
     g.b_raw = (uint32_t)BN * kw * 4;
@@ -211,14 +211,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
           } else {
           const bool pb = split_b && ((p.pre_b >> T.seg) & 1), pa = p.mode == TC_DA && p.pre_a;
           mbar_expect_tx(&full[s], (pa ? 2 : 1) * a_bytes + (split_b && !pb ? b_bytes : 2 * b_bytes));
-          if (p.mode == TC_DW) {
-            const int r0 = kb * BK;
+          if (p.mode == TC_DW) {  // atoms of 32 features x kw rows (128 kw bytes)
+            const int r0 = kb * kw;
+            const int ab = 128 * kw;
             for (int j = 0; j < p.a_feat / 32; ++j)
-              tma_load_2d(A + j * 4096, &p.map_a[p.merged ? (j >> 1) : T.seg], &full[s],
+              tma_load_2d(A + j * ab, &p.map_a[p.merged ? (j >> 1) : T.seg], &full[s],
                           p.merged ? 32 * (j & 1) : T.m0 + 32 * j, r0);
             for (int j = 0; j < p.BN / 32; ++j) {
-              tma_load_2d(B + j * 4096, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
-              if (pb) tma_load_2d(Blo + j * 4096, &p.map_lo[T.seg], &full[s], T.n0 + 32 * j, r0);
+              tma_load_2d(B + j * ab, &p.map_b[T.seg], &full[s], T.n0 + 32 * j, r0);
+              if (pb) tma_load_2d(Blo + j * ab, &p.map_lo[T.seg], &full[s], T.n0 + 32 * j, r0);
             }
           } else if (p.mode == TC_FWD) {
             const int seg = kb < p.kb_seg[0] ? 0 : 1;
@@ -296,14 +297,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_umma_gemm(const __grid_constant
             if (++s == S) { s = 0; ph ^= 1; }
             continue;
           }
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          const int nk = p.mode == TC_DW ? kw / 8 : BK / 8;
+          const uint32_t lbo = 128u * (uint32_t)kw;  // DW: MN-atom stride (32 features x kw rows)
+#pragma unroll 4
+          for (int kk = 0; kk < nk; ++kk) {
             uint64_t ah, al, bh, bl;
-            if (p.mode == TC_DW) {  // MN-major: MN atoms 4 KB apart (LBO), 4-row k-groups 512 B apart (SBO)
-              ah = make_desc(A + kk * 1024, 4096, 512, 1);
-              al = make_desc(Alo + kk * 1024, 4096, 512, 1);
-              bh = make_desc(B + kk * 1024, 4096, 512, 1);
-              bl = make_desc(Blo + kk * 1024, 4096, 512, 1);
+            if (p.mode == TC_DW) {  // MN-major: MN atoms lbo apart (LBO), 4-row k-groups 512 B apart (SBO)
+              ah = make_desc(A + kk * 1024, lbo, 512, 1);
+              al = make_desc(Alo + kk * 1024, lbo, 512, 1);
+              bh = make_desc(B + kk * 1024, lbo, 512, 1);
+              bl = make_desc(Blo + kk * 1024, lbo, 512, 1);
             } else {  // K-major: 8-row groups 1 KB apart (SBO); k-step = 32 bytes inside the swizzle row
               ah = make_desc(A + kk * 32, 16, 1024);
               al = make_desc(Alo + kk * 32, 16, 1024);
@@ -808,6 +811,9 @@ static void tc_common(TcParams& p, int BN, int bf, int mode) {
   // Dev knob PGCN_TC_BK16: 0 off, 1 n-tiles > 128 only, 2 (default) every n-tile (profiles/r2r_bk16.md)
   const int bk16 = knobs().tc_bk16;
   if (!bf && mode != TC_DW && (bk16 == 2 || (bk16 == 1 && BN > 128))) p.kbw = 16;
+  // dW: 16-row k-blocks with dev knob PGCN_TC_DW16=1 (half-size stages; measured slower on every config:
+  // the dW's bytes in flight do not change and the k-block count doubles -- profiles/r2r_bk16.md)
+  if (!bf && mode == TC_DW && knobs().tc_dw16) p.kbw = 16;
   p.stages = tc_stages(BN, bf, mode, p.a_feat, p.kbw);
   p.tmem_cols = tc_tmem_cols(BN);
 }
@@ -1038,12 +1044,13 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   const float* Bs[2] = {B0, B1};
   const int64_t rows[2] = {rows0, rows1};
   const float* Blos[2] = {B0lo, B1lo};
+  const int kr = bf ? 32 : (p.kbw > 0 ? p.kbw : 32);  // rows per k-block (3xTF32: 16 with PGCN_TC_DW16)
   bool ok = true;
   for (int s = 0; s < nseg && ok; ++s) {
-    ok = tc_map(&p.map_a[s], As[s], false, F, rows[s] > 0 ? rows[s] : 1, ldA, 32, 32, bf ? 0 : 2) &&
-         tc_map(&p.map_b[s], Bs[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, bf ? 0 : 2);
+    ok = tc_map(&p.map_a[s], As[s], false, F, rows[s] > 0 ? rows[s] : 1, ldA, 32, kr, bf ? 0 : 2) &&
+         tc_map(&p.map_b[s], Bs[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, kr, bf ? 0 : 2);
     if (ok && !bf && Blos[s] && PGCN_TF32_TRUNC_HI && presplit_enabled()) {
-      ok = tc_map(&p.map_lo[s], Blos[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, 32, 2);
+      ok = tc_map(&p.map_lo[s], Blos[s], false, N, rows[s] > 0 ? rows[s] : 1, ldB, 32, kr, 2);
       p.pre_b |= 1 << s;
     }
   }
@@ -1054,9 +1061,12 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.Z = Zs;
   for (int s = 0; s < nseg; ++s) {
     p.Zseg[s] = Zseg[s];
-    p.kb_seg[s] = (int)((rows[s] + 31) / 32);
-    p.kb_per_split[s] = (p.kb_seg[s] + Zseg[s] - 1) / Zseg[s];
-    if (p.kb_per_split[s] < 1) p.kb_per_split[s] = 1;
+    // the split plan is in 32-row k-blocks; the kernel walks kr-row k-blocks (same row ranges per split)
+    const int64_t kb32 = (rows[s] + 31) / 32;
+    int64_t kps = (kb32 + Zseg[s] - 1) / Zseg[s];
+    if (kps < 1) kps = 1;
+    p.kb_seg[s] = (int)((rows[s] + kr - 1) / kr);
+    p.kb_per_split[s] = (int)(kps * (32 / kr));
     p.out_row_off[s] = (int)(s * F);
   }
   p.n_ftiles = (int)((F + 127) / 128);

@@ -73,6 +73,7 @@ const DevKnobs& knobs() {
     k.spmm_nch = env_int("PGCN_SPMM_NCH", 2);
     k.tc_dw_bnmax = env_int("PGCN_TC_DW_BNMAX", 256);
     k.tc_bk16 = env_int("PGCN_TC_BK16", 2);
+    k.tc_dw16 = env_int("PGCN_TC_DW16", 0);
     if (k.tc_dw_bnmax < 32 || k.tc_dw_bnmax > 256 || k.tc_dw_bnmax % 32) k.tc_dw_bnmax = 256;
     if (k.spmm_nch < 2 || k.spmm_nch > 8) k.spmm_nch = 2;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
