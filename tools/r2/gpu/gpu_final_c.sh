@@ -2,7 +2,7 @@
 # round-2 final evidence of HEAD (after the BK16 GEMM change): GPU tests, smoke, default bench x2, reference arm,
 # every config, ncu launch list of the default bench
 cd "$(dirname "$0")/../../.."
-O=gpurun_out/fc; mkdir -p $O
+O=gpurun_out/${FINAL_DIR:-fc}; mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; echo "smoke rc=$?" >> $O/smoke.txt
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
