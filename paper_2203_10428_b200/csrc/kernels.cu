@@ -1397,6 +1397,7 @@ int spmm_fwd(Launch L, const int64_t* row_ptr, const int32_t* col, const float* 
     count(L);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
   };
+  L2Window l2w(L.s, b16 ? g16 : (const void*)D, (size_t)n_valid * (b16 ? ld8 * 16 : ld4 * 16));
   if (!tcu) return gather(L.s, work, self, 0);
   auto tile = [&](float* out) -> int {
     int rc;
@@ -1471,6 +1472,7 @@ int spmm_bwd(Launch L, const int64_t* t_row_ptr, const int32_t* t_col, const flo
     count(L);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : fail(PGCN_ECUDA, "SpMM launch failed");
   };
+  L2Window l2w(L.s, b16 ? g16 : (const void*)a, (size_t)n_in * (b16 ? ld8 * 16 : (size_t)lda4 * 16));
   if (!tcu) return gather(L.s, work, dDs, 0);
   auto tile = [&](float* out) -> int {
     int rc;

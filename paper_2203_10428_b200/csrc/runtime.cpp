@@ -2,6 +2,7 @@
 // developer A/B knobs, each initialised once and safe to call from several threads / contexts.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
@@ -39,6 +40,42 @@ int smem_attr_once(const void* func, int bytes) {
   return 0;
 }
 
+L2Window::L2Window(cudaStream_t st, const void* base, size_t bytes) : s(st) {
+  const int mb = knobs().l2_persist_mb;
+  if (mb <= 0 || !base || bytes == 0) return;
+  static std::mutex mu;
+  static std::set<int> carved;
+  int dev = 0, maxw = 0, maxp = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  size_t carve = std::min((size_t)mb << 20, (size_t)maxp);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!carved.count(dev)) {
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) { cudaGetLastError(); return; }
+      carved.insert(dev);
+    }
+  }
+  const size_t win = std::min(bytes, (size_t)maxw);
+  if (win == 0 || carve == 0) return;
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)carve / (double)win));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+  if (!on) cudaGetLastError();
+}
+
+L2Window::~L2Window() {
+  if (!on) return;
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+}
+
 namespace {
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -74,6 +111,7 @@ const DevKnobs& knobs() {
     k.tc_dw_bnmax = env_int("PGCN_TC_DW_BNMAX", 256);
     k.tc_bk16 = env_int("PGCN_TC_BK16", 2);
     k.tc_dw16 = env_int("PGCN_TC_DW16", 0);
+    k.l2_persist_mb = env_int("PGCN_L2_PERSIST_MB", 0);
     if (k.tc_dw_bnmax < 32 || k.tc_dw_bnmax > 256 || k.tc_dw_bnmax % 32) k.tc_dw_bnmax = 256;
     if (k.spmm_nch < 2 || k.spmm_nch > 8) k.spmm_nch = 2;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
