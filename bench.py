@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--transport", default="loopback", choices=["loopback", "local", "push"],
                     help="single-GPU runs: 'loopback' = the posted exchange of the NCCL path (pack -> comm stream "
                          "-> one device copy per peer segment -> events; App. F), 'local' = direct gathers, "
-                         "'push' = producers store the exchanged rows into the receivers from their epilogues (N2)")
+                         "'push' = producers store the exchanged rows into the receivers from their epilogues (N2); "
+                         "N > 1 GPUs: NCCL, or with 'push' (PIPE, fp32 payloads) the epilogue stores go into the "
+                         "peers' workspaces over NVLink (CUDA IPC)")
     ap.add_argument("--halo-payload", default="f32", choices=["f32", "bf16"],
                     help="bf16: exchange payloads rounded to bf16 (SURVEY N1(iv), 2e-2 tier)")
     ap.add_argument("--depth", type=int, default=1, help="pipeline depth s (R27)")
@@ -494,13 +496,14 @@ def main():
         t0 = time.time()
         part = pgcn.partition(g.n, g.row_ptr, g.col_idx, parts)
         t_part = time.time() - t0
-    transport = args.transport if world == 1 else "nccl"
+    transport = args.transport if world == 1 else ("nccl+push" if args.transport == "push" else "nccl")
     cfg = pgcn.make_config(m.widths, mode=args.mode, smooth_f="f" in args.smooth, smooth_g="g" in args.smooth,
                            gamma=m.gamma, dropout=m.dropout, loss=m.loss, opt="adam", lr=m.lr, n_global=g.n,
                            n_train_global=g.n_train, gemm=args.gemm, model=args.model, gather=args.gather,
                            train_sparse=not args.no_train_sparse, spmm_tiles=not args.no_tiles,
                            tile_min=args.tile_min, depth=args.depth,
-                           transport=transport if transport in ("loopback", "push") else "local",
+                           transport=transport if transport in ("loopback", "push") else
+                           ("push" if transport == "nccl+push" else "local"),
                            halo_payload=args.halo_payload, lean=args.lean)
     local_parts = list(range(parts)) if world == 1 else [rank]
     transport_note = None
@@ -533,6 +536,8 @@ def main():
     comm = pgcn.nccl_comm(rank, world) if world > 1 else None
     with torch.cuda.stream(stream):
         ctx = pgcn.Context(part, cfg, local_parts=local_parts, comm=comm, stream=stream)
+    if transport == "nccl+push" and args.mode == "pipe" and args.halo_payload == "f32":
+        ctx.ipc_connect()  # N2 over NVLink: producers store exchanged rows into the peers' workspaces
     views = [part.view(i) for i in local_parts]
     host = []
     for i, v in enumerate(views):
@@ -714,7 +719,9 @@ def main():
                                                             m.dropout, "" if args.model == "sage" else ", GCN-sym"),
                       "global_batch": g.n,
                       "parallelism": ("partition x%d on one GPU (%s transport)" % (parts, transport)) if world == 1 else
-                      ("partition x%d, one per GPU: NCCL p2p halo exchange on a comm stream + all-reduce" % world),
+                      ("partition x%d, one per GPU: %s + all-reduce" % (
+                          world, "halo rows stored into the peers' workspaces by the producing epilogues (N2, NVLink)"
+                          if transport == "nccl+push" else "NCCL p2p halo exchange on a comm stream")),
                       "gemm": args.gemm, "gather": args.gather, "depth": args.depth, "transport": transport,
                       "lean": bool(args.lean),
                       "transport_note": transport_note,

@@ -178,7 +178,8 @@ void pgcn_partition_free(pgcn_partitioning* p);
  *                       heavy tiles hold >= 25 % of a pattern's edges and every neighbour row is
  *                       valid (t > s).  0: gather SpMM only.
  *   tile_min            heavy-tile threshold in edges per 128 x 64 tile (0: default 96).
- *   transport           single-process contexts only (multi-process runs always use NCCL):
+ *   transport           single-process contexts (multi-process runs use NCCL, plus PUSH over peer memory when
+ *                       transport = 2 -- see pgcn_ipc_export):
  *                       0 LOCAL    -- the install reads the owners' rows straight out of their buffers
  *                                     and the accumulate reads the peers' boundary-row gradients (one
  *                                     gather kernel each, no message buffers);
@@ -264,7 +265,27 @@ typedef struct {
 int pgcn_nccl_id_bytes(void);
 int pgcn_nccl_unique_id(void* out);
 
+
 typedef struct pgcn_ctx pgcn_ctx;
+
+/* N2 over NVLink (App. F PAPER.md:981 puts the exchange on a second stream, here it rides in the
+ * producing epilogues): a multi-process context created with cfg.transport = 2 (PUSH) in PIPE mode with fp32
+ * payloads stores the rows its peers consume straight into their workspaces -- the node-update GEMM epilogue
+ * writes S_{i,j} rows of H^(l) into peer j's boundary rows of the slot read at t + s, the transposed SpMM /
+ * input-gradient GEMM epilogue writes J^(l-1)'s boundary rows into their owners' message rows -- instead of
+ * pack + ncclSend/ncclRecv (layer 1's one X exchange and GCN-sym transform-first layers keep NCCL).  Ordering:
+ * the per-iteration gradient all-reduce completes on a rank only after every rank's iteration-t kernels,
+ * pushes included, have run, so pushes of t are visible at t + 1 and a slot is rewritten only after its last
+ * reader (the rotation of the posted exchange).  Setup, after pgcn_ctx_create on every rank: each rank exports
+ * its workspace (a CUDA IPC handle of the allocation holding it, pgcn_ipc_handle_bytes() bytes, and the
+ * workspace's offset in it), the caller all-gathers the (handle, offset) pairs (e.g. torch.distributed), and
+ * each rank imports every peer's; pgcn_layer_fwd returns PGCN_ESTATE until all nranks - 1 peers are imported.
+ * Errors: PGCN_ESTATE (context not created for PUSH across ranks; rank imported twice), PGCN_EINVAL (bad rank /
+ * pointer), PGCN_ECUDA (the allocation cannot be exported / opened, e.g. no peer access).  VANILLA or bf16
+ * payloads with PUSH across ranks fall back to NCCL send / recv (no export needed).                       */
+int pgcn_ipc_handle_bytes(void);
+int pgcn_ipc_export(pgcn_ctx* ctx, void* handle /* [pgcn_ipc_handle_bytes()] out */, int64_t* offset);
+int pgcn_ipc_import(pgcn_ctx* ctx, int32_t rank, const void* handle, int64_t offset);
 
 /* Workspace bytes for hosting partitions local_parts[0..n_local) of p under cfg. */
 int pgcn_workspace_bytes(const pgcn_partitioning* p, const int32_t* local_parts, int32_t n_local,

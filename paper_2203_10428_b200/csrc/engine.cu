@@ -14,12 +14,14 @@
 //   emaG[l]  [n_send x ld_l]       EMA-G state per received gradient row (Sec. 3.4)
 //   G        [P]                   this partition's G_i, laid out like theta
 // ld_l = round_up(F_l, 4).  Boundary rows start at 0 (workspace zero-filled; Alg. 1 l.6).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -171,6 +173,16 @@ struct pgcn_ctx {
   // stream -- LOOPBACK (device copies between the hosted partitions) or NCCL (one partition per rank)
   int nccl = 0, rank = 0, nranks = 1;
   int xp = pgcn::XP_LOCAL;
+  // N2 over NVLink (multi-process PUSH, PIPE): producers store exchanged rows straight into the peers'
+  // workspaces, mapped with CUDA IPC (pgcn_ipc_export / pgcn_ipc_import); peer[j] = partition j's buffers
+  // laid out in peer j's workspace, addressed in this process
+  int ipc_push = 0;
+  std::vector<pgcn::PartCtx> peer;
+  std::vector<void*> ipc_open;  // mapped peer allocations (closed on destroy)
+  int n_imported = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  const pgcn_partitioning* part = nullptr;
   int posted = 0;           // xp != XP_LOCAL
   int p16 = 0;              // bf16 payloads (cfg.halo_payload)
   int64_t hook_spin_ns = 0; // pgcn_dev_exchange_hook: delay injected on the comm stream before each transfer
@@ -213,6 +225,7 @@ struct pgcn_ctx {
     if (ev_lab_free) cudaEventDestroy(ev_lab_free);
     if (ev_in_ready) cudaEventDestroy(ev_in_ready);
     if (cps) cudaStreamDestroy(cps);
+    for (void* q : ipc_open) cudaIpcCloseMemHandle(q);
   }
 };
 
@@ -284,8 +297,9 @@ bool staged_recv(const pgcn_ctx* C, int l) {
 
 // PUSH: whether layer l's output (layer l + 1's input) is stored into the receivers by its producer --
 // the node-update GEMM's epilogue; not GCN-sym transform-first layers (the SpMM produces H) or SIMT GEMMs.
+bool pushing(const pgcn_ctx* C) { return C->xp == XP_PUSH || C->ipc_push; }
 bool fwd_push_capable(const pgcn_ctx* C, int l) {
-  return C->xp == XP_PUSH && l < C->L && !(C->gcn && C->tf[l]) && C->cfg.gemm != 2;
+  return pushing(C) && l < C->L && !(C->gcn && C->tf[l]) && C->cfg.gemm != 2;
 }
 
 // Lays out every buffer (dry run when A.base == nullptr).
@@ -315,7 +329,7 @@ int layout(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* local, int
     p.inv_pos = A.take<int32_t>(p.n_send);
     p.halo_map = A.take<int32_t>(p.n_bd);
     p.msg_map = A.take<int32_t>(p.n_send);
-    if (C->xp == XP_PUSH) {
+    if (pushing(C)) {
       p.fpush_part = A.take<int32_t>(p.n_send);
       p.fpush_row = A.take<int32_t>(p.n_send);
       p.bpush_part = A.take<int32_t>(p.n_bd);
@@ -495,6 +509,9 @@ int init_ctx_shapes(pgcn_ctx* C, const pgcn_partitioning* part, const int32_t* l
     C->rank = comm->rank;
     C->nranks = comm->nranks;
     C->xp = XP_NCCL;
+    // transport PUSH across ranks (N2 over NVLink): PIPE only -- the per-iteration gradient all-reduce orders
+    // iteration t's pushes before every rank's iteration t + 1 (VANILLA would need a signal per layer)
+    C->ipc_push = cfg->transport == 2 && cfg->mode == 1 && cfg->halo_payload == 0;
 #endif
   } else {
     if (n_local != v0.n_parts)
@@ -743,9 +760,11 @@ int transfer(pgcn_ctx* C, int64_t t, int l, bool fwd) {
 // All partitions are hosted by this context and the compute stream orders every producer before its
 // consumer and after the previous reader of the slot (the rotation argument of the posted exchange).
 bool fwd_push(pgcn_ctx* C, PartCtx& p, int64_t t, int l, PushSpec& ps) {
-  if (C->xp != XP_PUSH || l >= C->L || p.n_send == 0) return false;
+  if (!pushing(C) || l >= C->L || p.n_send == 0) return false;
   ps = PushSpec{};
   for (auto& q : C->parts) ps.base[q.part] = static_cast<float*>(fwd_dst(C, q, t, l + 1));
+  for (auto& q : C->peer)  // multi-process: the peers' receive rows, mapped over NVLink
+    if (q.part != p.part && q.X) ps.base[q.part] = static_cast<float*>(fwd_dst(C, q, t, l + 1));
   ps.ptr = p.inv_ptr;
   ps.pos = p.inv_pos;
   ps.part = p.fpush_part;
@@ -755,9 +774,11 @@ bool fwd_push(pgcn_ctx* C, PartCtx& p, int64_t t, int l, PushSpec& ps) {
   return true;
 }
 bool bwd_push(pgcn_ctx* C, PartCtx& p, int64_t t, int l, PushSpec& ps) {
-  if (C->xp != XP_PUSH || l < 2 || p.n_bd == 0) return false;
+  if (!pushing(C) || l < 2 || p.n_bd == 0) return false;
   ps = PushSpec{};
   for (auto& q : C->parts) ps.base[q.part] = static_cast<float*>(q.recv_b[l][C->bi(t)]);
+  for (auto& q : C->peer)
+    if (q.part != p.part && q.X) ps.base[q.part] = static_cast<float*>(q.recv_b[l][C->bi(t)]);
   ps.part = p.bpush_part;
   ps.row = p.bpush_row;
   ps.row0 = p.n_in;
@@ -925,6 +946,9 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
   Arena A;
   A.base = static_cast<char*>(ws);
   layout(C, part, local, n_local, A);
+  C->ws = ws;
+  C->ws_bytes = ws_bytes;
+  C->part = part;
   C->s = static_cast<cudaStream_t>(stream);
   cudaStream_t s = C->s;
   cudaMemsetAsync(ws, 0, A.off, s);
@@ -967,7 +991,7 @@ extern "C" int pgcn_ctx_create(const pgcn_partitioning* part, const int32_t* loc
     cudaMemcpyAsync(p.halo_map, hmap.data(), sizeof(int32_t) * p.n_bd, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(p.msg_map, mmap.data(), sizeof(int32_t) * p.n_send, cudaMemcpyHostToDevice, s);
     std::vector<int32_t> fpp, fpr, bpp, bpr;
-    if (C->xp == XP_PUSH) {  // N2 destinations: send position k of peer j -> j's boundary row; boundary row
+    if (pushing(C)) {  // N2 destinations: send position k of peer j -> j's boundary row; boundary row
       fpp.resize(p.n_send);  // r of owner j -> j's message row (send order)
       fpr.resize(p.n_send);
       bpp.resize(p.n_bd);
@@ -1135,6 +1159,9 @@ extern "C" int pgcn_layer_fwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
   if (!C) return fail(PGCN_EINVAL, "ctx is NULL");
   int rc = expect(C, t, K_FWD, l, "pgcn_layer_fwd");
   if (rc) return rc;
+  if (C->ipc_push && C->n_imported < C->nranks - 1)
+    return fail(PGCN_ESTATE, "PUSH across ranks: pgcn_ipc_import every peer's workspace first (%d of %d)",
+                C->n_imported, C->nranks - 1);
   if (!params) return fail(PGCN_EINVAL, "params is NULL");
   const Launch Lk = C->launch();
   const int b = C->bi(t), bp = C->bi(t - 1), bs = C->bi(t - C->depth);
@@ -1522,7 +1549,7 @@ extern "C" int pgcn_layer_bwd(pgcn_ctx* C, int64_t t, int32_t l, const float* pa
     }
   }
   // phase B: S9 stale (PIPE) / fresh (VANILLA) boundary gradients (l.22-25) and M^(l-1)
-  if (l >= 2 && C->xp == XP_PUSH) C->bpushed[l] = t;  // every producer of J^(l-1) pushed its boundary rows
+  if (l >= 2 && pushing(C)) C->bpushed[l] = t;  // every producer of J^(l-1) pushed its boundary rows
   if (l >= 2) {
     bool posted_have = false;
     if (C->posted && (rc = post_bwd(C, t, l, Lk, &posted_have))) return rc;
@@ -1812,6 +1839,68 @@ extern "C" int pgcn_timing_read(pgcn_ctx* C, int32_t kind, double* ms, int64_t* 
 extern "C" int pgcn_timing_read_gather(pgcn_ctx* C, int32_t kind, double* gather_bytes) {
   if (!C || kind < 0 || kind >= PGCN_K_COUNT || !gather_bytes) return fail(PGCN_EINVAL, "bad argument");
   *gather_bytes = C->kt[kind].gbytes;
+  return PGCN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// N2 over NVLink: the workspaces of the ranks mapped into each other with CUDA IPC.
+namespace {
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<AddrRangeFn>(ptr);
+  });
+  return fn;
+}
+}  // namespace
+
+extern "C" int pgcn_ipc_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+extern "C" int pgcn_ipc_export(pgcn_ctx* C, void* handle, int64_t* offset) {
+  if (!C || !handle || !offset) return fail(PGCN_EINVAL, "pgcn_ipc_export: null argument");
+  if (!C->ipc_push) return fail(PGCN_ESTATE, "pgcn_ipc_export: context not created for PUSH across ranks");
+  AddrRangeFn f = addr_range_fn();
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!f || f(&base, &size, reinterpret_cast<CUdeviceptr>(C->ws)) != CUDA_SUCCESS)
+    return fail(PGCN_ECUDA, "pgcn_ipc_export: allocation range of the workspace unavailable");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(PGCN_ECUDA, "pgcn_ipc_export: %s", cudaGetErrorString(e));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(C->ws) - base);
+  return PGCN_OK;
+}
+
+extern "C" int pgcn_ipc_import(pgcn_ctx* C, int32_t rank, const void* handle, int64_t offset) {
+  if (!C || !handle || offset < 0) return fail(PGCN_EINVAL, "pgcn_ipc_import: bad argument");
+  if (!C->ipc_push) return fail(PGCN_ESTATE, "pgcn_ipc_import: context not created for PUSH across ranks");
+  if (rank < 0 || rank >= C->nranks || rank == C->rank) return fail(PGCN_EINVAL, "pgcn_ipc_import: bad rank %d", rank);
+  if ((int)C->peer.size() < C->nranks) C->peer.resize(C->nranks);
+  if (C->peer[rank].X) return fail(PGCN_ESTATE, "pgcn_ipc_import: rank %d already imported", rank);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* basep = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&basep, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(PGCN_ECUDA, "pgcn_ipc_import(rank %d): %s", rank, cudaGetErrorString(e));
+  // partition `rank`'s buffers at the offsets its own context laid them out at (same partitioning, config)
+  pgcn_ctx T;
+  const int32_t loc = rank;
+  pgcn_comm cm{rank, C->nranks, "x", "x"};  // shapes only (no communicator is created)
+  int rc = init_ctx_shapes(&T, C->part, &loc, 1, &C->cfg, &cm);
+  if (rc) { cudaIpcCloseMemHandle(basep); return rc; }
+  Arena A;
+  A.base = static_cast<char*>(basep) + offset;
+  if ((rc = layout(&T, C->part, &loc, 1, A))) { cudaIpcCloseMemHandle(basep); return rc; }
+  C->peer[rank] = T.parts[0];
+  C->ipc_open.push_back(basep);
+  ++C->n_imported;
   return PGCN_OK;
 }
 

@@ -117,6 +117,9 @@ def lib():
         L.pgcn_dev_exchange_hook.argtypes = [vp, i64, i32]
         L.pgcn_dev_exchange_bytes.argtypes = [vp, vp, vp]
         L.pgcn_nccl_id_bytes.restype = i32
+        L.pgcn_ipc_handle_bytes.restype = i32
+        L.pgcn_ipc_export.argtypes = [vp, vp, C.POINTER(C.c_int64)]
+        L.pgcn_ipc_import.argtypes = [vp, i32, vp, i64]
         _lib = L
     return _lib
 
@@ -324,6 +327,24 @@ class Context:
         self._keep = {}
         self.P = param_count(cfg)
         self.widths = [cfg.width[i] for i in range(cfg.n_layers + 1)]
+
+    def ipc_connect(self, group=None):
+        """N2 over NVLink (multi-process PUSH, include/pgcn.h pgcn_ipc_export): export this rank's workspace
+        as a CUDA IPC handle, all-gather the handles with torch.distributed and map every peer's."""
+        import torch.distributed as dist
+        nb = int(lib().pgcn_ipc_handle_bytes())
+        h = (C.c_uint8 * nb)()
+        off = C.c_int64()
+        _check(lib().pgcn_ipc_export(self.handle, C.addressof(h), C.byref(off)))
+        rank = dist.get_rank(group)
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, (rank, bytes(h), int(off.value)), group=group)
+        for r, hb, o in allh:
+            if r == rank:
+                continue
+            buf = (C.c_uint8 * nb).from_buffer_copy(hb)
+            _check(lib().pgcn_ipc_import(self.handle, int(r), C.addressof(buf), int(o)))
+        dist.barrier(group)
 
     def set_inputs(self, local, X, labels, train_mask):
         """pgcn_set_inputs: the copies are asynchronous on the context stream, so the sources are kept

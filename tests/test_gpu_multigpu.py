@@ -6,7 +6,9 @@ gradients with ncclSend/ncclRecv on the library's comm stream and all-reduces G 
 Every per-iteration record (partition loss, theta, G, H^(l), J^(l)) must match the single-process run of
 the same partitions through the LOOPBACK transport -- the same control flow with device copies as the
 transfer -- to 1e-5 relative (bit-identical is expected for two ranks: the all-reduce of two addends is
-one fp32 add either way), and the oracle to 1e-4.  Modes: VANILLA, PIPE, PIPE-GF, depth 2.
+one fp32 add either way).  Modes: VANILLA, PIPE, PIPE-GF, depth 2; NCCL send/recv, and PUSH across ranks
+(N2 over NVLink: the producing epilogues store the exchanged rows into the peers' workspaces, mapped with
+CUDA IPC; include/pgcn.h pgcn_ipc_export).
 
 Skipped when fewer than `world` GPUs are visible (the one-GPU boxes of this build); two ranks on one GPU
 are never used (NCCL rejects them, and ranks whose kernels wait on one another must not share a GPU).
@@ -20,7 +22,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-CASES = [("vanilla", False, False, 1), ("pipe", False, False, 1), ("pipe", True, True, 1), ("pipe", False, False, 2)]
+CASES = [("vanilla", False, False, 1, "nccl"), ("pipe", False, False, 1, "nccl"), ("pipe", True, True, 1, "nccl"),
+         ("pipe", False, False, 2, "nccl"),
+         # N2 over NVLink: producers store the exchanged rows into the peers' workspaces (CUDA IPC)
+         ("pipe", False, False, 1, "push"), ("pipe", True, True, 1, "push"), ("pipe", False, False, 2, "push")]
 
 
 def _free_port():
@@ -38,7 +43,7 @@ def _problem():
     return g, widths, glorot_params(widths, 5)
 
 
-def _kw(mode, sf, sg, depth):
+def _kw(mode, sf, sg, depth, transport="nccl"):
     return dict(mode=mode, smooth_f=sf, smooth_g=sg, gamma=0.7, dropout=0.3, loss="bce", opt="sgd", lr=2.0,
                 depth=depth)
 
@@ -75,9 +80,12 @@ def _worker(rank, world, port, case, T, q):
         from paper_2203_10428_b200 import pgcn as P
         g, widths, params0 = _problem()
         part = P.partition(g.n, g.row_ptr, g.col_idx, world)
-        cfg = P.make_config(widths, n_global=g.n, n_train_global=g.n_train, dump_j=True, **_kw(*case))
+        cfg = P.make_config(widths, n_global=g.n, n_train_global=g.n_train, dump_j=True,
+                            transport="push" if case[4] == "push" else "local", **_kw(*case))
         comm = P.nccl_comm(rank, world)
         ctx = P.Context(part, cfg, local_parts=[rank], comm=comm)
+        if case[4] == "push":
+            ctx.ipc_connect()
         gid = part.view(rank)["inner_gid"]
         ctx.set_inputs(0, torch.tensor(g.X[gid]).cuda(), torch.tensor(g.labels[gid]).cuda(),
                        torch.tensor(g.train_mask[gid]).cuda())
@@ -138,7 +146,8 @@ def test_nccl_ranks_match_loopback(world, case):
     theta = torch.tensor(P.flatten_params(params0)).cuda()
     ref = _records(P, ctx, list(range(world)), widths, T, theta, torch.zeros_like(theta), torch.zeros(1, device="cuda"))
     fb0, bb0 = ctx.exchange_bytes()
-    assert sum(r[2] for r in res) == fb0 and sum(r[3] for r in res) == bb0, "exchanged bytes differ"
+    if case[4] == "nccl":  # (PUSH counts the pushed rows, not the posted bytes)
+        assert sum(r[2] for r in res) == fb0 and sum(r[3] for r in res) == bb0, "exchanged bytes differ"
     worst = 0.0
     for t in range(T):
         for rank, recs, _, _, _ in res:
