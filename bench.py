@@ -247,7 +247,7 @@ def build_rank_workload(name, parts, rank, dist, pgcn, model="sage", n=None, nnz
 SHARDED_N = 50_000_000  # configs above this many nodes build per-rank inputs (build_rank_workload)
 
 
-def cpu_baseline(name, parts, mode, smooth, sample_n=16000, iters=2, model="sage"):
+def cpu_baseline(name, parts, mode, smooth, sample_n=16000, iters=5, model="sage"):
     """The oracle (oracle/, numpy/scipy fp64) as it stands, on a bounded sample of the same workload:
     the same generator recipe, degree, widths, dropout and partition count at N = sample_n, timed
     for `iters` PipeGCN iterations; per-epoch time extrapolated linearly in N (every term of the
