@@ -1372,6 +1372,17 @@ extern "C" int pgcn_loss(pgcn_ctx* C, int64_t t, float* loss_dev) {
       reduce_sum(Lk, p.row_loss, p.n_tr, C->part_loss + i);
       continue;
     }
+    if (C->cfg.train_sparse && p.tr_list && 2 * p.n_tr < p.n_in) {
+      // few train rows (products-shaped: 8 %): zero-fill M^(L) with one memset and run the loss warps on the
+      // train row list only -- not one warp per row that mostly stores a zero row (same M, same loss terms)
+      Scope sc(C, PGCN_K_LOSS, 4.0 * (p.Mlo ? 2 : 1) * p.n_in * C->ld[L] + 8.0 * p.n_tr * C->F[L] + 8.0 * p.n_tr);
+      cudaMemsetAsync(p.M, 0, sizeof(float) * (size_t)(p.n_in * C->ld[L]), C->s);
+      if (p.Mlo) cudaMemsetAsync(p.Mlo, 0, sizeof(float) * (size_t)(p.n_in * C->ld[L]), C->s);
+      loss_rows(Lk, C->cfg.loss, p.logits, p.n_tr, C->F[L], C->ld[L], p.labels, nullptr,
+                (double)C->cfg.n_train_global, p.M, p.row_loss, p.Mlo, p.tr_list);
+      reduce_sum(Lk, p.row_loss, p.n_tr, C->part_loss + i);
+      continue;
+    }
     Scope sc(C, PGCN_K_LOSS, (p.Mlo ? 12.0 : 8.0) * p.n_in * C->F[L] + 5.0 * p.n_in);
     loss_rows(Lk, C->cfg.loss, p.logits, p.n_in, C->F[L], C->ld[L], p.labels, p.train,
               (double)C->cfg.n_train_global, p.M, p.row_loss, p.Mlo);

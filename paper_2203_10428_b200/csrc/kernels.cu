@@ -788,13 +788,14 @@ __device__ __forceinline__ float warp_max(float v) {
 // Y and M may alias (compact train rows: the logits become J^(L) in place, each row read before written)
 __global__ void k_loss_ce(const float* Y, int64_t n, int64_t C, int64_t ld, const int32_t* __restrict__ lab,
                           const uint8_t* __restrict__ train, float inv_nt, float* M, float* __restrict__ rl,
-                          float* __restrict__ Mlo) {
+                          float* __restrict__ Mlo, const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; k < n; k += wpg) {
+    const int64_t v = rows ? (int64_t)rows[k] : k;  // rows: the train row list (row loss at position k)
     const float* y = Y + v * ld;
     float* m = M + v * ld;
-    if (train && !train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
+    if (!rows && train && !train[v]) {  // J^(L) = 0 off the train set: 16-byte stores (ld is a multiple of 4)
       for (int64_t c = lane; c < ld / 4; c += 32) {
         reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (Mlo) reinterpret_cast<float4*>(Mlo + v * ld)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -818,19 +819,20 @@ __global__ void k_loss_ce(const float* Y, int64_t n, int64_t C, int64_t ld, cons
       m[c] = g;
       if (Mlo) Mlo[v * ld + c] = lo_tf32(g);
     }
-    if (lane == 0) rl[v] = (ls + mx - yt) * inv_nt;
+    if (lane == 0) rl[k] = (ls + mx - yt) * inv_nt;
   }
 }
 
 __global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, const uint8_t* __restrict__ lab,
                            const uint8_t* __restrict__ train, float inv_ntc, float* M, float* __restrict__ rl,
-                           float* __restrict__ Mlo) {
+                           float* __restrict__ Mlo, const int32_t* __restrict__ rows) {
   const int lane = threadIdx.x & 31;
   const int64_t wpg = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; v < n; v += wpg) {
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; k < n; k += wpg) {
+    const int64_t v = rows ? (int64_t)rows[k] : k;  // rows: the train row list (row loss at position k)
     const float* y = Y + v * ld;
     float* m = M + v * ld;
-    const bool tr = !train || train[v] != 0;
+    const bool tr = rows || !train || train[v] != 0;
     if (!tr) {
       for (int64_t c = lane; c < ld / 4; c += 32) {
         reinterpret_cast<float4*>(m)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -851,7 +853,7 @@ __global__ void k_loss_bce(const float* Y, int64_t n, int64_t C, int64_t ld, con
       if (Mlo) Mlo[v * ld + c] = lo_tf32(g);
     }
     l = warp_sum(l);
-    if (lane == 0) rl[v] = l * inv_ntc;
+    if (lane == 0) rl[k] = l * inv_ntc;
   }
 }
 
@@ -1566,15 +1568,15 @@ void gather_bytes(Launch L, const void* src, const int32_t* list, int64_t n, int
 }
 
 void loss_rows(Launch L, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
-               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo) {
+               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo, const int32_t* rows) {
   if (n <= 0) return;
   const int grid = grid_for(n, kThreads / 32, sm_count() * 32);
   if (kind == 0)
     k_loss_ce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const int32_t*>(labels), train,
-                                          (float)(1.0 / n_train), M, row_loss, Mlo);
+                                          (float)(1.0 / n_train), M, row_loss, Mlo, rows);
   else
     k_loss_bce<<<grid, kThreads, 0, L.s>>>(Y, n, C, ld, static_cast<const uint8_t*>(labels), train,
-                                           (float)(1.0 / (n_train * (double)C)), M, row_loss, Mlo);
+                                           (float)(1.0 / (n_train * (double)C)), M, row_loss, Mlo, rows);
   count(L);
 }
 

@@ -143,8 +143,11 @@ void spin_ns(cudaStream_t s, int64_t ns);
 // every row is a train row).
 // M = J^(L) (zero outside the train set), row_loss[v] = loss term of v (already / n_train).
 // Mlo (optional; also grad_reduce): M's 3xTF32 lo term, x - trunc_tf32(x), for the GEMMs that read M.
+// rows (optional): only the listed rows (the train row list; n = its length), row_loss[k] for the k-th --
+// the caller zero-fills M elsewhere.
 void loss_rows(Launch, int kind, const float* Y, int64_t n, int64_t C, int64_t ld, const void* labels,
-               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo = nullptr);
+               const uint8_t* train, double n_train, float* M, float* row_loss, float* Mlo = nullptr,
+               const int32_t* rows = nullptr);
 // out[0] = sum of x[0..n) (single block, fixed order -> deterministic)
 void reduce_sum(Launch, const float* x, int64_t n, float* out);
 
