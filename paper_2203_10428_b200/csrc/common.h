@@ -40,7 +40,8 @@ struct DevKnobs {
   int tc_dw_bnmax = 256;
   int tc_bk16 = 2;
   int tc_dw16 = 0;
-  int l2_persist_mb = 0;  // L2 persisting window over the table a gather SpMM reads (PGCN_L2_PERSIST_MB)  // 3xTF32 dW: 16-row k-blocks (PGCN_TC_DW16; measured slower, profiles/r2r_bk16.md)  // 3xTF32 K-major GEMMs: 16-element k-blocks (PGCN_TC_BK16: 0 off, 1 n-tiles > 128, 2 all)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
+  int l2_persist_mb = 0;
+  int tc_dw_ctas = 2;  // dW CTAs per SM (PGCN_TC_DW_CTAS: 2 = two pipelines per SM where they fit, 1 = one)  // L2 persisting window over the table a gather SpMM reads (PGCN_L2_PERSIST_MB)  // 3xTF32 dW: 16-row k-blocks (PGCN_TC_DW16; measured slower, profiles/r2r_bk16.md)  // 3xTF32 K-major GEMMs: 16-element k-blocks (PGCN_TC_BK16: 0 off, 1 n-tiles > 128, 2 all)  // dW n-tile cap (PGCN_TC_DW_BNMAX: 32..256, multiple of 32)
   long long spmm_grab = 128;
   const char* spmm_table = nullptr;
 };

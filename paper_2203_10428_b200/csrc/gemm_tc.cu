@@ -760,7 +760,9 @@ cudaError_t tc_launch(const TcParams& p0, cudaStream_t s, int sms) {
   TcParams p = p0;
   int ctas = 1;
   // (the PUSH instantiation needs > 85 registers per thread: one CTA of 384 threads per SM)
-  if (gemm_ctas() == 2 && p.tmem_cols <= 256 && p.mode != TC_DW && !p.push.mode) {  // dW: split-K plan sized for 148 CTAs
+  // dW: its split-K plan is sized for sm_count() x PGCN_TC_DW_CTAS concurrent CTAs
+  const bool two = p.mode == TC_DW ? knobs().tc_dw_ctas == 2 : gemm_ctas() == 2;
+  if (two && p.tmem_cols <= 256 && !p.push.mode) {
     const size_t stage = tc::geometry(p.bf, p.mode, p.BN, p.a_feat, p.kbw).stage();
     int S = (int)((104 * 1024 - 1024 - 64) / stage);
     if (S >= 2) {
@@ -846,15 +848,15 @@ static int64_t zmin_for(int64_t kb) {
   const int64_t km = dw_kmax();
   return km > 0 ? std::max<int64_t>(1, (kb + km - 1) / km) : 1;
 }
-static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
+static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2], int slots_sm) {
   const int64_t ovh = 6;  // per-tile fill / drain, in k-block units
   int64_t best = INT64_MAX;
   const int64_t zm0 = zmin_for(kb0), zm1 = nseg > 1 ? zmin_for(kb1) : 0;
   Z[0] = (int)zm0;
   Z[1] = (int)zm1;
-  if ((zm0 + zm1) * base > (int64_t)kDwMaxWaves * sm_count()) return;  // chains cap the split count
+  if ((zm0 + zm1) * base > (int64_t)kDwMaxWaves * slots_sm) return;  // chains cap the split count
   for (int W = 1; W <= kDwMaxWaves; ++W) {
-    const int slots = W * sm_count() / base;
+    const int slots = W * slots_sm / base;
     if (slots < nseg) continue;
     const int lo = 1, hi = nseg > 1 ? slots - 1 : slots;
     for (int z0 = lo; z0 <= hi; ++z0) {
@@ -862,7 +864,7 @@ static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
       int64_t b = nseg > 1 ? (slots - z0 < kb1 ? slots - z0 : (kb1 > 0 ? kb1 : 1)) : 0;
       if (a < zm0 || (nseg > 1 && b < zm1)) continue;
       const int64_t kpt = std::max((kb0 + a - 1) / a, nseg > 1 ? (kb1 + b - 1) / b : (int64_t)0);
-      const int64_t waves = ((a + b) * base + sm_count() - 1) / sm_count();
+      const int64_t waves = ((a + b) * base + slots_sm - 1) / slots_sm;
       const int64_t cost = waves * (kpt + ovh);
       if (cost < best) {
         best = cost;
@@ -874,7 +876,7 @@ static void dw_plan(int64_t kb0, int64_t kb1, int nseg, int base, int Z[2]) {
 }
 
 int64_t tc_dw_ws_floats(int64_t M, int64_t F, int64_t N) {
-  int64_t Z = kDwMaxWaves * sm_count() / dw_base(F, N);
+  int64_t Z = kDwMaxWaves * sm_count() * knobs().tc_dw_ctas / dw_base(F, N);
   const int64_t kb = (M + 31) / 32;
   if (Z > kb) Z = kb;
   Z = std::max(Z, zmin_for(kb));
@@ -1030,12 +1032,17 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.merged = nseg == 2 && rows0 == rows1 && B0 == B1 && F <= 64 && knobs().dw_merge;
   p.a_feat = p.merged ? tc::BM : (F <= 96 ? (int)((F + 31) / 32 * 32) : tc::BM);
   tc_common(p, BN, bf, TC_DW);
+  // two CTAs per SM where their accumulators and two stages each fit (narrow n-tiles; PGCN_TC_DW_CTAS=2,
+  // default): the split plan then fills waves of 2 x sm_count() CTAs -- tc_launch applies the same test
+  const size_t dstage = tc::geometry(p.bf, TC_DW, p.BN, p.a_feat, p.kbw).stage();
+  const int slots_sm = sm_count() *
+      ((knobs().tc_dw_ctas == 2 && p.tmem_cols <= 256 && (104 * 1024 - 1024 - 64) / dstage >= 2) ? 2 : 1);
   int Zseg[2];
   if (p.merged) {
-    dw_plan((rows0 + 31) / 32, 0, 1, dw_base(F, N), Zseg);
+    dw_plan((rows0 + 31) / 32, 0, 1, dw_base(F, N), Zseg, slots_sm);
     Zseg[1] = Zseg[0];
   } else {
-    dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg);
+    dw_plan((rows0 + 31) / 32, (rows1 + 31) / 32, nseg, dw_base(F, N), Zseg, slots_sm);
   }
   const int Zs = std::max(Zseg[0], Zseg[1]);
   const int64_t NP = (N + 3) / 4 * 4;  // partial row stride (16-byte aligned epilogue stores)

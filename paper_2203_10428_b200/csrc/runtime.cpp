@@ -112,6 +112,7 @@ const DevKnobs& knobs() {
     k.tc_bk16 = env_int("PGCN_TC_BK16", 2);
     k.tc_dw16 = env_int("PGCN_TC_DW16", 0);
     k.l2_persist_mb = env_int("PGCN_L2_PERSIST_MB", 0);
+    k.tc_dw_ctas = env_int("PGCN_TC_DW_CTAS", 2) == 2 ? 2 : 1;
     if (k.tc_dw_bnmax < 32 || k.tc_dw_bnmax > 256 || k.tc_dw_bnmax % 32) k.tc_dw_bnmax = 256;
     if (k.spmm_nch < 2 || k.spmm_nch > 8) k.spmm_nch = 2;
     k.dw_kmax = env_int("PGCN_DW_KMAX", 128);
