@@ -1032,11 +1032,10 @@ int tc_dw_general(Launch L, const float* A0, const float* B0, int64_t rows0, con
   p.merged = nseg == 2 && rows0 == rows1 && B0 == B1 && F <= 64 && knobs().dw_merge;
   p.a_feat = p.merged ? tc::BM : (F <= 96 ? (int)((F + 31) / 32 * 32) : tc::BM);
   tc_common(p, BN, bf, TC_DW);
-  // two CTAs per SM where their accumulators and two stages each fit (narrow n-tiles; PGCN_TC_DW_CTAS=2,
-  // default): the split plan then fills waves of 2 x sm_count() CTAs -- tc_launch applies the same test
-  const size_t dstage = tc::geometry(p.bf, TC_DW, p.BN, p.a_feat, p.kbw).stage();
-  const int slots_sm = sm_count() *
-      ((knobs().tc_dw_ctas == 2 && p.tmem_cols <= 256 && (104 * 1024 - 1024 - 64) / dstage >= 2) ? 2 : 1);
+  // PGCN_TC_DW_CTAS=2 (default): the split plan fills waves of 2 x sm_count() CTAs, and tc_launch runs two
+  // CTAs per SM where their accumulators and two stages each fit (narrow n-tiles).  The finer split pays
+  // even where one CTA runs (products-shaped 128-wide dW: 5.06 -> 4.45 ms per step; r2x / r2y)
+  const int slots_sm = sm_count() * knobs().tc_dw_ctas;
   int Zseg[2];
   if (p.merged) {
     dw_plan((rows0 + 31) / 32, 0, 1, dw_base(F, N), Zseg, slots_sm);
